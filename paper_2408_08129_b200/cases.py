@@ -1,0 +1,187 @@
+"""Case inputs for the BASELINE configurations (harness, not hot path).
+
+Background, sponge and far-field recipes restate orodg/cases.py:29-174 so
+the GPU box (which has no reference tree) can build the same inputs; the
+warm bubble and the seeded smooth perturbation are the harness choices
+recorded in tests/golden/make_golden.py and SURVEY.md §8d.
+"""
+
+import math
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from .boundary import BoundaryCondition
+from .errors import ConfigurationError
+from .physics import CONST, PhysicalConstants
+
+
+@dataclass(frozen=True)
+class HillCaseConfig:
+    h_c: float = 400.0
+    a_c: float = 1000.0
+    x_c: float = 30.0e3
+    y_c: float = 20.0e3
+    N_buoyancy: float = 0.01
+    u_bar: float = 10.0
+    p_ref: float = 1.0e5
+    T_ref: float = 293.15
+    domain: tuple = (60.0e3, 40.0e3, 16.0e3)
+    t_final: float = 3600.0
+    dt: float = 2.0
+    constants: PhysicalConstants = CONST
+
+    @property
+    def dim(self):
+        return len(self.domain)
+
+    @property
+    def rho_ref(self):
+        return self.p_ref / (self.constants.R * self.T_ref)
+
+
+@dataclass(frozen=True)
+class SpongeConfig:
+    top_depth: float = 4.0e3
+    lateral_width: float = 10.0e3
+    sigma_max: float = 0.05
+
+    def __post_init__(self):
+        if self.sigma_max < 0 or self.top_depth < 0 or self.lateral_width < 0:
+            raise ConfigurationError("sponge parameters must be >= 0")
+
+
+def hydrostatic_state(z, cfg=HillCaseConfig()):
+    """Constant-N hydrostatic pair p(z), rho(z) with dp/dz = -rho g
+    (orodg/cases.py:80-106)."""
+    c = cfg.constants
+    z = np.asarray(z, dtype=float)
+    n2g = cfg.N_buoyancy ** 2 / c.g
+    e = np.exp(-n2g * z)
+    br = 1.0 - (c.g ** 2 / cfg.N_buoyancy ** 2) * c.Gamma * (cfg.rho_ref / cfg.p_ref) * (1.0 - e)
+    if np.any(br <= 0.0):
+        raise ConfigurationError("hydrostatic profile breaks down: domain too tall "
+                                 f"(min bracket {br.min():.4g})")
+    p = cfg.p_ref * br ** (1.0 / c.Gamma)
+    rho = cfg.rho_ref * (p / cfg.p_ref) ** (1.0 / c.gamma) * e
+    return p, rho, cfg.u_bar
+
+
+def hydrostatic_initial_state(cfg, u_bar=None):
+    ub = cfg.u_bar if u_bar is None else u_bar
+    g = cfg.constants.gamma
+    d = cfg.dim
+
+    def f(coords):
+        p, rho, _ = hydrostatic_state(coords[..., -1], cfg)
+        out = np.zeros(coords.shape[:-1] + (d + 2,))
+        out[..., 0] = rho
+        out[..., 1] = rho * ub
+        out[..., 1 + d] = p / (g - 1.0) + 0.5 * rho * ub ** 2
+        return out
+
+    return f
+
+
+def warm_bubble_state(dim=2, theta0=300.0, dtheta=2.0, xc=10.0e3, zc=2.0e3,
+                      rc=2.0e3, p0=1.0e5, constants=CONST):
+    """Warm bubble of BASELINE configs[0..1] (recipe in make_golden.py)."""
+    R, g, gam = constants.R, constants.g, constants.gamma
+    cp = R * gam / (gam - 1.0)
+
+    def f(coords):
+        x, z = coords[..., 0], coords[..., -1]
+        ex = 1.0 - g * z / (cp * theta0)
+        p = p0 * ex ** (cp / R)
+        r = np.sqrt((x - xc) ** 2 + (z - zc) ** 2)
+        th = theta0 + np.where(r < rc, dtheta * np.cos(0.5 * np.pi * r / rc) ** 2, 0.0)
+        out = np.zeros(coords.shape[:-1] + (dim + 2,))
+        out[..., 0] = p / (R * th * ex)
+        out[..., dim + 1] = p / (gam - 1.0)
+        return out
+
+    return f
+
+
+def smooth_noise(coords, extents, rng, n_modes=8, kmax=4):
+    d = coords.shape[-1]
+    s = np.zeros(coords.shape[:-1])
+    for _ in range(n_modes):
+        k = rng.integers(1, kmax + 1, size=d)
+        a = rng.normal() / 8.0
+        phi = rng.uniform(0.0, 2.0 * np.pi)
+        arg = phi + sum(2.0 * np.pi * k[i] * coords[..., i] / extents[i] for i in range(d))
+        s += a * np.sin(arg)
+    return s
+
+
+def perturbed_state(background, coords, extents, seed, u_scale=10.0):
+    """Background plus seeded smooth 1e-3 perturbations."""
+    rng = np.random.default_rng(seed)
+    U = background.copy()
+    d = coords.shape[-1]
+    U[:, 0] *= 1.0 + 1e-3 * smooth_noise(coords, extents, rng)
+    for a in range(d):
+        s_a = smooth_noise(coords, extents, rng)
+        U[:, 1 + a] = U[:, 1 + a] / background[:, 0] * U[:, 0] + U[:, 0] * 1e-3 * u_scale * s_a
+    U[:, d + 1] *= 1.0 + 1e-3 * smooth_noise(coords, extents, rng)
+    return U
+
+
+def energy_like(U, seed):
+    d = U.shape[1] - 2
+    rng = np.random.default_rng(seed)
+    return U[:, d + 1] * (1.0 + 1e-3 * rng.standard_normal(U[:, d + 1].shape))
+
+
+def sponge_sigma(geometry, sponge, extents, lateral_axes=(0,)):
+    """Nodal Rayleigh rate, sin^2 ramps combined by max (orodg/cases.py:127-146)."""
+    xyz = geometry.node_coords
+    sig = np.zeros(xyz.shape[:2])
+    if sponge.sigma_max == 0.0:
+        return sig
+    zt = extents[-1]
+    if sponge.top_depth > 0.0:
+        r = np.clip((xyz[..., -1] - (zt - sponge.top_depth)) / sponge.top_depth, 0.0, 1.0)
+        sig = np.maximum(sig, np.sin(0.5 * np.pi * r) ** 2)
+    if sponge.lateral_width > 0.0:
+        w = sponge.lateral_width
+        for a in lateral_axes:
+            lo = np.clip((w - xyz[..., a]) / w, 0.0, 1.0)
+            hi = np.clip((xyz[..., a] - (extents[a] - w)) / w, 0.0, 1.0)
+            sig = np.maximum(sig, np.sin(0.5 * np.pi * np.maximum(lo, hi)) ** 2)
+    return sponge.sigma_max * sig
+
+
+def farfield_bcs(geometry, background_data, wall_axes_sides=(("z", 0),)):
+    """Wall on the named (axis, side) batches, far-field background traces
+    elsewhere (orodg/cases.py:156-174)."""
+    mesh = geometry.mesh
+    d = mesh.dim
+    names = {"x": 0, "y": 1, "z": d - 1}
+    walls = {(names[a], s) for a, s in wall_axes_sides}
+    b = geometry.basis
+    out = []
+    for bt in mesh.topology.boundary:
+        if (bt.axis, bt.side) in walls:
+            out.append(BoundaryCondition("wall"))
+            continue
+        fidx = b.face_nodes[bt.axis][bt.side]
+        vals = background_data[bt.leaves][:, :, fidx]
+        out.append(BoundaryCondition("farfield", vals @ b.face_interp.T))
+    return out
+
+
+def gaussian_hill(h0=400.0, a=3.0e3, xc=30.0e3, yc=30.0e3):
+    """BASELINE configs[3] hill: h0 exp(-(r/a)^2), half-width a (harness pin)."""
+    def f(x, y):
+        return h0 * np.exp(-(((x - xc) ** 2 + (y - yc) ** 2) / a ** 2))
+    return f
+
+
+def schar_terrain(h0=250.0, a=5.0e3, lam=4.0e3, xc=25.0e3):
+    """BASELINE configs[2] terrain on [0, 50] km (shifted by 25 km)."""
+    def f(x):
+        xs = x - xc
+        return h0 * np.exp(-(xs / a) ** 2) * np.cos(np.pi * xs / lam) ** 2
+    return f

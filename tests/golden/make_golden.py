@@ -1,0 +1,499 @@
+"""Generate the golden parity fixtures by running the REFERENCE solver.
+
+Run only in the build container (it imports the read-only reference package
+from /root/reference/pkg/src); the GPU box never runs this.  Outputs are the
+committed ``tests/golden/*.npz`` files, one per case.
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [case ...]
+
+Cases (inputs built only through the reference's public API):
+
+  cfg1     BASELINE configs[0]: warm bubble 20x10 km, 32x16, r=2, walls,
+           ARS(2,2,2), dt=0.5 s, 10 steps
+  cfg2     BASELINE configs[1]: same bubble on 64x32 with z<5 km refined
+           once, r=4, krylov_tol=1e-10, 200 steps (slow: ~6-10 min)
+  hang2d   2D Gal-Chen terrain (bell hill), two refinement levels, far-field
+           + bottom wall, Rayleigh sponge, r=4 (the reference conftest mesh)
+  hang3d   3D terrain + hanging + far-field + sponge, r=3 (conftest mesh)
+  per3d    3D triply-periodic box, seeded once-refined cells, r=2 (cfg5 recipe
+           at toy size)
+  cfg3s    scaled-down Schar case (terrain, sponge, far-field, 2 refinement
+           levels near the ground), r=4, 3 steps
+  part     partition_leaves on the cfg2 mesh, P=1..8, unit and seeded weights
+
+Warm-bubble recipe (harness choice, recorded here and mirrored by
+paper_2408_08129_b200.cases.warm_bubble_state): constant theta0 = 300 K
+background with Exner pi = 1 - g z/(c_p theta0), p = p0 pi^(c_p/R), p0 = 1e5;
+theta' = 2 K cos^2(pi r / (2 rc)) for r < rc = 2 km around (10 km, 2 km);
+rho = p / (R theta pi); u = 0; rhoE = p/(gamma-1).
+"""
+
+import os
+import sys
+import time
+
+for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+if REF not in sys.path:
+    sys.path.insert(0, REF)
+
+import orodg  # noqa: E402
+from orodg import cases, imex, krylov  # noqa: E402
+from orodg.boundary import wall_everywhere  # noqa: E402
+from orodg.dgops import DGOperators  # noqa: E402
+from orodg.field import project_initial_data  # noqa: E402
+from orodg.geometry import build_geometry  # noqa: E402
+from orodg.mesh import build_uniform_mesh, refine_region  # noqa: E402
+from orodg.partition import partition_leaves  # noqa: E402
+from orodg.physics import CONST, FlowModel  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+# ----------------------------------------------------------------- inputs
+
+def warm_bubble(cfg_d=2, theta0=300.0, dtheta=2.0, xc=10.0e3, zc=2.0e3,
+                rc=2.0e3, p0=1.0e5):
+    R, g, gam = CONST.R, CONST.g, CONST.gamma
+    cp = R * gam / (gam - 1.0)
+
+    def f(coords):
+        x = coords[..., 0]
+        z = coords[..., -1]
+        exner = 1.0 - g * z / (cp * theta0)
+        p = p0 * exner ** (cp / R)
+        r = np.sqrt((x - xc) ** 2 + (z - zc) ** 2)
+        bump = np.where(r < rc, dtheta * np.cos(0.5 * np.pi * r / rc) ** 2, 0.0)
+        theta = theta0 + bump
+        rho = p / (R * theta * exner)
+        out = np.zeros(coords.shape[:-1] + (cfg_d + 2,))
+        out[..., 0] = rho
+        out[..., cfg_d + 1] = p / (gam - 1.0)
+        return out
+
+    return f
+
+
+def smooth_noise(coords, extents, rng, n_modes=8, kmax=4):
+    """Sum of seeded sines (SURVEY.md §8d cfg5 perturbation recipe)."""
+    d = coords.shape[-1]
+    s = np.zeros(coords.shape[:-1])
+    for _ in range(n_modes):
+        k = rng.integers(1, kmax + 1, size=d)
+        a = rng.normal() / 8.0
+        phi = rng.uniform(0.0, 2.0 * np.pi)
+        arg = phi + sum(2.0 * np.pi * k[i] * coords[..., i] / extents[i]
+                        for i in range(d))
+        s += a * np.sin(arg)
+    return s
+
+
+def perturbed(background, coords, extents, seed, u_scale=10.0):
+    """rho(1+1e-3 s), m += rho*1e-3*u_scale*s_a, rhoE(1+1e-3 s)."""
+    rng = np.random.default_rng(seed)
+    U = background.copy()
+    d = coords.shape[-1]
+    s_rho = smooth_noise(coords, extents, rng)
+    U[:, 0] *= 1.0 + 1e-3 * s_rho
+    for a in range(d):
+        s_a = smooth_noise(coords, extents, rng)
+        U[:, 1 + a] = U[:, 1 + a] / background[:, 0] * U[:, 0] \
+            + U[:, 0] * 1e-3 * u_scale * s_a
+    s_e = smooth_noise(coords, extents, rng)
+    U[:, d + 1] *= 1.0 + 1e-3 * s_e
+    return U
+
+
+def energy_like(U, seed):
+    d = U.shape[1] - 2
+    rng = np.random.default_rng(seed)
+    return U[:, d + 1] * (1.0 + 1e-3 * rng.standard_normal(U[:, d + 1].shape))
+
+
+def hill2d(x):
+    return 400.0 / (1.0 + ((x - 30.0e3) / 1.0e3) ** 2) ** 1.5
+
+
+def hill3d(x, y):
+    return 400.0 / (1.0 + ((x - 10.0e3) / 1.0e3) ** 2
+                    + ((y - 10.0e3) / 1.0e3) ** 2) ** 1.5
+
+
+def schar(x):
+    xs = x - 25.0e3
+    return 250.0 * np.exp(-(xs / 5.0e3) ** 2) * np.cos(np.pi * xs / 4.0e3) ** 2
+
+
+# ------------------------------------------------------------- recording
+
+def mesh_record(mesh, prefix="mesh_"):
+    rec = {}
+    lv = np.array([l for l, _ in mesh.leaves], dtype=np.int64)
+    org = np.array([o for _, o in mesh.leaves], dtype=np.int64)
+    rec[prefix + "levels"] = lv
+    rec[prefix + "origins"] = org
+    rec[prefix + "extents"] = np.array(mesh.extents)
+    rec[prefix + "root"] = np.array(mesh.root_counts)
+    rec[prefix + "periodic"] = np.array(mesh.periodic, dtype=np.int64)
+    topo = mesh.topology
+    rec[prefix + "conf_axis"] = np.array([b.axis for b in topo.conforming], dtype=np.int64)
+    for i, b in enumerate(topo.conforming):
+        rec[f"{prefix}conf{i}_left"] = b.left
+        rec[f"{prefix}conf{i}_right"] = b.right
+    rec[prefix + "hang_axis_orient"] = np.array(
+        [[b.axis, b.orient] for b in topo.hanging], dtype=np.int64).reshape(-1, 2)
+    for i, b in enumerate(topo.hanging):
+        rec[f"{prefix}hang{i}_coarse"] = b.coarse
+        rec[f"{prefix}hang{i}_fine"] = b.fine
+        rec[f"{prefix}hang{i}_subface"] = b.subface
+    rec[prefix + "bdry_axis_side"] = np.array(
+        [[b.axis, b.side] for b in topo.boundary], dtype=np.int64).reshape(-1, 2)
+    for i, b in enumerate(topo.boundary):
+        rec[f"{prefix}bdry{i}_leaves"] = b.leaves
+    rec[prefix + "fingerprint"] = np.array(mesh.fingerprint)
+    return rec
+
+
+def geometry_record(geom):
+    rec = {"geo_det_j": geom.det_j, "geo_ctrv": geom.ctrv,
+           "geo_mass_h_inv": geom.mass_h_inv, "geo_mass_v_inv": geom.mass_v_inv,
+           "geo_node_coords": geom.node_coords}
+    for name, lst in (("conf", geom.conforming), ("hang", geom.hanging),
+                      ("bdry", geom.boundary)):
+        for i, fg in enumerate(lst):
+            rec[f"geo_{name}{i}_normal"] = fg.normal
+            rec[f"geo_{name}{i}_ws"] = fg.ws
+    return rec
+
+
+def operator_record(ops, split, U, model, bcs, seed, a_dt):
+    """Every hot-path operator once, on U (and energy-like x)."""
+    geom = ops.geometry
+    d = ops.dim
+    rec = {"U": U}
+    t0 = time.perf_counter()
+    dual_adv = ops.divergence_advective(U, model, bcs)
+    rec["dual_adv"] = dual_adv
+    rec["minv_dual_adv"] = geom.apply_mass_inverse(dual_adv)
+    R = split.explicit_residual(U, 0.0)
+    rec["explicit_residual"] = R
+    rec["mass_rate"] = np.array(split._last_mass_rate)
+    W = orodg.conserved_to_primitive(U, model, var_axis=1, check=False)
+    rec["grad_dual"] = ops.gradient_scalar(W.p, model, bcs)
+    h, K = split.frozen_coefficients(U)
+    rec["frozen_h"], rec["frozen_K"] = h, K
+    rec["divhv_dual"] = ops.divergence_hv(U[:, 1:1 + d], h, model, bcs)
+    rec["divhv_prepared_dual"] = ops.prepare_divergence_hv(h, model, bcs)(U[:, 1:1 + d])
+    x = energy_like(U, seed)
+    rec["x"] = x
+    rec["a_dt"] = np.array(a_dt)
+    m_e = U[:, 1:1 + d].copy()
+    e_e = U[:, 1 + d].copy()
+    F, grad_p = split.energy_affine_map(a_dt, h, K, m_e, e_e)
+    rec["F0"] = F(np.zeros_like(x))
+    rec["Fx"] = F(x)
+    rec["grad_p_x"] = grad_p(x)
+    action = imex.build_helmholtz_action(split, a_dt, U)
+    rec["helm_x"] = action(x.ravel()).reshape(x.shape)
+    # linear composition (no cancellation noise): x + a_dt Minv Div_lin(V),
+    # V = -(a_dt/M^2)(gamma-1) Minv G_lin(x)   (imex.py:207-216)
+    rec["integrate_conserved"] = ops.integrate_conserved(U)
+    rec.update(noise_record(ops, split, U, model, bcs, x, a_dt, rec))
+    rec["inner_UU"] = np.array(ops.global_inner_product(U, U))
+    rec["op_seconds"] = np.array(time.perf_counter() - t0)
+    return rec
+
+
+def _per_var_noise(a, b):
+    tot = np.linalg.norm(b)
+    return np.array([np.linalg.norm(a[:, v] - b[:, v])
+                     / max(np.linalg.norm(b[:, v]), 1e-6 * tot, 1e-300)
+                     for v in range(b.shape[1])])
+
+
+def noise_record(ops, split, U, model, bcs, x, a_dt, rec):
+    """The reference's own rounding sensitivity: every output recomputed on
+    inputs perturbed by one ulp (relative 2^-52, random sign).  Parity gates
+    per variable are max(1e-12, 10 x this noise) -- a floor no
+    implementation with a different summation order can beat."""
+    d = ops.dim
+    rng = np.random.default_rng(1234)
+    ulp = 2.0 ** -52
+    Up = U * (1.0 + ulp * rng.choice([-1.0, 1.0], size=U.shape))
+    xp = x * (1.0 + ulp * rng.choice([-1.0, 1.0], size=x.shape))
+    out = {}
+    out["noise_dual_adv"] = _per_var_noise(ops.divergence_advective(Up, model, bcs),
+                                           rec["dual_adv"])
+    out["noise_explicit_residual"] = _per_var_noise(split.explicit_residual(Up, 0.0),
+                                                    rec["explicit_residual"])
+    Wp = orodg.conserved_to_primitive(Up, model, var_axis=1, check=False)
+    out["noise_grad_dual"] = _per_var_noise(ops.gradient_scalar(Wp.p, model, bcs),
+                                            rec["grad_dual"])
+    hp, Kp = split.frozen_coefficients(Up)
+    out["noise_divhv_dual"] = _per_var_noise(
+        ops.divergence_hv(Up[:, 1:1 + d], hp, model, bcs), rec["divhv_dual"])
+    h, K = split.frozen_coefficients(U)
+    F, grad_p = split.energy_affine_map(a_dt, h, K, U[:, 1:1 + d].copy(),
+                                        U[:, 1 + d].copy())
+    out["noise_Fx"] = _per_var_noise(F(xp)[:, None], rec["Fx"][:, None])
+    out["noise_grad_p_x"] = _per_var_noise(grad_p(xp), rec["grad_p_x"])
+    action = imex.build_helmholtz_action(split, a_dt, U)
+    out["noise_helm_x"] = _per_var_noise(action(xp.ravel()).reshape(x.shape)[:, None],
+                                         rec["helm_x"][:, None])
+    return out
+
+
+def gmres_record(split, U, a_dt, tol, seed):
+    """One standalone Helmholtz GMRES solve (krylov.py:27-115)."""
+    d = split.dim
+    h, K = split.frozen_coefficients(U)
+    m_e = U[:, 1:1 + d].copy()
+    e_e = U[:, 1 + d].copy()
+    F, _ = split.energy_affine_map(a_dt, h, K, m_e, e_e)
+    F0 = F(np.zeros_like(e_e))
+    action = imex.build_helmholtz_action(split, a_dt, U)
+    x0 = energy_like(U, seed + 1).ravel()
+    x, st = krylov.gmres(action, F0.ravel(), x0=x0, tol_rel=tol, restart=30,
+                         max_iter=1000)
+    return {"gm_rhs": F0, "gm_x0": x0.reshape(e_e.shape), "gm_x": x.reshape(e_e.shape),
+            "gm_iters": np.array(st.iterations), "gm_restarts": np.array(st.restarts),
+            "gm_residual": np.array(st.residual),
+            "gm_history": np.array(st.residual_history), "gm_tol": np.array(tol)}
+
+
+def steps_record(split, U0, dt, n_steps, solve_cfg, keep_every=None):
+    tab = imex.ars222()
+    U = U0.copy()
+    rec = {"dt": np.array(dt), "n_steps": np.array(n_steps)}
+    fp, kr, inc, mr = [], [], [], []
+    t = 0.0
+    t0 = time.perf_counter()
+    snaps = {}
+    for s in range(1, n_steps + 1):
+        U, st = imex.imex_step(U, t, dt, tab, split, solve_cfg)
+        t = s * dt
+        fp.append(st.fp_iters)
+        kr.append(st.krylov_iters)
+        inc.append(st.pressure_increments)
+        mr.append(st.mass_rate)
+        if s == 1:
+            snaps["U_step1"] = U.copy()
+        if keep_every and s % keep_every == 0:
+            snaps[f"U_step{s}"] = U.copy()
+        print(f"  step {s}: fp {st.fp_iters} krylov {st.krylov_iters}", flush=True)
+    rec["step_seconds"] = np.array((time.perf_counter() - t0) / n_steps)
+    rec["U_final"] = U
+    rec.update(snaps)
+    rec["fp_iters"] = _ragged(fp)
+    rec["krylov_iters"] = _ragged(kr)
+    rec["pressure_increments"] = _ragged(inc, float)
+    rec["mass_rate_steps"] = np.array(mr)
+    return rec
+
+
+def _ragged(lists, dtype=np.int64):
+    width = max(len(x) for x in lists)
+    out = np.full((len(lists), width), -1 if dtype is np.int64 else np.nan,
+                  dtype=dtype)
+    for i, x in enumerate(lists):
+        out[i, :len(x)] = x
+    return out
+
+
+def save(name, rec):
+    path = os.path.join(OUT, f"{name}.npz")
+    np.savez_compressed(path, **rec)
+    print(f"wrote {path} ({os.path.getsize(path) / 1e6:.2f} MB)")
+
+
+# ----------------------------------------------------------------- cases
+
+def bubble_case(root, refine_below=None, degree=2):
+    mesh = build_uniform_mesh((20.0e3, 10.0e3), root)
+    if refine_below is not None:
+        mesh = refine_region(mesh, lambda lf: lf.center[1] < refine_below, 1)
+    geom = build_geometry(mesh, degree)
+    ops = DGOperators(geom)
+    model = FlowModel.dimensional()
+    U0 = project_initial_data(geom, warm_bubble()).data
+    bcs = wall_everywhere(mesh)
+    split = imex.SplitOperators(ops, model, bcs)
+    return mesh, geom, ops, model, U0, bcs, split
+
+
+def case_cfg1():
+    mesh, geom, ops, model, U0, bcs, split = bubble_case((32, 16), None, 2)
+    dt = 0.5
+    a_dt = dt * (1.0 - 1.0 / np.sqrt(2.0))
+    rec = {"case": np.array("cfg1"), "degree": np.array(2)}
+    rec.update(mesh_record(mesh))
+    rec.update(geometry_record(geom))
+    rec.update(operator_record(ops, split, U0, model, bcs, 11, a_dt))
+    rec.update(gmres_record(split, U0, a_dt, 1e-8, 11))
+    # one implicit stage exactly as imex_step stage 1 forms it
+    scfg = imex.ImplicitSolveConfig()
+    KE0 = split.explicit_residual(U0, 0.0)
+    acc = U0 + (dt * (1.0 - 1.0 / np.sqrt(2.0))) * KE0
+    stats = imex.StepStats()
+    it, nfp = imex._solve_implicit_stage(acc, U0, a_dt, split, scfg, stats,
+                                         orodg.timing.NullTimer(), None)
+    rec.update({"stage_acc": acc, "stage_iterate": it, "stage_fp": np.array(nfp),
+                "stage_krylov": np.array(stats.krylov_iters),
+                "stage_incs": np.array(stats.pressure_increments)})
+    rec.update(steps_record(split, U0, dt, 10, scfg))
+    save("cfg1", rec)
+
+
+def case_cfg2(n_steps=200):
+    mesh, geom, ops, model, U0, bcs, split = bubble_case((64, 32), 5.0e3, 4)
+    dt = 0.5
+    a_dt = dt * (1.0 - 1.0 / np.sqrt(2.0))
+    rec = {"case": np.array("cfg2"), "degree": np.array(4)}
+    rec.update(mesh_record(mesh))
+    rec.update(operator_record(ops, split, U0, model, bcs, 12, a_dt))
+    rec.update(gmres_record(split, U0, a_dt, 1e-10, 12))
+    scfg = imex.ImplicitSolveConfig(krylov_tol=1e-10)
+    rec.update(steps_record(split, U0, dt, n_steps, scfg, keep_every=10))
+    save("cfg2", rec)
+
+
+def _terrain_case(mesh, degree, terrain, hill_cfg, sponge_cfg, lateral_axes,
+                  seed, extents):
+    geom = build_geometry(mesh, degree, terrain=terrain)
+    ops = DGOperators(geom)
+    model = FlowModel.dimensional()
+    bg = project_initial_data(geom, cases.hydrostatic_initial_state(hill_cfg)).data
+    U = perturbed(bg, geom.node_coords, extents, seed)
+    bcs = cases.farfield_bcs(geom, bg)
+    sigma = cases.sponge_sigma(geom, sponge_cfg, extents, lateral_axes=lateral_axes)
+    split = imex.SplitOperators(ops, model, bcs, sponge=(sigma, bg))
+    return geom, ops, model, bg, U, bcs, split, sigma
+
+
+def case_hang2d():
+    ext = (60.0e3, 16.0e3)
+    m = build_uniform_mesh(ext, (15, 4))
+    mesh = refine_region(
+        m, lambda lf: abs(lf.center[0] - 30.0e3) < 6.0e3 and lf.center[1] < 6.0e3,
+        times=2)
+    hill_cfg = cases.HillCaseConfig(domain=ext)
+    geom, ops, model, bg, U, bcs, split, sigma = _terrain_case(
+        mesh, 4, hill2d, hill_cfg, cases.SpongeConfig(), (0,), 21, ext)
+    rec = {"case": np.array("hang2d"), "degree": np.array(4),
+           "background": bg, "sigma": sigma}
+    rec.update(mesh_record(mesh))
+    rec.update(geometry_record(geom))
+    rec.update(operator_record(ops, split, U, model, bcs, 21, 0.3))
+    for i, bc in enumerate(bcs):
+        if bc.kind == "farfield":
+            rec[f"bc{i}_ghost"] = bc.ghost_conserved
+    rec.update(gmres_record(split, U, 0.3, 1e-8, 21))
+    save("hang2d", rec)
+
+
+def case_hang3d():
+    ext = (20.0e3, 20.0e3, 10.0e3)
+    m = build_uniform_mesh(ext, (4, 4, 2))
+    mesh = refine_region(
+        m, lambda lf: bool(np.all(np.abs(lf.center[:2] - 10.0e3) < 5.0e3)
+                           and lf.center[2] < 5.0e3), times=1)
+    hill_cfg = cases.HillCaseConfig(domain=ext)
+    geom, ops, model, bg, U, bcs, split, sigma = _terrain_case(
+        mesh, 3, hill3d, hill_cfg,
+        cases.SpongeConfig(top_depth=4.0e3, lateral_width=5.0e3), (0, 1), 31, ext)
+    rec = {"case": np.array("hang3d"), "degree": np.array(3),
+           "background": bg, "sigma": sigma}
+    rec.update(mesh_record(mesh))
+    rec.update(geometry_record(geom))
+    rec.update(operator_record(ops, split, U, model, bcs, 31, 0.3))
+    rec.update(gmres_record(split, U, 0.3, 1e-8, 31))
+    scfg = imex.ImplicitSolveConfig()
+    rec.update(steps_record(split, U, 0.5, 2, scfg))
+    save("hang3d", rec)
+
+
+def case_per3d():
+    ext = (10.0e3, 10.0e3, 10.0e3)
+    m = build_uniform_mesh(ext, (4, 4, 4), periodic=(True, True, True))
+    pick = np.random.default_rng(5).random(m.n_leaves) < 0.3
+    mesh = refine_region(m, lambda lf: bool(pick[lf.index]), 1)
+    geom = build_geometry(mesh, 2)
+    ops = DGOperators(geom)
+    model = FlowModel.dimensional()
+    hill_cfg = cases.HillCaseConfig(domain=ext)
+    bg = project_initial_data(geom, cases.hydrostatic_initial_state(hill_cfg)).data
+    U = perturbed(bg, geom.node_coords, ext, 41)
+    split = imex.SplitOperators(ops, model, [])
+    rec = {"case": np.array("per3d"), "degree": np.array(2), "pick": pick}
+    rec.update(mesh_record(mesh))
+    rec.update(geometry_record(geom))
+    rec.update(operator_record(ops, split, U, model, [], 41, 0.3))
+    save("per3d", rec)
+
+
+def case_cfg3s():
+    ext = (50.0e3, 21.0e3)
+    m = build_uniform_mesh(ext, (25, 8))
+    mesh = refine_region(m, lambda lf: lf.center[1] < 6.0e3, 1)
+    mesh = refine_region(mesh, lambda lf: lf.center[1] < 2.5e3, 1)
+    hill_cfg = cases.HillCaseConfig(domain=ext, T_ref=280.0)
+    geom, ops, model, bg, U, bcs, split, sigma = _terrain_case(
+        mesh, 4, schar, hill_cfg,
+        cases.SpongeConfig(top_depth=9.0e3, lateral_width=10.0e3), (0,), 51, ext)
+    U = bg.copy()   # the physical IC: background flow over the hill
+    rec = {"case": np.array("cfg3s"), "degree": np.array(4),
+           "background": bg, "sigma": sigma}
+    rec.update(mesh_record(mesh))
+    rec.update(operator_record(ops, split, U, model, bcs, 51, 0.5))
+    scfg = imex.ImplicitSolveConfig()
+    rec.update(steps_record(split, U, 1.0, 3, scfg))
+    save("cfg3s", rec)
+
+
+def case_part():
+    mesh = build_uniform_mesh((20.0e3, 10.0e3), (64, 32))
+    mesh = refine_region(mesh, lambda lf: lf.center[1] < 5.0e3, 1)
+    rec = {}
+    rec.update(mesh_record(mesh))
+    rng = np.random.default_rng(3)
+    w = rng.uniform(0.5, 2.0, size=mesh.n_leaves)
+    rec["weights"] = w
+    for P in range(1, 9):
+        for tag, wt in (("u", None), ("w", w)):
+            p = partition_leaves(mesh, P, wt)
+            rec[f"P{P}{tag}_owner"] = p.owner
+            rec[f"P{P}{tag}_ranges"] = np.array(p.ranges, dtype=np.int64)
+            rec[f"P{P}{tag}_ghost_len"] = np.array([len(g) for g in p.ghosts])
+            rec[f"P{P}{tag}_ghosts"] = (np.concatenate(p.ghosts) if p.ghosts
+                                        else np.empty(0, np.int64))
+    small = build_uniform_mesh((10.0, 1.0), (10, 1))
+    p = partition_leaves(small, 4)
+    rec["small10x4_ranges"] = np.array(p.ranges, dtype=np.int64)
+    save("part", rec)
+
+
+def case_cfg2ops():
+    """Refresh the operator records of cfg2.npz without rerunning 200 steps."""
+    mesh, geom, ops, model, U0, bcs, split = bubble_case((64, 32), 5.0e3, 4)
+    a_dt = 0.5 * (1.0 - 1.0 / np.sqrt(2.0))
+    path = os.path.join(OUT, "cfg2.npz")
+    rec = dict(np.load(path))
+    rec.update(operator_record(ops, split, U0, model, bcs, 12, a_dt))
+    save("cfg2", rec)
+
+
+CASES = {"cfg2ops": case_cfg2ops, "cfg1": case_cfg1, "hang2d": case_hang2d, "hang3d": case_hang3d,
+         "per3d": case_per3d, "cfg3s": case_cfg3s, "part": case_part,
+         "cfg2": case_cfg2}
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(CASES)
+    for n in names:
+        t0 = time.perf_counter()
+        print(f"== {n}", flush=True)
+        CASES[n]()
+        print(f"   {time.perf_counter() - t0:.1f} s", flush=True)
