@@ -1,0 +1,161 @@
+// Auxiliary per-element kernels: standalone factorised mass inverse
+// (orodg/geometry.py:372-396) and conserved-variable integrals
+// (orodg/dgops.py:505-511).  Same thread-per-point shared-memory passes as
+// the fused operator kernel.
+#pragma once
+#include "dg_operator.cuh"
+
+namespace dg {
+
+template <int N>
+struct AuxParams {
+  const int* elem;
+  const double* col;
+  GeoConst gc;
+  int n_el;
+  int ncomp;
+  CView in;          // dual (mass inverse) or state (integrate)
+  MView out;         // nodal result (mass inverse)
+  double* partial;   // integrate: (grid, ncomp)
+  Tab<N> tab;
+};
+
+template <int D, int N>
+struct AuxLayout {
+  static constexpr int NP = ipow(N, D);
+  static constexpr int KMAX = 5;
+  static constexpr int EPB = (256 / NP) > 1 ? (256 / NP) : 1;
+  static constexpr int THREADS = ((EPB * NP + 31) / 32) * 32;
+  static constexpr int SLOTS = (THREADS + NP - 1) / NP;
+  static constexpr int TABD = (int)(sizeof(Tab<N>) / sizeof(double));
+  static constexpr size_t SMEM = (size_t)(TABD + 64 + SLOTS * 2 * KMAX * NP) * sizeof(double);
+};
+
+template <int D, int N>
+__device__ __forceinline__ double wdet_at(const int* elem, const double* col, const GeoConst& gc,
+                                          long long e, int q, const Tab<N>& T) {
+  constexpr int NQH = ipow(N, D - 1);
+  const ElemGeo<D> g = elem_geo<D>(elem, gc, e);
+  const int qh = q / N;
+  double hq = 0.0;
+  if (gc.terrain) hq = col[(long long)g.col * gc.col_stride + qh];
+  (void)NQH;
+  const double zz = g.s[D - 1] * (1.0 - hq / gc.z_top);
+  double det = 1.0;
+  for (int a = 0; a < D - 1; ++a) det = det * g.s[a];
+  det = det * zz;
+  double w = 1.0;
+  for (int a = 0; a < D; ++a) w *= T.qw[digit<D, N>(q, a)];
+  return w * det;
+}
+
+// nodal = B^-1 (x) .. diag(1/(w det)) B^-T (x) .. dual
+template <int D, int N>
+__global__ void __launch_bounds__(AuxLayout<D, N>::THREADS)
+minv_kernel(const __grid_constant__ AuxParams<N> P) {
+  using L = AuxLayout<D, N>;
+  constexpr int NP = L::NP;
+  extern __shared__ double smem[];
+  double* tb = smem;
+  {
+    const double* src = reinterpret_cast<const double*>(&P.tab);
+    for (int i = threadIdx.x; i < L::TABD; i += blockDim.x) tb[i] = src[i];
+  }
+  const Tab<N>& T = *reinterpret_cast<const Tab<N>*>(tb);
+  const int el = threadIdx.x / NP, q = threadIdx.x - el * NP;
+  const long long e = (long long)blockIdx.x * L::EPB + el;
+  const bool valid = el < L::EPB && e < P.n_el;
+  const long long es = valid ? e : 0;
+  double* X = smem + L::TABD + 64 + el * 2 * L::KMAX * NP;
+  double* Y = X + L::KMAX * NP;
+  for (int c0 = 0; c0 < P.ncomp; c0 += L::KMAX) {
+    const int kc = min(L::KMAX, P.ncomp - c0);
+    for (int c = 0; c < L::KMAX; ++c) X[c * NP + q] = c < kc ? P.in(es, c0 + c, q) : 0.0;
+    __syncthreads();
+    // B^-T along every axis
+    double* s = X;
+    double* d = Y;
+    for (int a = D - 1; a >= 0; --a) {
+      pass1d<D, N, L::KMAX, true>(&T.Binv[0][0], s, d, q, a, NP);
+      __syncthreads();
+      double* t = s; s = d; d = t;
+    }
+    const double inv = 1.0 / wdet_at<D, N>(P.elem, P.col, P.gc, es, q, T);
+    for (int c = 0; c < L::KMAX; ++c) s[c * NP + q] *= inv;
+    __syncthreads();
+    for (int a = D - 1; a >= 0; --a) {
+      pass1d<D, N, L::KMAX, false>(&T.Binv[0][0], s, d, q, a, NP);
+      __syncthreads();
+      double* t = s; s = d; d = t;
+    }
+    if (valid)
+      for (int c = 0; c < kc; ++c)
+        P.out.p[e * P.out.estride + (c0 + c) * P.out.cstride + q] = s[c * NP + q];
+    __syncthreads();
+  }
+}
+
+// per-CTA partial integrals sum_q w det (B U)_q for every component
+template <int D, int N>
+__global__ void __launch_bounds__(AuxLayout<D, N>::THREADS)
+integrate_kernel(const __grid_constant__ AuxParams<N> P) {
+  using L = AuxLayout<D, N>;
+  constexpr int NP = L::NP;
+  extern __shared__ double smem[];
+  double* tb = smem;
+  {
+    const double* src = reinterpret_cast<const double*>(&P.tab);
+    for (int i = threadIdx.x; i < L::TABD; i += blockDim.x) tb[i] = src[i];
+  }
+  const Tab<N>& T = *reinterpret_cast<const Tab<N>*>(tb);
+  double* red = smem + L::TABD;
+  const int el = threadIdx.x / NP, q = threadIdx.x - el * NP;
+  const long long e = (long long)blockIdx.x * L::EPB + el;
+  const bool valid = el < L::EPB && e < P.n_el;
+  const long long es = valid ? e : 0;
+  double* X = smem + L::TABD + 64 + el * 2 * L::KMAX * NP;
+  double* Y = X + L::KMAX * NP;
+  const double wd = wdet_at<D, N>(P.elem, P.col, P.gc, es, q, T);
+  for (int c0 = 0; c0 < P.ncomp; c0 += L::KMAX) {
+    const int kc = min(L::KMAX, P.ncomp - c0);
+    for (int c = 0; c < L::KMAX; ++c) X[c * NP + q] = c < kc ? P.in(es, c0 + c, q) : 0.0;
+    __syncthreads();
+    double* s = X;
+    double* d = Y;
+    for (int a = D - 1; a >= 0; --a) {
+      pass1d<D, N, L::KMAX, false>(&T.B[0][0], s, d, q, a, NP);
+      __syncthreads();
+      double* t = s; s = d; d = t;
+    }
+    for (int c = 0; c < kc; ++c) {
+      double v = valid ? s[c * NP + q] * wd : 0.0;
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double acc = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) acc += red[w];
+        P.partial[(long long)blockIdx.x * P.ncomp + c0 + c] = acc;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+template <int D, int N>
+cudaError_t launch_aux(int which, const AuxParams<N>& P, cudaStream_t st, int* grid_out) {
+  using L = AuxLayout<D, N>;
+  const int grid = (P.n_el + L::EPB - 1) / L::EPB;
+  if (grid_out) *grid_out = grid;
+  if (grid == 0) return cudaSuccess;
+  if (which == 0) {
+    cudaFuncSetAttribute(minv_kernel<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
+    minv_kernel<D, N><<<grid, L::THREADS, L::SMEM, st>>>(P);
+  } else {
+    cudaFuncSetAttribute(integrate_kernel<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
+    integrate_kernel<D, N><<<grid, L::THREADS, L::SMEM, st>>>(P);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace dg

@@ -1,0 +1,103 @@
+// Host-side launcher for the templated element kernels (one translation
+// unit per dimension instantiates N = 2..7 and the three operator kinds).
+#pragma once
+#include <cstring>
+#include "dg_operator.cuh"
+
+namespace dg {
+
+// N-independent operator arguments; the launcher copies the 1D tables
+// (flat, Tab<N> layout) into the kernel parameter block.
+struct OpArgs {
+  MeshDev mesh;
+  GeoConst gc;
+  Model model;
+  CView in, inK, inH, base, bg;
+  const double* sigma;
+  MView out;
+  double alpha, beta, coef;
+  int has_K, has_base, homogeneous, mode;
+  double* mass_partial;
+  const double* tabs;  // host pointer, Tab<N> layout
+};
+
+struct LaunchInfo {
+  int epb;
+  int threads;
+  size_t smem;
+  int grid;
+};
+
+template <int D, int N, int OPK>
+cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
+  using L = Layout<D, N, OPK>;
+  KParams<N> P;
+  P.mesh = a.mesh;
+  P.gc = a.gc;
+  P.model = a.model;
+  P.in = a.in;
+  P.inK = a.inK;
+  P.inH = a.inH;
+  P.base = a.base;
+  P.bg = a.bg;
+  P.sigma = a.sigma;
+  P.out = a.out;
+  P.alpha = a.alpha;
+  P.beta = a.beta;
+  P.coef = a.coef;
+  P.has_K = a.has_K;
+  P.has_base = a.has_base;
+  P.homogeneous = a.homogeneous;
+  P.mode = a.mode;
+  P.mass_partial = a.mass_partial;
+  std::memcpy(&P.tab, a.tabs, sizeof(Tab<N>));
+  const int grid = (a.mesh.n_el + L::EPB - 1) / L::EPB;
+  if (info) {
+    info->epb = L::EPB;
+    info->threads = L::THREADS;
+    info->smem = L::SMEM;
+    info->grid = grid;
+  }
+  if (grid == 0) return cudaSuccess;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(elem_kernel<D, N, OPK>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)L::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  elem_kernel<D, N, OPK><<<grid, L::THREADS, L::SMEM, st>>>(P);
+  return cudaGetLastError();
+}
+
+// grid size only (for sizing the per-CTA partial buffers)
+template <int D, int N, int OPK>
+int elem_grid(int n_el) {
+  using L = Layout<D, N, OPK>;
+  return (n_el + L::EPB - 1) / L::EPB;
+}
+
+cudaError_t launch_elem_d2(int N, int opk, const OpArgs& a, cudaStream_t st, LaunchInfo* info);
+cudaError_t launch_elem_d3(int N, int opk, const OpArgs& a, cudaStream_t st, LaunchInfo* info);
+
+}  // namespace dg
+
+namespace dg {
+
+struct AuxArgs {
+  const int* elem;
+  const double* col;
+  GeoConst gc;
+  int n_el;
+  int ncomp;
+  CView in;
+  MView out;
+  double* partial;
+  const double* tabs;
+};
+
+cudaError_t launch_aux_d2(int N, int which, const AuxArgs& a, cudaStream_t st, int* grid);
+cudaError_t launch_aux_d3(int N, int which, const AuxArgs& a, cudaStream_t st, int* grid);
+
+}  // namespace dg

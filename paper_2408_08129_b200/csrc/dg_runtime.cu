@@ -1,0 +1,865 @@
+// libdg runtime: context, C ABI (include/dg.h), and the native solver loops
+// -- restarted GMRES (orodg/krylov.py:27-115), the pressure fixed point
+// (orodg/imex.py:302-370) and the ARS(2,2,2) IMEX step (imex.py:252-299) --
+// driving the fused element kernels and the streaming vector kernels on one
+// CUDA stream.  One context per GPU per process; not re-entrant across host
+// threads (same contract as the reference's single driving thread).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dg.h"
+#include "dg_launch.cuh"
+#include "dg_vector.cuh"
+#include "dg_comm.h"
+
+using namespace dg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                   \
+  do {                                                                             \
+    cudaError_t _e = (call);                                                       \
+    if (_e != cudaSuccess)                                                         \
+      return fail(DG_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+#define RET(call)                 \
+  do {                            \
+    int _r = (call);              \
+    if (_r != DG_OK) return _r;   \
+  } while (0)
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaError_t alloc(size_t count) {
+    if (count <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    if (count == 0) return cudaSuccess;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e == cudaSuccess) n = count;
+    return e;
+  }
+  cudaError_t upload(const T* h, size_t count) {
+    cudaError_t e = alloc(count);
+    if (e != cudaSuccess || count == 0) return e;
+    return cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+}  // namespace
+
+struct dg_ctx {
+  int dim = 0, N = 0, NP = 0, V = 0, NQF = 0, S = 0;
+  int n_el = 0, n_tot = 0;
+  long long n_global = 0;  // global scalar-field length (sum over ranks)
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  MeshDev mesh{};
+  GeoConst gc{};
+  Model model{};
+  std::vector<double> tabs;
+  DevBuf<int> elem, nbr, hang;
+  DevBuf<uint8_t> kind;
+  DevBuf<double> col, ffU, ffp, ffh, sigma, bg;
+  // scratch
+  DevBuf<double> mass_partial, partial, redout, coef_dev;
+  double* pinned = nullptr;  // 256 doubles
+  DevBuf<double> sV;         // vector field (n_tot, d, NP)
+  DevBuf<double> sh, sK, sx, srhs, spold, sw, sr, sx2;  // scalar fields
+  DevBuf<double> basis;      // (m+1) x (n_tot NP)
+  DevBuf<double> st[6];      // state fields (n_tot, V, NP)
+  LaunchInfo last{};
+  Comm comm;
+  long long scal() const { return (long long)n_tot * NP; }
+  long long stat() const { return (long long)n_tot * V * NP; }
+};
+
+namespace {
+
+// ------------------------------------------------------------------ basics
+int sync_read(dg_ctx* c, const double* dev, int n, double* host) {
+  CK(cudaMemcpyAsync(c->pinned, dev, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  std::memcpy(host, c->pinned, n * sizeof(double));
+  return DG_OK;
+}
+
+// global sums over ranks (in place on the device) then read to host
+int reduce_read(dg_ctx* c, double* dev, int n, double* host) {
+  if (c->comm.active()) {
+    if (!c->comm.allreduce_sum(dev, n, c->stream)) return fail(DG_ERR_COMM, c->comm.error());
+  }
+  return sync_read(c, dev, n, host);
+}
+
+int halo(dg_ctx* c, double* field, int ncomp) {
+  if (!c->comm.active()) return DG_OK;
+  if (!c->comm.exchange(field, ncomp, c->NP, c->stream)) return fail(DG_ERR_COMM, c->comm.error());
+  return DG_OK;
+}
+
+OpArgs base_args(dg_ctx* c) {
+  OpArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.mesh = c->mesh;
+  a.gc = c->gc;
+  a.model = c->model;
+  a.tabs = c->tabs.data();
+  a.alpha = 1.0;
+  a.coef = 1.0;
+  return a;
+}
+
+int launch(dg_ctx* c, int opk, const OpArgs& a) {
+  cudaError_t e = (c->dim == 2) ? launch_elem_d2(c->N, opk, a, c->stream, &c->last)
+                                : launch_elem_d3(c->N, opk, a, c->stream, &c->last);
+  if (e != cudaSuccess) return fail(DG_ERR_CUDA, std::string("element kernel: ") + cudaGetErrorString(e));
+  return DG_OK;
+}
+
+CView cv(const double* p, long long es, long long cs) { return CView{p, es, cs}; }
+MView mv(double* p, long long es, long long cs) { return MView{p, es, cs}; }
+
+// ---------------------------------------------------------------- operators
+int op_advective(dg_ctx* c, const double* U, double* out, int mode, double* mass_rate_host) {
+  OpArgs a = base_args(c);
+  a.in = cv(U, (long long)c->V * c->NP, c->NP);
+  a.out = mv(out, (long long)c->V * c->NP, c->NP);
+  a.mode = mode;
+  if (mode == OUT_MINV && c->sigma.p) {
+    a.sigma = c->sigma.p;
+    a.bg = cv(c->bg.p, (long long)c->V * c->NP, c->NP);
+  }
+  a.mass_partial = mass_rate_host ? c->mass_partial.p : nullptr;
+  RET(launch(c, OP_ADV, a));
+  if (mass_rate_host) {
+    CK(reduce_cols(c->stream, c->mass_partial.p, c->last.grid, 1, c->redout.p));
+    double s = 0.0;
+    RET(reduce_read(c, c->redout.p, 1, &s));
+    *mass_rate_host = -s;  // imex.py:148
+  }
+  return DG_OK;
+}
+
+// V_k = base_k + coef * [Minv] G(alpha (x - beta K))
+int op_grad(dg_ctx* c, const double* x, const double* K, double alpha, double beta, int homog,
+            int mode, MView out, CView base, int has_base, double coef) {
+  OpArgs a = base_args(c);
+  a.in = cv(x, c->NP, c->NP);
+  if (K) {
+    a.inK = cv(K, c->NP, c->NP);
+    a.has_K = 1;
+  }
+  a.alpha = alpha;
+  a.beta = beta;
+  a.homogeneous = homog;
+  a.mode = mode;
+  a.out = out;
+  a.base = base;
+  a.has_base = has_base;
+  a.coef = coef;
+  return launch(c, OP_GRAD, a);
+}
+
+// y = base + coef * [Minv] Div(h V)
+int op_divhv(dg_ctx* c, CView V, const double* h, int homog, int mode, MView out, CView base,
+             int has_base, double coef) {
+  OpArgs a = base_args(c);
+  a.in = V;
+  a.inH = cv(h, c->NP, c->NP);
+  a.homogeneous = homog;
+  a.mode = mode;
+  a.out = out;
+  a.base = base;
+  a.has_base = has_base;
+  a.coef = coef;
+  return launch(c, OP_DIVHV, a);
+}
+
+// homogeneous Helmholtz action y = x + a_dt Minv Div_h(V), V = -(a_dt/M^2)(g-1) Minv G(x)
+int helm_apply(dg_ctx* c, double a_dt, const double* h, double* x, double* y) {
+  const int d = c->dim;
+  RET(halo(c, x, 1));
+  const double gm1 = c->model.gamma - 1.0;
+  RET(op_grad(c, x, nullptr, gm1, 0.0, 1, OUT_MINV, mv(c->sV.p, (long long)d * c->NP, c->NP),
+              CView{}, 0, -(a_dt * c->model.inv_mach_sq)));
+  RET(halo(c, c->sV.p, d));
+  RET(op_divhv(c, cv(c->sV.p, (long long)d * c->NP, c->NP), h, 1, OUT_MINV, mv(y, c->NP, c->NP),
+               cv(x, c->NP, c->NP), 1, a_dt));
+  return DG_OK;
+}
+
+// F(x) = e_e - a_dt Minv Div_h(m_e - a_dt/M^2 Minv G((g-1)(x - kf K)))   (imex.py:190-218)
+int energy_F(dg_ctx* c, double a_dt, const double* h, const double* K, CView m_e, CView e_e,
+             double* x, double* Fx) {
+  const int d = c->dim;
+  if (x) RET(halo(c, x, 1));
+  const double gm1 = c->model.gamma - 1.0;
+  RET(op_grad(c, x, K, gm1, c->model.kinetic_factor, 0, OUT_MINV,
+              mv(c->sV.p, (long long)d * c->NP, c->NP), m_e, 1, -(a_dt * c->model.inv_mach_sq)));
+  RET(halo(c, c->sV.p, d));
+  RET(op_divhv(c, cv(c->sV.p, (long long)d * c->NP, c->NP), h, 0, OUT_MINV,
+               mv(Fx, c->NP, c->NP), e_e, 1, -a_dt));
+  return DG_OK;
+}
+
+// ----------------------------------------------------------------- GMRES
+struct Gm {
+  int iterations = 0, restarts = 0, converged = 0, breakdown = 0;
+  double residual = INFINITY;
+  std::vector<double> hist;
+};
+
+int norm2(dg_ctx* c, const double* x, double* out) {
+  const long long n = (long long)c->n_el * c->NP;
+  CK(multidot(c->stream, n, 0, nullptr, 0, x, c->partial.p, c->redout.p));
+  double v;
+  RET(reduce_read(c, c->redout.p, 1, &v));
+  *out = v;
+  return DG_OK;
+}
+
+int gmres(dg_ctx* c, double a_dt, const double* h, const double* rhs, double* x, double tol,
+          int restart, int max_iter, Gm& st) {
+  if (!(tol > 0.0 && tol < 1.0)) return fail(DG_ERR_CONFIG, "tol_rel must be in (0,1)");
+  const long long ns = c->scal();
+  const long long n = (long long)c->n_el * c->NP;
+  int m = restart < 1 ? 1 : restart;
+  if (m > c->n_global) m = (int)c->n_global;
+  if (m < 1) m = 1;
+  if (m > 31) return fail(DG_ERR_USAGE, "krylov_restart > 31 not supported on the device path");
+  CK(c->basis.alloc((size_t)(m + 1) * ns));
+  double* Vb = c->basis.p;
+  double* w = c->sw.p;
+  double* r = c->sr.p;
+  double bn2;
+  RET(norm2(c, rhs, &bn2));
+  const double bn = std::sqrt(bn2);
+  if (bn == 0.0) {
+    CK(cudaMemsetAsync(x, 0, n * sizeof(double), c->stream));
+    st.converged = 1;
+    st.residual = 0.0;
+    return DG_OK;
+  }
+  auto residual_into_r = [&]() -> int {
+    RET(helm_apply(c, a_dt, h, x, w));
+    const double cf[2] = {1.0, -1.0};
+    const double* xs[2] = {rhs, w};
+    CK(lincomb(c->stream, n, 2, cf, xs, r));
+    return DG_OK;
+  };
+  RET(residual_into_r());
+  const double target = tol * bn;
+  std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), y(m), hc(m + 2);
+  auto Hij = [&](int i, int j) -> double& { return H[(size_t)i * m + j]; };
+  while (true) {
+    double b2;
+    RET(norm2(c, r, &b2));
+    const double beta = std::sqrt(b2);
+    st.residual = beta / bn;
+    st.hist.push_back(st.residual);
+    if (beta <= target || st.iterations >= max_iter || st.breakdown) break;
+    CK(scale(c->stream, n, beta, true, r, Vb));
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int done = 0;
+    for (int j = 0; j < m; ++j) {
+      RET(helm_apply(c, a_dt, h, Vb + (size_t)j * ns, w));
+      // classical Gram-Schmidt: h_i = V_i . w, one pass
+      CK(multidot(c->stream, n, j + 1, Vb, ns, w, c->partial.p, c->redout.p));
+      RET(reduce_read(c, c->redout.p, j + 2, hc.data()));
+      const double nb = std::sqrt(hc[j + 1]);
+      for (int i = 0; i <= j; ++i) Hij(i, j) = hc[i];
+      CK(cudaMemcpyAsync(c->coef_dev.p, hc.data(), (j + 1) * sizeof(double),
+                         cudaMemcpyHostToDevice, c->stream));
+      CK(axpy_multi(c->stream, n, j + 1, Vb, ns, c->coef_dev.p, w, c->partial.p, c->redout.p));
+      double na2;
+      RET(reduce_read(c, c->redout.p, 1, &na2));
+      double na = std::sqrt(na2);
+      if (na < 0.7071067811865476 * nb) {
+        // one re-orthogonalisation pass (krylov.py:73-79)
+        CK(multidot(c->stream, n, j + 1, Vb, ns, w, c->partial.p, c->redout.p));
+        RET(reduce_read(c, c->redout.p, j + 2, hc.data()));
+        for (int i = 0; i <= j; ++i) Hij(i, j) += hc[i];
+        CK(cudaMemcpyAsync(c->coef_dev.p, hc.data(), (j + 1) * sizeof(double),
+                           cudaMemcpyHostToDevice, c->stream));
+        CK(axpy_multi(c->stream, n, j + 1, Vb, ns, c->coef_dev.p, w, c->partial.p, c->redout.p));
+        RET(reduce_read(c, c->redout.p, 1, &na2));
+        na = std::sqrt(na2);
+      }
+      Hij(j + 1, j) = na;
+      st.iterations += 1;
+      const bool happy = na <= 1e-14 * std::max(bn, nb);
+      if (!happy) CK(scale(c->stream, n, na, true, w, Vb + (size_t)(j + 1) * ns));
+      for (int i = 0; i < j; ++i) {
+        const double t = cs[i] * Hij(i, j) + sn[i] * Hij(i + 1, j);
+        Hij(i + 1, j) = -sn[i] * Hij(i, j) + cs[i] * Hij(i + 1, j);
+        Hij(i, j) = t;
+      }
+      const double den = std::hypot(Hij(j, j), Hij(j + 1, j));
+      cs[j] = den != 0.0 ? Hij(j, j) / den : 1.0;
+      sn[j] = den != 0.0 ? Hij(j + 1, j) / den : 0.0;
+      Hij(j, j) = den;
+      Hij(j + 1, j) = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      done = j + 1;
+      const double est = std::fabs(g[j + 1]);
+      st.hist.push_back(est / bn);
+      if (happy) {
+        st.breakdown = 1;
+        break;
+      }
+      if (est <= target || st.iterations >= max_iter) break;
+    }
+    if (done) {
+      for (int i = done - 1; i >= 0; --i) {
+        double s = g[i];
+        for (int k = i + 1; k < done; ++k) s -= Hij(i, k) * y[k];
+        y[i] = s / Hij(i, i);
+      }
+      // x <- x + V y  ==  x - sum(-y_i) V_i
+      for (int i = 0; i < done; ++i) hc[i] = -y[i];
+      CK(cudaMemcpyAsync(c->coef_dev.p, hc.data(), done * sizeof(double), cudaMemcpyHostToDevice,
+                         c->stream));
+      CK(axpy_multi(c->stream, n, done, Vb, ns, c->coef_dev.p, x, c->partial.p, nullptr));
+    }
+    RET(residual_into_r());
+    st.restarts += 1;
+  }
+  st.restarts = std::max(0, st.restarts - 1);
+  // the final true residual equals the last beta: x is unchanged since r
+  st.converged = st.residual <= tol ? 1 : 0;
+  return DG_OK;
+}
+
+// -------------------------------------------------------- implicit stage
+int check_positivity(dg_ctx* c, const double* U, dg_step_stats* stats, int stage) {
+  const double gm1 = c->model.gamma - 1.0;
+  CK(positivity(c->stream, c->n_el, c->NP, c->dim, U, gm1, c->model.kinetic_factor,
+                c->partial.p));
+  std::vector<double> part(RED_BLOCKS * 4);
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(part.data(), c->partial.p, part.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  double mr = INFINITY, mp = INFINITY;
+  long long ir = -1, ip = -1;
+  for (int b = 0; b < RED_BLOCKS; ++b) {
+    const double v = part[b * 4], iv = part[b * 4 + 1];
+    if (v < mr || (v == mr && (long long)iv < ir)) { mr = v; ir = (long long)iv; }
+    const double p = part[b * 4 + 2], ipv = part[b * 4 + 3];
+    if (p < mp || (p == mp && (long long)ipv < ip)) { mp = p; ip = (long long)ipv; }
+  }
+  if (c->comm.active()) {
+    // global minimum with the owning rank's global element id
+    double loc[4] = {mr, (double)(ir < 0 ? -1 : c->comm.global_index(ir / c->NP) * c->NP + ir % c->NP),
+                     mp, (double)(ip < 0 ? -1 : c->comm.global_index(ip / c->NP) * c->NP + ip % c->NP)};
+    if (!c->comm.allreduce_minloc(loc, c->stream)) return fail(DG_ERR_COMM, c->comm.error());
+    mr = loc[0]; ir = (long long)loc[1]; mp = loc[2]; ip = (long long)loc[3];
+  }
+  if (!(mr > 0.0) || !(mp > 0.0)) {
+    const bool dens = !(mr > 0.0);
+    const long long at = dens ? ir : ip;
+    if (stats) {
+      stats->fail_stage = stage;
+      stats->fail_kind = dens ? 0 : 1;
+      stats->fail_element = at / c->NP;
+      stats->fail_node = (int)(at % c->NP);
+      stats->fail_value = dens ? mr : mp;
+    }
+    char buf[256];
+    std::snprintf(buf, sizeof buf, "non-positive %s (%.6e) at index (%lld, %d) in stage %d",
+                  dens ? "density" : "pressure", dens ? mr : mp, at / c->NP, (int)(at % c->NP),
+                  stage);
+    return fail(DG_ERR_POSITIVITY, buf);
+  }
+  return DG_OK;
+}
+
+int solve_stage(dg_ctx* c, const double* acc, const double* guess, double a_dt,
+                const dg_solve_cfg& cfg, double* it, dg_step_stats* stats, int* n_fp) {
+  const int d = c->dim, NP = c->NP, V = c->V;
+  const long long n = (long long)c->n_el * NP;
+  const long long sst = (long long)V * NP;
+  const double gm1 = c->model.gamma - 1.0, kf = c->model.kinetic_factor;
+  CK(set_iterate(c->stream, c->n_el, NP, V, acc, guess, it));
+  CK(state_pressure(c->stream, c->n_el, NP, d, it, gm1, kf, c->spold.p));
+  CK(copy_comps(c->stream, c->n_el, NP, 1, it + (long long)(d + 1) * NP, sst, c->sx.p, NP));
+  const CView m_e = cv(acc + NP, sst, NP);
+  const CView e_e = cv(acc + (long long)(d + 1) * NP, sst, NP);
+  double last_dp = INFINITY;
+  for (int k = 0; k < cfg.fp_max_iter; ++k) {
+    CK(frozen(c->stream, c->n_el, NP, d, it, gm1, kf, c->sh.p, c->sK.p));
+    RET(halo(c, c->sh.p, 1));
+    RET(halo(c, c->sK.p, 1));
+    RET(energy_F(c, a_dt, c->sh.p, c->sK.p, m_e, e_e, nullptr, c->srhs.p));
+    Gm gs;
+    RET(gmres(c, a_dt, c->sh.p, c->srhs.p, c->sx.p, cfg.krylov_tol, cfg.krylov_restart,
+              cfg.krylov_max_iter, gs));
+    if (stats && stats->n_krylov < DG_MAX_SOLVES) stats->krylov_iters[stats->n_krylov++] = gs.iterations;
+    if (!gs.converged) {
+      if (stats) {
+        stats->fail_kind = 2;
+        stats->fail_value = gs.residual;
+      }
+      char buf[160];
+      std::snprintf(buf, sizeof buf, "GMRES stalled: residual %.3e after %d iterations",
+                    gs.residual, gs.iterations);
+      return fail(DG_ERR_SOLVER, buf);
+    }
+    double nrm[2];
+    CK(pressure_dp(c->stream, n, c->sx.p, c->sK.p, gm1, kf, c->spold.p, c->partial.p, c->redout.p));
+    RET(reduce_read(c, c->redout.p, 2, nrm));
+    // momentum back-substitution straight into the iterate (imex.py:356-358)
+    RET(halo(c, c->sx.p, 1));
+    RET(op_grad(c, c->sx.p, c->sK.p, gm1, kf, 0, OUT_MINV, mv(it + NP, sst, NP), m_e, 1,
+                -(a_dt * c->model.inv_mach_sq)));
+    CK(copy_comps(c->stream, c->n_el, NP, 1, c->sx.p, NP, it + (long long)(d + 1) * NP, sst));
+    const double dp = std::sqrt(nrm[0]) / std::max(std::sqrt(nrm[1]), 1e-300);
+    if (stats && stats->n_krylov - 1 < DG_MAX_SOLVES)
+      stats->pressure_increments[stats->n_krylov - 1] = dp;
+    last_dp = dp;
+    if (dp <= cfg.fp_tol) {
+      *n_fp = k + 1;
+      return DG_OK;
+    }
+  }
+  if (stats) {
+    stats->fail_kind = 3;
+    stats->fail_value = last_dp;
+  }
+  char buf[200];
+  std::snprintf(buf, sizeof buf,
+                "pressure fixed point did not converge: last increment %.3e after %d iterations",
+                last_dp, cfg.fp_max_iter);
+  return fail(DG_ERR_SOLVER, buf);
+}
+
+int ensure_work(dg_ctx* c) {
+  const long long ns = c->scal();
+  for (auto* b : {&c->sh, &c->sK, &c->sx, &c->srhs, &c->spold, &c->sw, &c->sr, &c->sx2})
+    CK(b->alloc(ns));
+  CK(c->sV.alloc((size_t)ns * c->dim));
+  return DG_OK;
+}
+
+int ensure_states(dg_ctx* c) {
+  for (auto& s : c->st) CK(s.alloc(c->stat()));
+  return DG_OK;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+const char* dg_last_error(void) { return g_err.c_str(); }
+int dg_version(void) { return 100; }
+
+int dg_ctx_create(const dg_ctx_desc* d, dg_ctx** out) {
+  if (!d || !out) return fail(DG_ERR_USAGE, "null argument");
+  if (d->dim != 2 && d->dim != 3) return fail(DG_ERR_USAGE, "dim must be 2 or 3");
+  if (d->degree < 1 || d->degree > 6) return fail(DG_ERR_USAGE, "degree must be in 1..6 on the device path");
+  if (d->n_tot < d->n_el || d->n_el < 0) return fail(DG_ERR_USAGE, "bad element counts");
+  CK(cudaSetDevice(d->device));
+  dg_ctx* c = new dg_ctx();
+  c->device = d->device;
+  c->dim = d->dim;
+  c->N = d->degree + 1;
+  int np = 1, nqf = 1;
+  for (int a = 0; a < d->dim; ++a) np *= c->N;
+  for (int a = 0; a < d->dim - 1; ++a) nqf *= c->N;
+  c->NP = np;
+  c->NQF = nqf;
+  c->V = d->dim + 2;
+  c->S = 1 << (d->dim - 1);
+  c->n_el = d->n_el;
+  c->n_tot = d->n_tot;
+  c->n_global = (long long)d->n_el * np;
+  const int N = c->N;
+  const int expect_tabs = 3 * N * N + 2 * N + 4 * N * N + 2 * N;
+  if (d->tabs_len != expect_tabs) {
+    delete c;
+    return fail(DG_ERR_USAGE, "basis table length mismatch");
+  }
+  c->tabs.assign(d->tabs, d->tabs + d->tabs_len);
+  auto up = [&](auto& buf, const auto* h, size_t cnt) -> cudaError_t { return buf.upload(h, cnt); };
+  const size_t nf = (size_t)d->n_tot * 2 * d->dim;
+  cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = up(c->elem, d->elem, (size_t)d->n_tot * (2 + d->dim));
+  if (e == cudaSuccess) e = up(c->nbr, d->nbr, nf);
+  if (e == cudaSuccess) e = up(c->kind, d->kind, nf);
+  if (e == cudaSuccess && d->n_hang_groups > 0)
+    e = up(c->hang, d->hang_children, (size_t)d->n_hang_groups * c->S);
+  if (e == cudaSuccess && d->terrain && d->n_col > 0)
+    e = up(c->col, d->col, (size_t)d->n_col * d->col_stride);
+  if (e == cudaSuccess && d->n_bface > 0) {
+    e = up(c->ffU, d->ff_U, (size_t)d->n_bface * c->V * nqf);
+    if (e == cudaSuccess) e = up(c->ffp, d->ff_p, (size_t)d->n_bface * nqf);
+    if (e == cudaSuccess) e = up(c->ffh, d->ff_h, (size_t)d->n_bface * nqf);
+  }
+  if (e == cudaSuccess && d->sigma) {
+    e = up(c->sigma, d->sigma, (size_t)d->n_el * np);
+    if (e == cudaSuccess) e = up(c->bg, d->background, (size_t)d->n_el * c->V * np);
+  }
+  const int max_grid = d->n_el + 1;
+  if (e == cudaSuccess) e = c->mass_partial.alloc(max_grid);
+  if (e == cudaSuccess) e = c->partial.alloc((size_t)RED_BLOCKS * 40 + (size_t)max_grid * 8);
+  if (e == cudaSuccess) e = c->redout.alloc(256);
+  if (e == cudaSuccess) e = c->coef_dev.alloc(64);
+  if (e == cudaSuccess) e = cudaMallocHost(&c->pinned, 256 * sizeof(double));
+  if (e != cudaSuccess) {
+    dg_ctx_destroy(c);
+    return fail(DG_ERR_CUDA, std::string("context allocation: ") + cudaGetErrorString(e));
+  }
+  c->mesh.elem = c->elem.p;
+  c->mesh.col = c->col.p;
+  c->mesh.nbr = c->nbr.p;
+  c->mesh.kind = c->kind.p;
+  c->mesh.hang_children = c->hang.p;
+  c->mesh.ff_U = c->ffU.p;
+  c->mesh.ff_p = c->ffp.p;
+  c->mesh.ff_h = c->ffh.p;
+  c->mesh.n_el = d->n_el;
+  for (int a = 0; a < 3; ++a) c->gc.per_root[a] = d->per_root[a];
+  c->gc.z_top = d->z_top;
+  c->gc.terrain = d->terrain;
+  c->gc.col_stride = d->col_stride;
+  c->model = Model{d->gamma, d->gravity, d->inv_mach_sq, d->kinetic_factor};
+  *out = c;
+  return DG_OK;
+}
+
+int dg_ctx_destroy(dg_ctx* c) {
+  if (!c) return DG_OK;
+  cudaSetDevice(c->device);
+  for (auto* b : {&c->col, &c->ffU, &c->ffp, &c->ffh, &c->sigma, &c->bg, &c->mass_partial,
+                  &c->partial, &c->redout, &c->coef_dev, &c->sV, &c->sh, &c->sK, &c->sx,
+                  &c->srhs, &c->spold, &c->sw, &c->sr, &c->sx2, &c->basis})
+    b->release();
+  for (auto& s : c->st) s.release();
+  c->elem.release();
+  c->nbr.release();
+  c->hang.release();
+  c->kind.release();
+  if (c->pinned) cudaFreeHost(c->pinned);
+  c->comm.shutdown();
+  delete c;
+  return DG_OK;
+}
+
+int dg_ctx_set_stream(dg_ctx* c, void* s) {
+  c->stream = (cudaStream_t)s;
+  return DG_OK;
+}
+
+int dg_ctx_sync(dg_ctx* c) {
+  CK(cudaStreamSynchronize(c->stream));
+  return DG_OK;
+}
+
+int dg_ctx_launch_info(dg_ctx* c, int* grid, int* threads, long long* smem) {
+  if (grid) *grid = c->last.grid;
+  if (threads) *threads = c->last.threads;
+  if (smem) *smem = (long long)c->last.smem;
+  return DG_OK;
+}
+
+int dg_divergence_advective(dg_ctx* c, const double* U, double* dual) {
+  RET(halo(c, const_cast<double*>(U), c->V));
+  return op_advective(c, U, dual, OUT_DUAL, nullptr);
+}
+
+int dg_explicit_residual(dg_ctx* c, const double* U, double* R, double* mass_rate) {
+  RET(halo(c, const_cast<double*>(U), c->V));
+  return op_advective(c, U, R, OUT_MINV, mass_rate);
+}
+
+int dg_gradient_scalar(dg_ctx* c, const double* p, int homogeneous, double* dual) {
+  RET(halo(c, const_cast<double*>(p), 1));
+  return op_grad(c, p, nullptr, 1.0, 0.0, homogeneous, OUT_DUAL,
+                 mv(dual, (long long)c->dim * c->NP, c->NP), CView{}, 0, 1.0);
+}
+
+int dg_divergence_hv(dg_ctx* c, const double* V, long long v_estride, const double* h,
+                     int homogeneous, double* dual) {
+  RET(halo(c, const_cast<double*>(h), 1));
+  if (c->comm.active() && !c->comm.exchange(const_cast<double*>(V), c->dim, c->NP, c->stream, v_estride))
+    return fail(DG_ERR_COMM, c->comm.error());
+  return op_divhv(c, cv(V, v_estride, c->NP), h, homogeneous, OUT_DUAL, mv(dual, c->NP, c->NP),
+                  CView{}, 0, 1.0);
+}
+
+int dg_apply_mass_inverse(dg_ctx* c, const double* dual, int ncomp, double* out) {
+  AuxArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.elem = c->elem.p;
+  a.col = c->col.p;
+  a.gc = c->gc;
+  a.n_el = c->n_el;
+  a.ncomp = ncomp;
+  a.in = cv(dual, (long long)ncomp * c->NP, c->NP);
+  a.out = mv(out, (long long)ncomp * c->NP, c->NP);
+  a.tabs = c->tabs.data();
+  int grid = 0;
+  cudaError_t e = c->dim == 2 ? launch_aux_d2(c->N, 0, a, c->stream, &grid)
+                              : launch_aux_d3(c->N, 0, a, c->stream, &grid);
+  CK(e);
+  return DG_OK;
+}
+
+int dg_frozen_coefficients(dg_ctx* c, const double* U, double* h, double* K) {
+  CK(frozen(c->stream, c->n_el, c->NP, c->dim, U, c->model.gamma - 1.0, c->model.kinetic_factor,
+            h, K));
+  return DG_OK;
+}
+
+int dg_grad_p(dg_ctx* c, const double* x, const double* K, double* out, long long out_estride,
+              const double* base, long long base_estride, double coef) {
+  RET(halo(c, const_cast<double*>(x), 1));
+  if (K) RET(halo(c, const_cast<double*>(K), 1));
+  return op_grad(c, x, K, c->model.gamma - 1.0, c->model.kinetic_factor, 0, OUT_MINV,
+                 mv(out, out_estride, c->NP), cv(base, base_estride, c->NP), base ? 1 : 0, coef);
+}
+
+int dg_energy_F(dg_ctx* c, double a_dt, const double* h, const double* K, const double* m_e,
+                long long m_estride, const double* e_e, long long e_estride, const double* x,
+                double* Fx) {
+  RET(ensure_work(c));
+  RET(halo(c, const_cast<double*>(h), 1));
+  RET(halo(c, const_cast<double*>(K), 1));
+  return energy_F(c, a_dt, h, K, cv(m_e, m_estride, c->NP), cv(e_e, e_estride, c->NP),
+                  const_cast<double*>(x), Fx);
+}
+
+int dg_helmholtz_apply(dg_ctx* c, double a_dt, const double* h, const double* x, double* y) {
+  RET(ensure_work(c));
+  RET(halo(c, const_cast<double*>(h), 1));
+  return helm_apply(c, a_dt, h, const_cast<double*>(x), y);
+}
+
+int dg_gmres_helmholtz(dg_ctx* c, double a_dt, const double* h, const double* rhs, double* x,
+                       double tol_rel, int restart, int max_iter, dg_krylov_stats* stats,
+                       double* history, int history_cap) {
+  RET(ensure_work(c));
+  RET(halo(c, const_cast<double*>(h), 1));
+  Gm gs;
+  RET(gmres(c, a_dt, h, rhs, x, tol_rel, restart, max_iter, gs));
+  if (stats) {
+    stats->iterations = gs.iterations;
+    stats->restarts = gs.restarts;
+    stats->converged = gs.converged;
+    stats->breakdown = gs.breakdown;
+    stats->residual = gs.residual;
+    const int nh = (int)std::min<size_t>(gs.hist.size(), history_cap > 0 ? history_cap : 0);
+    stats->n_history = nh;
+    if (history)
+      for (int i = 0; i < nh; ++i) history[i] = gs.hist[i];
+  }
+  return DG_OK;
+}
+
+int dg_solve_implicit_stage(dg_ctx* c, const double* acc, const double* guess, double a_dt,
+                            const dg_solve_cfg* cfg, double* iterate, dg_step_stats* stats) {
+  RET(ensure_work(c));
+  int nfp = 0;
+  RET(solve_stage(c, acc, guess, a_dt, *cfg, iterate, stats, &nfp));
+  if (stats && stats->n_fp < 8) stats->fp_iters[stats->n_fp++] = nfp;
+  return DG_OK;
+}
+
+int dg_imex_step(dg_ctx* c, const double* U, double* U_out, double t, double dt,
+                 const dg_solve_cfg* cfg, dg_step_stats* stats) {
+  (void)t;
+  RET(ensure_work(c));
+  RET(ensure_states(c));
+  const int d = c->dim, NP = c->NP, V = c->V;
+  const long long ns = (long long)c->n_el * V * NP;
+  const long long sst = (long long)V * NP;
+  double* U0 = c->st[0].p;
+  double* KE0 = c->st[1].p;   // later acc2
+  double* acc1 = c->st[2].p;  // later KI1
+  double* U1 = c->st[3].p;    // later U2
+  double* KE1 = c->st[4].p;
+  const double g = 1.0 - 1.0 / std::sqrt(2.0);
+  const double dl = 1.0 - 1.0 / (2.0 * g);
+  dg_step_stats local;
+  if (!stats) stats = &local;
+  std::memset(stats, 0, sizeof(*stats));
+  CK(copy_comps(c->stream, c->n_el, NP, V, U, sst, U0, sst));
+  // stage 0 (explicit): U_stage = U
+  RET(check_positivity(c, U0, stats, 0));
+  double mr = 0.0;
+  RET(halo(c, U0, V));
+  RET(op_advective(c, U0, KE0, OUT_MINV, &mr));
+  stats->mass_rate += dl * mr;
+  {
+    const double cf[2] = {1.0, dt * g};
+    const double* xs[2] = {U0, KE0};
+    CK(lincomb(c->stream, ns, 2, cf, xs, acc1));
+  }
+  // stage 1 (implicit)
+  int nfp = 0;
+  RET(solve_stage(c, acc1, U0, dt * g, *cfg, U1, stats, &nfp));
+  stats->fp_iters[stats->n_fp++] = nfp;
+  {
+    // KI1 = (U1 - acc1) / (dt g)   (in place over acc1)
+    const double cf[2] = {1.0, -1.0};
+    const double* xs[2] = {U1, acc1};
+    CK(lincomb(c->stream, ns, 2, cf, xs, acc1));
+    CK(scale(c->stream, ns, dt * g, true, acc1, acc1));
+  }
+  RET(check_positivity(c, U1, stats, 1));
+  RET(halo(c, U1, V));
+  RET(op_advective(c, U1, KE1, OUT_MINV, &mr));
+  stats->mass_rate += (1.0 - dl) * mr;
+  {
+    // acc2 = U + dt dl KE0 + dt (1-dl) KE1 + dt (1-g) KI1   (in place over KE0)
+    const double cf[4] = {1.0, dt * dl, dt * (1.0 - dl), dt * (1.0 - g)};
+    const double* xs[4] = {U0, KE0, KE1, acc1};
+    CK(lincomb(c->stream, ns, 4, cf, xs, KE0));
+  }
+  // stage 2 (implicit), guess = U1, result in place over U1
+  RET(solve_stage(c, KE0, U1, dt * g, *cfg, U1, stats, &nfp));
+  stats->fp_iters[stats->n_fp++] = nfp;
+  RET(check_positivity(c, U1, stats, 2));
+  CK(copy_comps(c->stream, c->n_el, NP, V, U1, sst, U_out, sst));
+  return DG_OK;
+}
+
+int dg_integrate_conserved(dg_ctx* c, const double* U, double* out_host) {
+  AuxArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.elem = c->elem.p;
+  a.col = c->col.p;
+  a.gc = c->gc;
+  a.n_el = c->n_el;
+  a.ncomp = c->V;
+  a.in = cv(U, (long long)c->V * c->NP, c->NP);
+  a.partial = c->partial.p;
+  a.tabs = c->tabs.data();
+  int grid = 0;
+  cudaError_t e = c->dim == 2 ? launch_aux_d2(c->N, 1, a, c->stream, &grid)
+                              : launch_aux_d3(c->N, 1, a, c->stream, &grid);
+  CK(e);
+  if (grid == 0) {
+    for (int v = 0; v < c->V; ++v) out_host[v] = 0.0;
+    return DG_OK;
+  }
+  CK(reduce_cols(c->stream, c->partial.p, grid, c->V, c->redout.p));
+  return reduce_read(c, c->redout.p, c->V, out_host);
+}
+
+int dg_check_positivity(dg_ctx* c, const double* U, double* min_rho, long long* at_rho,
+                        double* min_p, long long* at_p) {
+  dg_step_stats s;
+  std::memset(&s, 0, sizeof s);
+  int r = check_positivity(c, U, &s, -1);
+  if (min_rho) *min_rho = s.fail_kind == 0 ? s.fail_value : 0.0;
+  if (at_rho) *at_rho = s.fail_element;
+  if (min_p) *min_p = s.fail_value;
+  if (at_p) *at_p = s.fail_node;
+  return r;
+}
+
+int dg_lincomb(dg_ctx* c, long long n, int m, const double* coefs, const double* const* xs,
+               double* y) {
+  if (m < 1 || m > 4) return fail(DG_ERR_USAGE, "lincomb takes 1..4 terms");
+  CK(lincomb(c->stream, n, m, coefs, xs, y));
+  return DG_OK;
+}
+
+int dg_dots(dg_ctx* c, long long n, int nv, const double* V, long long vstride, const double* w,
+            double* out_host) {
+  if (nv < 0 || nv > 32) return fail(DG_ERR_USAGE, "dg_dots: 0..32 vectors");
+  CK(multidot(c->stream, n, nv, V, vstride, w, c->partial.p, c->redout.p));
+  return reduce_read(c, c->redout.p, nv + 1, out_host);
+}
+
+int dg_nccl_unique_id(void* out128) {
+  std::string err;
+  if (!Comm::unique_id(out128, &err)) return fail(DG_ERR_COMM, err);
+  return DG_OK;
+}
+
+int dg_ctx_set_comm(dg_ctx* c, const void* uid, int rank, int nranks, const int32_t* send_counts,
+                    const int32_t* send_elems, const int32_t* recv_counts) {
+  CK(cudaSetDevice(c->device));
+  if (!c->comm.init(uid, rank, nranks, send_counts, send_elems, recv_counts, c->n_el, c->n_tot))
+    return fail(DG_ERR_COMM, c->comm.error());
+  long long tot = (long long)c->n_el * c->NP;
+  double v = (double)tot;
+  DevBuf<double> tmp;
+  CK(tmp.upload(&v, 1));
+  if (!c->comm.allreduce_sum(tmp.p, 1, c->stream)) return fail(DG_ERR_COMM, c->comm.error());
+  CK(cudaMemcpy(&v, tmp.p, sizeof(double), cudaMemcpyDeviceToHost));
+  tmp.release();
+  c->n_global = (long long)v;
+  return DG_OK;
+}
+
+int dg_halo_exchange(dg_ctx* c, double* field, int ncomp) { return halo(c, field, ncomp); }
+
+int dg_split_contiguous(const double* w, long long n, int n_chunks, long long* bounds) {
+  // orodg/partition.py:45-67 : bisection on the capacity + greedy packing
+  if (n_chunks < 1) return fail(DG_ERR_CONFIG, "need >= 1 chunk");
+  if (n_chunks >= n) {
+    for (long long i = 0; i <= n; ++i) bounds[i] = i;
+    for (long long i = n + 1; i <= n_chunks; ++i) bounds[i] = n;
+    return DG_OK;
+  }
+  auto pack = [&](double cap, std::vector<long long>& b, long long limit) -> bool {
+    b.clear();
+    b.push_back(0);
+    double acc = 0.0;
+    for (long long i = 0; i < n; ++i) {
+      if (w[i] > cap) return false;
+      if (acc + w[i] > cap) {
+        b.push_back(i);
+        acc = w[i];
+        if ((long long)b.size() - 1 > limit) return true;
+      } else {
+        acc += w[i];
+      }
+    }
+    b.push_back(n);
+    return true;
+  };
+  double lo = 0.0, hi = 0.0;
+  for (long long i = 0; i < n; ++i) {
+    lo = std::max(lo, w[i]);
+    hi += w[i];
+  }
+  std::vector<long long> b;
+  for (int it = 0; it < 200; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    const bool ok = pack(mid, b, n_chunks) && (long long)b.size() - 1 <= n_chunks;
+    if (ok) hi = mid;
+    else lo = mid;
+    if (hi - lo <= 1e-12 * std::max(hi, 1.0)) break;
+  }
+  pack(hi * (1 + 1e-12), b, n);
+  while ((long long)b.size() - 1 < n_chunks) b.push_back(n);
+  for (int i = 0; i <= n_chunks; ++i) bounds[i] = b[i];
+  return DG_OK;
+}
+
+}  // extern "C"

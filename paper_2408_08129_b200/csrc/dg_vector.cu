@@ -1,0 +1,367 @@
+// Streaming vector kernels of the implicit solver: IMEX stage linear
+// combinations (orodg/imex.py:267-298), GMRES Gram-Schmidt dots/updates
+// (orodg/krylov.py:69-80, 105-109), pressure fixed-point norms
+// (imex.py:355-359), frozen coefficients (imex.py:182-188) and the
+// positivity check (physics.py:136-164).
+//
+// All reductions are deterministic: a fixed grid of RED_BLOCKS CTAs writes
+// per-CTA partials in a fixed traversal order, a second kernel combines
+// them with a fixed warp tree.  Results are bitwise reproducible run to run.
+#include <cstdint>
+#include "dg_vector.cuh"
+
+namespace dg {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// y = c0 x0 (+ c1 x1 (+ c2 x2 (+ c3 x3))), left to right, unfused like numpy
+__global__ void k_lincomb(long long n, int m, double c0, double c1, double c2, double c3,
+                          const double* __restrict__ x0, const double* __restrict__ x1,
+                          const double* __restrict__ x2, const double* __restrict__ x3,
+                          double* __restrict__ y) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double v = (c0 == 1.0) ? x0[i] : __dmul_rn(c0, x0[i]);
+    if (m > 1) v = __dadd_rn(v, __dmul_rn(c1, x1[i]));
+    if (m > 2) v = __dadd_rn(v, __dmul_rn(c2, x2[i]));
+    if (m > 3) v = __dadd_rn(v, __dmul_rn(c3, x3[i]));
+    y[i] = v;
+  }
+}
+
+// partials[b][i] = sum V_i . w  (i < nv),  partials[b][nv] = w . w
+template <int MAXV>
+__global__ void __launch_bounds__(RED_THREADS)
+k_multidot(long long n, int nv, const double* __restrict__ V, long long vstride,
+           const double* __restrict__ w, double* __restrict__ partials) {
+  double acc[MAXV + 1];
+#pragma unroll
+  for (int i = 0; i <= MAXV; ++i) acc[i] = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    const double wk = w[k];
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i)
+      if (i < nv) acc[i] = fma(V[i * vstride + k], wk, acc[i]);
+    acc[MAXV] = fma(wk, wk, acc[MAXV]);
+  }
+  __shared__ double red[RED_THREADS / 32][MAXV + 1];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i <= MAXV; ++i) {
+    if (i < nv || i == MAXV) {
+      const double v = warp_sum(acc[i]);
+      if (lane == 0) red[wid][i] = v;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= MAXV; i += blockDim.x) {
+    if (i < nv || i == MAXV) {
+      double s = 0.0;
+      for (int w2 = 0; w2 < RED_THREADS / 32; ++w2) s += red[w2][i];
+      partials[(long long)blockIdx.x * (nv + 1) + (i == MAXV ? nv : i)] = s;
+    }
+  }
+}
+
+// w <- w - sum_i c_i V_i ; partial |w|^2.  coefs on the device.
+template <int MAXV>
+__global__ void __launch_bounds__(RED_THREADS)
+k_axpy_multi(long long n, int nv, const double* __restrict__ V, long long vstride,
+             const double* __restrict__ coefs, double* __restrict__ w,
+             double* __restrict__ partials) {
+  __shared__ double c[MAXV];
+  for (int i = threadIdx.x; i < MAXV; i += blockDim.x) c[i] = i < nv ? coefs[i] : 0.0;
+  __syncthreads();
+  double acc = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    double t = 0.0;
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i)
+      if (i < nv) t = fma(c[i], V[i * vstride + k], t);
+    const double v = w[k] - t;
+    w[k] = v;
+    acc = fma(v, v, acc);
+  }
+  __shared__ double red[RED_THREADS / 32];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < RED_THREADS / 32; ++i) s += red[i];
+    if (partials) partials[blockIdx.x] = s;
+  }
+}
+
+// out[c] = sum_b partials[b][c]   (one warp per column, fixed order)
+__global__ void k_reduce_cols(const double* __restrict__ partials, int nblocks, int ncols,
+                              double* __restrict__ out) {
+  const int col = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (col >= ncols) return;
+  double s = 0.0;
+  for (int b = lane; b < nblocks; b += 32) s += partials[(long long)b * ncols + col];
+  s = warp_sum(s);
+  if (lane == 0) out[col] = s;
+}
+
+__global__ void k_scale(long long n, double a, int divide, const double* __restrict__ x,
+                        double* __restrict__ y) {
+  // y = x * a, or y = x / a (numpy's r / beta, w / norm)
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    y[i] = divide ? x[i] / a : x[i] * a;
+}
+
+// h = e + p/rho, K = rho k at every node (imex.py:182-188)
+__global__ void k_frozen(long long n_el, int np, int d, const double* __restrict__ U,
+                         double gm1, double kf, double* __restrict__ h, double* __restrict__ K) {
+  const long long n = n_el * np;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const int V = d + 2;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const long long e = i / np;
+    const int q = (int)(i - e * np);
+    const double* u = U + e * V * np + q;
+    const double rho = u[0];
+    double k = 0.0;
+    for (int a = 0; a < d; ++a) {
+      const double v = u[(1 + a) * np] / rho;
+      k += v * v;
+    }
+    k *= 0.5;
+    const double p = gm1 * (u[(d + 1) * np] - kf * rho * k);
+    h[i] = p / (gm1 * rho) + p / rho;
+    K[i] = rho * k;
+  }
+}
+
+// p from a conserved state (scalar field)
+__global__ void k_state_pressure(long long n_el, int np, int d, const double* __restrict__ U,
+                                 double gm1, double kf, double* __restrict__ p) {
+  const long long n = n_el * np;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const int V = d + 2;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const long long e = i / np;
+    const int q = (int)(i - e * np);
+    const double* u = U + e * V * np + q;
+    const double rho = u[0];
+    double k = 0.0;
+    for (int a = 0; a < d; ++a) {
+      const double v = u[(1 + a) * np] / rho;
+      k += v * v;
+    }
+    k *= 0.5;
+    p[i] = gm1 * (u[(d + 1) * np] - kf * rho * k);
+  }
+}
+
+// p_new = gm1 (x - kf K);  partials: |p_new - p_old|^2, |p_old|^2; p_old <- p_new
+__global__ void __launch_bounds__(RED_THREADS)
+k_pressure_dp(long long n, const double* __restrict__ x, const double* __restrict__ K,
+              double gm1, double kf, double* __restrict__ p_old, double* __restrict__ partials) {
+  double a = 0.0, b = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double pn = gm1 * (x[i] - kf * K[i]);
+    const double po = p_old[i];
+    const double df = pn - po;
+    a = fma(df, df, a);
+    b = fma(po, po, b);
+    p_old[i] = pn;
+  }
+  __shared__ double red[2][RED_THREADS / 32];
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = a;
+    red[1][threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sa = 0.0, sb = 0.0;
+    for (int i = 0; i < RED_THREADS / 32; ++i) {
+      sa += red[0][i];
+      sb += red[1][i];
+    }
+    partials[blockIdx.x * 2] = sa;
+    partials[blockIdx.x * 2 + 1] = sb;
+  }
+}
+
+// iterate = acc with components >= 1 taken from guess (imex.py:315-317)
+__global__ void k_set_iterate(long long n_el, int np, int V, const double* __restrict__ acc,
+                              const double* __restrict__ guess, double* __restrict__ it) {
+  const long long n = n_el * V * np;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int c = (int)((i / np) % V);
+    it[i] = c == 0 ? acc[i] : guess[i];
+  }
+}
+
+// strided component copy: dst(e, c0+c) = src(e, s0+c)
+__global__ void k_copy_comps(long long n_el, int np, int nc, const double* __restrict__ src,
+                             long long s_estride, double* __restrict__ dst, long long d_estride) {
+  const long long n = n_el * nc * np;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const long long e = i / (nc * np);
+    const long long r = i - e * nc * np;
+    dst[e * d_estride + r] = src[e * s_estride + r];
+  }
+}
+
+// positivity: per-CTA (min rho, idx, min p, idx); first index among ties
+struct MinLoc {
+  double v;
+  long long i;
+};
+__device__ __forceinline__ MinLoc minloc(MinLoc a, MinLoc b) {
+  if (b.v < a.v || (b.v == a.v && b.i < a.i)) return b;
+  return a;
+}
+__global__ void __launch_bounds__(RED_THREADS)
+k_positivity(long long n_el, int np, int d, const double* __restrict__ U, double gm1, double kf,
+             double* __restrict__ partials) {
+  MinLoc r{INFINITY, 0x7fffffffffffffffLL}, p{INFINITY, 0x7fffffffffffffffLL};
+  const long long n = n_el * np;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const int V = d + 2;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const long long e = i / np;
+    const int q = (int)(i - e * np);
+    const double* u = U + e * V * np + q;
+    const double rho = u[0];
+    double k = 0.0;
+    for (int a = 0; a < d; ++a) {
+      const double v = u[(1 + a) * np] / rho;
+      k += v * v;
+    }
+    k *= 0.5;
+    const double pr = gm1 * (u[(d + 1) * np] - kf * rho * k);
+    r = minloc(r, MinLoc{rho != rho ? -INFINITY : rho, i});
+    p = minloc(p, MinLoc{pr != pr ? -INFINITY : pr, i});
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    MinLoc r2{__shfl_xor_sync(0xffffffffu, r.v, o), __shfl_xor_sync(0xffffffffu, r.i, o)};
+    MinLoc p2{__shfl_xor_sync(0xffffffffu, p.v, o), __shfl_xor_sync(0xffffffffu, p.i, o)};
+    r = minloc(r, r2);
+    p = minloc(p, p2);
+  }
+  __shared__ MinLoc sr[RED_THREADS / 32], sp[RED_THREADS / 32];
+  if ((threadIdx.x & 31) == 0) {
+    sr[threadIdx.x >> 5] = r;
+    sp[threadIdx.x >> 5] = p;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < RED_THREADS / 32; ++i) {
+      r = minloc(sr[0], sr[i]);
+      sr[0] = r;
+      p = minloc(sp[0], sp[i]);
+      sp[0] = p;
+    }
+    partials[blockIdx.x * 4 + 0] = sr[0].v;
+    partials[blockIdx.x * 4 + 1] = (double)sr[0].i;
+    partials[blockIdx.x * 4 + 2] = sp[0].v;
+    partials[blockIdx.x * 4 + 3] = (double)sp[0].i;
+  }
+}
+
+// ------------------------------------------------------------ host wrappers
+static int grid_for(long long n) {
+  long long g = (n + RED_THREADS - 1) / RED_THREADS;
+  if (g > RED_BLOCKS) g = RED_BLOCKS;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+cudaError_t lincomb(cudaStream_t st, long long n, int m, const double* c, const double* const* x,
+                    double* y) {
+  if (n <= 0) return cudaSuccess;
+  k_lincomb<<<grid_for(n), RED_THREADS, 0, st>>>(
+      n, m, c[0], m > 1 ? c[1] : 0.0, m > 2 ? c[2] : 0.0, m > 3 ? c[3] : 0.0, x[0],
+      m > 1 ? x[1] : nullptr, m > 2 ? x[2] : nullptr, m > 3 ? x[3] : nullptr, y);
+  return cudaGetLastError();
+}
+
+cudaError_t multidot(cudaStream_t st, long long n, int nv, const double* V, long long vstride,
+                     const double* w, double* partials, double* out) {
+  // out[0..nv-1] = V_i . w, out[nv] = w . w  (fixed RED_BLOCKS grid)
+  if (nv <= 8) k_multidot<8><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, nv, V, vstride, w, partials);
+  else if (nv <= 16) k_multidot<16><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, nv, V, vstride, w, partials);
+  else if (nv <= 32) k_multidot<32><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, nv, V, vstride, w, partials);
+  else return cudaErrorInvalidValue;
+  const int ncols = nv + 1;
+  k_reduce_cols<<<(ncols + 7) / 8, 256, 0, st>>>(partials, RED_BLOCKS, ncols, out);
+  return cudaGetLastError();
+}
+
+cudaError_t axpy_multi(cudaStream_t st, long long n, int nv, const double* V, long long vstride,
+                       const double* coefs_dev, double* w, double* partials, double* norm2_out) {
+  if (nv <= 8) k_axpy_multi<8><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, nv, V, vstride, coefs_dev, w, partials);
+  else if (nv <= 16) k_axpy_multi<16><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, nv, V, vstride, coefs_dev, w, partials);
+  else if (nv <= 32) k_axpy_multi<32><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, nv, V, vstride, coefs_dev, w, partials);
+  else return cudaErrorInvalidValue;
+  if (norm2_out) k_reduce_cols<<<1, 32, 0, st>>>(partials, RED_BLOCKS, 1, norm2_out);
+  return cudaGetLastError();
+}
+
+cudaError_t scale(cudaStream_t st, long long n, double a, bool divide, const double* x,
+                  double* y) {
+  k_scale<<<grid_for(n), RED_THREADS, 0, st>>>(n, a, divide ? 1 : 0, x, y);
+  return cudaGetLastError();
+}
+
+cudaError_t frozen(cudaStream_t st, long long n_el, int np, int d, const double* U, double gm1,
+                   double kf, double* h, double* K) {
+  k_frozen<<<grid_for(n_el * np), RED_THREADS, 0, st>>>(n_el, np, d, U, gm1, kf, h, K);
+  return cudaGetLastError();
+}
+
+cudaError_t state_pressure(cudaStream_t st, long long n_el, int np, int d, const double* U,
+                           double gm1, double kf, double* p) {
+  k_state_pressure<<<grid_for(n_el * np), RED_THREADS, 0, st>>>(n_el, np, d, U, gm1, kf, p);
+  return cudaGetLastError();
+}
+
+cudaError_t pressure_dp(cudaStream_t st, long long n, const double* x, const double* K, double gm1,
+                        double kf, double* p_old, double* partials, double* out2) {
+  k_pressure_dp<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, x, K, gm1, kf, p_old, partials);
+  k_reduce_cols<<<1, 64, 0, st>>>(partials, RED_BLOCKS, 2, out2);
+  return cudaGetLastError();
+}
+
+cudaError_t set_iterate(cudaStream_t st, long long n_el, int np, int V, const double* acc,
+                        const double* guess, double* it) {
+  k_set_iterate<<<grid_for(n_el * V * np), RED_THREADS, 0, st>>>(n_el, np, V, acc, guess, it);
+  return cudaGetLastError();
+}
+
+cudaError_t copy_comps(cudaStream_t st, long long n_el, int np, int nc, const double* src,
+                       long long s_estride, double* dst, long long d_estride) {
+  k_copy_comps<<<grid_for(n_el * nc * np), RED_THREADS, 0, st>>>(n_el, np, nc, src, s_estride,
+                                                                  dst, d_estride);
+  return cudaGetLastError();
+}
+
+cudaError_t positivity(cudaStream_t st, long long n_el, int np, int d, const double* U, double gm1,
+                       double kf, double* partials) {
+  k_positivity<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n_el, np, d, U, gm1, kf, partials);
+  return cudaGetLastError();
+}
+
+cudaError_t reduce_cols(cudaStream_t st, const double* partials, int nblocks, int ncols, double* out) {
+  k_reduce_cols<<<(ncols + 7) / 8, 256, 0, st>>>(partials, nblocks, ncols, out);
+  return cudaGetLastError();
+}
+
+}  // namespace dg

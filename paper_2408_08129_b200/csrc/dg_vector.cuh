@@ -1,0 +1,32 @@
+// Host wrappers of the streaming vector kernels (dg_vector.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace dg {
+
+constexpr int RED_THREADS = 256;
+constexpr int RED_BLOCKS = 592;  // 4 x 148 SMs; fixed => deterministic reductions
+
+cudaError_t lincomb(cudaStream_t st, long long n, int m, const double* c, const double* const* x,
+                    double* y);
+cudaError_t multidot(cudaStream_t st, long long n, int nv, const double* V, long long vstride,
+                     const double* w, double* partials, double* out);
+cudaError_t axpy_multi(cudaStream_t st, long long n, int nv, const double* V, long long vstride,
+                       const double* coefs_dev, double* w, double* partials, double* norm2_out);
+cudaError_t scale(cudaStream_t st, long long n, double a, bool divide, const double* x,
+                  double* y);
+cudaError_t frozen(cudaStream_t st, long long n_el, int np, int d, const double* U, double gm1,
+                   double kf, double* h, double* K);
+cudaError_t state_pressure(cudaStream_t st, long long n_el, int np, int d, const double* U,
+                           double gm1, double kf, double* p);
+cudaError_t pressure_dp(cudaStream_t st, long long n, const double* x, const double* K, double gm1,
+                        double kf, double* p_old, double* partials, double* out2);
+cudaError_t set_iterate(cudaStream_t st, long long n_el, int np, int V, const double* acc,
+                        const double* guess, double* it);
+cudaError_t copy_comps(cudaStream_t st, long long n_el, int np, int nc, const double* src,
+                       long long s_estride, double* dst, long long d_estride);
+cudaError_t positivity(cudaStream_t st, long long n_el, int np, int d, const double* U, double gm1,
+                       double kf, double* partials);
+cudaError_t reduce_cols(cudaStream_t st, const double* partials, int nblocks, int ncols, double* out);
+
+}  // namespace dg
