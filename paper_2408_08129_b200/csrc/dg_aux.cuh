@@ -60,6 +60,7 @@ minv_kernel(const __grid_constant__ AuxParams<N> P) {
   {
     const double* src = reinterpret_cast<const double*>(&P.tab);
     for (int i = threadIdx.x; i < L::TABD; i += blockDim.x) tb[i] = src[i];
+    __syncthreads();
   }
   const Tab<N>& T = *reinterpret_cast<const Tab<N>*>(tb);
   const int el = threadIdx.x / NP, q = threadIdx.x - el * NP;
@@ -106,6 +107,7 @@ integrate_kernel(const __grid_constant__ AuxParams<N> P) {
   {
     const double* src = reinterpret_cast<const double*>(&P.tab);
     for (int i = threadIdx.x; i < L::TABD; i += blockDim.x) tb[i] = src[i];
+    __syncthreads();
   }
   const Tab<N>& T = *reinterpret_cast<const Tab<N>*>(tb);
   double* red = smem + L::TABD;

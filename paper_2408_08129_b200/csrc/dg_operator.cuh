@@ -213,6 +213,7 @@ elem_kernel(const __grid_constant__ KParams<N> P) {
   {
     const double* src = reinterpret_cast<const double*>(&P.tab);
     for (int i = threadIdx.x; i < L::TABD; i += blockDim.x) tb[i] = src[i];
+    __syncthreads();
   }
   const Tab<N>& T = *reinterpret_cast<const Tab<N>*>(tb);
   double* red = smem + L::TABD;  // 64 doubles for block reductions
