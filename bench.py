@@ -1,0 +1,318 @@
+"""Benchmark of the B200 IMEX-DG hot path (driver contract: one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload cfg4|cfg3|cfg2|cfg1]
+
+Workload (config.workload): BASELINE.json configs[3], the 3D Gaussian hill
+on the 3-level non-conforming hex mesh (2,505,600 cells, r=3, 801.8 M DoF),
+the configuration the metric is quoted on at 1/2/4/8 B200.  A step is one
+ARS(2,2,2) IMEX step (2 explicit residuals + the pressure fixed point with
+its GMRES solves).  metric = fp64 DoF/s per IMEX step (all d+2 variables),
+value = whole-job throughput with the state resident in HBM; e2e = the same
+through the public imex_step API with the state copied host->device and
+back every step.  The state is 6.4 GB >> 126 MB L2, so no flush is needed.
+
+--impl reference times the reference algorithm on the host CPU (the numpy
+oracle port, oracle/dg_oracle.py, all host threads) on a bounded sample of
+the same recipe (a smaller root grid), reported in the same unit.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="cfg4", choices=["cfg4", "cfg3", "cfg2", "cfg1"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+DESC = {
+    "cfg4": "BASELINE configs[3]: 3D flow over a Gaussian hill (400 m, a=3 km), 60x60x20 km, "
+            "120x120x20 roots refined below 6 km and 2 km (3 levels, 2,505,600 hexes), r=3, "
+            "N=0.01 1/s, U=10 m/s, far-field+sponge, dt=0.5 s",
+    "cfg3": "BASELINE configs[2]: 2D Schar orography, 220,800 cells, r=4",
+    "cfg2": "BASELINE configs[1]: 2D warm bubble 64x32 + z<5 km refined, r=4, tol 1e-10",
+    "cfg1": "BASELINE configs[0]: 2D warm bubble 32x16, r=2",
+}
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        import statistics
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if len(r) > 3 + k and r[3 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_step_sample(workload, threads, budget_s=30.0):
+    """Reference algorithm (numpy oracle port) on a bounded sample of the
+    workload recipe: one IMEX step on a shrunken root grid."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import dg_oracle as O
+    from paper_2408_08129_b200.cases import baseline_case
+    scale = {"cfg4": 3.0 / 120.0, "cfg3": 20.0 / 400.0, "cfg2": 1.0, "cfg1": 1.0}[workload]
+    c = baseline_case(workload, root_scale=scale)
+    ops = O.Operators(c.geometry, c.model, c.bcs, c.sponge)
+    d = c.mesh.dim
+    nn = c.geometry.basis.n_nodes
+    dofs = c.mesh.n_leaves * nn * (d + 2)
+    with threadpool_limits(threads):
+        t0 = time.perf_counter()
+        U, st = O.imex_step(ops, c.U0, 0.0, c.dt, **{k: v for k, v in c.solve.items()})
+        t = time.perf_counter() - t0
+    return {"value": dofs / t, "unit": "DoF/s", "cores": threads, "kind": "port",
+            "seconds_per_step": t,
+            "sample": f"1 ARS(2,2,2) step of the {workload} recipe on a "
+                      f"{'x'.join(map(str, c.mesh.root_counts))} root grid "
+                      f"({c.mesh.n_leaves} cells, {dofs} DoF), krylov {st.krylov_iters}"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    vals = []
+    last = None
+    for _ in range(args.steps):
+        last = cpu_step_sample(args.workload, threads)
+        vals.append(last["seconds_per_step"])
+    ms = 1e3 * sum(vals) / len(vals)
+    line = {"metric": "fp64 DoF/s per ARS(2,2,2) IMEX-RK step (all variables)",
+            "value": last["value"], "unit": "DoF/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": args.workload, "description": DESC[args.workload]},
+            "cpu_baseline": {k: last[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": last["value"], "unit": "DoF/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ B200
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+
+    from paper_2408_08129_b200 import _lib as L
+    from paper_2408_08129_b200.cases import baseline_case
+    from paper_2408_08129_b200.imex import ImplicitSolveConfig, ars222, imex_step
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+
+    t_setup = time.perf_counter()
+    case = baseline_case(args.workload)
+    cfg = ImplicitSolveConfig(**case.solve)
+    if world > 1:
+        from paper_2408_08129_b200.distributed import DistributedSolver
+        solver = DistributedSolver(case, cfg, rank, world, local)
+        U = solver.local_state()
+        step = solver.step
+        n_dof_local = solver.n_owned * case.geometry.basis.n_nodes * (case.mesh.dim + 2)
+    else:
+        from paper_2408_08129_b200.dgops import DGOperators
+        from paper_2408_08129_b200.imex import SplitOperators
+        ops = DGOperators(case.geometry)
+        split = SplitOperators(ops, case.model, case.bcs, case.sponge)
+        U = torch.from_numpy(case.U0).to(dev)
+        tab = ars222()
+
+        def step(U, t):
+            return imex_step(U, t, case.dt, tab, split, cfg)
+        n_dof_local = U.numel()
+    setup_s = time.perf_counter() - t_setup
+    n_dof = n_dof_local * world
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (also triggers every lazy allocation)
+    t = 0.0
+    kry = []
+    for _ in range(args.warmup):
+        U, st = step(U, t)
+        t += case.dt
+    barrier()
+    lib = L.lib()
+    n0 = lib.dg_launch_count()
+    lib.dg_profile_enable(1)
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            U, st = step(U, t)
+            kry.append((list(st.fp_iters), list(st.krylov_iters)))
+            t += case.dt
+        ev1.record(stream)
+        barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    launches = lib.dg_launch_count() - n0
+    import ctypes as C
+    ms_c = (C.c_double * 6)()
+    by_c = (C.c_double * 6)()
+    cnt = (C.c_longlong * 6)()
+    lib.dg_profile_read(ms_c, by_c, cnt)
+    lib.dg_profile_enable(0)
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([ms_total], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_total = float(tt)
+    ms_step = ms_total / args.steps
+    value = n_dof * args.steps / (ms_total * 1e-3)
+
+    # dominant kernel class over the timed region
+    classes = L.PROFILE_CLASSES
+    k_dom = max(range(6), key=lambda k: ms_c[k])
+    peak, peak_kind = peaks()
+    per_launch_ms = ms_c[k_dom] / max(cnt[k_dom], 1)
+    per_launch_bytes = by_c[k_dom] / max(cnt[k_dom], 1)
+    achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
+    breakdown = {classes[k]: {"ms": ms_c[k], "launches": int(cnt[k]),
+                              "GB_s": (by_c[k] / (ms_c[k] * 1e-3) / 1e9) if ms_c[k] else None}
+                 for k in range(6)}
+
+    # e2e through the public API with host buffers (rank-local state)
+    e2e = None
+    if world == 1:
+        Uh = torch.empty(U.shape, dtype=torch.float64, pin_memory=True)
+        Uh.copy_(U)
+        barrier()
+        e0 = time.perf_counter()
+        ev0.record(stream)
+        for _ in range(max(1, min(args.steps, 3))):
+            Ud = Uh.to(dev, non_blocking=True)
+            Ud, _ = step(Ud, t)
+            Uh.copy_(Ud, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        ev1.record(stream)
+        barrier()
+        ne = max(1, min(args.steps, 3))
+        ms_e2e = ev0.elapsed_time(ev1) / ne
+        e2e = {"value": n_dof / (ms_e2e * 1e-3), "unit": "DoF/s",
+               "h2d_bytes_per_step": int(U.numel() * 8), "d2h_bytes_per_step": int(U.numel() * 8),
+               "ms_per_step": ms_e2e, "wall_s_per_step": (time.perf_counter() - e0) / ne}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_step_sample(args.workload, 1)
+            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as err:  # pragma: no cover
+            cpu = {"error": str(err)}
+
+    if rank == 0:
+        line = {
+            "metric": "fp64 DoF/s per ARS(2,2,2) IMEX-RK step (all variables)",
+            "value": value, "unit": "DoF/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (analytic hydrostatic background flow over the hill, "
+                    "seeded recipe of SURVEY.md §8d; no dataset)",
+            "config": {"workload": args.workload, "description": DESC[args.workload],
+                       "n_el": case.mesh.n_leaves, "degree": case.geometry.basis.degree,
+                       "dof_total": n_dof, "dt": case.dt,
+                       "solver": {"fp_tol": cfg.fp_tol, "krylov_tol": cfg.krylov_tol,
+                                  "restart": cfg.krylov_restart},
+                       "parallelism": f"element-block partition x{world}",
+                       "l2": "inputs larger than L2 (state 8 B x DoF)",
+                       "iterations": kry, "setup_s": setup_s},
+            "roofline": {"bound": "hbm", "kernel": classes[k_dom], "achieved": achieved,
+                         "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "peak_kind": peak_kind, "traffic": None,
+                         "bytes_per_launch": per_launch_bytes,
+                         "ms_per_launch": per_launch_ms,
+                         "share_of_step": ms_c[k_dom] / ms_total},
+            "kernel_breakdown": breakdown,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

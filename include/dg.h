@@ -173,6 +173,13 @@ int dg_ctx_set_comm(dg_ctx* ctx, const void* unique_id128, int rank, int nranks,
                     const int32_t* recv_counts);
 int dg_halo_exchange(dg_ctx* ctx, double* field, int ncomp);
 
+/* ---- instrumentation (no reference counterpart; orodg/timing.py is host-only) ----
+   launches of libdg kernels since load; optional per-class CUDA-event timing
+   (classes: 0 explicit, 1 gradient, 2 div(hV), 3 multi-dot, 4 axpy, 5 other) */
+long long dg_launch_count(void);
+int dg_profile_enable(int on);
+int dg_profile_read(double* ms /*6*/, double* bytes /*6*/, long long* count /*6*/);
+
 /* ---- partitioner (orodg/partition.py:45-67): bounds has n_chunks+1 slots ---- */
 int dg_split_contiguous(const double* weights, long long n, int n_chunks, long long* bounds);
 

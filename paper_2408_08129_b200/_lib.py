@@ -81,7 +81,12 @@ _SIGS = {
     "dg_ctx_set_comm": ([P, P, I, I, P, P, P], I),
     "dg_halo_exchange": ([P, P, I], I),
     "dg_split_contiguous": ([P, LL, I, P], I),
+    "dg_launch_count": ([], LL),
+    "dg_profile_enable": ([I], I),
+    "dg_profile_read": ([P, P, P], I),
 }
+
+PROFILE_CLASSES = ("explicit", "gradient", "div_hv", "multidot", "axpy", "other")
 
 EXPORTS = tuple(_SIGS)
 

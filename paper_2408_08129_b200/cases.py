@@ -185,3 +185,89 @@ def schar_terrain(h0=250.0, a=5.0e3, lam=4.0e3, xc=25.0e3):
         xs = x - xc
         return h0 * np.exp(-(xs / a) ** 2) * np.cos(np.pi * xs / lam) ** 2
     return f
+
+
+# ------------------------------------------------------------------------
+# BASELINE.json configurations (presets for the drop-in)
+# ------------------------------------------------------------------------
+
+@dataclass
+class BaselineCase:
+    name: str
+    mesh: object
+    geometry: object
+    model: object
+    bcs: list
+    sponge: object          # (sigma, background) or None
+    U0: np.ndarray
+    dt: float
+    solve: dict             # ImplicitSolveConfig kwargs
+    description: str = ""
+
+
+def _subset_coords(geometry, elements):
+    nodes = geometry.basis.nodes_1d
+    return geometry._map_points(nodes, nodes, elements)
+
+
+def baseline_case(name, root_scale=1.0, with_state=True):
+    """Build one of the BASELINE configs (cfg1..cfg5) through the host API.
+
+    root_scale < 1 shrinks the horizontal root grid (same recipe, smaller
+    box) -- used for the bounded CPU-baseline samples.
+    """
+    from .boundary import wall_everywhere
+    from .field import project_initial_data
+    from .geometry import build_geometry
+    from .mesh import build_uniform_mesh, refine_region
+    from .physics import FlowModel
+
+    model = FlowModel.dimensional()
+    if name in ("cfg1", "cfg2"):
+        root = (32, 16) if name == "cfg1" else (64, 32)
+        mesh = build_uniform_mesh((20.0e3, 10.0e3), root)
+        if name == "cfg2":
+            mesh = refine_region(mesh, lambda lf: lf.center[1] < 5.0e3, 1)
+        geom = build_geometry(mesh, 2 if name == "cfg1" else 4)
+        U0 = project_initial_data(geom, warm_bubble_state()).data if with_state else None
+        return BaselineCase(name, mesh, geom, model, wall_everywhere(mesh), None, U0, 0.5,
+                            dict(krylov_tol=1e-8 if name == "cfg1" else 1e-10),
+                            "2D warm bubble 20x10 km, walls" + (
+                                ", 64x32 + z<5 km refined, r=4" if name == "cfg2" else
+                                ", 32x16, r=2"))
+    if name == "cfg3":
+        ext = (50.0e3, 21.0e3)
+        nx = max(2, int(round(400 * root_scale)))
+        mesh = build_uniform_mesh((ext[0] * nx / 400, ext[1]), (nx, 168))
+        zc = lambda lo, hi: 0.5 * (lo[:, -1] + hi[:, -1])  # noqa: E731
+        mesh = refine_region(mesh, lambda i, l, o, lo, hi: zc(lo, hi) < 6.0e3, 1, vectorized=True)
+        mesh = refine_region(mesh, lambda i, l, o, lo, hi: zc(lo, hi) < 2.5e3, 1, vectorized=True)
+        hc = HillCaseConfig(domain=mesh.extents, T_ref=280.0)
+        geom = build_geometry(mesh, 4, terrain=schar_terrain())
+        return _terrain_case(name, mesh, geom, model, hc,
+                             SpongeConfig(top_depth=9.0e3, lateral_width=10.0e3), (0,),
+                             with_state, 1.0, "2D Schar terrain, ~220k cells, r=4")
+    if name == "cfg4":
+        n = max(2, int(round(120 * root_scale)))
+        ext = (60.0e3 * n / 120, 60.0e3 * n / 120, 20.0e3)
+        mesh = build_uniform_mesh(ext, (n, n, 20))
+        zc = lambda lo, hi: 0.5 * (lo[:, -1] + hi[:, -1])  # noqa: E731
+        mesh = refine_region(mesh, lambda i, l, o, lo, hi: zc(lo, hi) < 6.0e3, 1, vectorized=True)
+        mesh = refine_region(mesh, lambda i, l, o, lo, hi: zc(lo, hi) < 2.0e3, 1, vectorized=True)
+        hc = HillCaseConfig(domain=ext, x_c=ext[0] / 2, y_c=ext[1] / 2)
+        geom = build_geometry(mesh, 3, terrain=gaussian_hill(xc=ext[0] / 2, yc=ext[1] / 2))
+        return _terrain_case(name, mesh, geom, model, hc, SpongeConfig(), (0, 1),
+                             with_state, 0.5,
+                             "3D Gaussian hill 60x60x20 km, 120x120x20 root, refined z<6 km "
+                             "and z<2 km (3 levels), r=3")
+    raise ConfigurationError(f"unknown baseline case {name!r}")
+
+
+def _terrain_case(name, mesh, geom, model, hc, sponge_cfg, lateral, with_state, dt, desc):
+    from .field import project_initial_data
+    bg = project_initial_data(geom, hydrostatic_initial_state(hc)).data
+    bcs = farfield_bcs(geom, bg)
+    sigma = sponge_sigma(geom, sponge_cfg, mesh.extents, lateral_axes=lateral)
+    geom._memo.pop("nc", None)   # node coordinates are no longer needed
+    U0 = bg.copy() if with_state else None
+    return BaselineCase(name, mesh, geom, model, bcs, (sigma, bg), U0, dt, dict(), desc)

@@ -14,6 +14,7 @@
 #include "dg_launch.cuh"
 #include "dg_vector.cuh"
 #include "dg_comm.h"
+#include "dg_prof.h"
 
 using namespace dg;
 
@@ -129,9 +130,25 @@ OpArgs base_args(dg_ctx* c) {
   return a;
 }
 
+// algorithmic bytes of one element-kernel launch (SURVEY.md §8d / DESIGN.md §3)
+double op_bytes(dg_ctx* c, int opk, const OpArgs& a) {
+  const double n = (double)c->n_el * c->NP * 8.0;
+  const int d = c->dim;
+  if (opk == OP_ADV) {
+    double b = 2.0 * c->V * n;                                // U in, R out
+    if (a.mode == OUT_MINV && a.sigma) b += c->V * n;          // sigma + (V-1) background
+    return b;
+  }
+  if (opk == OP_GRAD) return n * (1 + (a.has_K ? 1 : 0) + d + (a.has_base ? d : 0));
+  return n * (d + 1 + 1 + (a.has_base ? 1 : 0));               // V, h in, y out, base
+}
+
 int launch(dg_ctx* c, int opk, const OpArgs& a) {
+  prof_begin(c->stream);
   cudaError_t e = (c->dim == 2) ? launch_elem_d2(c->N, opk, a, c->stream, &c->last)
                                 : launch_elem_d3(c->N, opk, a, c->stream, &c->last);
+  prof_end(c->stream, opk == OP_ADV ? P_ADV : (opk == OP_GRAD ? P_GRAD : P_DIVHV),
+           op_bytes(c, opk, a), 1);
   if (e != cudaSuccess) return fail(DG_ERR_CUDA, std::string("element kernel: ") + cudaGetErrorString(e));
   return DG_OK;
 }
@@ -817,6 +834,35 @@ int dg_ctx_set_comm(dg_ctx* c, const void* uid, int rank, int nranks, const int3
 }
 
 int dg_halo_exchange(dg_ctx* c, double* field, int ncomp) { return halo(c, field, ncomp); }
+
+long long dg_launch_count(void) { return prof().launches; }
+
+int dg_profile_enable(int on) {
+  Profiler& p = prof();
+  p.on = on != 0;
+  p.used = 0;
+  p.cls.clear();
+  p.bytes.clear();
+  return DG_OK;
+}
+
+int dg_profile_read(double* ms, double* bytes, long long* count) {
+  Profiler& p = prof();
+  for (int k = 0; k < P_NCLS; ++k) {
+    ms[k] = 0.0;
+    bytes[k] = 0.0;
+    count[k] = 0;
+  }
+  if (p.used) CK(cudaEventSynchronize(p.ev[2 * p.used - 1]));
+  for (size_t i = 0; i < p.used; ++i) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, p.ev[2 * i], p.ev[2 * i + 1]));
+    ms[p.cls[i]] += t;
+    bytes[p.cls[i]] += p.bytes[i];
+    count[p.cls[i]] += 1;
+  }
+  return DG_OK;
+}
 
 int dg_split_contiguous(const double* w, long long n, int n_chunks, long long* bounds) {
   // orodg/partition.py:45-67 : bisection on the capacity + greedy packing

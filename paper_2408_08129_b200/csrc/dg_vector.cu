@@ -9,6 +9,7 @@
 // them with a fixed warp tree.  Results are bitwise reproducible run to run.
 #include <cstdint>
 #include "dg_vector.cuh"
+#include "dg_prof.h"
 
 namespace dg {
 
@@ -276,6 +277,35 @@ k_positivity(long long n_el, int np, int d, const double* __restrict__ U, double
   }
 }
 
+// ------------------------------------------------------------ profiling
+Profiler& prof() {
+  static Profiler p;
+  return p;
+}
+
+void prof_begin(cudaStream_t st) {
+  Profiler& p = prof();
+  if (!p.on) return;
+  if (2 * (p.used + 1) > p.ev.size()) {
+    for (int i = 0; i < 256; ++i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      p.ev.push_back(e);
+    }
+  }
+  cudaEventRecord(p.ev[2 * p.used], st);
+}
+
+void prof_end(cudaStream_t st, int cls, double bytes, int nlaunch) {
+  Profiler& p = prof();
+  p.launches += nlaunch;
+  if (!p.on) return;
+  cudaEventRecord(p.ev[2 * p.used + 1], st);
+  p.cls.push_back(cls);
+  p.bytes.push_back(bytes);
+  p.used += 1;
+}
+
 // ------------------------------------------------------------ host wrappers
 static int grid_for(long long n) {
   long long g = (n + RED_THREADS - 1) / RED_THREADS;
@@ -287,80 +317,102 @@ static int grid_for(long long n) {
 cudaError_t lincomb(cudaStream_t st, long long n, int m, const double* c, const double* const* x,
                     double* y) {
   if (n <= 0) return cudaSuccess;
+  prof_begin(st);
   k_lincomb<<<grid_for(n), RED_THREADS, 0, st>>>(
       n, m, c[0], m > 1 ? c[1] : 0.0, m > 2 ? c[2] : 0.0, m > 3 ? c[3] : 0.0, x[0],
       m > 1 ? x[1] : nullptr, m > 2 ? x[2] : nullptr, m > 3 ? x[3] : nullptr, y);
+  prof_end(st, P_OTHER, 8.0 * n * (m + 1), 1);
   return cudaGetLastError();
 }
 
 cudaError_t multidot(cudaStream_t st, long long n, int nv, const double* V, long long vstride,
                      const double* w, double* partials, double* out) {
   // out[0..nv-1] = V_i . w, out[nv] = w . w  (fixed RED_BLOCKS grid)
+  prof_begin(st);
   if (nv <= 8) k_multidot<8><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, nv, V, vstride, w, partials);
   else if (nv <= 16) k_multidot<16><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, nv, V, vstride, w, partials);
   else if (nv <= 32) k_multidot<32><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, nv, V, vstride, w, partials);
   else return cudaErrorInvalidValue;
   const int ncols = nv + 1;
   k_reduce_cols<<<(ncols + 7) / 8, 256, 0, st>>>(partials, RED_BLOCKS, ncols, out);
+  prof_end(st, P_DOT, 8.0 * n * (nv + 1), 2);
   return cudaGetLastError();
 }
 
 cudaError_t axpy_multi(cudaStream_t st, long long n, int nv, const double* V, long long vstride,
                        const double* coefs_dev, double* w, double* partials, double* norm2_out) {
+  prof_begin(st);
   if (nv <= 8) k_axpy_multi<8><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, nv, V, vstride, coefs_dev, w, partials);
   else if (nv <= 16) k_axpy_multi<16><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, nv, V, vstride, coefs_dev, w, partials);
   else if (nv <= 32) k_axpy_multi<32><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, nv, V, vstride, coefs_dev, w, partials);
   else return cudaErrorInvalidValue;
   if (norm2_out) k_reduce_cols<<<1, 32, 0, st>>>(partials, RED_BLOCKS, 1, norm2_out);
+  prof_end(st, P_AXPY, 8.0 * n * (nv + 2), norm2_out ? 2 : 1);
   return cudaGetLastError();
 }
 
 cudaError_t scale(cudaStream_t st, long long n, double a, bool divide, const double* x,
                   double* y) {
+  prof_begin(st);
   k_scale<<<grid_for(n), RED_THREADS, 0, st>>>(n, a, divide ? 1 : 0, x, y);
+  prof_end(st, P_OTHER, 16.0 * n, 1);
   return cudaGetLastError();
 }
 
 cudaError_t frozen(cudaStream_t st, long long n_el, int np, int d, const double* U, double gm1,
                    double kf, double* h, double* K) {
+  prof_begin(st);
   k_frozen<<<grid_for(n_el * np), RED_THREADS, 0, st>>>(n_el, np, d, U, gm1, kf, h, K);
+  prof_end(st, P_OTHER, 8.0 * n_el * np * (d + 4), 1);
   return cudaGetLastError();
 }
 
 cudaError_t state_pressure(cudaStream_t st, long long n_el, int np, int d, const double* U,
                            double gm1, double kf, double* p) {
+  prof_begin(st);
   k_state_pressure<<<grid_for(n_el * np), RED_THREADS, 0, st>>>(n_el, np, d, U, gm1, kf, p);
+  prof_end(st, P_OTHER, 8.0 * n_el * np * (d + 3), 1);
   return cudaGetLastError();
 }
 
 cudaError_t pressure_dp(cudaStream_t st, long long n, const double* x, const double* K, double gm1,
                         double kf, double* p_old, double* partials, double* out2) {
+  prof_begin(st);
   k_pressure_dp<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, x, K, gm1, kf, p_old, partials);
   k_reduce_cols<<<1, 64, 0, st>>>(partials, RED_BLOCKS, 2, out2);
+  prof_end(st, P_OTHER, 32.0 * n, 2);
   return cudaGetLastError();
 }
 
 cudaError_t set_iterate(cudaStream_t st, long long n_el, int np, int V, const double* acc,
                         const double* guess, double* it) {
+  prof_begin(st);
   k_set_iterate<<<grid_for(n_el * V * np), RED_THREADS, 0, st>>>(n_el, np, V, acc, guess, it);
+  prof_end(st, P_OTHER, 16.0 * n_el * V * np, 1);
   return cudaGetLastError();
 }
 
 cudaError_t copy_comps(cudaStream_t st, long long n_el, int np, int nc, const double* src,
                        long long s_estride, double* dst, long long d_estride) {
+  prof_begin(st);
   k_copy_comps<<<grid_for(n_el * nc * np), RED_THREADS, 0, st>>>(n_el, np, nc, src, s_estride,
                                                                   dst, d_estride);
+  prof_end(st, P_OTHER, 16.0 * n_el * nc * np, 1);
   return cudaGetLastError();
 }
 
 cudaError_t positivity(cudaStream_t st, long long n_el, int np, int d, const double* U, double gm1,
                        double kf, double* partials) {
+  prof_begin(st);
   k_positivity<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n_el, np, d, U, gm1, kf, partials);
+  prof_end(st, P_OTHER, 8.0 * n_el * np * (d + 2), 1);
   return cudaGetLastError();
 }
 
 cudaError_t reduce_cols(cudaStream_t st, const double* partials, int nblocks, int ncols, double* out) {
+  prof_begin(st);
   k_reduce_cols<<<(ncols + 7) / 8, 256, 0, st>>>(partials, nblocks, ncols, out);
+  prof_end(st, P_OTHER, 8.0 * nblocks * ncols, 1);
   return cudaGetLastError();
 }
 

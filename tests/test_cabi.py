@@ -18,7 +18,7 @@ HDR = os.path.join(ROOT, "include", "dg.h")
 
 def _declared():
     txt = open(HDR).read()
-    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(dg_\w+)\(", txt, re.M)))
+    return sorted(set(re.findall(r"^(?:int|long long|const char\*)\s+(dg_\w+)\(", txt, re.M)))
 
 
 @pytest.fixture(scope="module")
