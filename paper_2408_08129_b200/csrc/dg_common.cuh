@@ -61,6 +61,8 @@ struct MeshDev {
   const double* ff_p;       // (n_bface, nqf)
   const double* ff_h;       // (n_bface, nqf)
   int n_el;                 // owned elements processed by the kernels
+  const int* coarse_list;   // owned elements with >= 1 coarse hanging face
+  int n_coarse;
 };
 
 // Strided component view: comp c of element e at p + e*estride + c*cstride

@@ -1,0 +1,873 @@
+// Fused element-centric DG operator kernel, v2 (fp64, sm_100a).
+//
+// Evaluates one weak-form operator of the reference engine
+// (orodg/dgops.py:87-230) for EPB elements per CTA, owner-computes, no
+// atomics, and fuses the factorised mass inverse (geometry.py:240-251,
+// 372-396) and the operator's affine epilogue:
+//
+//   1. nodal input -> shared memory (KIN comps per element);
+//   2. nodes -> Gauss points: d pencil passes of B;
+//   3. volume: flux + contravariant metric (rebuilt in registers from the
+//      compact element/column tables, geometry.py:204-238) per point, then
+//      per reference direction bx one pencil pass of Dhat^T along bx,
+//      accumulated in Z = B^-T dual (Gauss-point coordinates);
+//   4. faces, all 2d at once: neighbour nodal face values gathered,
+//      tangential pencil passes (B, or the mortar halves for a fine leaf
+//      seeing its coarse parent), own trace = lift[side] . Gauss column,
+//      numerical flux with the minus-side (conforming) / fine-side (hanging)
+//      face metric exactly as the reference batches, then the rank-1 lift
+//      Z += lift[side] (x) flux*ws;
+//      the coarse side of hanging faces (2^(d-1) subfaces) is added by the
+//      small coarse_kernel over the compact list of coarse elements;
+//   5. epilogue: dual = B^T (x) Z, or nodal = B^-1 (x) diag(1/(w detJ)) Z
+//      fused with base + coef * nodal (explicit: sources and sponge).
+//
+// Pencil passes take the 1D matrices straight from the kernel-parameter
+// constant bank with compile-time indices (DFMA with a constant operand:
+// no shared-memory traffic for the matrices); every axis is a template
+// parameter so all index arithmetic folds at compile time.
+#pragma once
+#include "dg_operator.cuh"
+
+namespace dg {
+
+template <int D, int N, int OPK>
+struct Layout {
+  static constexpr int NP = ipow(N, D);
+  static constexpr int NQF = ipow(N, D - 1);
+  static constexpr int NF = 2 * D;
+  static constexpr int S = 1 << (D - 1);
+  static constexpr int KIN = OpDims<D, OPK>::KIN;
+  static constexpr int KOUT = OpDims<D, OPK>::KOUT;
+  static constexpr int KT = KIN > KOUT ? KIN : KOUT;
+  static constexpr int OFF_A = 0;
+  static constexpr int OFF_Q = OFF_A + KIN * NP;
+  static constexpr int OFF_Z = OFF_Q + KIN * NP;
+  static constexpr int OFF_T = OFF_Z + KOUT * NP;
+  static constexpr int OFF_G = OFF_T + KT * NP;
+  static constexpr int OFF_H = OFF_G + NF * KIN * NQF;
+  static constexpr int OFF_L = OFF_H + NF * KIN * NQF;
+  static constexpr int ELEM = OFF_L + NF * KOUT * NQF;
+  static constexpr int TABD = (int)(sizeof(Tab<N>) / sizeof(double));
+  static constexpr int EPB_T = (128 / NP) > 1 ? (128 / NP) : 1;
+  static constexpr int EPB_S = (12288 - TABD - 64) / ELEM > 1 ? (12288 - TABD - 64) / ELEM : 1;
+  static constexpr int EPB = EPB_T < EPB_S ? EPB_T : EPB_S;
+  static constexpr int THREADS = ((EPB * NP + 31) / 32) * 32;
+  static constexpr int SLOTS = (THREADS + NP - 1) / NP;
+  static constexpr size_t SMEM = (size_t)(TABD + 64 + SLOTS * ELEM) * sizeof(double);
+  static constexpr int REGCAP = (OPK == OP_ADV) ? 128 : 96;
+  static constexpr int MINB0 = 65536 / (THREADS * REGCAP);
+  static constexpr int MINB = MINB0 < 1 ? 1 : (MINB0 > 8 ? 8 : MINB0);
+  // coarse fix-up kernel (one CTA per coarse element)
+  static constexpr int CTHREADS = ((NP + 31) / 32) * 32;
+  static constexpr int C_A = 0;
+  static constexpr int C_FW = C_A + KIN * NP;
+  static constexpr int C_Z = C_FW + NF * S * KOUT * NQF;
+  static constexpr int C_T = C_Z + KOUT * NP;
+  static constexpr int CELEM = C_T + KOUT * NP;
+  static constexpr size_t CSMEM = (size_t)(TABD + 64 + CELEM) * sizeof(double);
+};
+
+// ---------------------------------------------------------------- passes
+// dst (op)= M along axis AX of a DIM-dim N^DIM tensor, for KC comps of nv
+// elements.  M from the parameter constant bank (compile-time indices).
+// MODE: 0 dst = M src, 1 dst = -M src, 2 dst -= M src.
+template <int DIM, int N, int AX, bool TRANS, int MODE, int KC, int ELEM, int CS>
+__device__ __forceinline__ void vpass(const double (&M)[N][N], double* base, int soff, int doff,
+                                      int nv) {
+  constexpr int NPEN = ipow(N, DIM - 1);
+  constexpr int ST = ipow(N, DIM - 1 - AX);
+  const int items = nv * KC * NPEN;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int p = it % NPEN;
+    const int r = it / NPEN;
+    const int c = r % KC;
+    const int e = r / KC;
+    const int b = (p / ST) * (ST * N) + (p % ST);
+    const double* s = base + e * ELEM + soff + c * CS + b;
+    double* d = base + e * ELEM + doff + c * CS + b;
+    double v[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) v[j] = s[j * ST];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) acc = fma(TRANS ? M[j][i] : M[i][j], v[j], acc);
+      if (MODE == 0) d[i * ST] = acc;
+      else if (MODE == 1) d[i * ST] = -acc;
+      else d[i * ST] -= acc;
+    }
+  }
+}
+
+// nodes -> Gauss points (all axes), src (A) preserved; result at Q
+template <int D, int N, int KC, int ELEM, int NP>
+__device__ __forceinline__ void interp_all(const double (&B)[N][N], double* base, int a_off,
+                                           int q_off, int t_off, int nv) {
+  if constexpr (D == 2) {
+    vpass<2, N, 1, false, 0, KC, ELEM, NP>(B, base, a_off, t_off, nv);
+    __syncthreads();
+    vpass<2, N, 0, false, 0, KC, ELEM, NP>(B, base, t_off, q_off, nv);
+  } else {
+    vpass<3, N, 2, false, 0, KC, ELEM, NP>(B, base, a_off, q_off, nv);
+    __syncthreads();
+    vpass<3, N, 1, false, 0, KC, ELEM, NP>(B, base, q_off, t_off, nv);
+    __syncthreads();
+    vpass<3, N, 0, false, 0, KC, ELEM, NP>(B, base, t_off, q_off, nv);
+  }
+}
+
+// tangential pass on the gathered face tensors: matrix per face from the
+// smem tables (B, or half[bit] for a fine leaf's view of its coarse parent)
+template <int D, int N, int TAX, int KC, int ELEM, int NF>
+__device__ __forceinline__ void fpass(const Tab<N>& TS, const uint8_t* __restrict__ kind,
+                                      long long e0, double* base, int soff, int doff, int nv) {
+  constexpr int NQF = ipow(N, D - 1);
+  constexpr int NPEN = NQF / N;
+  constexpr int ST = ipow(N, D - 2 - TAX);
+  const int items = nv * NF * KC * NPEN;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int p = it % NPEN;
+    int r = it / NPEN;
+    const int c = r % KC;
+    r /= KC;
+    const int f = r % NF;
+    const int e = r / NF;
+    const uint8_t kraw = kind[(e0 + e) * NF + f];
+    const int kd = kraw & 15;
+    if (kd != KIND_CONF && kd != KIND_FINE) continue;
+    const double* M = (kd == KIND_FINE) ? &TS.half[((kraw >> 4) >> TAX) & 1][0][0] : &TS.B[0][0];
+    const int b = (p / ST) * (ST * N) + (p % ST);
+    const double* s = base + e * ELEM + soff + (f * KC + c) * NQF + b;
+    double* d = base + e * ELEM + doff + (f * KC + c) * NQF + b;
+    double v[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) v[j] = s[j * ST];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) acc = fma(M[i * N + j], v[j], acc);
+      d[i * ST] = acc;
+    }
+  }
+}
+
+// Face metric of the owner's (AX, oside) face at face Gauss point qf, the
+// geometry.py:305-357 formulas specialised per axis: vertical faces have an
+// exact +-e_AX normal (the reference's ntilde/|ntilde| is exactly that), as
+// do horizontal faces without terrain, so only terrain z-faces pay the
+// sqrt and division.
+template <int D, int N, int AX>
+__device__ __forceinline__ void face_metric_ax(const GeoConst& gc, const double* __restrict__ col,
+                                               const ElemGeo<D>& g, int oside, bool outward,
+                                               int qf, const Tab<N>& T, double n[D],
+                                               double& ws) {
+  constexpr int HD = D - 1;
+  constexpr int NQH = ipow(N, HD);
+  const double fw = (D == 2) ? T.qw[qf] : T.qw[qf / N] * T.qw[qf % N];
+  const double sgn = (outward && oside == 0) ? -1.0 : 1.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) n[a] = 0.0;
+  if constexpr (AX < D - 1) {
+    const int qo = (D == 2) ? 0 : qf / N;
+    double he = 0.0;
+    if (gc.terrain) {
+      constexpr int NE = ipow(N, HD - 1);
+      he = col[(long long)g.col * gc.col_stride + NQH * (1 + HD) + (AX * 2 + oside) * NE + qo];
+    }
+    const double zzv = g.s[D - 1] * (1.0 - he / gc.z_top);
+    const double mag = (D == 2) ? zzv : g.s[1 - AX] * zzv;
+    n[AX] = sgn;
+    ws = fw * fabs(mag);
+  } else {
+    const double top = (D == 2) ? g.s[0] : g.s[0] * g.s[1];
+    if (!gc.terrain) {
+      n[D - 1] = sgn;
+      ws = fw * top;
+      return;
+    }
+    const double* c = col + (long long)g.col * gc.col_stride;
+    const double decay = 1.0 - (g.lo[D - 1] + g.s[D - 1] * (double)oside) / gc.z_top;
+    double nt[D];
+    if constexpr (D == 2) {
+      nt[0] = -c[NQH + qf] * g.s[0] * decay;
+    } else {
+      nt[0] = -g.s[1] * c[NQH + qf] * g.s[0] * decay;
+      nt[1] = -g.s[0] * c[2 * NQH + qf] * g.s[1] * decay;
+    }
+    nt[D - 1] = top;
+    double m2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) m2 += nt[a] * nt[a];
+    const double mag = sqrt(m2);
+#pragma unroll
+    for (int a = 0; a < D; ++a) n[a] = sgn * (nt[a] / mag);
+    ws = fw * mag;
+  }
+}
+
+// -------------------------------------------------------------- physics
+template <int D, int OPK, int KIN, int KOUT>
+__device__ __forceinline__ void num_flux(const double* TL, const double* TR, const double* n,
+                                         double kf, double* fl) {
+  if constexpr (OPK == OP_ADV) {
+    // Rusanov with the flow speed only (orodg/dgops.py:256-283)
+    double mnL = 0.0, mnR = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      mnL += TL[1 + a] * n[a];
+      mnR += TR[1 + a] * n[a];
+    }
+    const double rL = TL[0], rR = TR[0];
+    const double uL = mnL / rL, uR = mnR / rR;
+    const double lam = fmax(fabs(uL), fabs(uR));
+    double kL = 0.0, kR = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const double vl = TL[1 + a] / rL, vr = TR[1 + a] / rR;
+      kL += vl * vl;
+      kR += vr * vr;
+    }
+    fl[0] = 0.5 * (mnL + mnR);
+#pragma unroll
+    for (int a = 0; a < D; ++a) fl[1 + a] = 0.5 * (TL[1 + a] * uL + TR[1 + a] * uR);
+    fl[D + 1] = 0.25 * kf * (rL * kL * uL + rR * kR * uR);
+#pragma unroll
+    for (int c = 0; c < KOUT; ++c) fl[c] -= 0.5 * lam * (TR[c] - TL[c]);
+  } else if constexpr (OPK == OP_GRAD) {
+    // centred pressure (dgops.py:343-348)
+    const double ph = 0.5 * (TL[0] + TR[0]);
+#pragma unroll
+    for (int a = 0; a < D; ++a) fl[a] = ph * n[a];
+  } else {
+    // average of products (dgops.py:452-460)
+    double vL = 0.0, vR = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      vL += TL[a] * n[a];
+      vR += TR[a] * n[a];
+    }
+    fl[0] = 0.5 * (TL[D] * vL + TR[D] * vR);
+  }
+}
+
+// boundary ghost state (boundary.py:17-84, dgops.py:462-474)
+template <int D, int N, int OPK, int KIN>
+__device__ __forceinline__ void ghost(const KParams<N>& P, int kd, long long row, int qf,
+                                      const double* TO, const double* n, double* TN) {
+  constexpr int NQF = ipow(N, D - 1);
+  const MeshDev& mesh = P.mesh;
+  if constexpr (OPK == OP_ADV) {
+    if (kd == KIND_WALL) {
+      double mn = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) mn += TO[1 + a] * n[a];
+#pragma unroll
+      for (int c = 0; c < KIN; ++c) TN[c] = TO[c];
+#pragma unroll
+      for (int a = 0; a < D; ++a) TN[1 + a] = TO[1 + a] - 2.0 * mn * n[a];
+    } else {
+#pragma unroll
+      for (int c = 0; c < KIN; ++c) TN[c] = mesh.ff_U[(row * KIN + c) * NQF + qf];
+    }
+  } else if constexpr (OPK == OP_GRAD) {
+    TN[0] = (kd == KIND_WALL) ? TO[0] : (P.homogeneous ? 0.0 : mesh.ff_p[row * NQF + qf]);
+  } else {
+    if (kd == KIND_WALL) {
+      double vn = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) vn += TO[a] * n[a];
+#pragma unroll
+      for (int a = 0; a < D; ++a) TN[a] = TO[a] - 2.0 * vn * n[a];
+      TN[D] = TO[D];
+    } else {
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+        TN[a] = P.homogeneous ? 0.0 : mesh.ff_U[(row * (D + 2) + 1 + a) * NQF + qf];
+      TN[D] = mesh.ff_h[row * NQF + qf];
+    }
+  }
+}
+
+template <int D, int N, int OPK>
+__device__ __forceinline__ double load_input(const KParams<N>& P, long long ee, int c, int i) {
+  if constexpr (OPK == OP_GRAD) {
+    const double x = P.in.p ? P.in(ee, 0, i) : 0.0;
+    return P.has_K ? P.alpha * (x - P.beta * P.inK(ee, 0, i)) : P.alpha * x;
+  } else if constexpr (OPK == OP_DIVHV) {
+    return c < D ? P.in(ee, c, i) : P.inH(ee, 0, i);
+  } else {
+    return P.in(ee, c, i);
+  }
+}
+
+// Gauss-point metric: det J (z-independent) and the adjugate rows
+template <int D, int N>
+__device__ __forceinline__ void point_metric(const KParams<N>& P, const ElemGeo<D>& g, int q,
+                                             double& det, double ctrv[D][D]) {
+  constexpr int HD = D - 1;
+  constexpr int NQH = ipow(N, HD);
+  const int qh = q / N;
+  const int qz = q % N;
+#pragma unroll
+  for (int b = 0; b < D; ++b)
+#pragma unroll
+    for (int a = 0; a < D; ++a) ctrv[b][a] = 0.0;
+  if (!P.gc.terrain) {
+    // flat: zz = s_z exactly, diagonal adjugate (geometry.py:204-231 with h = 0)
+    if constexpr (D == 2) {
+      det = g.s[0] * g.s[1];
+      ctrv[0][0] = g.s[1];
+      ctrv[1][1] = g.s[0];
+    } else {
+      det = g.s[0] * g.s[1] * g.s[2];
+      ctrv[0][0] = g.s[1] * g.s[2];
+      ctrv[1][1] = g.s[0] * g.s[2];
+      ctrv[2][2] = g.s[0] * g.s[1];
+    }
+    return;
+  }
+  double hq = 0.0, dhq[2] = {0.0, 0.0};
+  {
+    const double* c = P.mesh.col + (long long)g.col * P.gc.col_stride;
+    hq = c[qh];
+#pragma unroll
+    for (int a = 0; a < HD; ++a) dhq[a] = c[NQH + a * NQH + qh];
+  }
+  const double zt = P.gc.z_top;
+  const double zz = g.s[D - 1] * (1.0 - hq / zt);
+  det = 1.0;
+#pragma unroll
+  for (int a = 0; a < HD; ++a) det = det * g.s[a];
+  det = det * zz;
+  const double decay = 1.0 - (g.lo[D - 1] + g.s[D - 1] * P.tab.qx[qz]) / zt;
+  double zg[2];
+#pragma unroll
+  for (int a = 0; a < HD; ++a) zg[a] = dhq[a] * g.s[a] * decay;
+#pragma unroll
+  for (int b = 0; b < D; ++b)
+#pragma unroll
+    for (int a = 0; a < D; ++a) ctrv[b][a] = 0.0;
+  if constexpr (D == 2) {
+    ctrv[0][0] = zz;
+    ctrv[1][0] = -zg[0];
+    ctrv[1][1] = g.s[0];
+  } else {
+    ctrv[0][0] = g.s[1] * zz;
+    ctrv[1][1] = g.s[0] * zz;
+    ctrv[2][0] = -g.s[1] * zg[0];
+    ctrv[2][1] = -g.s[0] * zg[1];
+    ctrv[2][2] = g.s[0] * g.s[1];
+  }
+}
+
+template <int D, int N>
+__device__ __forceinline__ double point_weight(const Tab<N>& T, int q) {
+  double w = 1.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) w *= T.qw[digit<D, N>(q, a)];
+  return w;
+}
+
+// --------------------------------------------------------- face flux phase
+// items (e, side, qf) of axis AX; writes L[f][k][qf] = +-flux*ws (0 for coarse)
+template <int D, int N, int OPK, int AX>
+__device__ __forceinline__ void face_flux_axis(const KParams<N>& P, const Tab<N>& TS, double* base,
+                                               long long e0, int nv, int nb_off) {
+  using L = Layout<D, N, OPK>;
+  constexpr int NQF = L::NQF, NF = L::NF, KIN = L::KIN, KOUT = L::KOUT, NP = L::NP;
+  constexpr int T0 = (AX == 0) ? 1 : 0;
+  constexpr int T1 = (D == 3) ? ((AX == 2) ? 1 : 2) : -1;
+  constexpr int SA = ipow(N, D - 1 - AX);
+  constexpr int S0 = ipow(N, D - 1 - T0);
+  constexpr int S1 = (D == 3) ? ipow(N, D - 1 - (T1 < 0 ? 0 : T1)) : 0;
+  const MeshDev& mesh = P.mesh;
+  const int items = nv * 2 * NQF;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int qf = it % NQF;
+    const int side = (it / NQF) & 1;
+    const int e = it / (2 * NQF);
+    const int f = 2 * AX + side;
+    const long long ge = e0 + e;
+    const uint8_t kraw = mesh.kind[ge * NF + f];
+    const int kd = kraw & 15;
+    double* Lf = base + e * L::ELEM + L::OFF_L + f * KOUT * NQF;
+    if (kd == KIND_COARSE) {
+#pragma unroll
+      for (int k = 0; k < KOUT; ++k) Lf[k * NQF + qf] = 0.0;
+      continue;
+    }
+    // own trace: nodal value at the face = lift[side] . Gauss column
+    const int qt0 = (D == 2) ? qf : qf / N;
+    const int qt1 = (D == 2) ? 0 : qf % N;
+    const int qv = qt0 * S0 + qt1 * S1;
+    const double* Qe = base + e * L::ELEM + L::OFF_Q;
+    double TO[KIN], TN[KIN];
+#pragma unroll
+    for (int c = 0; c < KIN; ++c) {
+      double acc = 0.0;
+#pragma unroll
+      for (int p = 0; p < N; ++p) acc = fma(TS.lift[side][p], Qe[c * NP + qv + p * SA], acc);
+      TO[c] = acc;
+    }
+    const long long nb = mesh.nbr[ge * NF + f];
+    ElemGeo<D> og = elem_geo<D>(mesh.elem, P.gc, (kd == KIND_CONF && side == 0) ? nb : ge);
+    const int oside = (kd == KIND_CONF && side == 0) ? 1 : side;
+    const bool outward = (kd == KIND_WALL || kd == KIND_FARFIELD);
+    double n[D], ws;
+    face_metric_ax<D, N, AX>(P.gc, mesh.col, og, oside, outward, qf, TS, n, ws);
+    if (outward) {
+      ghost<D, N, OPK, KIN>(P, kd, nb, qf, TO, n, TN);
+    } else {
+      const double* tn = base + e * L::ELEM + nb_off + f * KIN * NQF;
+#pragma unroll
+      for (int c = 0; c < KIN; ++c) TN[c] = tn[c * NQF + qf];
+    }
+    const bool minus = outward || side == 1;
+    double TLv[KIN], TRv[KIN];
+#pragma unroll
+    for (int c = 0; c < KIN; ++c) {
+      TLv[c] = minus ? TO[c] : TN[c];
+      TRv[c] = minus ? TN[c] : TO[c];
+    }
+    double fl[KOUT];
+    num_flux<D, OPK, KIN, KOUT>(TLv, TRv, n, P.model.kinetic_factor, fl);
+    const double sg = minus ? ws : -ws;
+#pragma unroll
+    for (int k = 0; k < KOUT; ++k) Lf[k * NQF + qf] = fl[k] * sg;
+  }
+}
+
+// ------------------------------------------------------------- the kernel
+template <int D, int N, int OPK>
+__global__ void __launch_bounds__(Layout<D, N, OPK>::THREADS, Layout<D, N, OPK>::MINB)
+elem_kernel(const __grid_constant__ KParams<N> P) {
+  using L = Layout<D, N, OPK>;
+  constexpr int NP = L::NP, NQF = L::NQF, NF = L::NF, KIN = L::KIN, KOUT = L::KOUT;
+  constexpr int E = L::ELEM;
+  extern __shared__ double smem[];
+  {
+    const double* src = reinterpret_cast<const double*>(&P.tab);
+    for (int i = threadIdx.x; i < L::TABD; i += blockDim.x) smem[i] = src[i];
+  }
+  const Tab<N>& TS = *reinterpret_cast<const Tab<N>*>(smem);
+  const Tab<N>& TC = P.tab;
+  double* red = smem + L::TABD;
+  double* base = red + 64;
+  const MeshDev& mesh = P.mesh;
+  const int tid = threadIdx.x;
+  const long long e0 = (long long)blockIdx.x * L::EPB;
+  const int nv = (int)min((long long)L::EPB, (long long)mesh.n_el - e0);
+  const int el = tid / NP;
+  const int q = tid - el * NP;
+  const bool act = el < nv;
+  double* A = base + el * E + L::OFF_A;
+  double* Q = base + el * E + L::OFF_Q;
+  double* Z = base + el * E + L::OFF_Z;
+  double* Tm = base + el * E + L::OFF_T;
+
+  // 1. nodal input
+  if (act) {
+#pragma unroll
+    for (int c = 0; c < KIN; ++c) A[c * NP + q] = load_input<D, N, OPK>(P, e0 + el, c, q);
+  }
+  // 4a (early). gather neighbour nodal face values: overlaps with the volume work
+  {
+    const int items = nv * NF * KIN * NQF;
+    for (int it = tid; it < items; it += blockDim.x) {
+      const int j = it % NQF;
+      int r = it / NQF;
+      const int c = r % KIN;
+      r /= KIN;
+      const int f = r % NF;
+      const int e = r / NF;
+      const long long ge = e0 + e;
+      const int kd = mesh.kind[ge * NF + f] & 15;
+      if (kd != KIND_CONF && kd != KIND_FINE) continue;
+      const long long src = mesh.nbr[ge * NF + f];
+      const int axis = f >> 1, side = f & 1;
+      base[e * E + L::OFF_G + (f * KIN + c) * NQF + j] =
+          load_input<D, N, OPK>(P, src, c, face_to_vol<D, N>(axis, 1 - side, j));
+    }
+  }
+  __syncthreads();
+
+  // 2. nodes -> Gauss points
+  interp_all<D, N, KIN, E, NP>(TC.B, base, L::OFF_A, L::OFF_Q, L::OFF_T, nv);
+  // tangential passes of the gathered faces (independent buffers: no sync)
+  if constexpr (D == 2) {
+    fpass<D, N, 0, KIN, E, NF>(TS, mesh.kind, e0, base, L::OFF_G, L::OFF_H, nv);
+  } else {
+    fpass<D, N, 0, KIN, E, NF>(TS, mesh.kind, e0, base, L::OFF_G, L::OFF_H, nv);
+  }
+  __syncthreads();
+  if constexpr (D == 3) fpass<D, N, 1, KIN, E, NF>(TS, mesh.kind, e0, base, L::OFF_H, L::OFF_G, nv);
+  constexpr int NB_OFF = (D == 2) ? L::OFF_H : L::OFF_G;  // neighbour traces at Gauss points
+
+  // 3. metric + volume flux at this Gauss point
+  const long long es = act ? e0 + el : e0;
+  const ElemGeo<D> g = elem_geo<D>(mesh.elem, P.gc, es);
+  double det, ctrv[D][D];
+  point_metric<D, N>(P, g, q, det, ctrv);
+  const double wq = point_weight<D, N>(TC, q);
+  double F[D][KOUT];
+  if constexpr (OPK == OP_ADV) {
+    const double rho = Q[q];
+    double u[D];
+    double k = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      u[a] = Q[(1 + a) * NP + q] / rho;
+      k += u[a] * u[a];
+    }
+    k *= 0.5;
+    const double kf = P.model.kinetic_factor;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      F[a][0] = Q[(1 + a) * NP + q];
+#pragma unroll
+      for (int b = 0; b < D; ++b) F[a][1 + b] = Q[(1 + b) * NP + q] * u[a];
+      F[a][D + 1] = kf * rho * k * u[a];
+    }
+  } else if constexpr (OPK == OP_DIVHV) {
+    const double h = Q[D * NP + q];
+#pragma unroll
+    for (int a = 0; a < D; ++a) F[a][0] = h * Q[a * NP + q];
+  } else {
+    const double p = Q[q];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int k = 0; k < KOUT; ++k) F[a][k] = (a == k) ? p : 0.0;
+  }
+  // Z = -sum_bx Dhat^T_bx (w sum_a ctrv[bx][a] F_a)
+  const bool flat = !P.gc.terrain;
+  if constexpr (OPK == OP_GRAD) {
+    // flux tensor p I: with a diagonal adjugate only component BX moves in
+    // direction BX, so the flat path runs one pass per direction
+    if (flat) {
+#pragma unroll
+      for (int k = 0; k < KOUT; ++k) Z[k * NP + q] = 0.0;
+    }
+  }
+  auto vol_dir = [&](auto bx_c) {
+    constexpr int BX = decltype(bx_c)::value;
+    if (OPK == OP_GRAD && flat) {
+      Tm[q] = F[BX][BX] * ctrv[BX][BX] * wq;
+      __syncthreads();
+      vpass<D, N, BX, true, 2, 1, E, NP>(TC.Dhat, base, L::OFF_T, L::OFF_Z + BX * NP, nv);
+      __syncthreads();
+      return;
+    }
+#pragma unroll
+    for (int k = 0; k < KOUT; ++k) {
+      double acc;
+      if (flat) {
+        acc = F[BX][k] * ctrv[BX][BX];
+      } else {
+        acc = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) acc += F[a][k] * ctrv[BX][a];
+      }
+      Tm[k * NP + q] = acc * wq;
+    }
+    __syncthreads();
+    vpass<D, N, BX, true, (BX == 0 ? 1 : 2), KOUT, E, NP>(TC.Dhat, base, L::OFF_T, L::OFF_Z, nv);
+    __syncthreads();
+  };
+  vol_dir(std::integral_constant<int, 0>{});
+  vol_dir(std::integral_constant<int, 1>{});
+  if constexpr (D == 3) vol_dir(std::integral_constant<int, 2>{});
+
+  // 4b. numerical fluxes on all faces (disjoint outputs per axis: no sync)
+  face_flux_axis<D, N, OPK, 0>(P, TS, base, e0, nv, NB_OFF);
+  face_flux_axis<D, N, OPK, 1>(P, TS, base, e0, nv, NB_OFF);
+  if constexpr (D == 3) face_flux_axis<D, N, OPK, 2>(P, TS, base, e0, nv, NB_OFF);
+  __syncthreads();
+  // 4c. lift: Z[k][q] += lift[side][q_a] * L_{a,side}[k][q_t]
+  if (act) {
+    const double* Lb = base + el * E + L::OFF_L;
+    int qi[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) qi[a] = digit<D, N>(q, a);
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      int qf;
+      if constexpr (D == 2) qf = qi[1 - a];
+      else qf = (a == 0) ? qi[1] * N + qi[2] : (a == 1 ? qi[0] * N + qi[2] : qi[0] * N + qi[1]);
+      const double l0 = TS.lift[0][qi[a]], l1 = TS.lift[1][qi[a]];
+#pragma unroll
+      for (int k = 0; k < KOUT; ++k)
+        Z[k * NP + q] += l0 * Lb[((2 * a) * KOUT + k) * NQF + qf] +
+                         l1 * Lb[((2 * a + 1) * KOUT + k) * NQF + qf];
+    }
+  }
+
+  // 5. epilogue
+  if constexpr (OPK == OP_ADV) {
+    if (P.mass_partial != nullptr) {
+      double v = act ? Z[q] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if ((tid & 31) == 0) red[tid >> 5] = v;
+    }
+  }
+  if (P.mode == OUT_MINV) {
+    const double inv = 1.0 / (wq * det);
+#pragma unroll
+    for (int k = 0; k < KOUT; ++k) Z[k * NP + q] *= inv;
+  }
+  __syncthreads();
+  if constexpr (OPK == OP_ADV) {
+    if (P.mass_partial != nullptr && tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+      P.mass_partial[blockIdx.x] = s;
+    }
+  }
+  const double* res;
+  if (P.mode == OUT_MINV) {
+    if constexpr (D == 2) {
+      vpass<2, N, 1, false, 0, KOUT, E, NP>(TC.Binv, base, L::OFF_Z, L::OFF_T, nv);
+      __syncthreads();
+      vpass<2, N, 0, false, 0, KOUT, E, NP>(TC.Binv, base, L::OFF_T, L::OFF_Z, nv);
+      res = Z;
+    } else {
+      vpass<3, N, 2, false, 0, KOUT, E, NP>(TC.Binv, base, L::OFF_Z, L::OFF_T, nv);
+      __syncthreads();
+      vpass<3, N, 1, false, 0, KOUT, E, NP>(TC.Binv, base, L::OFF_T, L::OFF_Z, nv);
+      __syncthreads();
+      vpass<3, N, 0, false, 0, KOUT, E, NP>(TC.Binv, base, L::OFF_Z, L::OFF_T, nv);
+      res = Tm;
+    }
+  } else {
+    if constexpr (D == 2) {
+      vpass<2, N, 1, true, 0, KOUT, E, NP>(TC.B, base, L::OFF_Z, L::OFF_T, nv);
+      __syncthreads();
+      vpass<2, N, 0, true, 0, KOUT, E, NP>(TC.B, base, L::OFF_T, L::OFF_Z, nv);
+      res = Z;
+    } else {
+      vpass<3, N, 2, true, 0, KOUT, E, NP>(TC.B, base, L::OFF_Z, L::OFF_T, nv);
+      __syncthreads();
+      vpass<3, N, 1, true, 0, KOUT, E, NP>(TC.B, base, L::OFF_T, L::OFF_Z, nv);
+      __syncthreads();
+      vpass<3, N, 0, true, 0, KOUT, E, NP>(TC.B, base, L::OFF_Z, L::OFF_T, nv);
+      res = Tm;
+    }
+  }
+  __syncthreads();
+  if (!act) return;
+  const long long e = e0 + el;
+  double* out = P.out.p + e * P.out.estride + q;
+  if (P.mode == OUT_DUAL) {
+#pragma unroll
+    for (int k = 0; k < KOUT; ++k) out[k * P.out.cstride] = res[k * NP + q];
+    return;
+  }
+  if constexpr (OPK == OP_ADV) {
+    // R = -Minv dual + gravity source - sigma (U - U_bg)   (imex.py:144-159)
+    const double rho = A[q];
+    const Model& md = P.model;
+    double R[KOUT];
+#pragma unroll
+    for (int k = 0; k < KOUT; ++k) R[k] = -res[k * NP + q];
+    R[D] += -md.gravity * rho;
+    R[D + 1] += -md.kinetic_factor * md.gravity * rho * (A[D * NP + q] / rho);
+    if (P.sigma != nullptr) {
+      const double sg = P.sigma[e * NP + q];
+#pragma unroll
+      for (int k = 1; k < KOUT; ++k) R[k] -= sg * (A[k * NP + q] - P.bg(e, k, q));
+    }
+#pragma unroll
+    for (int k = 0; k < KOUT; ++k) out[k * P.out.cstride] = R[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < KOUT; ++k) {
+      const double r = __dmul_rn(P.coef, res[k * NP + q]);
+      out[k * P.out.cstride] = P.has_base ? __dadd_rn(P.base(e, k, q), r) : r;
+    }
+  }
+}
+
+// ---------------------------------------------------- coarse-side fix-up
+// One CTA per element owning >= 1 coarse hanging face: the coarse side's
+// subface fluxes (fine-side metric, mortar traces, dgops.py:159-206) lifted
+// through halfq^T, then the same epilogue as the main kernel, ADDED to the
+// main kernel's output (linear in the lift).
+template <int D, int N, int OPK>
+__global__ void __launch_bounds__(Layout<D, N, OPK>::CTHREADS)
+coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clist, int ncoarse,
+              double* mass_partial) {
+  using L = Layout<D, N, OPK>;
+  constexpr int NP = L::NP, NQF = L::NQF, NF = L::NF, S = L::S, KIN = L::KIN, KOUT = L::KOUT;
+  extern __shared__ double smem[];
+  {
+    const double* src = reinterpret_cast<const double*>(&P.tab);
+    for (int i = threadIdx.x; i < L::TABD; i += blockDim.x) smem[i] = src[i];
+  }
+  const Tab<N>& T = *reinterpret_cast<const Tab<N>*>(smem);
+  double* red = smem + L::TABD;
+  double* A = red + 64 + L::C_A;
+  double* FW = red + 64 + L::C_FW;
+  double* Z = red + 64 + L::C_Z;
+  double* Tm = red + 64 + L::C_T;
+  const MeshDev& mesh = P.mesh;
+  const long long e = clist[blockIdx.x];
+  const int q = threadIdx.x;
+  const bool act = q < NP;
+  if (act)
+    for (int c = 0; c < KIN; ++c) A[c * NP + q] = load_input<D, N, OPK>(P, e, c, q);
+  __syncthreads();
+  // subface fluxes of every coarse face
+  for (int it = threadIdx.x; it < NF * S * NQF; it += blockDim.x) {
+    const int qf = it % NQF;
+    const int sub = (it / NQF) % S;
+    const int f = it / (NQF * S);
+    const int kd = mesh.kind[e * NF + f] & 15;
+    if (kd != KIND_COARSE) continue;
+    const int axis = f >> 1, side = f & 1;
+    const long long child = mesh.hang_children[(long long)mesh.nbr[e * NF + f] * S + sub];
+    const int qt0 = (D == 2) ? qf : qf / N;
+    const int qt1 = (D == 2) ? 0 : qf % N;
+    const int b0 = sub & 1, b1 = (sub >> 1) & 1;
+    double TO[KIN], TN[KIN];
+#pragma unroll
+    for (int c = 0; c < KIN; ++c) {
+      double ao = 0.0, an = 0.0;
+      for (int j = 0; j < NQF; ++j) {
+        const int j0 = (D == 2) ? j : j / N;
+        const int j1 = (D == 2) ? 0 : j % N;
+        double mo = T.half[b0][qt0][j0];
+        double mb = T.B[qt0][j0];
+        if (D == 3) {
+          mo *= T.half[b1][qt1][j1];
+          mb *= T.B[qt1][j1];
+        }
+        ao = fma(mo, A[c * NP + face_to_vol<D, N>(axis, side, j)], ao);
+        an = fma(mb, load_input<D, N, OPK>(P, child, c, face_to_vol<D, N>(axis, 1 - side, j)), an);
+      }
+      TO[c] = ao;
+      TN[c] = an;
+    }
+    const ElemGeo<D> og = elem_geo<D>(mesh.elem, P.gc, child);
+    double n[D], ws;
+    if (axis == 0) face_metric_ax<D, N, 0>(P.gc, mesh.col, og, 1 - side, false, qf, T, n, ws);
+    else if (axis == 1 || D == 2) face_metric_ax<D, N, (D == 2 ? 1 : 1)>(P.gc, mesh.col, og, 1 - side, false, qf, T, n, ws);
+    else face_metric_ax<D, N, D - 1>(P.gc, mesh.col, og, 1 - side, false, qf, T, n, ws);
+    const bool minus = side == 1;
+    double TLv[KIN], TRv[KIN];
+#pragma unroll
+    for (int c = 0; c < KIN; ++c) {
+      TLv[c] = minus ? TO[c] : TN[c];
+      TRv[c] = minus ? TN[c] : TO[c];
+    }
+    double fl[KOUT];
+    num_flux<D, OPK, KIN, KOUT>(TLv, TRv, n, P.model.kinetic_factor, fl);
+    const double sg = minus ? ws : -ws;
+#pragma unroll
+    for (int k = 0; k < KOUT; ++k) FW[((f * S + sub) * KOUT + k) * NQF + qf] = fl[k] * sg;
+  }
+  __syncthreads();
+  double wq = 1.0, det = 1.0;
+  if (act) {
+    int qi[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) qi[a] = digit<D, N>(q, a);
+#pragma unroll
+    for (int k = 0; k < KOUT; ++k) Z[k * NP + q] = 0.0;
+    for (int f = 0; f < NF; ++f) {
+      if ((mesh.kind[e * NF + f] & 15) != KIND_COARSE) continue;
+      const int a = f >> 1, side = f & 1;
+      int qt0, qt1 = 0;
+      if (D == 2) qt0 = qi[1 - a];
+      else {
+        qt0 = (a == 0) ? qi[1] : qi[0];
+        qt1 = (a == 2) ? qi[1] : qi[2];
+      }
+      const double lw = T.lift[side][qi[a]];
+#pragma unroll
+      for (int k = 0; k < KOUT; ++k) {
+        double acc = 0.0;
+        for (int sub = 0; sub < S; ++sub) {
+          const int b0 = sub & 1, b1 = (sub >> 1) & 1;
+          const double* fw = FW + ((f * S + sub) * KOUT + k) * NQF;
+          for (int j = 0; j < NQF; ++j) {
+            const int j0 = (D == 2) ? j : j / N;
+            const int j1 = (D == 2) ? 0 : j % N;
+            double m = T.halfq[b0][j0][qt0];
+            if (D == 3) m *= T.halfq[b1][j1][qt1];
+            acc = fma(m, fw[j], acc);
+          }
+        }
+        Z[k * NP + q] += lw * acc;
+      }
+    }
+    const ElemGeo<D> g = elem_geo<D>(mesh.elem, P.gc, e);
+    double ctrv[D][D];
+    point_metric<D, N>(P, g, q, det, ctrv);
+    wq = point_weight<D, N>(T, q);
+  }
+  if (OPK == OP_ADV && mass_partial != nullptr) {
+    double v = act ? Z[q] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (OPK == OP_ADV && mass_partial != nullptr && threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    mass_partial[blockIdx.x] = s;
+  }
+  const double* res;
+  const int qq = act ? q : 0;
+  if (P.mode == OUT_MINV) {
+    if (act) {
+      const double inv = 1.0 / (wq * det);
+      for (int k = 0; k < KOUT; ++k) Z[k * NP + q] *= inv;
+    }
+    __syncthreads();
+    if (D == 2) {
+      if (act) pass1d<D, N, KOUT,false>(&T.Binv[0][0], Z, Tm, qq, 1, NP);
+      __syncthreads();
+      if (act) pass1d<D, N, KOUT,false>(&T.Binv[0][0], Tm, Z, qq, 0, NP);
+      res = Z;
+    } else {
+      if (act) pass1d<D, N, KOUT,false>(&T.Binv[0][0], Z, Tm, qq, 2, NP);
+      __syncthreads();
+      if (act) pass1d<D, N, KOUT,false>(&T.Binv[0][0], Tm, Z, qq, 1, NP);
+      __syncthreads();
+      if (act) pass1d<D, N, KOUT,false>(&T.Binv[0][0], Z, Tm, qq, 0, NP);
+      res = Tm;
+    }
+  } else {
+    if (D == 2) {
+      if (act) pass1d<D, N, KOUT,true>(&T.B[0][0], Z, Tm, qq, 1, NP);
+      __syncthreads();
+      if (act) pass1d<D, N, KOUT,true>(&T.B[0][0], Tm, Z, qq, 0, NP);
+      res = Z;
+    } else {
+      if (act) pass1d<D, N, KOUT,true>(&T.B[0][0], Z, Tm, qq, 2, NP);
+      __syncthreads();
+      if (act) pass1d<D, N, KOUT,true>(&T.B[0][0], Tm, Z, qq, 1, NP);
+      __syncthreads();
+      if (act) pass1d<D, N, KOUT,true>(&T.B[0][0], Z, Tm, qq, 0, NP);
+      res = Tm;
+    }
+  }
+  __syncthreads();
+  if (!act) return;
+  double* out = P.out.p + e * P.out.estride + q;
+#pragma unroll
+  for (int k = 0; k < KOUT; ++k) {
+    const double r = res[k * NP + q];
+    double add;
+    if (P.mode == OUT_DUAL) add = r;
+    else if (OPK == OP_ADV) add = -r;
+    else add = __dmul_rn(P.coef, r);
+    out[k * P.out.cstride] += add;
+  }
+}
+
+}  // namespace dg

@@ -2,7 +2,8 @@
 // unit per dimension instantiates N = 2..7 and the three operator kinds).
 #pragma once
 #include <cstring>
-#include "dg_operator.cuh"
+#include <type_traits>
+#include "dg_kernel.cuh"
 
 namespace dg {
 
@@ -65,10 +66,25 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)L::SMEM);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(elem_kernel<D, N, OPK>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::CSMEM);
+    if (e != cudaSuccess) return e;
     configured = true;
   }
   elem_kernel<D, N, OPK><<<grid, L::THREADS, L::SMEM, st>>>(P);
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (a.mesh.n_coarse > 0) {
+    coarse_kernel<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
+        P, a.mesh.coarse_list, a.mesh.n_coarse,
+        a.mass_partial ? a.mass_partial + grid : nullptr);
+    e = cudaGetLastError();
+  }
+  if (info) info->grid = grid + a.mesh.n_coarse;  // partial slots written
+  return e;
 }
 
 // grid size only (for sizing the per-CTA partial buffers)

@@ -78,7 +78,7 @@ struct dg_ctx {
   GeoConst gc{};
   Model model{};
   std::vector<double> tabs;
-  DevBuf<int> elem, nbr, hang;
+  DevBuf<int> elem, nbr, hang, clist;
   DevBuf<uint8_t> kind;
   DevBuf<double> col, ffU, ffp, ffh, sigma, bg;
   // scratch
@@ -537,7 +537,20 @@ int dg_ctx_create(const dg_ctx_desc* d, dg_ctx** out) {
     e = up(c->sigma, d->sigma, (size_t)d->n_el * np);
     if (e == cudaSuccess) e = up(c->bg, d->background, (size_t)d->n_el * c->V * np);
   }
-  const int max_grid = d->n_el + 1;
+  // owned elements with a coarse hanging face -> coarse fix-up kernel list
+  {
+    std::vector<int> cl;
+    const int nf = 2 * d->dim;
+    for (int e2 = 0; e2 < d->n_el; ++e2)
+      for (int f = 0; f < nf; ++f)
+        if ((d->kind[(size_t)e2 * nf + f] & 15) == DG_FACE_COARSE) {
+          cl.push_back(e2);
+          break;
+        }
+    if (e == cudaSuccess && !cl.empty()) e = c->clist.upload(cl.data(), cl.size());
+    c->mesh.n_coarse = (int)cl.size();
+  }
+  const int max_grid = d->n_el + 1 + c->mesh.n_coarse;
   if (e == cudaSuccess) e = c->mass_partial.alloc(max_grid);
   if (e == cudaSuccess) e = c->partial.alloc((size_t)RED_BLOCKS * 40 + (size_t)max_grid * 8);
   if (e == cudaSuccess) e = c->redout.alloc(256);
@@ -556,6 +569,7 @@ int dg_ctx_create(const dg_ctx_desc* d, dg_ctx** out) {
   c->mesh.ff_p = c->ffp.p;
   c->mesh.ff_h = c->ffh.p;
   c->mesh.n_el = d->n_el;
+  c->mesh.coarse_list = c->clist.p;
   for (int a = 0; a < 3; ++a) c->gc.per_root[a] = d->per_root[a];
   c->gc.z_top = d->z_top;
   c->gc.terrain = d->terrain;
@@ -574,6 +588,7 @@ int dg_ctx_destroy(dg_ctx* c) {
     b->release();
   for (auto& s : c->st) s.release();
   c->elem.release();
+  c->clist.release();
   c->nbr.release();
   c->hang.release();
   c->kind.release();

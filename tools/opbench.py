@@ -1,0 +1,87 @@
+"""Operator microbenchmark: explicit residual and Helmholtz apply throughput
+on a BASELINE recipe (cfg4 3D hill by default), timed with CUDA events.
+
+    python tools/opbench.py [--case cfg4] [--scale 0.25] [--reps 10]
+
+Prints one JSON line per operator: DoF/s, ms per apply, algorithmic GB/s
+and the fraction of the measured HBM copy bandwidth (MEASURED_PEAKS.json).
+Used for ncu captures (one short command, one GPU).
+"""
+
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--case", default="cfg4")
+    ap.add_argument("--scale", type=float, default=0.25)
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--ops", default="explicit,helmholtz,grad,divhv")
+    a = ap.parse_args()
+    import numpy as np
+    import torch
+
+    from paper_2408_08129_b200 import _lib as L
+    from paper_2408_08129_b200.cases import baseline_case, energy_like
+    from paper_2408_08129_b200.device import DeviceContext, as_ptr
+
+    c = baseline_case(a.case, root_scale=a.scale)
+    ctx = DeviceContext(c.geometry, c.model, c.bcs, c.sponge)
+    h = ctx.handle
+    lib = ctx.lib
+    dev = torch.device("cuda:0")
+    U = torch.from_numpy(c.U0).to(dev)
+    nn = c.geometry.basis.n_nodes
+    d = c.mesh.dim
+    n_el = c.mesh.n_leaves
+    R = torch.empty_like(U)
+    x = torch.from_numpy(energy_like(c.U0, 1)).to(dev)
+    y = torch.empty_like(x)
+    hh = torch.empty_like(x)
+    K = torch.empty_like(x)
+    V = torch.empty((n_el, d, nn), dtype=torch.float64, device=dev)
+    dv = torch.empty((n_el, 1, nn), dtype=torch.float64, device=dev)
+    ctx.bind_stream()
+    lib.dg_frozen_coefficients(h, as_ptr(U), as_ptr(hh), as_ptr(K))
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+        peak = float(json.load(f)["hbm_gbs"])
+    N = n_el * nn
+    ops = {
+        "explicit": (lambda: lib.dg_explicit_residual(h, as_ptr(U), as_ptr(R), None),
+                     N * (d + 2), 8.0 * N * ((d + 2) * 3)),
+        "helmholtz": (lambda: lib.dg_helmholtz_apply(h, 0.3, as_ptr(hh), as_ptr(x), as_ptr(y)),
+                      N, 8.0 * N * (3 + 2 * d + 1)),
+        "grad": (lambda: lib.dg_gradient_scalar(h, as_ptr(x), 1, as_ptr(V)),
+                 N, 8.0 * N * (1 + d)),
+        "divhv": (lambda: lib.dg_divergence_hv(h, as_ptr(V), V.stride(0), as_ptr(hh), 1,
+                                               as_ptr(dv)), N, 8.0 * N * (d + 2)),
+    }
+    s = torch.cuda.current_stream()
+    for name in a.ops.split(","):
+        fn, dofs, byts = ops[name]
+        for _ in range(3):
+            L.check(fn())
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(a.reps):
+            fn()
+        e1.record(s)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / a.reps
+        gbs = byts / (ms * 1e-3) / 1e9
+        print(json.dumps({"op": name, "case": a.case, "n_el": n_el, "degree": c.geometry.basis.degree,
+                          "ms": ms, "dofs_per_s": dofs / (ms * 1e-3), "GB_s": gbs,
+                          "frac_hbm": gbs / peak, "launch": ctx.launch_info()}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
