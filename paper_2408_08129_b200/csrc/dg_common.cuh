@@ -92,10 +92,12 @@ __device__ __forceinline__ ElemGeo<D> elem_geo(const int* elem, const GeoConst& 
   ElemGeo<D> g;
   const int* r = elem + e * (2 + D);
   const int level = r[0];
-  const double scale = (double)(1LL << level);
+  // (extents/root) / 2^level is an exact power-of-two scaling
+  // (geometry.py:195-197): multiply by 2^-level instead of dividing
+  const double scale = __longlong_as_double((long long)(1023 - level) << 52);
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    g.s[a] = gc.per_root[a] / scale;     // geometry.py:195-197
+    g.s[a] = gc.per_root[a] * scale;
     g.lo[a] = g.s[a] * (double)r[1 + a];
   }
   g.col = r[1 + D];

@@ -448,10 +448,14 @@ elem_kernel(const __grid_constant__ KParams<N> P) {
   constexpr int NP = L::NP, NQF = L::NQF, NF = L::NF, KIN = L::KIN, KOUT = L::KOUT;
   constexpr int E = L::ELEM;
   extern __shared__ double smem[];
+  __shared__ short fnode[NF * NQF];  // volume node of face point j on face f
   {
     const double* src = reinterpret_cast<const double*>(&P.tab);
     for (int i = threadIdx.x; i < L::TABD; i += blockDim.x) smem[i] = src[i];
+    for (int i = threadIdx.x; i < NF * NQF; i += blockDim.x)
+      fnode[i] = (short)face_to_vol<D, N>((i / NQF) >> 1, (i / NQF) & 1, i % NQF);
   }
+  __syncthreads();
   const Tab<N>& TS = *reinterpret_cast<const Tab<N>*>(smem);
   const Tab<N>& TC = P.tab;
   double* red = smem + L::TABD;
@@ -487,9 +491,8 @@ elem_kernel(const __grid_constant__ KParams<N> P) {
       const int kd = mesh.kind[ge * NF + f] & 15;
       if (kd != KIND_CONF && kd != KIND_FINE) continue;
       const long long src = mesh.nbr[ge * NF + f];
-      const int axis = f >> 1, side = f & 1;
       base[e * E + L::OFF_G + (f * KIN + c) * NQF + j] =
-          load_input<D, N, OPK>(P, src, c, face_to_vol<D, N>(axis, 1 - side, j));
+          load_input<D, N, OPK>(P, src, c, fnode[(f ^ 1) * NQF + j]);
     }
   }
   __syncthreads();

@@ -264,8 +264,12 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* rhs, double* x,
   if (m > c->n_global) m = (int)c->n_global;
   if (m < 1) m = 1;
   if (m > 31) return fail(DG_ERR_USAGE, "krylov_restart > 31 not supported on the device path");
-  CK(c->basis.alloc((size_t)(m + 1) * ns));
+  // basis vectors at a padded stride: a power-of-two-rich stride makes the
+  // j+1 streams of one Gram-Schmidt pass collide in the same DRAM channels
+  const long long vs = ((ns + 31) / 32) * 32 + 32 * 13;
+  CK(c->basis.alloc((size_t)(m + 1) * vs));
   double* Vb = c->basis.p;
+  double* coefs = c->pinned + 128;  // pinned staging for the coefficient uploads
   double* w = c->sw.p;
   double* r = c->sr.p;
   double bn2;
@@ -300,33 +304,55 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* rhs, double* x,
     g[0] = beta;
     int done = 0;
     for (int j = 0; j < m; ++j) {
-      RET(helm_apply(c, a_dt, h, Vb + (size_t)j * ns, w));
-      // classical Gram-Schmidt: h_i = V_i . w, one pass
-      CK(multidot(c->stream, n, j + 1, Vb, ns, w, c->partial.p, c->redout.p));
+      RET(helm_apply(c, a_dt, h, Vb + (size_t)j * vs, w));
+      // classical Gram-Schmidt: h_i = V_i . w and |w|^2 in one pass
+      CK(multidot(c->stream, n, j + 1, Vb, vs, w, c->partial.p, c->redout.p));
       RET(reduce_read(c, c->redout.p, j + 2, hc.data()));
-      const double nb = std::sqrt(hc[j + 1]);
-      for (int i = 0; i <= j; ++i) Hij(i, j) = hc[i];
-      CK(cudaMemcpyAsync(c->coef_dev.p, hc.data(), (j + 1) * sizeof(double),
-                         cudaMemcpyHostToDevice, c->stream));
-      CK(axpy_multi(c->stream, n, j + 1, Vb, ns, c->coef_dev.p, w, c->partial.p, c->redout.p));
-      double na2;
-      RET(reduce_read(c, c->redout.p, 1, &na2));
-      double na = std::sqrt(na2);
-      if (na < 0.7071067811865476 * nb) {
-        // one re-orthogonalisation pass (krylov.py:73-79)
-        CK(multidot(c->stream, n, j + 1, Vb, ns, w, c->partial.p, c->redout.p));
-        RET(reduce_read(c, c->redout.p, j + 2, hc.data()));
-        for (int i = 0; i <= j; ++i) Hij(i, j) += hc[i];
-        CK(cudaMemcpyAsync(c->coef_dev.p, hc.data(), (j + 1) * sizeof(double),
-                           cudaMemcpyHostToDevice, c->stream));
-        CK(axpy_multi(c->stream, n, j + 1, Vb, ns, c->coef_dev.p, w, c->partial.p, c->redout.p));
+      const double nb2 = hc[j + 1];
+      const double nb = std::sqrt(nb2);
+      double s2 = 0.0;
+      for (int i = 0; i <= j; ++i) {
+        Hij(i, j) = hc[i];
+        s2 += hc[i] * hc[i];
+        coefs[i] = hc[i];
+      }
+      CK(cudaMemcpyAsync(c->coef_dev.p, coefs, (j + 1) * sizeof(double), cudaMemcpyHostToDevice,
+                         c->stream));
+      double* dst = Vb + (size_t)(j + 1) * vs;
+      // |w - V h|^2 = |w|^2 - |h|^2 for orthonormal V: when no more than half of
+      // |w|^2 cancels (the reference's re-orthogonalisation test, krylov.py:76,
+      // is then false) update and normalise in one fused pass
+      const double na2_est = nb2 - s2;
+      double na;
+      bool happy;
+      if (na2_est > 0.5 * nb2) {
+        na = std::sqrt(na2_est);
+        happy = na <= 1e-14 * std::max(bn, nb);
+        if (!happy) CK(axpy_div(c->stream, n, j + 1, Vb, vs, c->coef_dev.p, w, na, dst));
+      } else {
+        CK(axpy_multi(c->stream, n, j + 1, Vb, vs, c->coef_dev.p, w, c->partial.p, c->redout.p));
+        double na2;
         RET(reduce_read(c, c->redout.p, 1, &na2));
         na = std::sqrt(na2);
+        if (na < 0.7071067811865476 * nb) {
+          // one re-orthogonalisation pass (krylov.py:73-79)
+          CK(multidot(c->stream, n, j + 1, Vb, vs, w, c->partial.p, c->redout.p));
+          RET(reduce_read(c, c->redout.p, j + 2, hc.data()));
+          for (int i = 0; i <= j; ++i) {
+            Hij(i, j) += hc[i];
+            coefs[i] = hc[i];
+          }
+          CK(cudaMemcpyAsync(c->coef_dev.p, coefs, (j + 1) * sizeof(double),
+                             cudaMemcpyHostToDevice, c->stream));
+          CK(axpy_multi(c->stream, n, j + 1, Vb, vs, c->coef_dev.p, w, c->partial.p, c->redout.p));
+          RET(reduce_read(c, c->redout.p, 1, &na2));
+          na = std::sqrt(na2);
+        }
+        happy = na <= 1e-14 * std::max(bn, nb);
+        if (!happy) CK(scale(c->stream, n, na, true, w, dst));
       }
       Hij(j + 1, j) = na;
       st.iterations += 1;
-      const bool happy = na <= 1e-14 * std::max(bn, nb);
-      if (!happy) CK(scale(c->stream, n, na, true, w, Vb + (size_t)(j + 1) * ns));
       for (int i = 0; i < j; ++i) {
         const double t = cs[i] * Hij(i, j) + sn[i] * Hij(i + 1, j);
         Hij(i + 1, j) = -sn[i] * Hij(i, j) + cs[i] * Hij(i + 1, j);
@@ -355,10 +381,10 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* rhs, double* x,
         y[i] = s / Hij(i, i);
       }
       // x <- x + V y  ==  x - sum(-y_i) V_i
-      for (int i = 0; i < done; ++i) hc[i] = -y[i];
-      CK(cudaMemcpyAsync(c->coef_dev.p, hc.data(), done * sizeof(double), cudaMemcpyHostToDevice,
+      for (int i = 0; i < done; ++i) coefs[i] = -y[i];
+      CK(cudaMemcpyAsync(c->coef_dev.p, coefs, done * sizeof(double), cudaMemcpyHostToDevice,
                          c->stream));
-      CK(axpy_multi(c->stream, n, done, Vb, ns, c->coef_dev.p, x, c->partial.p, nullptr));
+      CK(axpy_multi(c->stream, n, done, Vb, vs, c->coef_dev.p, x, c->partial.p, nullptr));
     }
     RET(residual_into_r());
     st.restarts += 1;

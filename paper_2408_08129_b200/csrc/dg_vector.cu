@@ -100,6 +100,26 @@ k_axpy_multi(long long n, int nv, const double* __restrict__ V, long long vstrid
   }
 }
 
+// dst <- (w - sum_i c_i V_i) / na : Gram-Schmidt update and normalisation in
+// one pass (the norm comes from the Pythagorean identity)
+template <int MAXV>
+__global__ void __launch_bounds__(RED_THREADS)
+k_axpy_div(long long n, int nv, const double* __restrict__ V, long long vstride,
+           const double* __restrict__ coefs, const double* __restrict__ w, double na,
+           double* __restrict__ dst) {
+  __shared__ double c[MAXV];
+  for (int i = threadIdx.x; i < MAXV; i += blockDim.x) c[i] = i < nv ? coefs[i] : 0.0;
+  __syncthreads();
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    double t = 0.0;
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i)
+      if (i < nv) t = fma(c[i], V[i * vstride + k], t);
+    dst[k] = (w[k] - t) / na;
+  }
+}
+
 // out[c] = sum_b partials[b][c]   (one warp per column, fixed order)
 __global__ void k_reduce_cols(const double* __restrict__ partials, int nblocks, int ncols,
                               double* __restrict__ out) {
@@ -325,29 +345,85 @@ cudaError_t lincomb(cudaStream_t st, long long n, int m, const double* c, const 
   return cudaGetLastError();
 }
 
+// Gram-Schmidt passes run in groups of GS = 8 basis vectors: the 8-wide
+// kernels stream at the HBM copy rate (tools/vecbench.py), the 16/32-wide
+// ones are register-limited to ~40% of it, so w is re-read once per extra
+// group instead (+1 vector pass per 8).
+constexpr int GS = 8;
+
+// out[c] for grouped multidot partials (one warp per column)
+__global__ void k_reduce_groups(const double* __restrict__ partials, int nblocks, int nv,
+                                double* __restrict__ out) {
+  const int col = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (col > nv) return;
+  int g, i, cnt;
+  if (col == nv) {
+    g = 0;
+    cnt = nv < GS ? nv : GS;
+    i = cnt;
+  } else {
+    g = col / GS;
+    i = col % GS;
+    cnt = (nv - g * GS) < GS ? (nv - g * GS) : GS;
+  }
+  const double* p = partials + (long long)g * nblocks * (GS + 1);
+  double s = 0.0;
+  for (int b = lane; b < nblocks; b += 32) s += p[(long long)b * (cnt + 1) + i];
+  s = warp_sum(s);
+  if (lane == 0) out[col] = s;
+}
+
 cudaError_t multidot(cudaStream_t st, long long n, int nv, const double* V, long long vstride,
                      const double* w, double* partials, double* out) {
   // out[0..nv-1] = V_i . w, out[nv] = w . w  (fixed RED_BLOCKS grid)
+  if (nv > 32) return cudaErrorInvalidValue;
   prof_begin(st);
-  if (nv <= 8) k_multidot<8><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, nv, V, vstride, w, partials);
-  else if (nv <= 16) k_multidot<16><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, nv, V, vstride, w, partials);
-  else if (nv <= 32) k_multidot<32><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, nv, V, vstride, w, partials);
-  else return cudaErrorInvalidValue;
-  const int ncols = nv + 1;
-  k_reduce_cols<<<(ncols + 7) / 8, 256, 0, st>>>(partials, RED_BLOCKS, ncols, out);
-  prof_end(st, P_DOT, 8.0 * n * (nv + 1), 2);
+  const int ng = nv == 0 ? 1 : (nv + GS - 1) / GS;
+  for (int g = 0; g < ng; ++g) {
+    const int cnt = nv - g * GS < GS ? nv - g * GS : GS;
+    k_multidot<GS><<<RED_BLOCKS, RED_THREADS, 0, st>>>(
+        n, cnt, V + (long long)g * GS * vstride, vstride, w,
+        partials + (long long)g * RED_BLOCKS * (GS + 1));
+  }
+  k_reduce_groups<<<(nv + 1 + 7) / 8, 256, 0, st>>>(partials, RED_BLOCKS, nv, out);
+  prof_end(st, P_DOT, 8.0 * n * (nv + ng), ng + 1);
   return cudaGetLastError();
 }
 
 cudaError_t axpy_multi(cudaStream_t st, long long n, int nv, const double* V, long long vstride,
                        const double* coefs_dev, double* w, double* partials, double* norm2_out) {
+  if (nv > 32 || nv < 1) return cudaErrorInvalidValue;
   prof_begin(st);
-  if (nv <= 8) k_axpy_multi<8><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, nv, V, vstride, coefs_dev, w, partials);
-  else if (nv <= 16) k_axpy_multi<16><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, nv, V, vstride, coefs_dev, w, partials);
-  else if (nv <= 32) k_axpy_multi<32><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, nv, V, vstride, coefs_dev, w, partials);
-  else return cudaErrorInvalidValue;
+  const int ng = (nv + GS - 1) / GS;
+  for (int g = 0; g < ng; ++g) {
+    const int cnt = nv - g * GS < GS ? nv - g * GS : GS;
+    k_axpy_multi<GS><<<RED_BLOCKS, RED_THREADS, 0, st>>>(
+        n, cnt, V + (long long)g * GS * vstride, vstride, coefs_dev + g * GS, w,
+        g == ng - 1 ? partials : nullptr);
+  }
   if (norm2_out) k_reduce_cols<<<1, 32, 0, st>>>(partials, RED_BLOCKS, 1, norm2_out);
-  prof_end(st, P_AXPY, 8.0 * n * (nv + 2), norm2_out ? 2 : 1);
+  prof_end(st, P_AXPY, 8.0 * n * (nv + 2 * ng), ng + (norm2_out ? 1 : 0));
+  return cudaGetLastError();
+}
+
+cudaError_t axpy_div(cudaStream_t st, long long n, int nv, const double* V, long long vstride,
+                     const double* coefs_dev, double* w, double na, double* dst) {
+  // w is scratch: earlier groups update it in place, the last one divides
+  if (nv > 32 || nv < 1) return cudaErrorInvalidValue;
+  prof_begin(st);
+  const int ng = (nv + GS - 1) / GS;
+  for (int g = 0; g < ng; ++g) {
+    const int cnt = nv - g * GS < GS ? nv - g * GS : GS;
+    const double* Vg = V + (long long)g * GS * vstride;
+    if (g < ng - 1)
+      k_axpy_multi<GS><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, cnt, Vg, vstride, coefs_dev + g * GS,
+                                                           w, nullptr);
+    else
+      k_axpy_div<GS><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, cnt, Vg, vstride, coefs_dev + g * GS,
+                                                         w, na, dst);
+  }
+  prof_end(st, P_AXPY, 8.0 * n * (nv + 2 * ng), ng);
   return cudaGetLastError();
 }
 

@@ -13,6 +13,8 @@ cudaError_t multidot(cudaStream_t st, long long n, int nv, const double* V, long
                      const double* w, double* partials, double* out);
 cudaError_t axpy_multi(cudaStream_t st, long long n, int nv, const double* V, long long vstride,
                        const double* coefs_dev, double* w, double* partials, double* norm2_out);
+cudaError_t axpy_div(cudaStream_t st, long long n, int nv, const double* V, long long vstride,
+                     const double* coefs_dev, double* w, double na, double* dst);
 cudaError_t scale(cudaStream_t st, long long n, double a, bool divide, const double* x,
                   double* y);
 cudaError_t frozen(cudaStream_t st, long long n_el, int np, int d, const double* U, double gm1,

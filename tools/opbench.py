@@ -64,6 +64,17 @@ def main():
         "divhv": (lambda: lib.dg_divergence_hv(h, as_ptr(V), V.stride(0), as_ptr(hh), 1,
                                                as_ptr(dv)), N, 8.0 * N * (d + 2)),
     }
+    rhs = torch.empty_like(x)
+    lib.dg_helmholtz_apply(h, 0.3, as_ptr(hh), as_ptr(x), as_ptr(rhs))
+    x0 = torch.empty_like(x)
+
+    def gm():
+        x0.copy_(x)
+        x0.mul_(1.0 + 1e-6)
+        st = L.KrylovStatsC()
+        return lib.dg_gmres_helmholtz(h, 0.3, as_ptr(hh), as_ptr(rhs), as_ptr(x0), 1e-8, 30, 1000,
+                                      C.byref(st), None, 0)
+    ops["gmres"] = (gm, N, 0.0)
     s = torch.cuda.current_stream()
     for name in a.ops.split(","):
         fn, dofs, byts = ops[name]
