@@ -104,6 +104,45 @@ def face_tables(mesh, bcs, model, basis):
     return kind, nbr, hang, ffU, ffp, ffh
 
 
+def localize(kind, nbr, hang, ffU, ffp, ffh, local_ids, n_owned, n_glob):
+    """Face records of one rank's [owned..., ghosts...] elements in local
+    numbering (host-only; unit-tested on CPU).  Raises UsageError when an
+    owned element's face neighbour is missing from the local set."""
+    local_ids = np.asarray(local_ids, dtype=np.int64)
+    n_tot = len(local_ids)
+    d2 = kind.shape[1]
+    g2l = np.full(n_glob, -1, dtype=np.int64)
+    g2l[local_ids] = np.arange(n_tot)
+    kl = kind[local_ids].copy()
+    nl = nbr[local_ids].copy()
+    k4 = kl & 15
+    inter = (k4 == L.FACE_CONF) | (k4 == L.FACE_FINE)
+    nl[inter] = g2l[nl[inter]]
+    coarse = k4 == L.FACE_COARSE
+    gids = np.unique(nl[coarse]) if np.any(coarse) else np.zeros(0, np.int64)
+    hmap = np.full(max(len(hang), 1), -1, dtype=np.int64)
+    hmap[gids] = np.arange(len(gids))
+    S = hang.shape[1] if hang.ndim == 2 else 1
+    hang_l = g2l[hang[gids]] if len(gids) else np.zeros((0, S), np.int64)
+    nl[coarse] = hmap[nl[coarse]]
+    bnd = (k4 == L.FACE_WALL) | (k4 == L.FACE_FARFIELD)
+    rows = np.unique(nl[bnd]) if np.any(bnd) else np.zeros(0, np.int64)
+    rmap = np.full(max(len(ffU), 1), -1, dtype=np.int64)
+    rmap[rows] = np.arange(len(rows))
+    nl[bnd] = rmap[nl[bnd]]
+    if np.any(nl[:n_owned] < 0):
+        e, f = np.argwhere(nl[:n_owned] < 0)[0]
+        raise UsageError(f"halo plan misses face {f} neighbour of owned element {e}")
+    coarse_owned = np.any(coarse[:n_owned], axis=1)
+    used_groups = np.unique(nl[:n_owned][coarse[:n_owned]])
+    if len(used_groups) and np.any(hang_l[used_groups] < 0):
+        raise UsageError("halo plan misses a fine child of an owned coarse face")
+    del coarse_owned, d2
+    return (kl, nl, hang_l, ffU[rows] if len(rows) else np.zeros((0,) + ffU.shape[1:]),
+            ffp[rows] if len(rows) else np.zeros((0,) + ffp.shape[1:]),
+            ffh[rows] if len(rows) else np.zeros((0,) + ffh.shape[1:]))
+
+
 class DeviceContext:
     """Owns one dg_ctx (one GPU, one element range) and its host tables.
 
@@ -138,39 +177,19 @@ class DeviceContext:
         self.local_ids = local_ids
         self.n_el = int(n_owned)
         self.n_tot = len(local_ids)
-        g2l = np.full(n_glob, -1, dtype=np.int64)
-        g2l[local_ids] = np.arange(self.n_tot)
         own = local_ids[:self.n_el]
-        # remap face records of the local elements to local numbering
-        kl = kind[local_ids].copy()
-        nl = nbr[local_ids].copy()
-        k4 = kl & 15
-        inter = (k4 == L.FACE_CONF) | (k4 == L.FACE_FINE)
-        nl[inter] = g2l[nl[inter]]
-        coarse = k4 == L.FACE_COARSE
-        gids = np.unique(nl[coarse]) if np.any(coarse) else np.zeros(0, np.int64)
-        hmap = np.full(max(len(hang), 1), -1, dtype=np.int64)
-        hmap[gids] = np.arange(len(gids))
-        hang_l = g2l[hang[gids]] if len(gids) else np.zeros((0, 2 ** (d - 1)), np.int64)
-        nl[coarse] = hmap[nl[coarse]]
-        bnd = (k4 == L.FACE_WALL) | (k4 == L.FACE_FARFIELD)
-        rows = np.unique(nl[bnd]) if np.any(bnd) else np.zeros(0, np.int64)
-        rmap = np.full(max(len(ffU), 1), -1, dtype=np.int64)
-        rmap[rows] = np.arange(len(rows))
-        nl[bnd] = rmap[nl[bnd]]
-        owned_rows = np.zeros(self.n_tot, dtype=bool)
-        owned_rows[:self.n_el] = True
-        if np.any(nl[owned_rows] < 0) or np.any(hang_l < 0):
-            raise UsageError("halo plan misses a face neighbour of an owned element")
+        kl, nl, hang_l, fU, fp, fh = localize(kind, nbr, hang, ffU, ffp, ffh, local_ids,
+                                              self.n_el, n_glob)
+        rows = np.arange(len(fU))
         self._host = dict(
             elem=np.ascontiguousarray(elem[local_ids]),
             col=np.ascontiguousarray(col) if col_stride else np.zeros(1),
             nbr=np.ascontiguousarray(nl.astype(np.int32)),
             kind=np.ascontiguousarray(kl),
             hang=np.ascontiguousarray(hang_l.astype(np.int32)) if len(hang_l) else np.zeros((1, 1), np.int32),
-            ffU=np.ascontiguousarray(ffU[rows]) if len(rows) else np.zeros(1),
-            ffp=np.ascontiguousarray(ffp[rows]) if len(rows) else np.zeros(1),
-            ffh=np.ascontiguousarray(ffh[rows]) if len(rows) else np.zeros(1),
+            ffU=np.ascontiguousarray(fU) if len(rows) else np.zeros(1),
+            ffp=np.ascontiguousarray(fp) if len(rows) else np.zeros(1),
+            ffh=np.ascontiguousarray(fh) if len(rows) else np.zeros(1),
             tabs=basis_tables(b))
         self.has_sponge = sponge is not None
         if sponge is not None:

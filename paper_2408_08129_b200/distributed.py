@@ -1,0 +1,142 @@
+"""Element-block domain decomposition over GPUs (one process per GPU).
+
+The partition is the reference's Morton-contiguous split (orodg/partition.py,
+``partition_leaves``); each rank owns one contiguous leaf range and keeps
+ghost COPIES of the face neighbours it reads.  Local element
+numbering is [owned..., ghosts...] with ghosts ordered by (owner rank,
+global id), so the ghosts received from one peer form one contiguous block.
+Collectives (libdg, NCCL over NVLink/NVSwitch): a grouped send/recv halo
+exchange before every face-coupled kernel and allreduces of the Krylov,
+fixed-point and diagnostic scalars.  Nothing else crosses GPUs.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .partition import neighbor_pairs, partition_leaves
+
+
+@dataclass
+class HaloPlan:
+    rank: int
+    nranks: int
+    owned: tuple                # (start, stop) global leaf range
+    ghosts: np.ndarray          # global ids, ordered by (owner, id)
+    recv_counts: np.ndarray     # ghosts received from each peer
+    send_counts: np.ndarray     # owned leaves sent to each peer
+    send_elems: np.ndarray      # LOCAL ids of the sent leaves, grouped by peer
+
+    @property
+    def local_ids(self):
+        a, b = self.owned
+        return np.concatenate([np.arange(a, b, dtype=np.int64), self.ghosts])
+
+    @property
+    def n_owned(self):
+        return self.owned[1] - self.owned[0]
+
+
+def halo_plans(mesh, nranks, weights=None, part=None):
+    """Plans for every rank (deterministic; each rank can build all of them)."""
+    part = part or partition_leaves(mesh, nranks, weights)
+    owner = part.owner
+    pairs = neighbor_pairs(mesh)
+    plans = []
+    ghost_sets = []
+    for p in range(nranks):
+        g = part.ghosts[p] if len(pairs) else np.empty(0, np.int64)
+        g = np.asarray(g, dtype=np.int64)
+        g = g[np.lexsort((g, owner[g]))] if len(g) else g
+        ghost_sets.append(g)
+    for p in range(nranks):
+        a, b = part.ranges[p]
+        recv = np.array([np.sum(owner[ghost_sets[p]] == q) for q in range(nranks)], dtype=np.int64)
+        send_lists = []
+        for q in range(nranks):
+            gq = ghost_sets[q]
+            mine = gq[owner[gq] == p] if len(gq) else gq
+            send_lists.append(np.sort(mine) - a)     # global -> local (owned block)
+        send_counts = np.array([len(s) for s in send_lists], dtype=np.int64)
+        send_elems = (np.concatenate(send_lists) if send_lists else np.empty(0, np.int64))
+        plans.append(HaloPlan(rank=p, nranks=nranks, owned=(a, b), ghosts=ghost_sets[p],
+                              recv_counts=recv, send_counts=send_counts,
+                              send_elems=send_elems.astype(np.int64)))
+    return plans
+
+
+def exchange_host(plans, local_arrays):
+    """Reference (host) execution of one halo exchange for all ranks:
+    local_arrays[p] has rows [owned..., ghosts...]; ghost rows are filled
+    from their owners using exactly the send/recv lists libdg uses."""
+    out = [a.copy() for a in local_arrays]
+    for p, pl in enumerate(plans):
+        off = 0
+        for q in range(pl.nranks):
+            n = int(pl.recv_counts[q])
+            if n == 0:
+                continue
+            plq = plans[q]
+            s0 = int(np.sum(plq.send_counts[:p]))
+            rows = plq.send_elems[s0:s0 + n]
+            out[p][pl.n_owned + off:pl.n_owned + off + n] = local_arrays[q][rows]
+            off += n
+    return out
+
+
+class DistributedSolver:
+    """One rank of a partitioned ARS(2,2,2) run on its GPU (bench.py N>1)."""
+
+    def __init__(self, case, cfg, rank, world, local_rank):
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib as L
+        from .device import DeviceContext
+
+        if not dist.is_initialized():
+            dist.init_process_group("gloo")
+        self.plan = halo_plans(case.mesh, world)[rank]
+        pl = self.plan
+        ids = pl.local_ids
+        sponge = case.sponge
+        self.ctx = DeviceContext(case.geometry, case.model, case.bcs, sponge,
+                                 device=local_rank, local_ids=ids, n_owned=pl.n_owned)
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            L.check(self.ctx.lib.dg_nccl_unique_id(uid))
+        obj = [bytes(uid) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = (C.c_char * 128).from_buffer_copy(obj[0])
+        sc = np.ascontiguousarray(pl.send_counts.astype(np.int32))
+        se = np.ascontiguousarray(pl.send_elems.astype(np.int32))
+        rc = np.ascontiguousarray(pl.recv_counts.astype(np.int32))
+        L.check(self.ctx.lib.dg_ctx_set_comm(self.ctx.handle, uid, rank, world,
+                                            sc.ctypes.data_as(C.c_void_p),
+                                            se.ctypes.data_as(C.c_void_p),
+                                            rc.ctypes.data_as(C.c_void_p)))
+        self.case = case
+        self.cfg = cfg
+        self.n_owned = pl.n_owned
+        self.torch = torch
+
+    def local_state(self):
+        U = self.case.U0[self.plan.local_ids]
+        return self.torch.from_numpy(np.ascontiguousarray(U)).to(f"cuda:{self.ctx.device}")
+
+    def step(self, U, t):
+        import ctypes as C
+
+        from . import _lib as L
+        from .device import as_ptr
+        from .imex import StepStats, _step_error_info
+        out = self.torch.empty_like(U)
+        cs = L.StepStatsC()
+        code = self.ctx.lib.dg_imex_step(self.ctx.bind_stream(), as_ptr(U), as_ptr(out), float(t),
+                                         float(self.case.dt), C.byref(self.cfg.c()), C.byref(cs))
+        st = StepStats()
+        st.absorb(cs)
+        L.check(code, stats=st, **_step_error_info(cs))
+        return out, st
