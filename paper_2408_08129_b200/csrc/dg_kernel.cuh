@@ -72,13 +72,18 @@ struct Layout {
 // dst (op)= M along axis AX of a DIM-dim N^DIM tensor, for KC comps of nv
 // elements.  M from the parameter constant bank (compile-time indices).
 // MODE: 0 dst = M src, 1 dst = -M src, 2 dst -= M src.
-template <int DIM, int N, int AX, bool TRANS, int MODE, int KC, int ELEM, int CS>
-__device__ __forceinline__ void vpass(const double (&M)[N][N], double* base, int soff, int doff,
-                                      int nv) {
+// Runs over all EPB element slots of the CTA (compile-time trip count; slots
+// past the last valid element compute on their own scratch and are never
+// stored to global memory).
+template <int DIM, int N, int AX, bool TRANS, int MODE, int KC, int ELEM, int CS, int NE, int TH>
+__device__ __forceinline__ void vpass(const double (&M)[N][N], double* base, int soff, int doff) {
   constexpr int NPEN = ipow(N, DIM - 1);
   constexpr int ST = ipow(N, DIM - 1 - AX);
-  const int items = nv * KC * NPEN;
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+  constexpr int ITEMS = NE * KC * NPEN;
+#pragma unroll
+  for (int rr = 0; rr < (ITEMS + TH - 1) / TH; ++rr) {
+    const int it = rr * TH + (int)threadIdx.x;
+    if ((ITEMS % TH) != 0 && it >= ITEMS) break;
     const int p = it % NPEN;
     const int r = it / NPEN;
     const int c = r % KC;
@@ -102,38 +107,42 @@ __device__ __forceinline__ void vpass(const double (&M)[N][N], double* base, int
 }
 
 // nodes -> Gauss points (all axes), src (A) preserved; result at Q
-template <int D, int N, int KC, int ELEM, int NP>
+template <int D, int N, int KC, int ELEM, int NP, int NE, int TH>
 __device__ __forceinline__ void interp_all(const double (&B)[N][N], double* base, int a_off,
-                                           int q_off, int t_off, int nv) {
+                                           int q_off, int t_off) {
   if constexpr (D == 2) {
-    vpass<2, N, 1, false, 0, KC, ELEM, NP>(B, base, a_off, t_off, nv);
+    vpass<2, N, 1, false, 0, KC, ELEM, NP, NE, TH>(B, base, a_off, t_off);
     __syncthreads();
-    vpass<2, N, 0, false, 0, KC, ELEM, NP>(B, base, t_off, q_off, nv);
+    vpass<2, N, 0, false, 0, KC, ELEM, NP, NE, TH>(B, base, t_off, q_off);
   } else {
-    vpass<3, N, 2, false, 0, KC, ELEM, NP>(B, base, a_off, q_off, nv);
+    vpass<3, N, 2, false, 0, KC, ELEM, NP, NE, TH>(B, base, a_off, q_off);
     __syncthreads();
-    vpass<3, N, 1, false, 0, KC, ELEM, NP>(B, base, q_off, t_off, nv);
+    vpass<3, N, 1, false, 0, KC, ELEM, NP, NE, TH>(B, base, q_off, t_off);
     __syncthreads();
-    vpass<3, N, 0, false, 0, KC, ELEM, NP>(B, base, t_off, q_off, nv);
+    vpass<3, N, 0, false, 0, KC, ELEM, NP, NE, TH>(B, base, t_off, q_off);
   }
 }
 
 // tangential pass on the gathered face tensors: matrix per face from the
 // smem tables (B, or half[bit] for a fine leaf's view of its coarse parent)
-template <int D, int N, int TAX, int KC, int ELEM, int NF>
+template <int D, int N, int TAX, int KC, int ELEM, int NF, int NE, int TH>
 __device__ __forceinline__ void fpass(const Tab<N>& TS, const uint8_t* __restrict__ kind,
                                       long long e0, double* base, int soff, int doff, int nv) {
   constexpr int NQF = ipow(N, D - 1);
   constexpr int NPEN = NQF / N;
   constexpr int ST = ipow(N, D - 2 - TAX);
-  const int items = nv * NF * KC * NPEN;
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+  constexpr int ITEMS = NE * NF * KC * NPEN;
+#pragma unroll
+  for (int rr = 0; rr < (ITEMS + TH - 1) / TH; ++rr) {
+    const int it = rr * TH + (int)threadIdx.x;
+    if ((ITEMS % TH) != 0 && it >= ITEMS) break;
     const int p = it % NPEN;
     int r = it / NPEN;
     const int c = r % KC;
     r /= KC;
     const int f = r % NF;
     const int e = r / NF;
+    if (e >= nv) continue;
     const uint8_t kraw = kind[(e0 + e) * NF + f];
     const int kd = kraw & 15;
     if (kd != KIND_CONF && kd != KIND_FINE) continue;
@@ -478,7 +487,8 @@ elem_kernel(const __grid_constant__ KParams<N> P) {
     for (int c = 0; c < KIN; ++c) A[c * NP + q] = load_input<D, N, OPK>(P, e0 + el, c, q);
   }
   // 4a (early). gather neighbour nodal face values: overlaps with the volume work
-  {
+  const bool do_faces = !(P.dbg & 1);
+  if (do_faces) {
     const int items = nv * NF * KIN * NQF;
     for (int it = tid; it < items; it += blockDim.x) {
       const int j = it % NQF;
@@ -498,15 +508,15 @@ elem_kernel(const __grid_constant__ KParams<N> P) {
   __syncthreads();
 
   // 2. nodes -> Gauss points
-  interp_all<D, N, KIN, E, NP>(TC.B, base, L::OFF_A, L::OFF_Q, L::OFF_T, nv);
+  interp_all<D, N, KIN, E, NP, L::EPB, L::THREADS>(TC.B, base, L::OFF_A, L::OFF_Q, L::OFF_T);
   // tangential passes of the gathered faces (independent buffers: no sync)
   if constexpr (D == 2) {
-    fpass<D, N, 0, KIN, E, NF>(TS, mesh.kind, e0, base, L::OFF_G, L::OFF_H, nv);
+    fpass<D, N, 0, KIN, E, NF, L::EPB, L::THREADS>(TS, mesh.kind, e0, base, L::OFF_G, L::OFF_H, nv);
   } else {
-    fpass<D, N, 0, KIN, E, NF>(TS, mesh.kind, e0, base, L::OFF_G, L::OFF_H, nv);
+    fpass<D, N, 0, KIN, E, NF, L::EPB, L::THREADS>(TS, mesh.kind, e0, base, L::OFF_G, L::OFF_H, nv);
   }
   __syncthreads();
-  if constexpr (D == 3) fpass<D, N, 1, KIN, E, NF>(TS, mesh.kind, e0, base, L::OFF_H, L::OFF_G, nv);
+  if constexpr (D == 3) fpass<D, N, 1, KIN, E, NF, L::EPB, L::THREADS>(TS, mesh.kind, e0, base, L::OFF_H, L::OFF_G, nv);
   constexpr int NB_OFF = (D == 2) ? L::OFF_H : L::OFF_G;  // neighbour traces at Gauss points
 
   // 3. metric + volume flux at this Gauss point
@@ -548,19 +558,18 @@ elem_kernel(const __grid_constant__ KParams<N> P) {
   // Z = -sum_bx Dhat^T_bx (w sum_a ctrv[bx][a] F_a)
   const bool flat = !P.gc.terrain;
   if constexpr (OPK == OP_GRAD) {
-    // flux tensor p I: with a diagonal adjugate only component BX moves in
-    // direction BX, so the flat path runs one pass per direction
-    if (flat) {
+    // flux tensor p I: Z starts at zero, every direction subtracts
 #pragma unroll
-      for (int k = 0; k < KOUT; ++k) Z[k * NP + q] = 0.0;
-    }
+    for (int k = 0; k < KOUT; ++k) Z[k * NP + q] = 0.0;
   }
   auto vol_dir = [&](auto bx_c) {
     constexpr int BX = decltype(bx_c)::value;
-    if (OPK == OP_GRAD && flat) {
+    // gradient: rows bx < d-1 of the adjugate are structurally diagonal
+    // (geometry.py:219-231), so only component bx moves in those directions
+    if (OPK == OP_GRAD && (flat || BX < D - 1)) {
       Tm[q] = F[BX][BX] * ctrv[BX][BX] * wq;
       __syncthreads();
-      vpass<D, N, BX, true, 2, 1, E, NP>(TC.Dhat, base, L::OFF_T, L::OFF_Z + BX * NP, nv);
+      vpass<D, N, BX, true, 2, 1, E, NP, L::EPB, L::THREADS>(TC.Dhat, base, L::OFF_T, L::OFF_Z + BX * NP);
       __syncthreads();
       return;
     }
@@ -577,7 +586,7 @@ elem_kernel(const __grid_constant__ KParams<N> P) {
       Tm[k * NP + q] = acc * wq;
     }
     __syncthreads();
-    vpass<D, N, BX, true, (BX == 0 ? 1 : 2), KOUT, E, NP>(TC.Dhat, base, L::OFF_T, L::OFF_Z, nv);
+    vpass<D, N, BX, true, (BX == 0 ? 1 : 2), KOUT, E, NP, L::EPB, L::THREADS>(TC.Dhat, base, L::OFF_T, L::OFF_Z);
     __syncthreads();
   };
   vol_dir(std::integral_constant<int, 0>{});
@@ -585,12 +594,14 @@ elem_kernel(const __grid_constant__ KParams<N> P) {
   if constexpr (D == 3) vol_dir(std::integral_constant<int, 2>{});
 
   // 4b. numerical fluxes on all faces (disjoint outputs per axis: no sync)
-  face_flux_axis<D, N, OPK, 0>(P, TS, base, e0, nv, NB_OFF);
-  face_flux_axis<D, N, OPK, 1>(P, TS, base, e0, nv, NB_OFF);
-  if constexpr (D == 3) face_flux_axis<D, N, OPK, 2>(P, TS, base, e0, nv, NB_OFF);
+  if (do_faces) {
+    face_flux_axis<D, N, OPK, 0>(P, TS, base, e0, nv, NB_OFF);
+    face_flux_axis<D, N, OPK, 1>(P, TS, base, e0, nv, NB_OFF);
+    if constexpr (D == 3) face_flux_axis<D, N, OPK, 2>(P, TS, base, e0, nv, NB_OFF);
+  }
   __syncthreads();
   // 4c. lift: Z[k][q] += lift[side][q_a] * L_{a,side}[k][q_t]
-  if (act) {
+  if (act && do_faces) {
     const double* Lb = base + el * E + L::OFF_L;
     int qi[D];
 #pragma unroll
@@ -633,30 +644,30 @@ elem_kernel(const __grid_constant__ KParams<N> P) {
   const double* res;
   if (P.mode == OUT_MINV) {
     if constexpr (D == 2) {
-      vpass<2, N, 1, false, 0, KOUT, E, NP>(TC.Binv, base, L::OFF_Z, L::OFF_T, nv);
+      vpass<2, N, 1, false, 0, KOUT, E, NP, L::EPB, L::THREADS>(TC.Binv, base, L::OFF_Z, L::OFF_T);
       __syncthreads();
-      vpass<2, N, 0, false, 0, KOUT, E, NP>(TC.Binv, base, L::OFF_T, L::OFF_Z, nv);
+      vpass<2, N, 0, false, 0, KOUT, E, NP, L::EPB, L::THREADS>(TC.Binv, base, L::OFF_T, L::OFF_Z);
       res = Z;
     } else {
-      vpass<3, N, 2, false, 0, KOUT, E, NP>(TC.Binv, base, L::OFF_Z, L::OFF_T, nv);
+      vpass<3, N, 2, false, 0, KOUT, E, NP, L::EPB, L::THREADS>(TC.Binv, base, L::OFF_Z, L::OFF_T);
       __syncthreads();
-      vpass<3, N, 1, false, 0, KOUT, E, NP>(TC.Binv, base, L::OFF_T, L::OFF_Z, nv);
+      vpass<3, N, 1, false, 0, KOUT, E, NP, L::EPB, L::THREADS>(TC.Binv, base, L::OFF_T, L::OFF_Z);
       __syncthreads();
-      vpass<3, N, 0, false, 0, KOUT, E, NP>(TC.Binv, base, L::OFF_Z, L::OFF_T, nv);
+      vpass<3, N, 0, false, 0, KOUT, E, NP, L::EPB, L::THREADS>(TC.Binv, base, L::OFF_Z, L::OFF_T);
       res = Tm;
     }
   } else {
     if constexpr (D == 2) {
-      vpass<2, N, 1, true, 0, KOUT, E, NP>(TC.B, base, L::OFF_Z, L::OFF_T, nv);
+      vpass<2, N, 1, true, 0, KOUT, E, NP, L::EPB, L::THREADS>(TC.B, base, L::OFF_Z, L::OFF_T);
       __syncthreads();
-      vpass<2, N, 0, true, 0, KOUT, E, NP>(TC.B, base, L::OFF_T, L::OFF_Z, nv);
+      vpass<2, N, 0, true, 0, KOUT, E, NP, L::EPB, L::THREADS>(TC.B, base, L::OFF_T, L::OFF_Z);
       res = Z;
     } else {
-      vpass<3, N, 2, true, 0, KOUT, E, NP>(TC.B, base, L::OFF_Z, L::OFF_T, nv);
+      vpass<3, N, 2, true, 0, KOUT, E, NP, L::EPB, L::THREADS>(TC.B, base, L::OFF_Z, L::OFF_T);
       __syncthreads();
-      vpass<3, N, 1, true, 0, KOUT, E, NP>(TC.B, base, L::OFF_T, L::OFF_Z, nv);
+      vpass<3, N, 1, true, 0, KOUT, E, NP, L::EPB, L::THREADS>(TC.B, base, L::OFF_T, L::OFF_Z);
       __syncthreads();
-      vpass<3, N, 0, true, 0, KOUT, E, NP>(TC.B, base, L::OFF_Z, L::OFF_T, nv);
+      vpass<3, N, 0, true, 0, KOUT, E, NP, L::EPB, L::THREADS>(TC.B, base, L::OFF_Z, L::OFF_T);
       res = Tm;
     }
   }

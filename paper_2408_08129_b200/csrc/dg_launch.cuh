@@ -18,6 +18,7 @@ struct OpArgs {
   MView out;
   double alpha, beta, coef;
   int has_K, has_base, homogeneous, mode;
+  int dbg;  // phase-skip flags for profiling experiments only (0 in production)
   double* mass_partial;
   const double* tabs;  // host pointer, Tab<N> layout
 };
@@ -50,6 +51,7 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
   P.has_base = a.has_base;
   P.homogeneous = a.homogeneous;
   P.mode = a.mode;
+  P.dbg = a.dbg;
   P.mass_partial = a.mass_partial;
   std::memcpy(&P.tab, a.tabs, sizeof(Tab<N>));
   const int grid = (a.mesh.n_el + L::EPB - 1) / L::EPB;

@@ -48,6 +48,7 @@ struct KParams {
   MView out;
   double alpha, beta, coef;
   int has_K, has_base, homogeneous, mode;
+  int dbg;  // phase-skip flags for profiling experiments only (0 in production)
   double* mass_partial;  // ADV: per-CTA sum of the density dual (or null)
   Tab<N> tab;
 };

@@ -6,6 +6,7 @@
 // threads (same contract as the reference's single driving thread).
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -127,6 +128,8 @@ OpArgs base_args(dg_ctx* c) {
   a.tabs = c->tabs.data();
   a.alpha = 1.0;
   a.coef = 1.0;
+  static const int dbg = getenv("DG_DEBUG_SKIP") ? atoi(getenv("DG_DEBUG_SKIP")) : 0;
+  a.dbg = dbg;
   return a;
 }
 
