@@ -47,7 +47,9 @@ struct Layout {
   static constexpr int OFF_G = OFF_T + KT * NP;
   static constexpr int OFF_H = OFF_G + NF * KIN * NQF;
   static constexpr int OFF_L = OFF_H + NF * KIN * NQF;
-  static constexpr int ELEM = OFF_L + NF * KOUT * NQF;
+  static constexpr int KW = (OPK == OP_GRAD) ? 1 : KOUT;  // comps per direction bx < d-1
+  static constexpr int OFF_W = OFF_L + NF * KOUT * NQF;
+  static constexpr int ELEM = OFF_W + (D - 1) * KW * NP;
   static constexpr int TABD = (int)(sizeof(Tab<N>) / sizeof(double));
   static constexpr int EPB_T = (128 / NP) > 1 ? (128 / NP) : 1;
   static constexpr int EPB_S = (12288 - TABD - 64) / ELEM > 1 ? (12288 - TABD - 64) / ELEM : 1;
@@ -555,43 +557,44 @@ elem_kernel(const __grid_constant__ KParams<N> P) {
 #pragma unroll
       for (int k = 0; k < KOUT; ++k) F[a][k] = (a == k) ? p : 0.0;
   }
-  // Z = -sum_bx Dhat^T_bx (w sum_a ctrv[bx][a] F_a)
+  // Z = -sum_bx Dhat^T_bx G_bx, G_bx = w sum_a ctrv[bx][a] F_a: every
+  // direction is written at once (bx < d-1 to W, bx = d-1 to T), passed in
+  // place concurrently and summed into Z in the lift phase -- one barrier
+  // instead of two per direction
   const bool flat = !P.gc.terrain;
+  constexpr int KW = L::KW;
+  double* W = base + el * E + L::OFF_W;
   if constexpr (OPK == OP_GRAD) {
-    // flux tensor p I: Z starts at zero, every direction subtracts
+    // rows bx < d-1 of the adjugate are structurally diagonal
+    // (geometry.py:219-231): only component bx moves in those directions
 #pragma unroll
-    for (int k = 0; k < KOUT; ++k) Z[k * NP + q] = 0.0;
-  }
-  auto vol_dir = [&](auto bx_c) {
-    constexpr int BX = decltype(bx_c)::value;
-    // gradient: rows bx < d-1 of the adjugate are structurally diagonal
-    // (geometry.py:219-231), so only component bx moves in those directions
-    if (OPK == OP_GRAD && (flat || BX < D - 1)) {
-      Tm[q] = F[BX][BX] * ctrv[BX][BX] * wq;
-      __syncthreads();
-      vpass<D, N, BX, true, 2, 1, E, NP, L::EPB, L::THREADS>(TC.Dhat, base, L::OFF_T, L::OFF_Z + BX * NP);
-      __syncthreads();
-      return;
-    }
+    for (int bx = 0; bx < D - 1; ++bx) W[bx * NP + q] = F[bx][bx] * ctrv[bx][bx] * wq;
 #pragma unroll
-    for (int k = 0; k < KOUT; ++k) {
-      double acc;
-      if (flat) {
-        acc = F[BX][k] * ctrv[BX][BX];
-      } else {
-        acc = 0.0;
+    for (int k = 0; k < KOUT; ++k) Tm[k * NP + q] = F[k][k] * ctrv[D - 1][k] * wq;
+  } else {
 #pragma unroll
-        for (int a = 0; a < D; ++a) acc += F[a][k] * ctrv[BX][a];
+    for (int bx = 0; bx < D; ++bx) {
+      double* dst = (bx < D - 1) ? W + bx * KOUT * NP : Tm;
+#pragma unroll
+      for (int k = 0; k < KOUT; ++k) {
+        double acc;
+        if (flat) {
+          acc = F[bx][k] * ctrv[bx][bx];
+        } else {
+          acc = 0.0;
+#pragma unroll
+          for (int a = 0; a < D; ++a) acc += F[a][k] * ctrv[bx][a];
+        }
+        dst[k * NP + q] = acc * wq;
       }
-      Tm[k * NP + q] = acc * wq;
     }
-    __syncthreads();
-    vpass<D, N, BX, true, (BX == 0 ? 1 : 2), KOUT, E, NP, L::EPB, L::THREADS>(TC.Dhat, base, L::OFF_T, L::OFF_Z);
-    __syncthreads();
-  };
-  vol_dir(std::integral_constant<int, 0>{});
-  vol_dir(std::integral_constant<int, 1>{});
-  if constexpr (D == 3) vol_dir(std::integral_constant<int, 2>{});
+  }
+  __syncthreads();
+  vpass<D, N, 0, true, 1, KW, E, NP, L::EPB, L::THREADS>(TC.Dhat, base, L::OFF_W, L::OFF_W);
+  if constexpr (D == 3)
+    vpass<D, N, 1, true, 1, KW, E, NP, L::EPB, L::THREADS>(TC.Dhat, base, L::OFF_W + KW * NP,
+                                                           L::OFF_W + KW * NP);
+  vpass<D, N, D - 1, true, 1, KOUT, E, NP, L::EPB, L::THREADS>(TC.Dhat, base, L::OFF_T, L::OFF_T);
 
   // 4b. numerical fluxes on all faces (disjoint outputs per axis: no sync)
   if (do_faces) {
@@ -600,23 +603,40 @@ elem_kernel(const __grid_constant__ KParams<N> P) {
     if constexpr (D == 3) face_flux_axis<D, N, OPK, 2>(P, TS, base, e0, nv, NB_OFF);
   }
   __syncthreads();
-  // 4c. lift: Z[k][q] += lift[side][q_a] * L_{a,side}[k][q_t]
-  if (act && do_faces) {
-    const double* Lb = base + el * E + L::OFF_L;
-    int qi[D];
+  // 4c. Z = (volume directions) + lift[side][q_a] * L_{a,side}[k][q_t]
+  if (act) {
+    double zk[KOUT];
 #pragma unroll
-    for (int a = 0; a < D; ++a) qi[a] = digit<D, N>(q, a);
+    for (int k = 0; k < KOUT; ++k) {
+      zk[k] = Tm[k * NP + q];
 #pragma unroll
-    for (int a = 0; a < D; ++a) {
-      int qf;
-      if constexpr (D == 2) qf = qi[1 - a];
-      else qf = (a == 0) ? qi[1] * N + qi[2] : (a == 1 ? qi[0] * N + qi[2] : qi[0] * N + qi[1]);
-      const double l0 = TS.lift[0][qi[a]], l1 = TS.lift[1][qi[a]];
-#pragma unroll
-      for (int k = 0; k < KOUT; ++k)
-        Z[k * NP + q] += l0 * Lb[((2 * a) * KOUT + k) * NQF + qf] +
-                         l1 * Lb[((2 * a + 1) * KOUT + k) * NQF + qf];
+      for (int bx = 0; bx < D - 1; ++bx) {
+        if constexpr (OPK == OP_GRAD) {
+          if (k == bx) zk[k] += W[bx * NP + q];
+        } else {
+          zk[k] += W[(bx * KOUT + k) * NP + q];
+        }
+      }
     }
+    if (do_faces) {
+      const double* Lb = base + el * E + L::OFF_L;
+      int qi[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) qi[a] = digit<D, N>(q, a);
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        int qf;
+        if constexpr (D == 2) qf = qi[1 - a];
+        else qf = (a == 0) ? qi[1] * N + qi[2] : (a == 1 ? qi[0] * N + qi[2] : qi[0] * N + qi[1]);
+        const double l0 = TS.lift[0][qi[a]], l1 = TS.lift[1][qi[a]];
+#pragma unroll
+        for (int k = 0; k < KOUT; ++k)
+          zk[k] += l0 * Lb[((2 * a) * KOUT + k) * NQF + qf] +
+                   l1 * Lb[((2 * a + 1) * KOUT + k) * NQF + qf];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < KOUT; ++k) Z[k * NP + q] = zk[k];
   }
 
   // 5. epilogue
