@@ -2,8 +2,10 @@
 // unit per dimension instantiates N = 2..7 and the three operator kinds).
 #pragma once
 #include <cstring>
+#include <cstdlib>
+#include <string>
 #include <type_traits>
-#include "dg_kernel.cuh"
+#include "dg_wkernel.cuh"
 
 namespace dg {
 
@@ -54,6 +56,45 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
   P.dbg = a.dbg;
   P.mass_partial = a.mass_partial;
   std::memcpy(&P.tab, a.tabs, sizeof(Tab<N>));
+  using WL = WLayout<D, N, OPK>;
+  if constexpr (WL::OK) {
+    // warp-element kernel (v3) for the Helmholtz pair unless DG_KERNEL=v2
+    static const bool use_w = !(getenv("DG_KERNEL") && std::string(getenv("DG_KERNEL")) == "v2");
+    if (use_w) {
+      constexpr int EPC = WL::EPW * WL::WPB;
+      const int wgrid = (a.mesh.n_el + EPC - 1) / EPC;
+      if (info) {
+        info->epb = EPC;
+        info->threads = WL::THREADS;
+        info->smem = WL::SMEM;
+        info->grid = wgrid;
+      }
+      if (wgrid == 0) return cudaSuccess;
+      static bool wconf = false;
+      if (!wconf) {
+        cudaError_t e = cudaFuncSetAttribute(welem_kernel<D, N, OPK>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)WL::SMEM);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(welem_kernel<D, N, OPK>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::CSMEM);
+        if (e != cudaSuccess) return e;
+        wconf = true;
+      }
+      welem_kernel<D, N, OPK><<<wgrid, WL::THREADS, WL::SMEM, st>>>(P);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      if (a.mesh.n_coarse > 0) {
+        coarse_kernel<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
+            P, a.mesh.coarse_list, a.mesh.n_coarse, nullptr);
+        e = cudaGetLastError();
+      }
+      return e;
+    }
+  }
   const int grid = (a.mesh.n_el + L::EPB - 1) / L::EPB;
   if (info) {
     info->epb = L::EPB;

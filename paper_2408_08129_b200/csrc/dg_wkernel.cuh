@@ -1,0 +1,415 @@
+// Warp-element DG operator kernel (v3) for the Helmholtz pair
+// (gradient H1 and div(hV) H2), fp64, sm_100a.
+//
+// Each element is owned by NC = n^(d-1) consecutive lanes of ONE warp; lane
+// c holds the z-column c of the element (points c*n + k, k = 0..n-1) in
+// registers.  Consequently:
+//   * z passes (interpolation, Dhat^T, B^-1) are register-only;
+//   * x / y passes go through a per-element shared-memory tile with a padded
+//     column stride, synchronised by __syncwarp() only -- the kernel has no
+//     CTA-wide barrier at all;
+//   * lane c also owns face point c of EVERY face, and that face point lies
+//     on the lane's pencil along the face normal: own traces are pencil
+//     contractions, neighbour traces are one global load per face followed
+//     by 2 tangential passes done with warp shuffles, and each face's lift
+//     is added straight onto the lane's normal-direction pencil while that
+//     direction's volume pass is in registers.
+// Same algebra and reference citations as dg_kernel.cuh (weak form
+// dgops.py:87-230, centred fluxes dgops.py:343-348 / 452-460, metric
+// geometry.py:204-238 / 305-357, factorised mass inverse geometry.py:372-396).
+// The coarse side of hanging faces is added afterwards by coarse_kernel.
+#pragma once
+#include "dg_kernel.cuh"
+
+namespace dg {
+
+template <int D, int N, int OPK>
+struct WLayout {
+  static constexpr int NP = ipow(N, D);
+  static constexpr int NC = ipow(N, D - 1);  // lanes per element
+  static constexpr int EPW = 32 / NC;          // elements per warp
+  static constexpr int KIN = OpDims<D, OPK>::KIN;
+  static constexpr int KOUT = OpDims<D, OPK>::KOUT;
+  static constexpr int KW = (OPK == OP_GRAD) ? 1 : KOUT;
+  static constexpr int CS = N + 1;             // padded column stride
+  static constexpr int TSZ = NC * CS;          // one tensor
+  static constexpr int KX0 = KIN > KOUT ? KIN : KOUT;
+  static constexpr int KX1 = (D - 1) * KW;
+  static constexpr int KX = KX0 > KX1 ? KX0 : KX1;
+  static constexpr int SLOT = ((KX * TSZ) % 2 == 0) ? KX * TSZ + 1 : KX * TSZ;  // odd: bank shift
+  static constexpr int WPB = 4;                // warps per CTA
+  static constexpr int THREADS = 32 * WPB;
+  static constexpr int TABD = (int)(sizeof(Tab<N>) / sizeof(double));
+  static constexpr size_t SMEM = (size_t)(TABD + WPB * (EPW + 1) * SLOT) * sizeof(double);
+  static constexpr bool OK = (NC <= 32) && (OPK != OP_ADV);
+};
+
+// pencil helpers on the per-element tile (3D: (i, j) column index c = i*N + j)
+template <int D, int N>
+__device__ __forceinline__ int xoff(int c, int ii) {  // x-pencil of lane c, point ii
+  if constexpr (D == 3) return (ii * N + c / N) * (N + 1) + c % N;
+  else return ii * (N + 1) + c;
+}
+template <int N>
+__device__ __forceinline__ int yoff(int c, int jj) {  // 3D y-pencil of lane c, point jj
+  return ((c / N) * N + jj) * (N + 1) + c % N;
+}
+
+template <int N, bool TRANS>
+__device__ __forceinline__ void mat_apply(const double (&M)[N][N], const double* v, double* o) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) acc = fma(TRANS ? M[j][i] : M[i][j], v[j], acc);
+    o[i] = acc;
+  }
+}
+
+template <int D, int N, int OPK>
+__global__ void __launch_bounds__(WLayout<D, N, OPK>::THREADS)
+welem_kernel(const __grid_constant__ KParams<N> P) {
+  using WL = WLayout<D, N, OPK>;
+  constexpr int NP = WL::NP, NC = WL::NC, EPW = WL::EPW, KIN = WL::KIN, KOUT = WL::KOUT;
+  constexpr int KW = WL::KW, TSZ = WL::TSZ, NF = 2 * D;
+  extern __shared__ double smem[];
+  {
+    const double* src = reinterpret_cast<const double*>(&P.tab);
+    for (int i = threadIdx.x; i < WL::TABD; i += blockDim.x) smem[i] = src[i];
+  }
+  __syncthreads();  // the only CTA barrier: tables
+  const Tab<N>& TS = *reinterpret_cast<const Tab<N>*>(smem);
+  const Tab<N>& TC = P.tab;
+  const MeshDev& mesh = P.mesh;
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int eiw = lane / NC;
+  const int c = lane - eiw * NC;
+  const bool slot_ok = eiw < EPW;
+  const long long e = ((long long)blockIdx.x * WL::WPB + wid) * EPW + eiw;
+  const bool act = slot_ok && e < mesh.n_el;
+  const long long es = act ? e : 0;
+  const int b0 = slot_ok ? eiw * NC : 0;  // first lane of this element
+  // padding lanes (32 % NC != 0) scribble on a private scratch slot
+  double* X = smem + WL::TABD + (wid * (EPW + 1) + (slot_ok ? eiw : EPW)) * WL::SLOT;
+  const bool flat = !P.gc.terrain;
+
+  // ---- 1. nodal column, z interpolation in registers -------------------
+  double q[KIN][N];
+#pragma unroll
+  for (int cp = 0; cp < KIN; ++cp) {
+    double a[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) a[k] = act ? load_input<D, N, OPK>(P, es, cp, c * N + k) : 0.0;
+    mat_apply<N, false>(TC.B, a, q[cp]);
+  }
+  // ---- 2. x (and y) interpolation through the tile ------------------------
+#pragma unroll
+  for (int cp = 0; cp < KIN; ++cp)
+#pragma unroll
+    for (int k = 0; k < N; ++k) X[cp * TSZ + c * (N + 1) + k] = q[cp][k];
+  __syncwarp();
+  if constexpr (D == 3) {
+#pragma unroll
+    for (int cp = 0; cp < KIN; ++cp) {
+      double v[N], o[N];
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj) v[jj] = X[cp * TSZ + yoff<N>(c, jj)];
+      mat_apply<N, false>(TC.B, v, o);
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj) X[cp * TSZ + yoff<N>(c, jj)] = o[jj];
+    }
+    __syncwarp();
+  }
+  // x pass; the x-pencil of lane c carries face point c of both x faces
+  double tox[2][KIN];
+#pragma unroll
+  for (int cp = 0; cp < KIN; ++cp) {
+    double v[N], o[N];
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii) v[ii] = X[cp * TSZ + xoff<D, N>(c, ii)];
+    mat_apply<N, false>(TC.B, v, o);
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii) X[cp * TSZ + xoff<D, N>(c, ii)] = o[ii];
+    double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii) {
+      t0 = fma(TC.lift[0][ii], o[ii], t0);
+      t1 = fma(TC.lift[1][ii], o[ii], t1);
+    }
+    tox[0][cp] = t0;
+    tox[1][cp] = t1;
+  }
+  __syncwarp();
+  double toy[2][KIN];
+#pragma unroll
+  for (int cp = 0; cp < KIN; ++cp) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) q[cp][k] = X[cp * TSZ + c * (N + 1) + k];
+    if constexpr (D == 3) {
+      double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj) {
+        const double v = X[cp * TSZ + yoff<N>(c, jj)];
+        t0 = fma(TC.lift[0][jj], v, t0);
+        t1 = fma(TC.lift[1][jj], v, t1);
+      }
+      toy[0][cp] = t0;
+      toy[1][cp] = t1;
+    }
+  }
+  // ---- 3. faces: flux at face point c of every face --------------------
+  // fl_l[f][k]: lifted flux*ws (with sign) at face point c of face f
+  double fl[NF][KOUT];
+  const uint8_t* kind_e = mesh.kind + es * NF;
+  const int* nbr_e = mesh.nbr + es * NF;
+  const ElemGeo<D> g = elem_geo<D>(mesh.elem, P.gc, es);
+  auto face = [&](auto ax_c, int side) {
+    constexpr int AX = decltype(ax_c)::value;
+    const int f = 2 * AX + side;
+    const uint8_t kraw = kind_e[f];
+    const int kd = kraw & 15;
+    const bool inter = (kd == KIND_CONF || kd == KIND_FINE);
+    const long long nb = nbr_e[f];
+    // neighbour trace at face point c: gather node c of the neighbour's
+    // opposite face, then tangential passes across the element's lanes
+    double TN[KIN], TO[KIN];
+    const int fa = (D == 2) ? c : c / N;   // tangential index t0
+    const int fb = (D == 2) ? 0 : c % N;   // tangential index t1
+    const int sf = (kraw >> 4) & 3;
+    const double* M0 = (kd == KIND_FINE) ? &TS.half[sf & 1][0][0] : &TS.B[0][0];
+    const double* M1 = (kd == KIND_FINE) ? &TS.half[(sf >> 1) & 1][0][0] : &TS.B[0][0];
+#pragma unroll
+    for (int cp = 0; cp < KIN; ++cp) {
+      double gval = 0.0;
+      if (act && inter) {
+        int node;
+        // node of face point c on the neighbour's face (AX, 1 - side)
+        const int endn = (1 - side) ? N - 1 : 0;
+        if constexpr (D == 2) {
+          node = (AX == 0) ? endn * N + c : c * N + endn;
+        } else {
+          if (AX == 0) node = (endn * N + fa) * N + fb;
+          else if (AX == 1) node = (fa * N + endn) * N + fb;
+          else node = (fa * N + fb) * N + endn;
+        }
+        gval = load_input<D, N, OPK>(P, nb, cp, node);
+      }
+      double t1v = 0.0;
+      if constexpr (D == 2) {
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+          t1v = fma(M0[fa * N + j], __shfl_sync(0xffffffffu, gval, b0 + j), t1v);
+        TN[cp] = t1v;
+      } else {
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+          t1v = fma(M0[fa * N + j], __shfl_sync(0xffffffffu, gval, b0 + j * N + fb), t1v);
+        double t2v = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+          t2v = fma(M1[fb * N + j], __shfl_sync(0xffffffffu, t1v, b0 + fa * N + j), t2v);
+        TN[cp] = t2v;
+      }
+      // own trace
+      if constexpr (AX == D - 1) {
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) t = fma(TC.lift[side][k], q[cp][k], t);
+        TO[cp] = t;
+      } else if constexpr (AX == 0) {
+        TO[cp] = tox[side][cp];
+      } else {
+        TO[cp] = toy[side][cp];
+      }
+    }
+    if (kd == KIND_COARSE || !act) {
+#pragma unroll
+      for (int k = 0; k < KOUT; ++k) fl[f][k] = 0.0;
+      return;
+    }
+    const bool outward = (kd == KIND_WALL || kd == KIND_FARFIELD);
+    const bool own_metric = !(kd == KIND_CONF && side == 0);
+    const ElemGeo<D> og = own_metric ? g : elem_geo<D>(mesh.elem, P.gc, nb);
+    double n[D], ws;
+    face_metric_ax<D, N, AX>(P.gc, mesh.col, og, own_metric ? side : 1, outward, c, TS, n, ws);
+    if (outward) ghost<D, N, OPK, KIN>(P, kd, nb, c, TO, n, TN);
+    const bool minus = outward || side == 1;
+    double TLv[KIN], TRv[KIN];
+#pragma unroll
+    for (int cp = 0; cp < KIN; ++cp) {
+      TLv[cp] = minus ? TO[cp] : TN[cp];
+      TRv[cp] = minus ? TN[cp] : TO[cp];
+    }
+    double fv[KOUT];
+    num_flux<D, OPK, KIN, KOUT>(TLv, TRv, n, P.model.kinetic_factor, fv);
+    const double sg = minus ? ws : -ws;
+#pragma unroll
+    for (int k = 0; k < KOUT; ++k) fl[f][k] = fv[k] * sg;
+  };
+  face(std::integral_constant<int, 0>{}, 0);
+  face(std::integral_constant<int, 0>{}, 1);
+  face(std::integral_constant<int, 1>{}, 0);
+  face(std::integral_constant<int, 1>{}, 1);
+  if constexpr (D == 3) {
+    face(std::integral_constant<int, 2>{}, 0);
+    face(std::integral_constant<int, 2>{}, 1);
+  }
+
+  // ---- 4. volume: metric + flux per column point -------------------------
+  __syncwarp();  // every lane is done reading Q from the tile
+  double Zc[KOUT][N];
+  double det_c = 1.0;  // det J is z-independent: one value per column
+  {
+    double Gz[KOUT][N];
+#pragma unroll
+    for (int kz = 0; kz < N; ++kz) {
+      const int qp = c * N + kz;
+      double det, ctrv[D][D];
+      point_metric<D, N>(P, g, qp, det, ctrv);
+      const double wq = point_weight<D, N>(TC, qp);
+      double F[D][KOUT];
+      if constexpr (OPK == OP_DIVHV) {
+        const double h = q[D][kz];
+#pragma unroll
+        for (int a = 0; a < D; ++a) F[a][0] = h * q[a][kz];
+      } else {
+        const double p = q[0][kz];
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+          for (int k = 0; k < KOUT; ++k) F[a][k] = (a == k) ? p : 0.0;
+      }
+#pragma unroll
+      for (int bx = 0; bx < D; ++bx) {
+#pragma unroll
+        for (int k = 0; k < KOUT; ++k) {
+          double acc;
+          if (OPK == OP_GRAD) {
+            acc = F[k][k] * ctrv[bx][k];
+          } else if (flat) {
+            acc = F[bx][k] * ctrv[bx][bx];
+          } else {
+            acc = 0.0;
+#pragma unroll
+            for (int a = 0; a < D; ++a) acc += F[a][k] * ctrv[bx][a];
+          }
+          acc *= wq;
+          if (bx == D - 1) {
+            Gz[k][kz] = acc;
+          } else if (OPK == OP_GRAD) {
+            if (k == bx) X[(bx * KW) * TSZ + c * (N + 1) + kz] = acc;
+          } else {
+            X[(bx * KW + k) * TSZ + c * (N + 1) + kz] = acc;
+          }
+        }
+      }
+      det_c = det;
+    }
+    // z direction in registers: Zc = -Dhat^T Gz + z-face lifts
+#pragma unroll
+    for (int k = 0; k < KOUT; ++k) {
+      mat_apply<N, true>(TC.Dhat, Gz[k], Zc[k]);
+#pragma unroll
+      for (int kz = 0; kz < N; ++kz)
+        Zc[k][kz] = TC.lift[0][kz] * fl[2 * (D - 1)][k] + TC.lift[1][kz] * fl[2 * (D - 1) + 1][k] -
+                    Zc[k][kz];
+    }
+  }
+  __syncwarp();
+  // x (and y) directions on the lane's pencils, with that direction's lifts
+#pragma unroll
+  for (int k = 0; k < KW; ++k) {
+    const int kx = (OPK == OP_GRAD) ? 0 : k;
+    double* T0 = X + (0 * KW + k) * TSZ;
+    double v[N], o[N];
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii) v[ii] = T0[xoff<D, N>(c, ii)];
+    mat_apply<N, true>(TC.Dhat, v, o);
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii)
+      T0[xoff<D, N>(c, ii)] = TC.lift[0][ii] * fl[0][kx] + TC.lift[1][ii] * fl[1][kx] - o[ii];
+    if constexpr (D == 3) {
+      const int ky = (OPK == OP_GRAD) ? 1 : k;
+      double* T1 = X + (1 * KW + k) * TSZ;
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj) v[jj] = T1[yoff<N>(c, jj)];
+      mat_apply<N, true>(TC.Dhat, v, o);
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj)
+        T1[yoff<N>(c, jj)] = TC.lift[0][jj] * fl[2][ky] + TC.lift[1][jj] * fl[3][ky] - o[jj];
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int kz = 0; kz < N; ++kz) {
+    if constexpr (OPK == OP_GRAD) {
+      Zc[0][kz] += X[0 * TSZ + c * (N + 1) + kz];
+      if constexpr (D == 3) Zc[1][kz] += X[1 * TSZ + c * (N + 1) + kz];
+    } else {
+#pragma unroll
+      for (int k = 0; k < KOUT; ++k) {
+        Zc[k][kz] += X[(0 * KW + k) * TSZ + c * (N + 1) + kz];
+        if constexpr (D == 3) Zc[k][kz] += X[(1 * KW + k) * TSZ + c * (N + 1) + kz];
+      }
+    }
+  }
+  // ---- 5. epilogue: B^-1 diag(1/(w det)) (MINV) or B^T (DUAL) -----------
+  const bool minv = (P.mode == OUT_MINV);
+#pragma unroll
+  for (int k = 0; k < KOUT; ++k) {
+    double t[N];
+    if (minv) {
+#pragma unroll
+      for (int kz = 0; kz < N; ++kz)
+        t[kz] = Zc[k][kz] * (1.0 / (point_weight<D, N>(TC, c * N + kz) * det_c));
+      mat_apply<N, false>(TC.Binv, t, Zc[k]);
+    } else {
+#pragma unroll
+      for (int kz = 0; kz < N; ++kz) t[kz] = Zc[k][kz];
+      mat_apply<N, true>(TC.B, t, Zc[k]);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < KOUT; ++k)
+#pragma unroll
+    for (int kz = 0; kz < N; ++kz) X[k * TSZ + c * (N + 1) + kz] = Zc[k][kz];
+  __syncwarp();
+  if constexpr (D == 3) {
+#pragma unroll
+    for (int k = 0; k < KOUT; ++k) {
+      double v[N], o[N];
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj) v[jj] = X[k * TSZ + yoff<N>(c, jj)];
+      if (minv) mat_apply<N, false>(TC.Binv, v, o);
+      else mat_apply<N, true>(TC.B, v, o);
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj) X[k * TSZ + yoff<N>(c, jj)] = o[jj];
+    }
+    __syncwarp();
+  }
+  if (!act) return;
+  // x pass and store from the x-pencil: points (ii, [j,] k) of lane c
+#pragma unroll
+  for (int k = 0; k < KOUT; ++k) {
+    double v[N], o[N];
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii) v[ii] = X[k * TSZ + xoff<D, N>(c, ii)];
+    if (minv) mat_apply<N, false>(TC.Binv, v, o);
+    else mat_apply<N, true>(TC.B, v, o);
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii) {
+      const int node = (D == 3) ? ii * N * N + c : ii * N + c;
+      double* out = P.out.p + e * P.out.estride + (long long)k * P.out.cstride + node;
+      if (!minv) {
+        *out = o[ii];
+      } else {
+        const double r = __dmul_rn(P.coef, o[ii]);
+        *out = P.has_base ? __dadd_rn(P.base(e, k, node), r) : r;
+      }
+    }
+  }
+}
+
+}  // namespace dg
