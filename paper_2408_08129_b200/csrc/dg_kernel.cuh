@@ -66,7 +66,8 @@ struct Layout {
   static constexpr int C_FW = C_A + KIN * NP;
   static constexpr int C_Z = C_FW + NF * S * KOUT * NQF;
   static constexpr int C_T = C_Z + KOUT * NP;
-  static constexpr int CELEM = C_T + KOUT * NP;
+  static constexpr int C_CH = C_T + KOUT * NP;  // children's nodal face values
+  static constexpr int CELEM = C_CH + NF * S * KIN * NQF;
   static constexpr size_t CSMEM = (size_t)(TABD + 64 + CELEM) * sizeof(double);
 };
 
@@ -754,6 +755,23 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
   if (act)
     for (int c = 0; c < KIN; ++c) A[c * NP + q] = load_input<D, N, OPK>(P, e, c, q);
   __syncthreads();
+  // stage the children's nodal face values (coalescing the L2 gathers)
+  __shared__ short cfnode[NF * NQF];
+  for (int i = threadIdx.x; i < NF * NQF; i += blockDim.x)
+    cfnode[i] = (short)face_to_vol<D, N>((i / NQF) >> 1, (i / NQF) & 1, i % NQF);
+  double* CH = red + 64 + L::C_CH;
+  for (int it = threadIdx.x; it < NF * S * KIN * NQF; it += blockDim.x) {
+    const int j = it % NQF;
+    int r = it / NQF;
+    const int cp = r % KIN;
+    r /= KIN;
+    const int sub = r % S;
+    const int f = r / S;
+    if ((mesh.kind[e * NF + f] & 15) != KIND_COARSE) continue;
+    const long long child = mesh.hang_children[(long long)mesh.nbr[e * NF + f] * S + sub];
+    CH[it] = load_input<D, N, OPK>(P, child, cp, face_to_vol<D, N>(f >> 1, 1 - (f & 1), j));
+  }
+  __syncthreads();
   // subface fluxes of every coarse face
   for (int it = threadIdx.x; it < NF * S * NQF; it += blockDim.x) {
     const int qf = it % NQF;
@@ -767,6 +785,7 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
     const int qt1 = (D == 2) ? 0 : qf % N;
     const int b0 = sub & 1, b1 = (sub >> 1) & 1;
     double TO[KIN], TN[KIN];
+    const double* chv = CH + ((f * S + sub) * KIN) * NQF;
 #pragma unroll
     for (int c = 0; c < KIN; ++c) {
       double ao = 0.0, an = 0.0;
@@ -779,8 +798,8 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
           mo *= T.half[b1][qt1][j1];
           mb *= T.B[qt1][j1];
         }
-        ao = fma(mo, A[c * NP + face_to_vol<D, N>(axis, side, j)], ao);
-        an = fma(mb, load_input<D, N, OPK>(P, child, c, face_to_vol<D, N>(axis, 1 - side, j)), an);
+        ao = fma(mo, A[c * NP + cfnode[f * NQF + j]], ao);
+        an = fma(mb, chv[c * NQF + j], an);
       }
       TO[c] = ao;
       TN[c] = an;

@@ -67,7 +67,7 @@ __device__ __forceinline__ void mat_apply(const double (&M)[N][N], const double*
 }
 
 template <int D, int N, int OPK>
-__global__ void __launch_bounds__(WLayout<D, N, OPK>::THREADS)
+__global__ void __launch_bounds__(WLayout<D, N, OPK>::THREADS, 4)
 welem_kernel(const __grid_constant__ KParams<N> P) {
   using WL = WLayout<D, N, OPK>;
   constexpr int NP = WL::NP, NC = WL::NC, EPW = WL::EPW, KIN = WL::KIN, KOUT = WL::KOUT;
