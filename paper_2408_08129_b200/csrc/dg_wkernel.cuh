@@ -55,6 +55,21 @@ __device__ __forceinline__ int yoff(int c, int jj) {  // 3D y-pencil of lane c, 
   return ((c / N) * N + jj) * (N + 1) + c % N;
 }
 
+// nodal index of face point c (tangential C-order) on the NEIGHBOUR's face
+// (ax, 1 - side), i.e. the node this lane gathers for its face (ax, side)
+template <int D, int N>
+__device__ __forceinline__ int nbr_face_node(int ax, int side, int c) {
+  const int endn = (1 - side) ? N - 1 : 0;
+  if constexpr (D == 2) {
+    return (ax == 0) ? endn * N + c : c * N + endn;
+  } else {
+    const int fa = c / N, fb = c % N;
+    if (ax == 0) return (endn * N + fa) * N + fb;
+    if (ax == 1) return (fa * N + endn) * N + fb;
+    return (fa * N + fb) * N + endn;
+  }
+}
+
 template <int N, bool TRANS>
 __device__ __forceinline__ void mat_apply(const double (&M)[N][N], const double* v, double* o) {
 #pragma unroll
@@ -94,6 +109,31 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
   double* X = smem + WL::TABD + (wid * (EPW + 1) + (slot_ok ? eiw : EPW)) * WL::SLOT;
   const bool flat = !P.gc.terrain;
 
+  // ---- 0. face records, and (small KIN) the neighbour face-node values,
+  // issued first so their L2 latency overlaps the interpolation work
+  const uint8_t* kind_e = mesh.kind + es * NF;
+  const int* nbr_e = mesh.nbr + es * NF;
+  uint8_t kf[NF];
+  int nf[NF];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    kf[f] = act ? kind_e[f] : (uint8_t)KIND_WALL;
+    nf[f] = act ? nbr_e[f] : 0;
+  }
+  constexpr bool PRE = KIN <= 2;
+  double gpre[PRE ? NF : 1][PRE ? KIN : 1];
+  if constexpr (PRE) {
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      const int kd = kf[f] & 15;
+      const bool inter = act && (kd == KIND_CONF || kd == KIND_FINE);
+#pragma unroll
+      for (int cp = 0; cp < KIN; ++cp)
+        gpre[f][cp] = inter ? load_input<D, N, OPK>(P, nf[f], cp,
+                                                   nbr_face_node<D, N>(f >> 1, f & 1, c))
+                            : 0.0;
+    }
+  }
   // ---- 1. nodal column, z interpolation in registers -------------------
   double q[KIN][N];
 #pragma unroll
@@ -161,16 +201,14 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
   // ---- 3. faces: flux at face point c of every face --------------------
   // fl_l[f][k]: lifted flux*ws (with sign) at face point c of face f
   double fl[NF][KOUT];
-  const uint8_t* kind_e = mesh.kind + es * NF;
-  const int* nbr_e = mesh.nbr + es * NF;
   const ElemGeo<D> g = elem_geo<D>(mesh.elem, P.gc, es);
   auto face = [&](auto ax_c, int side) {
     constexpr int AX = decltype(ax_c)::value;
     const int f = 2 * AX + side;
-    const uint8_t kraw = kind_e[f];
+    const uint8_t kraw = kf[f];
     const int kd = kraw & 15;
     const bool inter = (kd == KIND_CONF || kd == KIND_FINE);
-    const long long nb = nbr_e[f];
+    const long long nb = nf[f];
     // neighbour trace at face point c: gather node c of the neighbour's
     // opposite face, then tangential passes across the element's lanes
     double TN[KIN], TO[KIN];
@@ -182,18 +220,10 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
 #pragma unroll
     for (int cp = 0; cp < KIN; ++cp) {
       double gval = 0.0;
-      if (act && inter) {
-        int node;
-        // node of face point c on the neighbour's face (AX, 1 - side)
-        const int endn = (1 - side) ? N - 1 : 0;
-        if constexpr (D == 2) {
-          node = (AX == 0) ? endn * N + c : c * N + endn;
-        } else {
-          if (AX == 0) node = (endn * N + fa) * N + fb;
-          else if (AX == 1) node = (fa * N + endn) * N + fb;
-          else node = (fa * N + fb) * N + endn;
-        }
-        gval = load_input<D, N, OPK>(P, nb, cp, node);
+      if constexpr (PRE) {
+        gval = gpre[f][cp];
+      } else if (act && inter) {
+        gval = load_input<D, N, OPK>(P, nb, cp, nbr_face_node<D, N>(AX, side, c));
       }
       double t1v = 0.0;
       if constexpr (D == 2) {
