@@ -37,10 +37,10 @@ __device__ __forceinline__ double wdet_at(const int* elem, const double* col, co
   constexpr int NQH = ipow(N, D - 1);
   const ElemGeo<D> g = elem_geo<D>(elem, gc, e);
   const int qh = q / N;
-  double hq = 0.0;
-  if (gc.terrain) hq = col[(long long)g.col * gc.col_stride + qh];
+  double omh = 1.0;  // 1 - h/z_top (column table)
+  if (gc.terrain) omh = col[(long long)g.col * gc.col_stride + qh];
   (void)NQH;
-  const double zz = g.s[D - 1] * (1.0 - hq / gc.z_top);
+  const double zz = g.s[D - 1] * omh;
   double det = 1.0;
   for (int a = 0; a < D - 1; ++a) det = det * g.s[a];
   det = det * zz;

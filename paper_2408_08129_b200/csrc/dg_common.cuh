@@ -36,6 +36,7 @@ struct Tab {
   double halfq[2][N][N];  // half[s] B^-1 (mortar acting on Gauss traces)
   double qw[N];
   double qx[N];
+  double iqw[N];       // 1 / qw (mass-inverse epilogue without divisions)
 };
 
 struct Model {

@@ -184,12 +184,12 @@ __device__ __forceinline__ void face_metric_ax(const GeoConst& gc, const double*
   for (int a = 0; a < D; ++a) n[a] = 0.0;
   if constexpr (AX < D - 1) {
     const int qo = (D == 2) ? 0 : qf / N;
-    double he = 0.0;
+    double omh = 1.0;  // 1 - h_edge/z_top from the column table
     if (gc.terrain) {
       constexpr int NE = ipow(N, HD - 1);
-      he = col[(long long)g.col * gc.col_stride + NQH * (1 + HD) + (AX * 2 + oside) * NE + qo];
+      omh = col[(long long)g.col * gc.col_stride + NQH * (1 + HD) + (AX * 2 + oside) * NE + qo];
     }
-    const double zzv = g.s[D - 1] * (1.0 - he / gc.z_top);
+    const double zzv = g.s[D - 1] * omh;
     const double mag = (D == 2) ? zzv : g.s[1 - AX] * zzv;
     n[AX] = sgn;
     ws = fw * fabs(mag);
@@ -341,15 +341,15 @@ __device__ __forceinline__ void point_metric(const KParams<N>& P, const ElemGeo<
     }
     return;
   }
-  double hq = 0.0, dhq[2] = {0.0, 0.0};
+  double omh, dhq[2] = {0.0, 0.0};
   {
     const double* c = P.mesh.col + (long long)g.col * P.gc.col_stride;
-    hq = c[qh];
+    omh = c[qh];  // 1 - h/z_top
 #pragma unroll
     for (int a = 0; a < HD; ++a) dhq[a] = c[NQH + a * NQH + qh];
   }
   const double zt = P.gc.z_top;
-  const double zz = g.s[D - 1] * (1.0 - hq / zt);
+  const double zz = g.s[D - 1] * omh;
   det = 1.0;
 #pragma unroll
   for (int a = 0; a < HD; ++a) det = det * g.s[a];

@@ -114,66 +114,4 @@ __device__ __forceinline__ void pass1d(const double* __restrict__ M, const doubl
   }
 }
 
-// face metric (geometry.py:305-357) of the owner's (axis, oside) face at
-// face Gauss point qf; returns unit normal (+axis oriented, or outward) and
-// the quadrature weight times the surface Jacobian.
-template <int D, int N>
-__device__ __forceinline__ void face_metric(const GeoConst& gc, const double* __restrict__ col,
-                                            const ElemGeo<D>& g, int axis, int oside,
-                                            bool outward, int qf, const double* qw,
-                                            double n[D], double& ws) {
-  constexpr int HD = D - 1;
-  constexpr int NQH = ipow(N, HD);
-  const double zt = gc.z_top;
-  double nt[D];
-  double fw;
-  if (axis == D - 1) {
-    double dh[2] = {0.0, 0.0};
-    if (gc.terrain) {
-      const double* c = col + (long long)g.col * gc.col_stride;
-      for (int a = 0; a < HD; ++a) dh[a] = c[NQH + a * NQH + qf];
-    }
-    const double decay = 1.0 - (g.lo[D - 1] + g.s[D - 1] * (double)oside) / zt;
-    if (D == 2) {
-      nt[0] = -dh[0] * g.s[0] * decay;
-      nt[1] = g.s[0];
-      fw = qw[qf];
-    } else {
-      nt[0] = -g.s[1] * dh[0] * g.s[0] * decay;
-      nt[1] = -g.s[0] * dh[1] * g.s[1] * decay;
-      nt[D - 1] = g.s[0] * g.s[1];
-      fw = qw[qf / N] * qw[qf % N];
-    }
-  } else {
-    const int qo = (D == 2) ? 0 : qf / N;
-    double he = 0.0;
-    if (gc.terrain) {
-      const double* c = col + (long long)g.col * gc.col_stride;
-      constexpr int NE = ipow(N, HD - 1);
-      he = c[NQH * (1 + HD) + (axis * 2 + oside) * NE + qo];
-    }
-    const double zzv = g.s[D - 1] * (1.0 - he / zt);
-#pragma unroll
-    for (int a = 0; a < D; ++a) nt[a] = 0.0;
-    if (D == 2) {
-      nt[0] = zzv;
-      fw = qw[qf];
-    } else {
-      nt[axis] = g.s[1 - axis] * zzv;
-      fw = qw[qf / N] * qw[qf % N];
-    }
-  }
-  if (outward && oside == 0) {
-#pragma unroll
-    for (int a = 0; a < D; ++a) nt[a] = -nt[a];
-  }
-  double m2 = 0.0;
-#pragma unroll
-  for (int a = 0; a < D; ++a) m2 += nt[a] * nt[a];
-  const double mag = sqrt(m2);
-#pragma unroll
-  for (int a = 0; a < D; ++a) n[a] = nt[a] / mag;
-  ws = fw * mag;
-}
-
 }  // namespace dg

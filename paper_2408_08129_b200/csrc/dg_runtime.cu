@@ -541,7 +541,7 @@ int dg_ctx_create(const dg_ctx_desc* d, dg_ctx** out) {
   c->n_tot = d->n_tot;
   c->n_global = (long long)d->n_el * np;
   const int N = c->N;
-  const int expect_tabs = 3 * N * N + 2 * N + 4 * N * N + 2 * N;
+  const int expect_tabs = 3 * N * N + 2 * N + 4 * N * N + 3 * N;
   if (d->tabs_len != expect_tabs) {
     delete c;
     return fail(DG_ERR_USAGE, "basis table length mismatch");

@@ -386,13 +386,16 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
   }
   // ---- 5. epilogue: B^-1 diag(1/(w det)) (MINV) or B^T (DUAL) -----------
   const bool minv = (P.mode == OUT_MINV);
+  // 1/(w det): det is z-independent, 1/w a product of 1D reciprocals
+  double iwh = 1.0 / det_c;
+  if constexpr (D == 3) iwh *= TC.iqw[c / N] * TC.iqw[c % N];
+  else iwh *= TC.iqw[c];
 #pragma unroll
   for (int k = 0; k < KOUT; ++k) {
     double t[N];
     if (minv) {
 #pragma unroll
-      for (int kz = 0; kz < N; ++kz)
-        t[kz] = Zc[k][kz] * (1.0 / (point_weight<D, N>(TC, c * N + kz) * det_c));
+      for (int kz = 0; kz < N; ++kz) t[kz] = Zc[k][kz] * (iwh * TC.iqw[kz]);
       mat_apply<N, false>(TC.Binv, t, Zc[k]);
     } else {
 #pragma unroll

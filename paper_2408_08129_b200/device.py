@@ -32,7 +32,7 @@ def basis_tables(basis):
                          "(the factorised B^-1 mass inverse, SURVEY.md §7)")
     parts = [basis.interp_1d, basis.Binv, basis.Dhat, basis.lift,
              np.stack(basis.half_interp_1d), np.stack(basis.half_q),
-             basis.quad_w, basis.quad_x]
+             basis.quad_w, basis.quad_x, 1.0 / basis.quad_w]
     return np.ascontiguousarray(np.concatenate([np.asarray(p, dtype=np.float64).ravel()
                                                 for p in parts]))
 

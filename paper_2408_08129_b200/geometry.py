@@ -181,8 +181,11 @@ class MeshGeometry:
         hq, dhq = self._colq()
         edges = self._col_edges()
         n = hq.shape[0]
-        col = np.concatenate([hq, np.moveaxis(dhq, 2, 1).reshape(n, -1),
-                              edges.reshape(n, -1)], axis=1)
+        zt = self.z_top
+        # the kernels need 1 - h/z_top (geometry.py:208, 341): stored here with
+        # the reference's own arithmetic, so the device does no division
+        col = np.concatenate([1.0 - hq / zt, np.moveaxis(dhq, 2, 1).reshape(n, -1),
+                              (1.0 - edges / zt).reshape(n, -1)], axis=1)
         return elem, np.ascontiguousarray(col), col.shape[1]
 
     # ------------------------------------------------------- volume metric

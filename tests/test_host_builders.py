@@ -61,8 +61,8 @@ def test_device_tables_reproduce_dense_metric():
     lv, org, cid = elem[:, 0], elem[:, 1:4], elem[:, 4]
     s = np.array([e / r for e, r in zip(c.mesh.extents, c.mesh.root_counts)])[None, :] \
         / (2.0 ** lv)[:, None]
-    hq = col[cid, :nqh]
-    zz = s[:, 2][:, None] * (1.0 - hq / g.z_top)
+    omh = col[cid, :nqh]            # 1 - h/z_top at the horizontal Gauss grid
+    zz = s[:, 2][:, None] * omh
     det = (s[:, 0] * s[:, 1])[:, None] * zz
     assert rel(np.repeat(det, b.n_quad_1d, axis=1), g.det_j) <= 1e-15
 
