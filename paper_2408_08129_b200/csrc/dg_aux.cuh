@@ -144,6 +144,44 @@ integrate_kernel(const __grid_constant__ AuxParams<N> P) {
   }
 }
 
+// nodes -> Gauss points for ncomp components (frozen h of the Helmholtz pair,
+// evaluated once per pressure fixed-point iterate)
+template <int D, int N>
+__global__ void __launch_bounds__(AuxLayout<D, N>::THREADS)
+interp_kernel(const __grid_constant__ AuxParams<N> P) {
+  using L = AuxLayout<D, N>;
+  constexpr int NP = L::NP;
+  extern __shared__ double smem[];
+  {
+    const double* src = reinterpret_cast<const double*>(&P.tab);
+    for (int i = threadIdx.x; i < L::TABD; i += blockDim.x) smem[i] = src[i];
+    __syncthreads();
+  }
+  const Tab<N>& T = *reinterpret_cast<const Tab<N>*>(smem);
+  const int el = threadIdx.x / NP, q = threadIdx.x - el * NP;
+  const long long e = (long long)blockIdx.x * L::EPB + el;
+  const bool valid = el < L::EPB && e < P.n_el;
+  const long long es = valid ? e : 0;
+  double* X = smem + L::TABD + 64 + el * 2 * L::KMAX * NP;
+  double* Y = X + L::KMAX * NP;
+  for (int c0 = 0; c0 < P.ncomp; c0 += L::KMAX) {
+    const int kc = min(L::KMAX, P.ncomp - c0);
+    for (int c = 0; c < L::KMAX; ++c) X[c * NP + q] = c < kc ? P.in(es, c0 + c, q) : 0.0;
+    __syncthreads();
+    double* s = X;
+    double* d = Y;
+    for (int a = D - 1; a >= 0; --a) {
+      pass1d<D, N, L::KMAX, false>(&T.B[0][0], s, d, q, a, NP);
+      __syncthreads();
+      double* t = s; s = d; d = t;
+    }
+    if (valid)
+      for (int c = 0; c < kc; ++c)
+        P.out.p[e * P.out.estride + (c0 + c) * P.out.cstride + q] = s[c * NP + q];
+    __syncthreads();
+  }
+}
+
 template <int D, int N>
 cudaError_t launch_aux(int which, const AuxParams<N>& P, cudaStream_t st, int* grid_out) {
   using L = AuxLayout<D, N>;
@@ -153,9 +191,12 @@ cudaError_t launch_aux(int which, const AuxParams<N>& P, cudaStream_t st, int* g
   if (which == 0) {
     cudaFuncSetAttribute(minv_kernel<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
     minv_kernel<D, N><<<grid, L::THREADS, L::SMEM, st>>>(P);
-  } else {
+  } else if (which == 1) {
     cudaFuncSetAttribute(integrate_kernel<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
     integrate_kernel<D, N><<<grid, L::THREADS, L::SMEM, st>>>(P);
+  } else {
+    cudaFuncSetAttribute(interp_kernel<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
+    interp_kernel<D, N><<<grid, L::THREADS, L::SMEM, st>>>(P);
   }
   return cudaGetLastError();
 }

@@ -769,7 +769,16 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
     const int f = r / S;
     if ((mesh.kind[e * NF + f] & 15) != KIND_COARSE) continue;
     const long long child = mesh.hang_children[(long long)mesh.nbr[e * NF + f] * S + sub];
-    CH[it] = load_input<D, N, OPK>(P, child, cp, face_to_vol<D, N>(f >> 1, 1 - (f & 1), j));
+    if (OPK == OP_DIVHV && P.in_quad) {
+      // Gauss-point input: the child's trace at its face Gauss point j
+      const int ax = f >> 1, cs = 1 - (f & 1);
+      const int b = face_to_vol<D, N>(ax, 0, j), st = stride_of<D, N>(ax);
+      double t = 0.0;
+      for (int p = 0; p < N; ++p) t = fma(T.lift[cs][p], load_input<D, N, OPK>(P, child, cp, b + p * st), t);
+      CH[it] = t;
+    } else {
+      CH[it] = load_input<D, N, OPK>(P, child, cp, face_to_vol<D, N>(f >> 1, 1 - (f & 1), j));
+    }
   }
   __syncthreads();
   // subface fluxes of every coarse face
@@ -786,20 +795,38 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
     const int b0 = sub & 1, b1 = (sub >> 1) & 1;
     double TO[KIN], TN[KIN];
     const double* chv = CH + ((f * S + sub) * KIN) * NQF;
+    const bool iq = (OPK == OP_DIVHV) && P.in_quad;
 #pragma unroll
     for (int c = 0; c < KIN; ++c) {
       double ao = 0.0, an = 0.0;
-      for (int j = 0; j < NQF; ++j) {
-        const int j0 = (D == 2) ? j : j / N;
-        const int j1 = (D == 2) ? 0 : j % N;
-        double mo = T.half[b0][qt0][j0];
-        double mb = T.B[qt0][j0];
-        if (D == 3) {
-          mo *= T.half[b1][qt1][j1];
-          mb *= T.B[qt1][j1];
+      if (iq) {
+        // own coarse-face Gauss trace (lift contraction) -> fine Gauss points
+        // through halfq (x) halfq; the child's trace was staged at qf
+        const int st = stride_of<D, N>(axis);
+        for (int j = 0; j < NQF; ++j) {
+          const int j0 = (D == 2) ? j : j / N;
+          const int j1 = (D == 2) ? 0 : j % N;
+          double mo = T.halfq[b0][qt0][j0];
+          if (D == 3) mo *= T.halfq[b1][qt1][j1];
+          const int bj = face_to_vol<D, N>(axis, 0, j);
+          double tg = 0.0;
+          for (int p = 0; p < N; ++p) tg = fma(T.lift[side][p], A[c * NP + bj + p * st], tg);
+          ao = fma(mo, tg, ao);
         }
-        ao = fma(mo, A[c * NP + cfnode[f * NQF + j]], ao);
-        an = fma(mb, chv[c * NQF + j], an);
+        an = chv[c * NQF + qf];
+      } else {
+        for (int j = 0; j < NQF; ++j) {
+          const int j0 = (D == 2) ? j : j / N;
+          const int j1 = (D == 2) ? 0 : j % N;
+          double mo = T.half[b0][qt0][j0];
+          double mb = T.B[qt0][j0];
+          if (D == 3) {
+            mo *= T.half[b1][qt1][j1];
+            mb *= T.B[qt1][j1];
+          }
+          ao = fma(mo, A[c * NP + cfnode[f * NQF + j]], ao);
+          an = fma(mb, chv[c * NQF + j], an);
+        }
       }
       TO[c] = ao;
       TN[c] = an;
@@ -875,6 +902,14 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
   }
   const double* res;
   const int qq = act ? q : 0;
+  if (OPK == OP_GRAD && P.out_quad) {
+    // Gauss-point output (Helmholtz H1): coef * Z / (w det), no B^-1
+    if (!act) return;
+    const double inv = 1.0 / (wq * det);
+    for (int k = 0; k < KOUT; ++k)
+      P.out.p[e * P.out.estride + k * P.out.cstride + q] += P.coef * (Z[k * NP + q] * inv);
+    return;
+  }
   if (P.mode == OUT_MINV) {
     if (act) {
       const double inv = 1.0 / (wq * det);

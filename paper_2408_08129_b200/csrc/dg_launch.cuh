@@ -21,6 +21,7 @@ struct OpArgs {
   double alpha, beta, coef;
   int has_K, has_base, homogeneous, mode;
   int dbg;  // phase-skip flags for profiling experiments only (0 in production)
+  int in_quad, out_quad;
   double* mass_partial;
   const double* tabs;  // host pointer, Tab<N> layout
 };
@@ -54,6 +55,8 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
   P.homogeneous = a.homogeneous;
   P.mode = a.mode;
   P.dbg = a.dbg;
+  P.in_quad = a.in_quad;
+  P.out_quad = a.out_quad;
   P.mass_partial = a.mass_partial;
   std::memcpy(&P.tab, a.tabs, sizeof(Tab<N>));
   using WL = WLayout<D, N, OPK>;
@@ -72,19 +75,23 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
       if (wgrid == 0) return cudaSuccess;
       static bool wconf = false;
       if (!wconf) {
-        cudaError_t e = cudaFuncSetAttribute(welem_kernel<D, N, OPK>,
+        for (auto kfn : {welem_kernel<D, N, OPK, false>, welem_kernel<D, N, OPK, OPK == OP_DIVHV>}) {
+          cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)WL::SMEM);
+          if (e != cudaSuccess) return e;
+          e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+          if (e != cudaSuccess) return e;
+        }
+        cudaError_t e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)WL::SMEM);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(welem_kernel<D, N, OPK>,
-                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::CSMEM);
+                                             (int)L::CSMEM);
         if (e != cudaSuccess) return e;
         wconf = true;
       }
-      welem_kernel<D, N, OPK><<<wgrid, WL::THREADS, WL::SMEM, st>>>(P);
+      if (OPK == OP_DIVHV && a.in_quad)
+        welem_kernel<D, N, OPK, OPK == OP_DIVHV><<<wgrid, WL::THREADS, WL::SMEM, st>>>(P);
+      else
+        welem_kernel<D, N, OPK, false><<<wgrid, WL::THREADS, WL::SMEM, st>>>(P);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       if (a.mesh.n_coarse > 0) {
@@ -128,6 +135,15 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
   }
   if (info) info->grid = grid + a.mesh.n_coarse;  // partial slots written
   return e;
+}
+
+// is the warp-element kernel (and with it Gauss-point storage of the
+// Helmholtz intermediate) used for this (dim, n)?
+inline bool welem_enabled(int D, int N) {
+  int nc = 1;
+  for (int a = 0; a < D - 1; ++a) nc *= N;
+  static const bool v2 = getenv("DG_KERNEL") && std::string(getenv("DG_KERNEL")) == "v2";
+  return nc <= 32 && !v2;
 }
 
 // grid size only (for sizing the per-CTA partial buffers)

@@ -49,6 +49,10 @@ struct KParams {
   double alpha, beta, coef;
   int has_K, has_base, homogeneous, mode;
   int dbg;  // phase-skip flags for profiling experiments only (0 in production)
+  // Gauss-point storage (warp-element kernel only): H1 writes V at the Gauss
+  // points (out_quad), H2 reads V and h there (in_quad) -- B^-1 then B is
+  // the identity, so the Helmholtz pair skips both transforms
+  int in_quad, out_quad;
   double* mass_partial;  // ADV: per-CTA sum of the density dual (or null)
   Tab<N> tab;
 };

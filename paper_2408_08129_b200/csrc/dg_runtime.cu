@@ -86,7 +86,7 @@ struct dg_ctx {
   DevBuf<double> mass_partial, partial, redout, coef_dev;
   double* pinned = nullptr;  // 256 doubles
   DevBuf<double> sV;         // vector field (n_tot, d, NP)
-  DevBuf<double> sh, sK, sx, srhs, spold, sw, sr, sx2;  // scalar fields
+  DevBuf<double> sh, sK, sx, srhs, spold, sw, sr, sx2, shq;  // scalar fields
   DevBuf<double> basis;      // (m+1) x (n_tot NP)
   DevBuf<double> st[6];      // state fields (n_tot, V, NP)
   LaunchInfo last{};
@@ -182,7 +182,7 @@ int op_advective(dg_ctx* c, const double* U, double* out, int mode, double* mass
 
 // V_k = base_k + coef * [Minv] G(alpha (x - beta K))
 int op_grad(dg_ctx* c, const double* x, const double* K, double alpha, double beta, int homog,
-            int mode, MView out, CView base, int has_base, double coef) {
+            int mode, MView out, CView base, int has_base, double coef, int out_quad = 0) {
   OpArgs a = base_args(c);
   a.in = cv(x, c->NP, c->NP);
   if (K) {
@@ -197,12 +197,13 @@ int op_grad(dg_ctx* c, const double* x, const double* K, double alpha, double be
   a.base = base;
   a.has_base = has_base;
   a.coef = coef;
+  a.out_quad = out_quad;
   return launch(c, OP_GRAD, a);
 }
 
 // y = base + coef * [Minv] Div(h V)
 int op_divhv(dg_ctx* c, CView V, const double* h, int homog, int mode, MView out, CView base,
-             int has_base, double coef) {
+             int has_base, double coef, int in_quad = 0) {
   OpArgs a = base_args(c);
   a.in = V;
   a.inH = cv(h, c->NP, c->NP);
@@ -212,19 +213,51 @@ int op_divhv(dg_ctx* c, CView V, const double* h, int homog, int mode, MView out
   a.base = base;
   a.has_base = has_base;
   a.coef = coef;
+  a.in_quad = in_quad;
   return launch(c, OP_DIVHV, a);
 }
 
-// homogeneous Helmholtz action y = x + a_dt Minv Div_h(V), V = -(a_dt/M^2)(g-1) Minv G(x)
-int helm_apply(dg_ctx* c, double a_dt, const double* h, double* x, double* y) {
+bool quad_mode(dg_ctx* c) {
+  // Gauss-point storage of the Helmholtz intermediate: measured neutral on
+  // B200 (the removed B / B^-1 passes are paid back by n-deep neighbour
+  // gathers), so it is opt-in (DG_QUAD=1) and the nodal path is the default
+  static const bool on = getenv("DG_QUAD") != nullptr;
+  return on && welem_enabled(c->dim, c->N);
+}
+
+// frozen h at the Gauss points (once per fixed-point iterate)
+int interp_h(dg_ctx* c, const double* h, double* hq) {
+  AuxArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.elem = c->elem.p;
+  a.col = c->col.p;
+  a.gc = c->gc;
+  a.n_el = c->n_el;
+  a.ncomp = 1;
+  a.in = cv(h, c->NP, c->NP);
+  a.out = mv(hq, c->NP, c->NP);
+  a.tabs = c->tabs.data();
+  int grid = 0;
+  prof_begin(c->stream);
+  cudaError_t e = c->dim == 2 ? launch_aux_d2(c->N, 2, a, c->stream, &grid)
+                              : launch_aux_d3(c->N, 2, a, c->stream, &grid);
+  prof_end(c->stream, P_OTHER, 16.0 * c->n_el * c->NP, 1);
+  CK(e);
+  return halo(c, hq, 1);
+}
+
+// homogeneous Helmholtz action y = x + a_dt Minv Div_h(V), V = -(a_dt/M^2)(g-1) Minv G(x).
+// With hq (Gauss-point h) the intermediate V stays at the Gauss points.
+int helm_apply(dg_ctx* c, double a_dt, const double* h, const double* hq, double* x, double* y) {
   const int d = c->dim;
   RET(halo(c, x, 1));
   const double gm1 = c->model.gamma - 1.0;
+  const int qd = hq != nullptr;
   RET(op_grad(c, x, nullptr, gm1, 0.0, 1, OUT_MINV, mv(c->sV.p, (long long)d * c->NP, c->NP),
-              CView{}, 0, -(a_dt * c->model.inv_mach_sq)));
+              CView{}, 0, -(a_dt * c->model.inv_mach_sq), qd));
   RET(halo(c, c->sV.p, d));
-  RET(op_divhv(c, cv(c->sV.p, (long long)d * c->NP, c->NP), h, 1, OUT_MINV, mv(y, c->NP, c->NP),
-               cv(x, c->NP, c->NP), 1, a_dt));
+  RET(op_divhv(c, cv(c->sV.p, (long long)d * c->NP, c->NP), qd ? hq : h, 1, OUT_MINV,
+               mv(y, c->NP, c->NP), cv(x, c->NP, c->NP), 1, a_dt, qd));
   return DG_OK;
 }
 
@@ -258,8 +291,8 @@ int norm2(dg_ctx* c, const double* x, double* out) {
   return DG_OK;
 }
 
-int gmres(dg_ctx* c, double a_dt, const double* h, const double* rhs, double* x, double tol,
-          int restart, int max_iter, Gm& st) {
+int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const double* rhs, double* x,
+          double tol, int restart, int max_iter, Gm& st) {
   if (!(tol > 0.0 && tol < 1.0)) return fail(DG_ERR_CONFIG, "tol_rel must be in (0,1)");
   const long long ns = c->scal();
   const long long n = (long long)c->n_el * c->NP;
@@ -285,7 +318,7 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* rhs, double* x,
     return DG_OK;
   }
   auto residual_into_r = [&]() -> int {
-    RET(helm_apply(c, a_dt, h, x, w));
+    RET(helm_apply(c, a_dt, h, hq, x, w));
     const double cf[2] = {1.0, -1.0};
     const double* xs[2] = {rhs, w};
     CK(lincomb(c->stream, n, 2, cf, xs, r));
@@ -307,7 +340,7 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* rhs, double* x,
     g[0] = beta;
     int done = 0;
     for (int j = 0; j < m; ++j) {
-      RET(helm_apply(c, a_dt, h, Vb + (size_t)j * vs, w));
+      RET(helm_apply(c, a_dt, h, hq, Vb + (size_t)j * vs, w));
       // classical Gram-Schmidt: h_i = V_i . w and |w|^2 in one pass
       CK(multidot(c->stream, n, j + 1, Vb, vs, w, c->partial.p, c->redout.p));
       RET(reduce_read(c, c->redout.p, j + 2, hc.data()));
@@ -457,8 +490,13 @@ int solve_stage(dg_ctx* c, const double* acc, const double* guess, double a_dt,
     RET(halo(c, c->sh.p, 1));
     RET(halo(c, c->sK.p, 1));
     RET(energy_F(c, a_dt, c->sh.p, c->sK.p, m_e, e_e, nullptr, c->srhs.p));
+    const double* hq = nullptr;
+    if (quad_mode(c)) {
+      RET(interp_h(c, c->sh.p, c->shq.p));
+      hq = c->shq.p;
+    }
     Gm gs;
-    RET(gmres(c, a_dt, c->sh.p, c->srhs.p, c->sx.p, cfg.krylov_tol, cfg.krylov_restart,
+    RET(gmres(c, a_dt, c->sh.p, hq, c->srhs.p, c->sx.p, cfg.krylov_tol, cfg.krylov_restart,
               cfg.krylov_max_iter, gs));
     if (stats && stats->n_krylov < DG_MAX_SOLVES) stats->krylov_iters[stats->n_krylov++] = gs.iterations;
     if (!gs.converged) {
@@ -501,7 +539,7 @@ int solve_stage(dg_ctx* c, const double* acc, const double* guess, double a_dt,
 
 int ensure_work(dg_ctx* c) {
   const long long ns = c->scal();
-  for (auto* b : {&c->sh, &c->sK, &c->sx, &c->srhs, &c->spold, &c->sw, &c->sr, &c->sx2})
+  for (auto* b : {&c->sh, &c->sK, &c->sx, &c->srhs, &c->spold, &c->sw, &c->sr, &c->sx2, &c->shq})
     CK(b->alloc(ns));
   CK(c->sV.alloc((size_t)ns * c->dim));
   return DG_OK;
@@ -714,7 +752,12 @@ int dg_energy_F(dg_ctx* c, double a_dt, const double* h, const double* K, const 
 int dg_helmholtz_apply(dg_ctx* c, double a_dt, const double* h, const double* x, double* y) {
   RET(ensure_work(c));
   RET(halo(c, const_cast<double*>(h), 1));
-  return helm_apply(c, a_dt, h, const_cast<double*>(x), y);
+  const double* hq = nullptr;
+  if (quad_mode(c)) {
+    RET(interp_h(c, h, c->shq.p));
+    hq = c->shq.p;
+  }
+  return helm_apply(c, a_dt, h, hq, const_cast<double*>(x), y);
 }
 
 int dg_gmres_helmholtz(dg_ctx* c, double a_dt, const double* h, const double* rhs, double* x,
@@ -722,8 +765,13 @@ int dg_gmres_helmholtz(dg_ctx* c, double a_dt, const double* h, const double* rh
                        double* history, int history_cap) {
   RET(ensure_work(c));
   RET(halo(c, const_cast<double*>(h), 1));
+  const double* hq = nullptr;
+  if (quad_mode(c)) {
+    RET(interp_h(c, h, c->shq.p));
+    hq = c->shq.p;
+  }
   Gm gs;
-  RET(gmres(c, a_dt, h, rhs, x, tol_rel, restart, max_iter, gs));
+  RET(gmres(c, a_dt, h, hq, rhs, x, tol_rel, restart, max_iter, gs));
   if (stats) {
     stats->iterations = gs.iterations;
     stats->restarts = gs.restarts;

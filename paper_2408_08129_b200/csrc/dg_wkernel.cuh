@@ -36,7 +36,14 @@ struct WLayout {
   static constexpr int KX0 = KIN > KOUT ? KIN : KOUT;
   static constexpr int KX1 = (D - 1) * KW;
   static constexpr int KX = KX0 > KX1 ? KX0 : KX1;
-  static constexpr int SLOT = ((KX * TSZ) % 2 == 0) ? KX * TSZ + 1 : KX * TSZ;  // odd: bank shift
+  // raw input components behind one face value (gradient: x and K)
+  static constexpr int RAW = (OPK == OP_GRAD) ? 2 : KIN;
+  // async prefetch of the neighbour face nodes: gradient only -- for div(hV)
+  // the (d+1)-component staging area costs more occupancy than it hides
+  static constexpr bool ASYNC = (OPK == OP_GRAD);
+  static constexpr int FGN = ASYNC ? 2 * D * RAW * NC : 0;
+  static constexpr int SLOT0 = KX * TSZ + FGN;
+  static constexpr int SLOT = (SLOT0 % 2 == 0) ? SLOT0 + 1 : SLOT0;  // odd: bank shift
   static constexpr int WPB = 4;                // warps per CTA
   static constexpr int THREADS = 32 * WPB;
   static constexpr int TABD = (int)(sizeof(Tab<N>) / sizeof(double));
@@ -70,6 +77,29 @@ __device__ __forceinline__ int nbr_face_node(int ax, int side, int c) {
   }
 }
 
+// nodal/Gauss index of point p of the NEIGHBOUR's pencil along ax through
+// face point c (tangential C-order)
+template <int D, int N>
+__device__ __forceinline__ int nbr_pencil_node(int ax, int p, int c) {
+  if constexpr (D == 2) {
+    return (ax == 0) ? p * N + c : c * N + p;
+  } else {
+    const int fa = c / N, fb = c % N;
+    if (ax == 0) return (p * N + fa) * N + fb;
+    if (ax == 1) return (fa * N + p) * N + fb;
+    return (fa * N + fb) * N + p;
+  }
+}
+
+__device__ __forceinline__ void cp_async8(void* smem_ptr, const void* gptr) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_ptr);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gptr));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
 template <int N, bool TRANS>
 __device__ __forceinline__ void mat_apply(const double (&M)[N][N], const double* v, double* o) {
 #pragma unroll
@@ -81,7 +111,9 @@ __device__ __forceinline__ void mat_apply(const double (&M)[N][N], const double*
   }
 }
 
-template <int D, int N, int OPK>
+// IQ: Gauss-point input (H2 of the Helmholtz pair in quad mode) -- a
+// separate instantiation so the nodal path carries none of its registers
+template <int D, int N, int OPK, bool IQ = false>
 __global__ void __launch_bounds__(WLayout<D, N, OPK>::THREADS, 4)
 welem_kernel(const __grid_constant__ KParams<N> P) {
   using WL = WLayout<D, N, OPK>;
@@ -120,28 +152,52 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
     kf[f] = act ? kind_e[f] : (uint8_t)KIND_WALL;
     nf[f] = act ? nbr_e[f] : 0;
   }
-  constexpr bool PRE = KIN <= 2;
-  double gpre[PRE ? NF : 1][PRE ? KIN : 1];
-  if constexpr (PRE) {
+  // neighbour face node c of every face, copied asynchronously (cp.async)
+  // into this lane's private smem slots: the L2 gathers run underneath the
+  // interpolation and volume work and are waited for only at the face phase
+  constexpr int RAW = WL::RAW;
+  double* FGs = X + WL::KX * TSZ;
+  constexpr bool iq0 = (OPK == OP_DIVHV) && IQ;
+  if (WL::ASYNC && !iq0) {
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
       const int kd = kf[f] & 15;
       const bool inter = act && (kd == KIND_CONF || kd == KIND_FINE);
+      const long long nb = nf[f];
+      const int node = nbr_face_node<D, N>(f >> 1, f & 1, c);
 #pragma unroll
-      for (int cp = 0; cp < KIN; ++cp)
-        gpre[f][cp] = inter ? load_input<D, N, OPK>(P, nf[f], cp,
-                                                   nbr_face_node<D, N>(f >> 1, f & 1, c))
-                            : 0.0;
+      for (int r = 0; r < RAW; ++r) {
+        double* dst = FGs + (f * RAW + r) * NC + c;
+        const double* src = nullptr;
+        if (inter) {
+          if constexpr (OPK == OP_GRAD) {
+            if (r == 0 && P.in.p) src = P.in.p + nb * P.in.estride + node;
+            if (r == 1 && P.has_K) src = P.inK.p + nb * P.inK.estride + node;
+          } else {
+            src = (r < D) ? P.in.p + nb * P.in.estride + r * P.in.cstride + node
+                          : P.inH.p + nb * P.inH.estride + node;
+          }
+        }
+        if (src) cp_async8(dst, src);
+        else *dst = 0.0;
+      }
     }
   }
   // ---- 1. nodal column, z interpolation in registers -------------------
+  // in_quad (H2 of the Helmholtz pair): inputs are already Gauss values
+  constexpr bool iq = iq0;
   double q[KIN][N];
 #pragma unroll
   for (int cp = 0; cp < KIN; ++cp) {
     double a[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) a[k] = act ? load_input<D, N, OPK>(P, es, cp, c * N + k) : 0.0;
-    mat_apply<N, false>(TC.B, a, q[cp]);
+    if (iq) {
+#pragma unroll
+      for (int k = 0; k < N; ++k) q[cp][k] = a[k];
+    } else {
+      mat_apply<N, false>(TC.B, a, q[cp]);
+    }
   }
   // ---- 2. x (and y) interpolation through the tile ------------------------
 #pragma unroll
@@ -150,16 +206,18 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
     for (int k = 0; k < N; ++k) X[cp * TSZ + c * (N + 1) + k] = q[cp][k];
   __syncwarp();
   if constexpr (D == 3) {
+    if (!iq) {
 #pragma unroll
-    for (int cp = 0; cp < KIN; ++cp) {
-      double v[N], o[N];
+      for (int cp = 0; cp < KIN; ++cp) {
+        double v[N], o[N];
 #pragma unroll
-      for (int jj = 0; jj < N; ++jj) v[jj] = X[cp * TSZ + yoff<N>(c, jj)];
-      mat_apply<N, false>(TC.B, v, o);
+        for (int jj = 0; jj < N; ++jj) v[jj] = X[cp * TSZ + yoff<N>(c, jj)];
+        mat_apply<N, false>(TC.B, v, o);
 #pragma unroll
-      for (int jj = 0; jj < N; ++jj) X[cp * TSZ + yoff<N>(c, jj)] = o[jj];
+        for (int jj = 0; jj < N; ++jj) X[cp * TSZ + yoff<N>(c, jj)] = o[jj];
+      }
+      __syncwarp();
     }
-    __syncwarp();
   }
   // x pass; the x-pencil of lane c carries face point c of both x faces
   double tox[2][KIN];
@@ -168,9 +226,14 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
     double v[N], o[N];
 #pragma unroll
     for (int ii = 0; ii < N; ++ii) v[ii] = X[cp * TSZ + xoff<D, N>(c, ii)];
-    mat_apply<N, false>(TC.B, v, o);
+    if (iq) {
 #pragma unroll
-    for (int ii = 0; ii < N; ++ii) X[cp * TSZ + xoff<D, N>(c, ii)] = o[ii];
+      for (int ii = 0; ii < N; ++ii) o[ii] = v[ii];
+    } else {
+      mat_apply<N, false>(TC.B, v, o);
+#pragma unroll
+      for (int ii = 0; ii < N; ++ii) X[cp * TSZ + xoff<D, N>(c, ii)] = o[ii];
+    }
     double t0 = 0.0, t1 = 0.0;
 #pragma unroll
     for (int ii = 0; ii < N; ++ii) {
@@ -217,11 +280,52 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
     const int sf = (kraw >> 4) & 3;
     const double* M0 = (kd == KIND_FINE) ? &TS.half[sf & 1][0][0] : &TS.B[0][0];
     const double* M1 = (kd == KIND_FINE) ? &TS.half[(sf >> 1) & 1][0][0] : &TS.B[0][0];
+    bool need_pass = true;
+    if (iq) {
+      // Gauss-point input: the neighbour's trace at its own face Gauss point
+      // (fa, fb) is a lift contraction of its normal pencil; conforming faces
+      // need no tangential transform, a fine leaf applies halfq (x) halfq
+      need_pass = __any_sync(0xffffffffu, act && kd == KIND_FINE);
+    }
+    const double* Mq0 = &TS.halfq[sf & 1][0][0];
+    const double* Mq1 = &TS.halfq[(sf >> 1) & 1][0][0];
 #pragma unroll
     for (int cp = 0; cp < KIN; ++cp) {
       double gval = 0.0;
-      if constexpr (PRE) {
-        gval = gpre[f][cp];
+      if (iq) {
+        if (act && inter) {
+          double t = 0.0;
+#pragma unroll
+          for (int p = 0; p < N; ++p)
+            t = fma(TC.lift[1 - side][p],
+                    load_input<D, N, OPK>(P, nb, cp, nbr_pencil_node<D, N>(AX, p, c)), t);
+          gval = t;
+        }
+        if (!need_pass) {
+          TN[cp] = gval;
+        } else {
+          const bool fine = kd == KIND_FINE;
+          double t1v = 0.0;
+          if constexpr (D == 2) {
+#pragma unroll
+            for (int j = 0; j < N; ++j)
+              t1v = fma(Mq0[fa * N + j], __shfl_sync(0xffffffffu, gval, b0 + j), t1v);
+            TN[cp] = fine ? t1v : gval;
+          } else {
+#pragma unroll
+            for (int j = 0; j < N; ++j)
+              t1v = fma(Mq0[fa * N + j], __shfl_sync(0xffffffffu, gval, b0 + j * N + fb), t1v);
+            double t2v = 0.0;
+#pragma unroll
+            for (int j = 0; j < N; ++j)
+              t2v = fma(Mq1[fb * N + j], __shfl_sync(0xffffffffu, t1v, b0 + fa * N + j), t2v);
+            TN[cp] = fine ? t2v : gval;
+          }
+        }
+      } else {
+      if constexpr (WL::ASYNC) {
+        const double xv = FGs[(f * RAW + 0) * NC + c];
+        gval = P.has_K ? P.alpha * (xv - P.beta * FGs[(f * RAW + 1) * NC + c]) : P.alpha * xv;
       } else if (act && inter) {
         gval = load_input<D, N, OPK>(P, nb, cp, nbr_face_node<D, N>(AX, side, c));
       }
@@ -241,6 +345,7 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
           t2v = fma(M1[fb * N + j], __shfl_sync(0xffffffffu, t1v, b0 + fa * N + j), t2v);
         TN[cp] = t2v;
       }
+      }  // nodal input
       // own trace
       if constexpr (AX == D - 1) {
         double t = 0.0;
@@ -277,6 +382,8 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
 #pragma unroll
     for (int k = 0; k < KOUT; ++k) fl[f][k] = fv[k] * sg;
   };
+  // each lane reads back only the face slots it issued itself
+  if (WL::ASYNC && !iq0) cp_async_wait_all();
   face(std::integral_constant<int, 0>{}, 0);
   face(std::integral_constant<int, 0>{}, 1);
   face(std::integral_constant<int, 1>{}, 0);
@@ -390,6 +497,18 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
   double iwh = 1.0 / det_c;
   if constexpr (D == 3) iwh *= TC.iqw[c / N] * TC.iqw[c % N];
   else iwh *= TC.iqw[c];
+  if (OPK == OP_GRAD && P.out_quad) {
+    // H1 of the Helmholtz pair: V = coef * diag(1/(w det)) Z at the Gauss
+    // points -- the B^-1 transform and H2's B interpolation cancel exactly
+    if (!act) return;
+#pragma unroll
+    for (int k = 0; k < KOUT; ++k) {
+      double* out = P.out.p + e * P.out.estride + (long long)k * P.out.cstride + c * N;
+#pragma unroll
+      for (int kz = 0; kz < N; ++kz) out[kz] = P.coef * (Zc[k][kz] * (iwh * TC.iqw[kz]));
+    }
+    return;
+  }
 #pragma unroll
   for (int k = 0; k < KOUT; ++k) {
     double t[N];
