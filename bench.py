@@ -111,6 +111,16 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def traffic(workload, kernel_class):
+    """DRAM bytes per operator call of the dominant class from the committed
+    ncu --set full capture (profiles/r1_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            return float(json.load(f)[workload][kernel_class])
+    except Exception:
+        return None
+
+
 # ------------------------------------------------------------ CPU baseline
 def cpu_step_sample(workload, threads, budget_s=30.0):
     """Reference algorithm (numpy oracle port) on a bounded sample of the
@@ -301,7 +311,8 @@ def main():
                        "iterations": kry, "setup_s": setup_s},
             "roofline": {"bound": "hbm", "kernel": classes[k_dom], "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "peak_kind": peak_kind, "traffic": None,
+                         "peak_kind": peak_kind,
+                         "traffic": traffic(args.workload, classes[k_dom]),
                          "bytes_per_launch": per_launch_bytes,
                          "ms_per_launch": per_launch_ms,
                          "share_of_step": ms_c[k_dom] / ms_total},
