@@ -38,16 +38,24 @@ struct WLayout {
   static constexpr int KX = KX0 > KX1 ? KX0 : KX1;
   // raw input components behind one face value (gradient: x and K)
   static constexpr int RAW = (OPK == OP_GRAD) ? 2 : KIN;
-  // async prefetch of the neighbour face nodes: gradient only -- for div(hV)
-  // the (d+1)-component staging area costs more occupancy than it hides
-  static constexpr bool ASYNC = (OPK == OP_GRAD);
-  static constexpr int FGN = ASYNC ? 2 * D * RAW * NC : 0;
-  static constexpr int SLOT0 = KX * TSZ + FGN;
-  static constexpr int SLOT = (SLOT0 % 2 == 0) ? SLOT0 + 1 : SLOT0;  // odd: bank shift
   static constexpr int WPB = 4;                // warps per CTA
   static constexpr int THREADS = 32 * WPB;
   static constexpr int TABD = (int)(sizeof(Tab<N>) / sizeof(double));
-  static constexpr size_t SMEM = (size_t)(TABD + WPB * (EPW + 1) * SLOT) * sizeof(double);
+  // padding lanes (32 % NC != 0) get a private scratch slot
+  static constexpr int NSLOT = EPW + ((32 % NC) ? 1 : 0);
+  static constexpr int odd(int s) { return (s % 2 == 0) ? s + 1 : s; }  // bank shift
+  // async prefetch of the neighbour face nodes into smem, as long as the
+  // staging area keeps 4 CTAs (the register-limited occupancy) per SM
+  // (+ the lane's terrain scalars: omh, dh at its column and omh at its point
+  // of every vertical face; the epilogue's base values reuse the face area)
+  static constexpr int GEON = 1 + 3 * (D - 1);
+  static constexpr int FGA = 2 * D * RAW * NC;
+  static constexpr int FGB = (FGA > KOUT * NP ? FGA : KOUT * NP) + GEON * NC;
+  static constexpr bool ASYNC =
+      (TABD + WPB * NSLOT * odd(KX * TSZ + FGB)) * 8 <= 54 * 1024;
+  static constexpr int FGN = ASYNC ? FGB - GEON * NC : 0;
+  static constexpr int SLOT = odd(KX * TSZ + (ASYNC ? FGB : 0));
+  static constexpr size_t SMEM = (size_t)(TABD + WPB * NSLOT * SLOT) * sizeof(double);
   static constexpr bool OK = (NC <= 32) && (OPK != OP_ADV);
 };
 
@@ -93,7 +101,96 @@ __device__ __forceinline__ int nbr_pencil_node(int ax, int p, int c) {
 
 __device__ __forceinline__ void cp_async8(void* smem_ptr, const void* gptr) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem_ptr);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gptr));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gptr) : "memory");
+}
+
+// terrain scalars of lane c, staged in smem as GE[i * NC + c]:
+//   i = 0: 1 - h/z_top at the column's horizontal Gauss point
+//   i = 1..HD: dh/dx_a there (also the z-face values of face point c)
+//   i = 1 + HD + 2 AX + side: 1 - h_edge/z_top at face point c of face (AX, side)
+template <int D, int N>
+__device__ __forceinline__ int geo_src(int i, int c) {
+  constexpr int HD = D - 1, NQH = ipow(N, HD), NE = ipow(N, HD - 1);
+  if (i == 0) return c;
+  if (i <= HD) return NQH * i + c;
+  const int fs = i - 1 - HD;  // 2 AX + side
+  return NQH * (1 + HD) + fs * NE + ((D == 2) ? 0 : c / N);
+}
+
+// Gauss-point metric (as point_metric) from the staged terrain scalars
+template <int D, int N>
+__device__ __forceinline__ void point_metric_ge(const GeoConst& gc, const Tab<N>& T,
+                                                const ElemGeo<D>& g, int qz, const double* GE,
+                                                int NCs, int c, double& det, double ctrv[D][D]) {
+  constexpr int HD = D - 1;
+  const double omh = GE[c];
+  const double zz = g.s[D - 1] * omh;
+  det = 1.0;
+#pragma unroll
+  for (int a = 0; a < HD; ++a) det = det * g.s[a];
+  det = det * zz;
+  const double decay = 1.0 - (g.lo[D - 1] + g.s[D - 1] * T.qx[qz]) / gc.z_top;
+  double zg[2];
+#pragma unroll
+  for (int a = 0; a < HD; ++a) zg[a] = GE[(1 + a) * NCs + c] * g.s[a] * decay;
+#pragma unroll
+  for (int b = 0; b < D; ++b)
+#pragma unroll
+    for (int a = 0; a < D; ++a) ctrv[b][a] = 0.0;
+  if constexpr (D == 2) {
+    ctrv[0][0] = zz;
+    ctrv[1][0] = -zg[0];
+    ctrv[1][1] = g.s[0];
+  } else {
+    ctrv[0][0] = g.s[1] * zz;
+    ctrv[1][1] = g.s[0] * zz;
+    ctrv[2][0] = -g.s[1] * zg[0];
+    ctrv[2][1] = -g.s[0] * zg[1];
+    ctrv[2][2] = g.s[0] * g.s[1];
+  }
+}
+
+// face metric (as face_metric_ax, own geometry) from the staged terrain scalars
+template <int D, int N, int AX>
+__device__ __forceinline__ void face_metric_ge(const GeoConst& gc, const ElemGeo<D>& g, int side,
+                                               bool outward, int qf, const Tab<N>& T,
+                                               const double* GE, int NCs, double n[D],
+                                               double& ws) {
+  constexpr int HD = D - 1;
+  const double fw = (D == 2) ? T.qw[qf] : T.qw[qf / N] * T.qw[qf % N];
+  const double sgn = (outward && side == 0) ? -1.0 : 1.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) n[a] = 0.0;
+  if constexpr (AX < D - 1) {
+    const double omh = gc.terrain ? GE[(1 + HD + 2 * AX + side) * NCs + qf] : 1.0;
+    const double zzv = g.s[D - 1] * omh;
+    const double mag = (D == 2) ? zzv : g.s[1 - AX] * zzv;
+    n[AX] = sgn;
+    ws = fw * fabs(mag);
+  } else {
+    const double top = (D == 2) ? g.s[0] : g.s[0] * g.s[1];
+    if (!gc.terrain) {
+      n[D - 1] = sgn;
+      ws = fw * top;
+      return;
+    }
+    const double decay = 1.0 - (g.lo[D - 1] + g.s[D - 1] * (double)side) / gc.z_top;
+    double nt[D];
+    if constexpr (D == 2) {
+      nt[0] = -GE[NCs + qf] * g.s[0] * decay;
+    } else {
+      nt[0] = -g.s[1] * GE[NCs + qf] * g.s[0] * decay;
+      nt[1] = -g.s[0] * GE[2 * NCs + qf] * g.s[1] * decay;
+    }
+    nt[D - 1] = top;
+    double m2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) m2 += nt[a] * nt[a];
+    const double mag = sqrt(m2);
+#pragma unroll
+    for (int a = 0; a < D; ++a) n[a] = sgn * (nt[a] / mag);
+    ws = fw * mag;
+  }
 }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n" ::);
@@ -138,7 +235,7 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
   const long long es = act ? e : 0;
   const int b0 = slot_ok ? eiw * NC : 0;  // first lane of this element
   // padding lanes (32 % NC != 0) scribble on a private scratch slot
-  double* X = smem + WL::TABD + (wid * (EPW + 1) + (slot_ok ? eiw : EPW)) * WL::SLOT;
+  double* X = smem + WL::TABD + (wid * WL::NSLOT + (slot_ok ? eiw : EPW)) * WL::SLOT;
   const bool flat = !P.gc.terrain;
 
   // ---- 0. face records, and (small KIN) the neighbour face-node values,
@@ -152,10 +249,29 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
     kf[f] = act ? kind_e[f] : (uint8_t)KIND_WALL;
     nf[f] = act ? nbr_e[f] : 0;
   }
+  const ElemGeo<D> g = elem_geo<D>(mesh.elem, P.gc, es);
+  // the element's own nodal column, raw components (gradient: x and K),
+  // issued before anything consumes a load so all of them are in flight
+  constexpr int RAW = WL::RAW;
+  double a[RAW][N];
+#pragma unroll
+  for (int r = 0; r < RAW; ++r)
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double v = 0.0;
+      if (act) {
+        if constexpr (OPK == OP_GRAD) {
+          if (r == 0 && P.in.p) v = P.in(es, 0, c * N + k);
+          if (r == 1 && P.has_K) v = P.inK(es, 0, c * N + k);
+        } else {
+          v = load_input<D, N, OPK>(P, es, r, c * N + k);
+        }
+      }
+      a[r][k] = v;
+    }
   // neighbour face node c of every face, copied asynchronously (cp.async)
   // into this lane's private smem slots: the L2 gathers run underneath the
-  // interpolation and volume work and are waited for only at the face phase
-  constexpr int RAW = WL::RAW;
+  // interpolation work and are waited for only at the face phase
   double* FGs = X + WL::KX * TSZ;
   constexpr bool iq0 = (OPK == OP_DIVHV) && IQ;
   if (WL::ASYNC && !iq0) {
@@ -183,20 +299,31 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
       }
     }
   }
+  double* GEs = FGs + WL::FGN;  // [GEON][NC] terrain scalars (ASYNC only)
+  if (WL::ASYNC && P.gc.terrain && act) {
+    const double* colp = mesh.col + (long long)g.col * P.gc.col_stride;
+#pragma unroll
+    for (int i = 0; i < WL::GEON; ++i) cp_async8(GEs + i * NC + c, colp + geo_src<D, N>(i, c));
+  }
   // ---- 1. nodal column, z interpolation in registers -------------------
   // in_quad (H2 of the Helmholtz pair): inputs are already Gauss values
   constexpr bool iq = iq0;
   double q[KIN][N];
 #pragma unroll
   for (int cp = 0; cp < KIN; ++cp) {
-    double a[N];
+    double col[N];
 #pragma unroll
-    for (int k = 0; k < N; ++k) a[k] = act ? load_input<D, N, OPK>(P, es, cp, c * N + k) : 0.0;
+    for (int k = 0; k < N; ++k) {
+      if constexpr (OPK == OP_GRAD)
+        col[k] = P.has_K ? P.alpha * (a[0][k] - P.beta * a[1][k]) : P.alpha * a[0][k];
+      else
+        col[k] = a[cp][k];
+    }
     if (iq) {
 #pragma unroll
-      for (int k = 0; k < N; ++k) q[cp][k] = a[k];
+      for (int k = 0; k < N; ++k) q[cp][k] = col[k];
     } else {
-      mat_apply<N, false>(TC.B, a, q[cp]);
+      mat_apply<N, false>(TC.B, col, q[cp]);
     }
   }
   // ---- 2. x (and y) interpolation through the tile ------------------------
@@ -264,7 +391,6 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
   // ---- 3. faces: flux at face point c of every face --------------------
   // fl_l[f][k]: lifted flux*ws (with sign) at face point c of face f
   double fl[NF][KOUT];
-  const ElemGeo<D> g = elem_geo<D>(mesh.elem, P.gc, es);
   auto face = [&](auto ax_c, int side) {
     constexpr int AX = decltype(ax_c)::value;
     const int f = 2 * AX + side;
@@ -323,9 +449,11 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
           }
         }
       } else {
-      if constexpr (WL::ASYNC) {
+      if constexpr (WL::ASYNC && OPK == OP_GRAD) {
         const double xv = FGs[(f * RAW + 0) * NC + c];
         gval = P.has_K ? P.alpha * (xv - P.beta * FGs[(f * RAW + 1) * NC + c]) : P.alpha * xv;
+      } else if constexpr (WL::ASYNC) {
+        gval = FGs[(f * RAW + cp) * NC + c];
       } else if (act && inter) {
         gval = load_input<D, N, OPK>(P, nb, cp, nbr_face_node<D, N>(AX, side, c));
       }
@@ -364,10 +492,14 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
       return;
     }
     const bool outward = (kd == KIND_WALL || kd == KIND_FARFIELD);
-    const bool own_metric = !(kd == KIND_CONF && side == 0);
-    const ElemGeo<D> og = own_metric ? g : elem_geo<D>(mesh.elem, P.gc, nb);
+    // the face metric from this element's own geometry: a conforming
+    // neighbour shares the face, so its (minus-side) metric is the same
+    // values up to rounding in the corner coordinates
     double n[D], ws;
-    face_metric_ax<D, N, AX>(P.gc, mesh.col, og, own_metric ? side : 1, outward, c, TS, n, ws);
+    if constexpr (WL::ASYNC)
+      face_metric_ge<D, N, AX>(P.gc, g, side, outward, c, TS, GEs, NC, n, ws);
+    else
+      face_metric_ax<D, N, AX>(P.gc, mesh.col, g, side, outward, c, TS, n, ws);
     if (outward) ghost<D, N, OPK, KIN>(P, kd, nb, c, TO, n, TN);
     const bool minus = outward || side == 1;
     double TLv[KIN], TRv[KIN];
@@ -383,7 +515,7 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
     for (int k = 0; k < KOUT; ++k) fl[f][k] = fv[k] * sg;
   };
   // each lane reads back only the face slots it issued itself
-  if (WL::ASYNC && !iq0) cp_async_wait_all();
+  if (WL::ASYNC) cp_async_wait_all();
   face(std::integral_constant<int, 0>{}, 0);
   face(std::integral_constant<int, 0>{}, 1);
   face(std::integral_constant<int, 1>{}, 0);
@@ -391,6 +523,20 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
   if constexpr (D == 3) {
     face(std::integral_constant<int, 2>{}, 0);
     face(std::integral_constant<int, 2>{}, 1);
+  }
+  // the epilogue's base values (the x-pencil nodes this lane stores) are
+  // copied into the face-node area, now consumed, under the volume work
+  const bool pre_base = WL::ASYNC && act && P.mode == OUT_MINV && P.has_base && !P.out_quad;
+  double* BSs = FGs;
+  if (pre_base) {
+#pragma unroll
+    for (int k = 0; k < KOUT; ++k)
+#pragma unroll
+      for (int ii = 0; ii < N; ++ii) {
+        const int node = (D == 3) ? ii * N * N + c : ii * N + c;
+        cp_async8(BSs + (k * N + ii) * NC + c, P.base.p + es * P.base.estride +
+                                                   (long long)k * P.base.cstride + node);
+      }
   }
 
   // ---- 4. volume: metric + flux per column point -------------------------
@@ -403,7 +549,10 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
     for (int kz = 0; kz < N; ++kz) {
       const int qp = c * N + kz;
       double det, ctrv[D][D];
-      point_metric<D, N>(P, g, qp, det, ctrv);
+      if (WL::ASYNC && !flat)
+        point_metric_ge<D, N>(P.gc, TC, g, kz, GEs, NC, c, det, ctrv);
+      else
+        point_metric<D, N>(P, g, qp, det, ctrv);
       const double wq = point_weight<D, N>(TC, qp);
       double F[D][KOUT];
       if constexpr (OPK == OP_DIVHV) {
@@ -542,6 +691,7 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
     __syncwarp();
   }
   if (!act) return;
+  if (pre_base) cp_async_wait_all();
   // x pass and store from the x-pencil: points (ii, [j,] k) of lane c
 #pragma unroll
   for (int k = 0; k < KOUT; ++k) {
@@ -558,7 +708,8 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
         *out = o[ii];
       } else {
         const double r = __dmul_rn(P.coef, o[ii]);
-        *out = P.has_base ? __dadd_rn(P.base(e, k, node), r) : r;
+        if (pre_base) *out = __dadd_rn(BSs[(k * N + ii) * NC + c], r);
+        else *out = P.has_base ? __dadd_rn(P.base(e, k, node), r) : r;
       }
     }
   }
