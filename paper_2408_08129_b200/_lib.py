@@ -12,7 +12,7 @@ from .errors import (ConfigurationError, DeviceError, PositivityError,
                      SolverError, UsageError)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdg.so")
+LIB_PATH = os.environ.get("DG_LIB_PATH") or os.path.join(HERE, "libdg.so")
 
 DG_OK, DG_ERR_CUDA, DG_ERR_USAGE, DG_ERR_CONFIG, DG_ERR_POSITIVITY, DG_ERR_SOLVER, DG_ERR_COMM = range(7)
 FACE_WALL, FACE_FARFIELD, FACE_CONF, FACE_FINE, FACE_COARSE = range(5)

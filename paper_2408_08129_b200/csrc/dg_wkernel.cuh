@@ -48,15 +48,33 @@ struct WLayout {
   // staging area keeps 4 CTAs (the register-limited occupancy) per SM
   // (+ the lane's terrain scalars: omh, dh at its column and omh at its point
   // of every vertical face; the epilogue's base values reuse the face area)
-  static constexpr int GEON = 1 + 3 * (D - 1);
-  static constexpr int FGA = 2 * D * RAW * NC;
-  static constexpr int FGB = (FGA > KOUT * NP ? FGA : KOUT * NP) + GEON * NC;
+  static constexpr int GEON = 1 + (D - 1);  // + the compact edge table GEE
+  static constexpr int NE = ipow(N, D - 2);  // distinct edge values per vertical face
+  static constexpr int GEE = 2 * (D - 1) * NE;
+  // staged components per face: a vertical face has the exact normal
+  // +-e_AX, so div(hV) needs only (V_AX, h) of the neighbour there
+  static constexpr int FCX = (OPK == OP_DIVHV) ? 2 : RAW;
+  static constexpr int FCZ = RAW;
+  static constexpr int FGA = (2 * (D - 1) * FCX + 2 * FCZ) * NC;
+  static constexpr int FGB = (FGA > KOUT * NP ? FGA : KOUT * NP) + GEON * NC + GEE;
   static constexpr bool ASYNC =
       (TABD + WPB * NSLOT * odd(KX * TSZ + FGB)) * 8 <= 54 * 1024;
-  static constexpr int FGN = ASYNC ? FGB - GEON * NC : 0;
+  static constexpr int FGN = ASYNC ? FGB - GEON * NC - GEE : 0;
+  __host__ __device__ static constexpr int fg_off(int f) {  // staged face f
+    return (f < 2 * (D - 1)) ? f * FCX * NC : (2 * (D - 1) * FCX + (f - 2 * (D - 1)) * FCZ) * NC;
+  }
+  __host__ __device__ static constexpr int fg_cnt(int f) { return (f < 2 * (D - 1)) ? FCX : FCZ; }
   static constexpr int SLOT = odd(KX * TSZ + (ASYNC ? FGB : 0));
   static constexpr size_t SMEM = (size_t)(TABD + WPB * NSLOT * SLOT) * sizeof(double);
   static constexpr bool OK = (NC <= 32) && (OPK != OP_ADV);
+  // resident CTAs per SM the register allocation is capped for
+#ifndef DG_WMINB_GRAD
+#define DG_WMINB_GRAD 5
+#endif
+#ifndef DG_WMINB_DIVHV
+#define DG_WMINB_DIVHV 4
+#endif
+  static constexpr int MINB = (OPK == OP_GRAD) ? DG_WMINB_GRAD : DG_WMINB_DIVHV;
 };
 
 // pencil helpers on the per-element tile (3D: (i, j) column index c = i*N + j)
@@ -104,17 +122,15 @@ __device__ __forceinline__ void cp_async8(void* smem_ptr, const void* gptr) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gptr) : "memory");
 }
 
-// terrain scalars of lane c, staged in smem as GE[i * NC + c]:
+// terrain scalars, staged in smem: GE[i * NC + c] for lane c,
 //   i = 0: 1 - h/z_top at the column's horizontal Gauss point
 //   i = 1..HD: dh/dx_a there (also the z-face values of face point c)
-//   i = 1 + HD + 2 AX + side: 1 - h_edge/z_top at face point c of face (AX, side)
+// followed by the compact edge table GE[GEON * NC + (2 AX + side) * NE + qo]:
+// 1 - h_edge/z_top along vertical face (AX, side) (column table order)
 template <int D, int N>
 __device__ __forceinline__ int geo_src(int i, int c) {
-  constexpr int HD = D - 1, NQH = ipow(N, HD), NE = ipow(N, HD - 1);
-  if (i == 0) return c;
-  if (i <= HD) return NQH * i + c;
-  const int fs = i - 1 - HD;  // 2 AX + side
-  return NQH * (1 + HD) + fs * NE + ((D == 2) ? 0 : c / N);
+  constexpr int HD = D - 1, NQH = ipow(N, HD);
+  return (i == 0) ? c : NQH * i + c;
 }
 
 // Gauss-point metric (as point_metric) from the staged terrain scalars
@@ -162,7 +178,9 @@ __device__ __forceinline__ void face_metric_ge(const GeoConst& gc, const ElemGeo
 #pragma unroll
   for (int a = 0; a < D; ++a) n[a] = 0.0;
   if constexpr (AX < D - 1) {
-    const double omh = gc.terrain ? GE[(1 + HD + 2 * AX + side) * NCs + qf] : 1.0;
+    constexpr int NE = ipow(N, HD - 1);
+    const double omh =
+        gc.terrain ? GE[(1 + HD) * NCs + (2 * AX + side) * NE + ((D == 2) ? 0 : qf / N)] : 1.0;
     const double zzv = g.s[D - 1] * omh;
     const double mag = (D == 2) ? zzv : g.s[1 - AX] * zzv;
     n[AX] = sgn;
@@ -211,10 +229,10 @@ __device__ __forceinline__ void mat_apply(const double (&M)[N][N], const double*
 // IQ: Gauss-point input (H2 of the Helmholtz pair in quad mode) -- a
 // separate instantiation so the nodal path carries none of its registers
 template <int D, int N, int OPK, bool IQ = false>
-__global__ void __launch_bounds__(WLayout<D, N, OPK>::THREADS, 4)
+__global__ void __launch_bounds__(WLayout<D, N, OPK>::THREADS, WLayout<D, N, OPK>::MINB)
 welem_kernel(const __grid_constant__ KParams<N> P) {
   using WL = WLayout<D, N, OPK>;
-  constexpr int NP = WL::NP, NC = WL::NC, EPW = WL::EPW, KIN = WL::KIN, KOUT = WL::KOUT;
+  constexpr int NC = WL::NC, EPW = WL::EPW, KIN = WL::KIN, KOUT = WL::KOUT;
   constexpr int KW = WL::KW, TSZ = WL::TSZ, NF = 2 * D;
   extern __shared__ double smem[];
   {
@@ -274,6 +292,7 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
   // interpolation work and are waited for only at the face phase
   double* FGs = X + WL::KX * TSZ;
   constexpr bool iq0 = (OPK == OP_DIVHV) && IQ;
+  constexpr bool SMP = WL::ASYNC && !iq0;  // tangential passes through smem
   if (WL::ASYNC && !iq0) {
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
@@ -282,16 +301,18 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
       const long long nb = nf[f];
       const int node = nbr_face_node<D, N>(f >> 1, f & 1, c);
 #pragma unroll
-      for (int r = 0; r < RAW; ++r) {
-        double* dst = FGs + (f * RAW + r) * NC + c;
+      for (int r = 0; r < WL::fg_cnt(f); ++r) {
+        double* dst = FGs + WL::fg_off(f) + r * NC + c;
         const double* src = nullptr;
         if (inter) {
           if constexpr (OPK == OP_GRAD) {
             if (r == 0 && P.in.p) src = P.in.p + nb * P.in.estride + node;
             if (r == 1 && P.has_K) src = P.inK.p + nb * P.inK.estride + node;
           } else {
-            src = (r < D) ? P.in.p + nb * P.in.estride + r * P.in.cstride + node
-                          : P.inH.p + nb * P.inH.estride + node;
+            // vertical face: (V_AX, h); z face: every component
+            const int cin = (WL::fg_cnt(f) == KIN) ? r : (r == 0 ? (f >> 1) : D);
+            src = (cin < D) ? P.in.p + nb * P.in.estride + cin * P.in.cstride + node
+                            : P.inH.p + nb * P.inH.estride + node;
           }
         }
         if (src) cp_async8(dst, src);
@@ -304,6 +325,9 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
     const double* colp = mesh.col + (long long)g.col * P.gc.col_stride;
 #pragma unroll
     for (int i = 0; i < WL::GEON; ++i) cp_async8(GEs + i * NC + c, colp + geo_src<D, N>(i, c));
+    constexpr int NQH = ipow(N, D - 1);
+    for (int i = c; i < WL::GEE; i += NC)
+      cp_async8(GEs + WL::GEON * NC + i, colp + NQH * D + i);
   }
   // ---- 1. nodal column, z interpolation in registers -------------------
   // in_quad (H2 of the Helmholtz pair): inputs are already Gauss values
@@ -346,48 +370,20 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
       __syncwarp();
     }
   }
-  // x pass; the x-pencil of lane c carries face point c of both x faces
-  double tox[2][KIN];
+  // x pass: the tile now holds the element's Gauss-point values, kept intact
+  // through the face phase (own traces are pencil contractions read from it)
+  if (!iq) {
 #pragma unroll
-  for (int cp = 0; cp < KIN; ++cp) {
-    double v[N], o[N];
+    for (int cp = 0; cp < KIN; ++cp) {
+      double v[N], o[N];
 #pragma unroll
-    for (int ii = 0; ii < N; ++ii) v[ii] = X[cp * TSZ + xoff<D, N>(c, ii)];
-    if (iq) {
-#pragma unroll
-      for (int ii = 0; ii < N; ++ii) o[ii] = v[ii];
-    } else {
+      for (int ii = 0; ii < N; ++ii) v[ii] = X[cp * TSZ + xoff<D, N>(c, ii)];
       mat_apply<N, false>(TC.B, v, o);
 #pragma unroll
       for (int ii = 0; ii < N; ++ii) X[cp * TSZ + xoff<D, N>(c, ii)] = o[ii];
     }
-    double t0 = 0.0, t1 = 0.0;
-#pragma unroll
-    for (int ii = 0; ii < N; ++ii) {
-      t0 = fma(TC.lift[0][ii], o[ii], t0);
-      t1 = fma(TC.lift[1][ii], o[ii], t1);
-    }
-    tox[0][cp] = t0;
-    tox[1][cp] = t1;
   }
   __syncwarp();
-  double toy[2][KIN];
-#pragma unroll
-  for (int cp = 0; cp < KIN; ++cp) {
-#pragma unroll
-    for (int k = 0; k < N; ++k) q[cp][k] = X[cp * TSZ + c * (N + 1) + k];
-    if constexpr (D == 3) {
-      double t0 = 0.0, t1 = 0.0;
-#pragma unroll
-      for (int jj = 0; jj < N; ++jj) {
-        const double v = X[cp * TSZ + yoff<N>(c, jj)];
-        t0 = fma(TC.lift[0][jj], v, t0);
-        t1 = fma(TC.lift[1][jj], v, t1);
-      }
-      toy[0][cp] = t0;
-      toy[1][cp] = t1;
-    }
-  }
   // ---- 3. faces: flux at face point c of every face --------------------
   // fl_l[f][k]: lifted flux*ws (with sign) at face point c of face f
   double fl[NF][KOUT];
@@ -415,6 +411,46 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
     }
     const double* Mq0 = &TS.halfq[sf & 1][0][0];
     const double* Mq1 = &TS.halfq[(sf >> 1) & 1][0][0];
+    if constexpr (SMP) {
+      // the element's staged neighbour face nodes are read straight from
+      // smem by the first tangential pass, whose results replace them in
+      // place for the second pass
+      // (vertical faces of div(hV): only V_AX and h are staged and needed --
+      // the other components meet an exact zero normal component)
+      double* G0 = FGs + WL::fg_off(f);
+      constexpr int FC = (OPK == OP_DIVHV && AX < D - 1) ? 2 : KIN;  // passed comps
+      auto slot_comp = [&](int r) { return (FC == KIN) ? r : (r == 0 ? AX : D); };
+#pragma unroll
+      for (int cp = 0; cp < KIN; ++cp) TN[cp] = 0.0;
+      double t1[FC];
+#pragma unroll
+      for (int r = 0; r < FC; ++r) {
+        double t1v = 0.0;
+        if constexpr (D == 2) {
+#pragma unroll
+          for (int j = 0; j < N; ++j) t1v = fma(M0[fa * N + j], G0[r * NC + j], t1v);
+          TN[slot_comp(r)] = t1v;
+        } else {
+#pragma unroll
+          for (int j = 0; j < N; ++j) t1v = fma(M0[fa * N + j], G0[r * NC + j * N + fb], t1v);
+          t1[r] = t1v;
+        }
+      }
+      if constexpr (D == 3) {
+        double* S = G0;
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < FC; ++r) S[r * NC + c] = t1[r];
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < FC; ++r) {
+          double t2v = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) t2v = fma(M1[fb * N + j], S[r * NC + fa * N + j], t2v);
+          TN[slot_comp(r)] = t2v;
+        }
+      }
+    }
 #pragma unroll
     for (int cp = 0; cp < KIN; ++cp) {
       double gval = 0.0;
@@ -448,13 +484,8 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
             TN[cp] = fine ? t2v : gval;
           }
         }
-      } else {
-      if constexpr (WL::ASYNC && OPK == OP_GRAD) {
-        const double xv = FGs[(f * RAW + 0) * NC + c];
-        gval = P.has_K ? P.alpha * (xv - P.beta * FGs[(f * RAW + 1) * NC + c]) : P.alpha * xv;
-      } else if constexpr (WL::ASYNC) {
-        gval = FGs[(f * RAW + cp) * NC + c];
-      } else if (act && inter) {
+      } else if constexpr (!SMP) {
+      if (act && inter) {
         gval = load_input<D, N, OPK>(P, nb, cp, nbr_face_node<D, N>(AX, side, c));
       }
       double t1v = 0.0;
@@ -474,16 +505,17 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
         TN[cp] = t2v;
       }
       }  // nodal input
-      // own trace
-      if constexpr (AX == D - 1) {
+      // own trace: lift contraction of the lane's pencil along AX
+      {
         double t = 0.0;
 #pragma unroll
-        for (int k = 0; k < N; ++k) t = fma(TC.lift[side][k], q[cp][k], t);
+        for (int k = 0; k < N; ++k) {
+          const int off = (AX == D - 1) ? c * (N + 1) + k
+                        : (AX == 0)     ? xoff<D, N>(c, k)
+                                        : yoff<N>(c, k);
+          t = fma(TC.lift[side][k], X[cp * TSZ + off], t);
+        }
         TO[cp] = t;
-      } else if constexpr (AX == 0) {
-        TO[cp] = tox[side][cp];
-      } else {
-        TO[cp] = toy[side][cp];
       }
     }
     if (kd == KIND_COARSE || !act) {
@@ -516,6 +548,18 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
   };
   // each lane reads back only the face slots it issued itself
   if (WL::ASYNC) cp_async_wait_all();
+  if constexpr (SMP) {
+    if constexpr (OPK == OP_GRAD) {
+      // p = alpha (x - beta K) at the staged nodes, in place (own slots)
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+        const double xv = FGs[WL::fg_off(f) + c];
+        FGs[WL::fg_off(f) + c] =
+            P.has_K ? P.alpha * (xv - P.beta * FGs[WL::fg_off(f) + NC + c]) : P.alpha * xv;
+      }
+    }
+    __syncwarp();  // staged nodes visible warp-wide; the tile is free
+  }
   face(std::integral_constant<int, 0>{}, 0);
   face(std::integral_constant<int, 0>{}, 1);
   face(std::integral_constant<int, 1>{}, 0);
@@ -556,11 +600,12 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
       const double wq = point_weight<D, N>(TC, qp);
       double F[D][KOUT];
       if constexpr (OPK == OP_DIVHV) {
-        const double h = q[D][kz];
+        // own column of the Gauss-point tile (read before G overwrites it)
+        const double h = X[D * TSZ + c * (N + 1) + kz];
 #pragma unroll
-        for (int a = 0; a < D; ++a) F[a][0] = h * q[a][kz];
+        for (int a = 0; a < D; ++a) F[a][0] = h * X[a * TSZ + c * (N + 1) + kz];
       } else {
-        const double p = q[0][kz];
+        const double p = X[c * (N + 1) + kz];
 #pragma unroll
         for (int a = 0; a < D; ++a)
 #pragma unroll
