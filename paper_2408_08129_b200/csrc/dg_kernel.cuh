@@ -945,16 +945,43 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
     }
   }
   __syncthreads();
-  if (!act) return;
-  double* out = P.out.p + e * P.out.estride + q;
+  double yv = 0.0;  // final value (KOUT == 1 when the Gram-Schmidt dots are fused)
+  if (act) {
+    double* out = P.out.p + e * P.out.estride + q;
 #pragma unroll
-  for (int k = 0; k < KOUT; ++k) {
-    const double r = res[k * NP + q];
-    double add;
-    if (P.mode == OUT_DUAL) add = r;
-    else if (OPK == OP_ADV) add = -r;
-    else add = __dmul_rn(P.coef, r);
-    out[k * P.out.cstride] += add;
+    for (int k = 0; k < KOUT; ++k) {
+      const double r = res[k * NP + q];
+      double add;
+      if (P.mode == OUT_DUAL) add = r;
+      else if (OPK == OP_ADV) add = -r;
+      else add = __dmul_rn(P.coef, r);
+      const double y = out[k * P.out.cstride] + add;
+      out[k * P.out.cstride] = y;
+      yv = y;
+    }
+  }
+  if constexpr (OPK == OP_DIVHV) {
+    // fused Gram-Schmidt dots of this (complete) coarse element, row
+    // gs_row0 + CTA of gs_part (see gs_dots in dg_wkernel.cuh)
+    if (P.gs_part != nullptr) {
+      const int nvt = P.gs_nv + 1;
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+      constexpr int NW = L::CTHREADS / 32;
+      static_assert(L::CELEM - L::C_CH >= NW * 32, "coarse gs scratch");
+      double* wr = CH;  // children face values, free by now: NW x 32 warp sums
+      for (int col = 0; col < nvt; ++col) {
+        double s = act ? (col < P.gs_nv ? P.gsV[(long long)col * P.gs_vs + e * NP + q] : yv) * yv
+                       : 0.0;
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) wr[wid * 32 + col] = s;
+      }
+      __syncthreads();
+      if (threadIdx.x < nvt) {
+        double s = 0.0;
+        for (int w = 0; w < NW; ++w) s += wr[w * 32 + threadIdx.x];
+        P.gs_part[((long long)P.gs_row0 + blockIdx.x) * nvt + threadIdx.x] = s;
+      }
+    }
   }
 }
 

@@ -23,6 +23,10 @@ struct OpArgs {
   int dbg;  // phase-skip flags for profiling experiments only (0 in production)
   int in_quad, out_quad;
   double* mass_partial;
+  const double* gsV;  // fused Gram-Schmidt dots (see KParams)
+  long long gs_vs;
+  int gs_nv;
+  double* gs_part;
   const double* tabs;  // host pointer, Tab<N> layout
 };
 
@@ -58,6 +62,11 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
   P.in_quad = a.in_quad;
   P.out_quad = a.out_quad;
   P.mass_partial = a.mass_partial;
+  P.gsV = a.gsV;
+  P.gs_vs = a.gs_vs;
+  P.gs_nv = a.gs_nv;
+  P.gs_part = a.gs_part;
+  P.gs_row0 = 0;
   std::memcpy(&P.tab, a.tabs, sizeof(Tab<N>));
   using WL = WLayout<D, N, OPK>;
   if constexpr (WL::OK) {
@@ -95,10 +104,12 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       if (a.mesh.n_coarse > 0) {
+        P.gs_row0 = wgrid;  // coarse elements' dot partials follow the CTA rows
         coarse_kernel<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
             P, a.mesh.coarse_list, a.mesh.n_coarse, nullptr);
         e = cudaGetLastError();
       }
+      if (info) info->grid = wgrid + a.mesh.n_coarse;  // partial rows written
       return e;
     }
   }
@@ -138,7 +149,7 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
 }
 
 // is the warp-element kernel (and with it Gauss-point storage of the
-// Helmholtz intermediate) used for this (dim, n)?
+// Helmholtz intermediate and the fused Gram-Schmidt dots) used for this (dim, n)?
 inline bool welem_enabled(int D, int N) {
   int nc = 1;
   for (int a = 0; a < D - 1; ++a) nc *= N;

@@ -54,6 +54,12 @@ struct KParams {
   // the identity, so the Helmholtz pair skips both transforms
   int in_quad, out_quad;
   double* mass_partial;  // ADV: per-CTA sum of the density dual (or null)
+  // fused Gram-Schmidt dots of the result y (div(hV) MINV only, GMRES):
+  // row (gs_row0 + CTA) of gs_part gets (V_0.y, .., V_{nv-1}.y, y.y) partials
+  const double* gsV;
+  long long gs_vs;
+  int gs_nv, gs_row0;
+  double* gs_part;
   Tab<N> tab;
 };
 

@@ -83,7 +83,7 @@ struct dg_ctx {
   DevBuf<uint8_t> kind;
   DevBuf<double> col, ffU, ffp, ffh, sigma, bg;
   // scratch
-  DevBuf<double> mass_partial, partial, redout, coef_dev;
+  DevBuf<double> mass_partial, partial, redout, coef_dev, gs_part;
   double* pinned = nullptr;  // 256 doubles
   DevBuf<double> sV;         // vector field (n_tot, d, NP)
   DevBuf<double> sh, sK, sx, srhs, spold, sw, sr, sx2, shq;  // scalar fields
@@ -143,7 +143,8 @@ double op_bytes(dg_ctx* c, int opk, const OpArgs& a) {
     return b;
   }
   if (opk == OP_GRAD) return n * (1 + (a.has_K ? 1 : 0) + d + (a.has_base ? d : 0));
-  return n * (d + 1 + 1 + (a.has_base ? 1 : 0));               // V, h in, y out, base
+  // V, h in, y out, base; + the basis vectors of fused Gram-Schmidt dots
+  return n * (d + 1 + 1 + (a.has_base ? 1 : 0) + (a.gs_part ? a.gs_nv : 0));
 }
 
 int launch(dg_ctx* c, int opk, const OpArgs& a) {
@@ -202,9 +203,22 @@ int op_grad(dg_ctx* c, const double* x, const double* K, double alpha, double be
 }
 
 // y = base + coef * [Minv] Div(h V)
+struct GsFuse {  // fused Gram-Schmidt dots of the div(hV) result (gs_dots)
+  const double* V = nullptr;
+  long long vs = 0;
+  int nv = 0;
+  double* part = nullptr;
+};
+
 int op_divhv(dg_ctx* c, CView V, const double* h, int homog, int mode, MView out, CView base,
-             int has_base, double coef, int in_quad = 0) {
+             int has_base, double coef, int in_quad = 0, const GsFuse* gs = nullptr) {
   OpArgs a = base_args(c);
+  if (gs) {
+    a.gsV = gs->V;
+    a.gs_vs = gs->vs;
+    a.gs_nv = gs->nv;
+    a.gs_part = gs->part;
+  }
   a.in = V;
   a.inH = cv(h, c->NP, c->NP);
   a.homogeneous = homog;
@@ -248,7 +262,8 @@ int interp_h(dg_ctx* c, const double* h, double* hq) {
 
 // homogeneous Helmholtz action y = x + a_dt Minv Div_h(V), V = -(a_dt/M^2)(g-1) Minv G(x).
 // With hq (Gauss-point h) the intermediate V stays at the Gauss points.
-int helm_apply(dg_ctx* c, double a_dt, const double* h, const double* hq, double* x, double* y) {
+int helm_apply(dg_ctx* c, double a_dt, const double* h, const double* hq, double* x, double* y,
+               const GsFuse* gs = nullptr) {
   const int d = c->dim;
   RET(halo(c, x, 1));
   const double gm1 = c->model.gamma - 1.0;
@@ -257,8 +272,14 @@ int helm_apply(dg_ctx* c, double a_dt, const double* h, const double* hq, double
               CView{}, 0, -(a_dt * c->model.inv_mach_sq), qd));
   RET(halo(c, c->sV.p, d));
   RET(op_divhv(c, cv(c->sV.p, (long long)d * c->NP, c->NP), qd ? hq : h, 1, OUT_MINV,
-               mv(y, c->NP, c->NP), cv(x, c->NP, c->NP), 1, a_dt, qd));
+               mv(y, c->NP, c->NP), cv(x, c->NP, c->NP), 1, a_dt, qd, gs));
   return DG_OK;
+}
+
+// the warp-element div(hV) kernel can fuse the Gram-Schmidt dots
+bool gs_fusable(dg_ctx* c) {
+  static const bool off = getenv("DG_GS_FUSE") && std::string(getenv("DG_GS_FUSE")) == "0";
+  return !off && welem_enabled(c->dim, c->N) && !quad_mode(c);
 }
 
 // F(x) = e_e - a_dt Minv Div_h(m_e - a_dt/M^2 Minv G((g-1)(x - kf K)))   (imex.py:190-218)
@@ -305,6 +326,13 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const doubl
   const long long vs = ((ns + 31) / 32) * 32 + 32 * 13;
   CK(c->basis.alloc((size_t)(m + 1) * vs));
   double* Vb = c->basis.p;
+  const bool fuse = gs_fusable(c);
+  if (fuse) {
+    // one row of <= m + 1 dot partials per element-kernel CTA (>= 4 elements
+    // each) and per coarse element
+    const long long rows = ((long long)c->n_el + 3) / 4 + c->mesh.n_coarse + 1;
+    CK(c->gs_part.alloc((size_t)rows * 32));
+  }
   double* coefs = c->pinned + 128;  // pinned staging for the coefficient uploads
   double* w = c->sw.p;
   double* r = c->sr.p;
@@ -340,9 +368,16 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const doubl
     g[0] = beta;
     int done = 0;
     for (int j = 0; j < m; ++j) {
-      RET(helm_apply(c, a_dt, h, hq, Vb + (size_t)j * vs, w));
-      // classical Gram-Schmidt: h_i = V_i . w and |w|^2 in one pass
-      CK(multidot(c->stream, n, j + 1, Vb, vs, w, c->partial.p, c->redout.p));
+      // classical Gram-Schmidt: h_i = V_i . w and |w|^2 in one pass,
+      // fused into the div(hV) kernel that produces w when it can
+      if (fuse) {
+        GsFuse gs{Vb, vs, j + 1, c->gs_part.p};
+        RET(helm_apply(c, a_dt, h, hq, Vb + (size_t)j * vs, w, &gs));
+        CK(reduce_rows(c->stream, c->gs_part.p, c->last.grid, j + 2, c->partial.p, c->redout.p));
+      } else {
+        RET(helm_apply(c, a_dt, h, hq, Vb + (size_t)j * vs, w));
+        CK(multidot(c->stream, n, j + 1, Vb, vs, w, c->partial.p, c->redout.p));
+      }
       RET(reduce_read(c, c->redout.p, j + 2, hc.data()));
       const double nb2 = hc[j + 1];
       const double nb = std::sqrt(nb2);
@@ -650,7 +685,7 @@ int dg_ctx_destroy(dg_ctx* c) {
   if (!c) return DG_OK;
   cudaSetDevice(c->device);
   for (auto* b : {&c->col, &c->ffU, &c->ffp, &c->ffh, &c->sigma, &c->bg, &c->mass_partial,
-                  &c->partial, &c->redout, &c->coef_dev, &c->sV, &c->sh, &c->sK, &c->sx,
+                  &c->partial, &c->redout, &c->coef_dev, &c->gs_part, &c->sV, &c->sh, &c->sK, &c->sx,
                   &c->srhs, &c->spold, &c->sw, &c->sr, &c->sx2, &c->basis})
     b->release();
   for (auto& s : c->st) s.release();

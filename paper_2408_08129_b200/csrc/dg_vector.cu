@@ -485,6 +485,37 @@ cudaError_t positivity(cudaStream_t st, long long n_el, int np, int d, const dou
   return cudaGetLastError();
 }
 
+// many rows (e.g. one per element-kernel CTA) x ncols <= 32: RED_BLOCKS CTAs
+// each sum a contiguous row range in order, then k_reduce_cols (deterministic)
+__global__ void __launch_bounds__(RED_THREADS)
+k_reduce_rows(const double* __restrict__ partials, long long nrows, int ncols,
+              double* __restrict__ out) {
+  const long long per = (nrows + gridDim.x - 1) / gridDim.x;
+  const long long r0 = (long long)blockIdx.x * per;
+  const long long r1 = r0 + per < nrows ? r0 + per : nrows;
+  const int col = threadIdx.x & 31, grp = threadIdx.x >> 5;  // 8 row groups
+  double s = 0.0;
+  if (col < ncols)
+    for (long long r = r0 + grp; r < r1; r += RED_THREADS / 32) s += partials[r * ncols + col];
+  __shared__ double red[RED_THREADS / 32][32];
+  red[grp][col] = s;
+  __syncthreads();
+  if (threadIdx.x < ncols) {
+    double t = 0.0;
+    for (int g = 0; g < RED_THREADS / 32; ++g) t += red[g][threadIdx.x];
+    out[(long long)blockIdx.x * ncols + threadIdx.x] = t;
+  }
+}
+
+cudaError_t reduce_rows(cudaStream_t st, const double* partials, long long nrows, int ncols,
+                        double* tmp, double* out) {
+  prof_begin(st);
+  k_reduce_rows<<<RED_BLOCKS, RED_THREADS, 0, st>>>(partials, nrows, ncols, tmp);
+  k_reduce_cols<<<(ncols + 7) / 8, 256, 0, st>>>(tmp, RED_BLOCKS, ncols, out);
+  prof_end(st, P_DOT, 8.0 * nrows * ncols, 2);
+  return cudaGetLastError();
+}
+
 cudaError_t reduce_cols(cudaStream_t st, const double* partials, int nblocks, int ncols, double* out) {
   prof_begin(st);
   k_reduce_cols<<<(ncols + 7) / 8, 256, 0, st>>>(partials, nblocks, ncols, out);

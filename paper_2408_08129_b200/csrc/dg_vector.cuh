@@ -30,5 +30,7 @@ cudaError_t copy_comps(cudaStream_t st, long long n_el, int np, int nc, const do
 cudaError_t positivity(cudaStream_t st, long long n_el, int np, int d, const double* U, double gm1,
                        double kf, double* partials);
 cudaError_t reduce_cols(cudaStream_t st, const double* partials, int nblocks, int ncols, double* out);
+cudaError_t reduce_rows(cudaStream_t st, const double* partials, long long nrows, int ncols,
+                        double* tmp, double* out);
 
 }  // namespace dg

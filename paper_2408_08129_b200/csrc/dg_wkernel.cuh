@@ -226,6 +226,74 @@ __device__ __forceinline__ void mat_apply(const double (&M)[N][N], const double*
   }
 }
 
+// Fused Gram-Schmidt dots (GMRES, krylov.py:69-72 with the classical
+// variant of DESIGN.md §4): the CTA's partial sums of V_i . y (i < nv) and
+// y . y over its elements' nodes, written as row (gs_row0 + CTA) of gs_part.
+// The lane's stored values wv[] are its x-pencil nodes (ii, c).  Elements
+// with a coarse-side hanging face are left to coarse_kernel, which adds to
+// their result afterwards.  Deterministic: fixed lane / warp / row order.
+template <int D, int N, int OPK>
+__device__ __forceinline__ void gs_dots(const KParams<N>& P, double* smem, const uint8_t* kf,
+                                        bool act, long long e, int c, const double* wv) {
+  using WL = WLayout<D, N, OPK>;
+  constexpr int NP = WL::NP, NF = 2 * D;
+  constexpr int AREA = WL::NSLOT * WL::SLOT;  // this warp's element slots
+  constexpr int CH0 = AREA / 33;
+  constexpr int CH = CH0 < 32 ? CH0 : 32;
+  static_assert(CH >= 16, "warp area too small for the fused dots");
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  bool own = act;
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+    if ((kf[f] & 15) == KIND_COARSE) own = false;
+  const int nvt = P.gs_nv + 1;
+  double* area = smem + WL::TABD + wid * AREA;
+  __syncwarp();  // every lane is done with this warp's tiles
+  double tot[2] = {0.0, 0.0};
+  for (int i0 = 0, ch = 0; i0 < nvt; i0 += CH, ++ch) {
+    const int cnt = min(CH, nvt - i0);
+    // four columns at a time: their 4 N loads are all in flight together
+    for (int i = 0; i < cnt; i += 4) {
+      double vv[4][N];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int col = i0 + i + u;
+        const bool ld = own && (i + u < cnt) && col < P.gs_nv;
+        const double* vp = P.gsV + (long long)col * P.gs_vs + e * NP;
+#pragma unroll
+        for (int ii = 0; ii < N; ++ii) {
+          const int node = (D == 3) ? ii * N * N + c : ii * N + c;
+          vv[u][ii] = ld ? vp[node] : wv[ii];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        double s = 0.0;
+#pragma unroll
+        for (int ii = 0; ii < N; ++ii) s = fma(vv[u][ii], wv[ii], s);
+        if (i + u < cnt) area[(i + u) * 33 + lane] = own ? s : 0.0;
+      }
+    }
+    __syncwarp();
+    if (lane < cnt) {
+      double t = 0.0;
+      for (int l = 0; l < 32; ++l) t += area[lane * 33 + l];
+      tot[ch] = t;
+    }
+    __syncwarp();
+  }
+  __syncthreads();  // every warp is done with its area: reuse the first one
+  double* red = smem + WL::TABD;
+  for (int i0 = 0, ch = 0; i0 < nvt; i0 += CH, ++ch)
+    if (lane < min(CH, nvt - i0)) red[wid * 32 + i0 + lane] = tot[ch];
+  __syncthreads();
+  if (wid == 0 && lane < nvt) {
+    double s = 0.0;
+    for (int w = 0; w < WL::WPB; ++w) s += red[w * 32 + lane];
+    P.gs_part[((long long)P.gs_row0 + blockIdx.x) * nvt + lane] = s;
+  }
+}
+
 // IQ: Gauss-point input (H2 of the Helmholtz pair in quad mode) -- a
 // separate instantiation so the nodal path carries none of its registers
 template <int D, int N, int OPK, bool IQ = false>
@@ -735,28 +803,38 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
     }
     __syncwarp();
   }
-  if (!act) return;
   if (pre_base) cp_async_wait_all();
   // x pass and store from the x-pencil: points (ii, [j,] k) of lane c
+  double wv[N];  // the stored values (KOUT == 1 when the dots are fused)
 #pragma unroll
-  for (int k = 0; k < KOUT; ++k) {
-    double v[N], o[N];
+  for (int ii = 0; ii < N; ++ii) wv[ii] = 0.0;
+  if (act) {
 #pragma unroll
-    for (int ii = 0; ii < N; ++ii) v[ii] = X[k * TSZ + xoff<D, N>(c, ii)];
-    if (minv) mat_apply<N, false>(TC.Binv, v, o);
-    else mat_apply<N, true>(TC.B, v, o);
+    for (int k = 0; k < KOUT; ++k) {
+      double v[N], o[N];
 #pragma unroll
-    for (int ii = 0; ii < N; ++ii) {
-      const int node = (D == 3) ? ii * N * N + c : ii * N + c;
-      double* out = P.out.p + e * P.out.estride + (long long)k * P.out.cstride + node;
-      if (!minv) {
-        *out = o[ii];
-      } else {
-        const double r = __dmul_rn(P.coef, o[ii]);
-        if (pre_base) *out = __dadd_rn(BSs[(k * N + ii) * NC + c], r);
-        else *out = P.has_base ? __dadd_rn(P.base(e, k, node), r) : r;
+      for (int ii = 0; ii < N; ++ii) v[ii] = X[k * TSZ + xoff<D, N>(c, ii)];
+      if (minv) mat_apply<N, false>(TC.Binv, v, o);
+      else mat_apply<N, true>(TC.B, v, o);
+#pragma unroll
+      for (int ii = 0; ii < N; ++ii) {
+        const int node = (D == 3) ? ii * N * N + c : ii * N + c;
+        double* out = P.out.p + e * P.out.estride + (long long)k * P.out.cstride + node;
+        double val;
+        if (!minv) {
+          val = o[ii];
+        } else {
+          const double r = __dmul_rn(P.coef, o[ii]);
+          if (pre_base) val = __dadd_rn(BSs[(k * N + ii) * NC + c], r);
+          else val = P.has_base ? __dadd_rn(P.base(e, k, node), r) : r;
+        }
+        *out = val;
+        wv[ii] = val;
       }
     }
+  }
+  if constexpr (OPK == OP_DIVHV && !IQ) {
+    if (P.gs_part != nullptr) gs_dots<D, N, OPK>(P, smem, kf, act, e, c, wv);
   }
 }
 
