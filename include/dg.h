@@ -81,6 +81,12 @@ typedef struct dg_solve_cfg {
   double krylov_tol;
   int krylov_restart;
   int krylov_max_iter;
+  /* preconditioner == 1: block_jacobi with a caller-side cache (imex.py:334-342:
+     cfg.preconditioner == "block_jacobi" and precond is not None); the context
+     keeps the blocks, their age (solves since the last build) and rebuilds when
+     age >= precond_refresh */
+  int preconditioner;
+  int precond_refresh;
 } dg_solve_cfg;
 
 /* KrylovStats (orodg/krylov.py:17-24) */
@@ -150,6 +156,30 @@ int dg_helmholtz_apply(dg_ctx* ctx, double a_dt, const double* h, const double* 
 int dg_gmres_helmholtz(dg_ctx* ctx, double a_dt, const double* h, const double* rhs, double* x,
                        double tol_rel, int restart, int max_iter, dg_krylov_stats* stats,
                        double* history, int history_cap);
+
+/* right-preconditioned variant: precond != 0 applies the context's block-Jacobi
+   inverse (dg_bj_build) as M in A M y = rhs, x = M y (krylov.py:27-115) */
+int dg_gmres_helmholtz_pc(dg_ctx* ctx, double a_dt, const double* h, const double* rhs, double* x,
+                          double tol_rel, int restart, int max_iter, int precond,
+                          dg_krylov_stats* stats, double* history, int history_cap);
+
+/* ---- block-Jacobi preconditioner (orodg/krylov.py:118-178) ----
+   greedy colouring of the face-adjacency graph given as element pairs
+   (element_coloring, krylov.py:118-140); host only, no device needed */
+int dg_element_coloring(long long n_el, long long n_pairs, const long long* a, const long long* b,
+                        long long* colors, int* n_colors);
+/* colours of the owned elements (host array) used to probe the blocks */
+int dg_bj_set_coloring(dg_ctx* ctx, const long long* colors, long long n_el);
+/* probe + invert the diagonal blocks of the Helmholtz action at (a_dt, h)
+   (block_jacobi_preconditioner, krylov.py:143-178); singular blocks become
+   the identity (count returned); generation increments per build */
+int dg_bj_build(dg_ctx* ctx, double a_dt, const double* h, int* n_singular,
+                long long* generation);
+/* out = M in (the blockwise inverse, krylov.py:175-176) */
+int dg_bj_apply(dg_ctx* ctx, const double* in, double* out);
+/* refresh state mirrored to the caller's cache object (_PrecondCache) */
+int dg_bj_state(dg_ctx* ctx, int* valid, int* age, long long* generation);
+int dg_bj_set_state(dg_ctx* ctx, int valid, int age);
 
 /* ---- one implicit stage and one IMEX step (orodg/imex.py:252-370) ---- */
 int dg_solve_implicit_stage(dg_ctx* ctx, const double* acc, const double* guess, double a_dt,

@@ -37,7 +37,8 @@ class CtxDesc(C.Structure):
 
 class SolveCfg(C.Structure):
     _fields_ = [("fp_tol", D), ("fp_max_iter", I), ("krylov_tol", D),
-                ("krylov_restart", I), ("krylov_max_iter", I)]
+                ("krylov_restart", I), ("krylov_max_iter", I),
+                ("preconditioner", I), ("precond_refresh", I)]
 
 
 class KrylovStatsC(C.Structure):
@@ -71,6 +72,13 @@ _SIGS = {
     "dg_energy_F": ([P, D, P, P, P, LL, P, LL, P, P], I),
     "dg_helmholtz_apply": ([P, D, P, P, P], I),
     "dg_gmres_helmholtz": ([P, D, P, P, P, D, I, I, C.POINTER(KrylovStatsC), P, I], I),
+    "dg_gmres_helmholtz_pc": ([P, D, P, P, P, D, I, I, I, C.POINTER(KrylovStatsC), P, I], I),
+    "dg_element_coloring": ([LL, LL, P, P, P, C.POINTER(I)], I),
+    "dg_bj_set_coloring": ([P, P, LL], I),
+    "dg_bj_build": ([P, D, P, C.POINTER(I), C.POINTER(LL)], I),
+    "dg_bj_apply": ([P, P, P], I),
+    "dg_bj_state": ([P, C.POINTER(I), C.POINTER(I), C.POINTER(LL)], I),
+    "dg_bj_set_state": ([P, I, I], I),
     "dg_solve_implicit_stage": ([P, P, P, D, C.POINTER(SolveCfg), P, C.POINTER(StepStatsC)], I),
     "dg_imex_step": ([P, P, P, D, D, C.POINTER(SolveCfg), C.POINTER(StepStatsC)], I),
     "dg_integrate_conserved": ([P, P, P], I),

@@ -151,6 +151,12 @@ bool Comm::allreduce_sum(double* dev, int n, cudaStream_t st) {
   return true;
 }
 
+bool Comm::allreduce_max(double* dev, int n, cudaStream_t st) {
+  if (nranks_ <= 1) return true;
+  NCCK(ncclAllReduce(dev, dev, n, ncclDouble, ncclMax, (ncclComm_t)comm_, st));
+  return true;
+}
+
 bool Comm::allreduce_minloc(double loc[4], cudaStream_t st) {
   if (nranks_ <= 1) return true;
   ncclComm_t c = (ncclComm_t)comm_;

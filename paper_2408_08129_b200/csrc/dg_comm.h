@@ -22,6 +22,7 @@ class Comm {
   bool active() const { return nranks_ > 1; }
   bool exchange(double* field, int ncomp, int np, cudaStream_t st, long long estride = -1);
   bool allreduce_sum(double* dev, int n, cudaStream_t st);
+  bool allreduce_max(double* dev, int n, cudaStream_t st);
   bool allreduce_minloc(double loc[4], cudaStream_t st);  // (v0, i0, v1, i1) global min
   long long global_index(long long local) const { return offset_ + local; }
   const std::string& error() const { return err_; }

@@ -16,6 +16,7 @@
 #include "dg_vector.cuh"
 #include "dg_comm.h"
 #include "dg_prof.h"
+#include "dg_precond.cuh"
 
 using namespace dg;
 
@@ -89,6 +90,13 @@ struct dg_ctx {
   DevBuf<double> sh, sK, sx, srhs, spold, sw, sr, sx2, shq;  // scalar fields
   DevBuf<double> basis;      // (m+1) x (n_tot NP)
   DevBuf<double> st[6];      // state fields (n_tot, V, NP)
+  // block-Jacobi preconditioner (dg_precond.cu): colouring of the owned
+  // elements, inverse blocks (transposed), probe / apply scratch, refresh state
+  DevBuf<int> bj_colors, bj_sing;
+  int bj_ncolors = 0;
+  DevBuf<double> bj_inv, sz, su;
+  int bj_valid = 0, bj_age = 1 << 30;
+  long long bj_gen = 0;
   LaunchInfo last{};
   Comm comm;
   long long scal() const { return (long long)n_tot * NP; }
@@ -312,8 +320,15 @@ int norm2(dg_ctx* c, const double* x, double* out) {
   return DG_OK;
 }
 
+int bj_apply_ctx(dg_ctx* c, const double* in, double* out) {
+  if (!c->bj_valid) return fail(DG_ERR_USAGE, "block-Jacobi preconditioner not built");
+  CK(bj_apply(c->stream, c->n_el, c->NP, c->bj_inv.p, in, out));
+  return DG_OK;
+}
+
+// right-preconditioned (pc: M = block-Jacobi inverse, krylov.py:56-66,105-109)
 int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const double* rhs, double* x,
-          double tol, int restart, int max_iter, Gm& st) {
+          double tol, int restart, int max_iter, Gm& st, bool pc = false) {
   if (!(tol > 0.0 && tol < 1.0)) return fail(DG_ERR_CONFIG, "tol_rel must be in (0,1)");
   const long long ns = c->scal();
   const long long n = (long long)c->n_el * c->NP;
@@ -370,12 +385,17 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const doubl
     for (int j = 0; j < m; ++j) {
       // classical Gram-Schmidt: h_i = V_i . w and |w|^2 in one pass,
       // fused into the div(hV) kernel that produces w when it can
+      double* src = Vb + (size_t)j * vs;
+      if (pc) {
+        RET(bj_apply_ctx(c, src, c->sz.p));  // w = A M v_j
+        src = c->sz.p;
+      }
       if (fuse) {
         GsFuse gs{Vb, vs, j + 1, c->gs_part.p};
-        RET(helm_apply(c, a_dt, h, hq, Vb + (size_t)j * vs, w, &gs));
+        RET(helm_apply(c, a_dt, h, hq, src, w, &gs));
         CK(reduce_rows(c->stream, c->gs_part.p, c->last.grid, j + 2, c->partial.p, c->redout.p));
       } else {
-        RET(helm_apply(c, a_dt, h, hq, Vb + (size_t)j * vs, w));
+        RET(helm_apply(c, a_dt, h, hq, src, w));
         CK(multidot(c->stream, n, j + 1, Vb, vs, w, c->partial.p, c->redout.p));
       }
       RET(reduce_read(c, c->redout.p, j + 2, hc.data()));
@@ -455,7 +475,17 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const doubl
       for (int i = 0; i < done; ++i) coefs[i] = -y[i];
       CK(cudaMemcpyAsync(c->coef_dev.p, coefs, done * sizeof(double), cudaMemcpyHostToDevice,
                          c->stream));
-      CK(axpy_multi(c->stream, n, done, Vb, vs, c->coef_dev.p, x, c->partial.p, nullptr));
+      if (!pc) {
+        CK(axpy_multi(c->stream, n, done, Vb, vs, c->coef_dev.p, x, c->partial.p, nullptr));
+      } else {
+        // x <- x + M (V y)
+        CK(cudaMemsetAsync(c->su.p, 0, n * sizeof(double), c->stream));
+        CK(axpy_multi(c->stream, n, done, Vb, vs, c->coef_dev.p, c->su.p, c->partial.p, nullptr));
+        RET(bj_apply_ctx(c, c->su.p, c->sz.p));
+        const double cf[2] = {1.0, 1.0};
+        const double* xs[2] = {x, c->sz.p};
+        CK(lincomb(c->stream, n, 2, cf, xs, x));
+      }
     }
     RET(residual_into_r());
     st.restarts += 1;
@@ -463,6 +493,41 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const doubl
   st.restarts = std::max(0, st.restarts - 1);
   // the final true residual equals the last beta: x is unchanged since r
   st.converged = st.residual <= tol ? 1 : 0;
+  return DG_OK;
+}
+
+// ------------------------------------------------ block-Jacobi (dg_precond.cu)
+// probe the diagonal blocks of the homogeneous Helmholtz action at (a_dt, h)
+// colour by colour, node by node (krylov.py:143-160), then invert them
+int bj_build(dg_ctx* c, double a_dt, const double* h, const double* hq, int* n_sing) {
+  if (c->bj_ncolors <= 0)
+    return fail(DG_ERR_USAGE, "block-Jacobi: no element colouring set (dg_bj_set_coloring)");
+  const long long ns = c->scal();
+  const int NP = c->NP;
+  CK(c->bj_inv.alloc((size_t)c->n_el * NP * NP));
+  CK(c->sz.alloc(ns));
+  CK(c->su.alloc(ns));
+  CK(c->bj_sing.alloc(1));
+  CK(cudaMemsetAsync(c->bj_sing.p, 0, sizeof(int), c->stream));
+  for (int col = 0; col < c->bj_ncolors; ++col)
+    for (int node = 0; node < NP; ++node) {
+      CK(bj_probe(c->stream, c->n_el, NP, c->bj_colors.p, col, node, c->sz.p));
+      RET(helm_apply(c, a_dt, h, hq, c->sz.p, c->su.p));
+      CK(bj_scatter(c->stream, c->n_el, NP, c->bj_colors.p, col, node, c->su.p, c->bj_inv.p));
+    }
+  CK(bj_invert(c->stream, c->n_el, NP, c->bj_inv.p, c->bj_inv.p, c->bj_sing.p));
+  int ns_local = 0;
+  CK(cudaMemcpyAsync(&ns_local, c->bj_sing.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  double tot = ns_local;
+  if (c->comm.active()) {
+    c->pinned[0] = tot;
+    CK(cudaMemcpyAsync(c->redout.p, c->pinned, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    RET(reduce_read(c, c->redout.p, 1, &tot));
+  }
+  if (n_sing) *n_sing = (int)tot;
+  c->bj_valid = 1;
+  c->bj_gen += 1;
   return DG_OK;
 }
 
@@ -530,9 +595,19 @@ int solve_stage(dg_ctx* c, const double* acc, const double* guess, double a_dt,
       RET(interp_h(c, c->sh.p, c->shq.p));
       hq = c->shq.p;
     }
+    // block-Jacobi refresh cadence of imex.py:334-342 (age counts solves)
+    bool pc = false;
+    if (cfg.preconditioner == 1) {
+      if (!c->bj_valid || c->bj_age >= cfg.precond_refresh) {
+        RET(bj_build(c, a_dt, c->sh.p, hq, nullptr));
+        c->bj_age = 0;
+      }
+      c->bj_age += 1;
+      pc = true;
+    }
     Gm gs;
     RET(gmres(c, a_dt, c->sh.p, hq, c->srhs.p, c->sx.p, cfg.krylov_tol, cfg.krylov_restart,
-              cfg.krylov_max_iter, gs));
+              cfg.krylov_max_iter, gs, pc));
     if (stats && stats->n_krylov < DG_MAX_SOLVES) stats->krylov_iters[stats->n_krylov++] = gs.iterations;
     if (!gs.converged) {
       if (stats) {
@@ -798,6 +873,13 @@ int dg_helmholtz_apply(dg_ctx* c, double a_dt, const double* h, const double* x,
 int dg_gmres_helmholtz(dg_ctx* c, double a_dt, const double* h, const double* rhs, double* x,
                        double tol_rel, int restart, int max_iter, dg_krylov_stats* stats,
                        double* history, int history_cap) {
+  return dg_gmres_helmholtz_pc(c, a_dt, h, rhs, x, tol_rel, restart, max_iter, 0, stats, history,
+                               history_cap);
+}
+
+int dg_gmres_helmholtz_pc(dg_ctx* c, double a_dt, const double* h, const double* rhs, double* x,
+                          double tol_rel, int restart, int max_iter, int precond,
+                          dg_krylov_stats* stats, double* history, int history_cap) {
   RET(ensure_work(c));
   RET(halo(c, const_cast<double*>(h), 1));
   const double* hq = nullptr;
@@ -806,7 +888,7 @@ int dg_gmres_helmholtz(dg_ctx* c, double a_dt, const double* h, const double* rh
     hq = c->shq.p;
   }
   Gm gs;
-  RET(gmres(c, a_dt, h, hq, rhs, x, tol_rel, restart, max_iter, gs));
+  RET(gmres(c, a_dt, h, hq, rhs, x, tol_rel, restart, max_iter, gs, precond != 0));
   if (stats) {
     stats->iterations = gs.iterations;
     stats->restarts = gs.restarts;
@@ -988,6 +1070,101 @@ int dg_profile_read(double* ms, double* bytes, long long* count) {
     bytes[p.cls[i]] += p.bytes[i];
     count[p.cls[i]] += 1;
   }
+  return DG_OK;
+}
+
+// greedy colouring of the face-adjacency graph (orodg/krylov.py:118-140):
+// elements in order, each takes the smallest colour none of its already
+// coloured neighbours has; self pairs (periodic wraps) are ignored
+int dg_element_coloring(long long n_el, long long n_pairs, const long long* a, const long long* b,
+                        long long* colors, int* n_colors) {
+  if (n_el < 0 || n_pairs < 0) return fail(DG_ERR_USAGE, "negative sizes");
+  std::vector<long long> deg(n_el + 1, 0);
+  for (long long k = 0; k < n_pairs; ++k) {
+    const long long i = a[k], j = b[k];
+    if (i < 0 || j < 0 || i >= n_el || j >= n_el) return fail(DG_ERR_USAGE, "pair out of range");
+    if (i == j) continue;
+    deg[i + 1] += 1;
+    deg[j + 1] += 1;
+  }
+  for (long long i = 0; i < n_el; ++i) deg[i + 1] += deg[i];
+  std::vector<long long> adj(deg[n_el]), fill(deg.begin(), deg.end() - 1);
+  for (long long k = 0; k < n_pairs; ++k) {
+    const long long i = a[k], j = b[k];
+    if (i == j) continue;
+    adj[fill[i]++] = j;
+    adj[fill[j]++] = i;
+  }
+  std::vector<long long> stamp;  // stamp[c] == i + 1: colour c used around element i
+  long long maxc = -1;
+  for (long long i = 0; i < n_el; ++i) colors[i] = -1;
+  for (long long i = 0; i < n_el; ++i) {
+    for (long long k = deg[i]; k < deg[i + 1]; ++k) {
+      const long long cj = colors[adj[k]];
+      if (cj >= 0) {
+        if ((long long)stamp.size() <= cj) stamp.resize(cj + 1, 0);
+        stamp[cj] = i + 1;
+      }
+    }
+    long long col = 0;
+    while (col < (long long)stamp.size() && stamp[col] == i + 1) ++col;
+    colors[i] = col;
+    maxc = std::max(maxc, col);
+  }
+  if (n_colors) *n_colors = (int)(maxc + 1);
+  return DG_OK;
+}
+
+int dg_bj_set_coloring(dg_ctx* c, const long long* colors, long long n) {
+  if (n != c->n_el) return fail(DG_ERR_USAGE, "colouring must cover the owned elements");
+  std::vector<int> h(n);
+  int nc = 0;
+  for (long long i = 0; i < n; ++i) {
+    if (colors[i] < 0) return fail(DG_ERR_USAGE, "negative colour");
+    h[i] = (int)colors[i];
+    nc = std::max(nc, h[i] + 1);
+  }
+  if (c->comm.active()) {
+    // every rank probes every colour (the action's halo exchanges are collective)
+    c->pinned[0] = nc;
+    CK(cudaMemcpyAsync(c->redout.p, c->pinned, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (!c->comm.allreduce_max(c->redout.p, 1, c->stream)) return fail(DG_ERR_COMM, c->comm.error());
+    double v;
+    RET(sync_read(c, c->redout.p, 1, &v));
+    nc = (int)v;
+  }
+  CK(c->bj_colors.upload(h.data(), h.size()));
+  c->bj_ncolors = nc;
+  c->bj_valid = 0;
+  return DG_OK;
+}
+
+int dg_bj_build(dg_ctx* c, double a_dt, const double* h, int* n_singular, long long* generation) {
+  RET(ensure_work(c));
+  RET(halo(c, const_cast<double*>(h), 1));
+  const double* hq = nullptr;
+  if (quad_mode(c)) {
+    RET(interp_h(c, h, c->shq.p));
+    hq = c->shq.p;
+  }
+  RET(bj_build(c, a_dt, h, hq, n_singular));
+  if (generation) *generation = c->bj_gen;
+  return DG_OK;
+}
+
+int dg_bj_apply(dg_ctx* c, const double* in, double* out) { return bj_apply_ctx(c, in, out); }
+
+int dg_bj_state(dg_ctx* c, int* valid, int* age, long long* generation) {
+  if (valid) *valid = c->bj_valid;
+  if (age) *age = c->bj_age;
+  if (generation) *generation = c->bj_gen;
+  return DG_OK;
+}
+
+int dg_bj_set_state(dg_ctx* c, int valid, int age) {
+  c->bj_valid = (valid && c->bj_inv.p) ? 1 : 0;
+  c->bj_age = age;
   return DG_OK;
 }
 

@@ -101,14 +101,60 @@ class ImplicitSolveConfig:
         if self.preconditioner not in ("none", "block_jacobi"):
             raise ConfigurationError(f"unknown preconditioner {self.preconditioner!r}")
 
-    def c(self):
+    def c(self, precond_active=False):
         s = L.SolveCfg()
         s.fp_tol = self.fp_tol
         s.fp_max_iter = self.fp_max_iter
         s.krylov_tol = self.krylov_tol
         s.krylov_restart = self.krylov_restart
         s.krylov_max_iter = self.krylov_max_iter
+        # imex.py:334: block_jacobi only with a cache object from the caller
+        s.preconditioner = 1 if (self.preconditioner == "block_jacobi" and precond_active) else 0
+        s.precond_refresh = self.precond_refresh
         return s
+
+
+class PrecondCache:
+    """The caller-side block-Jacobi cache of the reference (imex.py:245-249):
+    ``apply`` (the current preconditioner or None), ``age`` (solves since it
+    was built) and ``coloring`` (element colours, built on first use).  The
+    blocks themselves live on the device context; ``age`` is mirrored."""
+
+    def __init__(self):
+        self.apply = None
+        self.age = 10 ** 9
+        self.coloring = None
+
+
+_PrecondCache = PrecondCache
+
+
+def _bj_enter(split, cfg, precond):
+    """Arm the context's block-Jacobi state from the caller's cache; returns
+    whether the stage solves precondition (imex.py:334)."""
+    if cfg.preconditioner != "block_jacobi" or precond is None:
+        return False
+    from .krylov import BlockJacobi, _set_coloring, element_coloring
+    ctx = split.ctx
+    if precond.coloring is None:
+        precond.coloring = element_coloring(split.ops.mesh)
+    _set_coloring(ctx, precond.coloring)
+    valid = isinstance(precond.apply, BlockJacobi) and precond.apply.ctx is ctx \
+        and precond.apply.current()
+    age = int(min(precond.age, 2 ** 30))
+    L.check(ctx.lib.dg_bj_set_state(ctx.handle, 1 if valid else 0, age))
+    return True
+
+
+def _bj_exit(split, precond):
+    from .krylov import BlockJacobi
+    ctx = split.ctx
+    valid, age, gen = C.c_int(), C.c_int(), C.c_longlong()
+    L.check(ctx.lib.dg_bj_state(ctx.handle, C.byref(valid), C.byref(age), C.byref(gen)))
+    precond.age = age.value
+    if valid.value and not (isinstance(precond.apply, BlockJacobi)
+                            and precond.apply.generation == gen.value):
+        precond.apply = BlockJacobi(ctx, gen.value)
 
 
 @dataclass
@@ -207,14 +253,15 @@ class HelmholtzAction:
                                            as_ptr(xt), as_ptr(y)))
         return from_device(y.reshape(-1), host)
 
-    def _native_gmres(self, rhs, x0, tol_rel, restart, max_iter):
+    def _native_gmres(self, rhs, x0, tol_rel, restart, max_iter, precond=False):
         ctx = self.ctx
         b, host = to_device(rhs, ctx)
         b = b.reshape(self.shape).contiguous()
         x = None
         if x0 is not None:
             x = to_device(x0, ctx)[0].reshape(self.shape).contiguous()
-        xs, st = native_gmres(ctx, self.a_dt, self.h, b, x, tol_rel, restart, max_iter)
+        xs, st = native_gmres(ctx, self.a_dt, self.h, b, x, tol_rel, restart, max_iter,
+                              precond=precond)
         return from_device(xs.reshape(-1), host), st
 
 
@@ -239,20 +286,23 @@ def _step_error_info(cs):
 
 def imex_step(data, t, dt, tableau, split, cfg, timer=None, precond=None):
     """One IMEX-RK step (imex.py:252-299); returns (new_data, StepStats)."""
-    if cfg.preconditioner != "none":
-        raise UsageError("block-Jacobi preconditioning is not on the device path yet")
     ctx = split.ctx
     U, host = to_device(data, ctx)
     st = StepStats()
-    if _is_ars222(tableau):
-        out = ctx.empty(split.dim + 2, split.geometry.basis.n_nodes)
-        cs = L.StepStatsC()
-        code = ctx.lib.dg_imex_step(ctx.bind_stream(), as_ptr(U), as_ptr(out), float(t),
-                                    float(dt), C.byref(cfg.c()), C.byref(cs))
-        st.absorb(cs)
-        L.check(code, stats=st, **_step_error_info(cs))
-        return from_device(out, host), st
-    return _generic_step(U, host, t, dt, tableau, split, cfg, st)
+    pc = _bj_enter(split, cfg, precond)
+    try:
+        if _is_ars222(tableau):
+            out = ctx.empty(split.dim + 2, split.geometry.basis.n_nodes)
+            cs = L.StepStatsC()
+            code = ctx.lib.dg_imex_step(ctx.bind_stream(), as_ptr(U), as_ptr(out), float(t),
+                                        float(dt), C.byref(cfg.c(pc)), C.byref(cs))
+            st.absorb(cs)
+            L.check(code, stats=st, **_step_error_info(cs))
+            return from_device(out, host), st
+        return _generic_step(U, host, t, dt, tableau, split, cfg, st, pc)
+    finally:
+        if pc:
+            _bj_exit(split, precond)
 
 
 def _lincomb(ctx, coefs, xs, out):
@@ -262,7 +312,7 @@ def _lincomb(ctx, coefs, xs, out):
     L.check(ctx.lib.dg_lincomb(ctx.handle, n, len(xs), arr, ptrs, as_ptr(out)))
 
 
-def _generic_step(U, host, t, dt, tab, split, cfg, st):
+def _generic_step(U, host, t, dt, tab, split, cfg, st, pc=False):
     """Arbitrary tableau: the reference's stage loop over device operators."""
     ctx = split.ctx
     ctx.bind_stream()
@@ -285,7 +335,7 @@ def _generic_step(U, host, t, dt, tab, split, cfg, st):
             it = ctx.empty(*acc.shape[1:])
             cs = L.StepStatsC()
             code = ctx.lib.dg_solve_implicit_stage(ctx.handle, as_ptr(acc), as_ptr(U_stage),
-                                                   dt * a_ll, C.byref(cfg.c()), as_ptr(it),
+                                                   dt * a_ll, C.byref(cfg.c(pc)), as_ptr(it),
                                                    C.byref(cs))
             st.absorb(cs)
             L.check(code, stats=st, **_step_error_info(cs))
@@ -324,8 +374,14 @@ def _solve_implicit_stage(acc, guess, a_dt, split, cfg, stats, timer=None, preco
     Gt, _ = to_device(guess, ctx)
     it = ctx.empty(*At.shape[1:])
     cs = L.StepStatsC()
-    code = ctx.lib.dg_solve_implicit_stage(ctx.bind_stream(), as_ptr(At), as_ptr(Gt), float(a_dt),
-                                           C.byref(cfg.c()), as_ptr(it), C.byref(cs))
+    pc = _bj_enter(split, cfg, precond)
+    try:
+        code = ctx.lib.dg_solve_implicit_stage(ctx.bind_stream(), as_ptr(At), as_ptr(Gt),
+                                               float(a_dt), C.byref(cfg.c(pc)), as_ptr(it),
+                                               C.byref(cs))
+    finally:
+        if pc:
+            _bj_exit(split, precond)
     stats.fp_iters += []  # the caller appends fp counts, as the reference does
     stats.krylov_iters += list(cs.krylov_iters[:cs.n_krylov])
     stats.pressure_increments += list(cs.pressure_increments[:cs.n_krylov])

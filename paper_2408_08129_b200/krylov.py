@@ -16,6 +16,7 @@ one fused multi-dot per pass instead of j+1 dependent MGS dots.
 """
 
 import ctypes as C
+import warnings
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -42,7 +43,122 @@ def gmres(action, rhs, x0=None, tol_rel=1e-8, restart=30, max_iter=1000,
     native = getattr(action, "_native_gmres", None)
     if native is not None and preconditioner is None:
         return native(rhs, x0, tol_rel, restart, max_iter)
+    if (native is not None and isinstance(preconditioner, BlockJacobi)
+            and preconditioner.ctx is action.ctx and preconditioner.current()):
+        return native(rhs, x0, tol_rel, restart, max_iter, precond=True)
     return _gmres_torch(action, rhs, x0, tol_rel, restart, max_iter, preconditioner)
+
+
+# ---------------------------------------------------------------- block Jacobi
+def element_coloring(mesh):
+    """Greedy colouring of the face-adjacency graph (krylov.py:118-140), in
+    libdg (host code): conforming (left, right) and hanging (coarse, fine)
+    pairs; returns int64 colours per leaf."""
+    topo = mesh.topology
+    a = [np.asarray(b.left, dtype=np.int64) for b in topo.conforming]
+    a += [np.asarray(b.coarse, dtype=np.int64) for b in topo.hanging]
+    b = [np.asarray(x.right, dtype=np.int64) for x in topo.conforming]
+    b += [np.asarray(x.fine, dtype=np.int64) for x in topo.hanging]
+    a = np.ascontiguousarray(np.concatenate(a) if a else np.zeros(0, np.int64))
+    b = np.ascontiguousarray(np.concatenate(b) if b else np.zeros(0, np.int64))
+    n = mesh.n_leaves
+    colors = np.empty(n, dtype=np.int64)
+    nc = C.c_int()
+    lib = L.lib()
+    L.check(lib.dg_element_coloring(n, a.size, a.ctypes.data, b.ctypes.data, colors.ctypes.data,
+                                    C.byref(nc)))
+    return colors
+
+
+class BlockJacobi:
+    """The device block-Jacobi inverse of one build (dg_bj_build) on a
+    context: ``M(v)`` returns the blockwise inverse applied to v (a CUDA
+    tensor or a host array, returned in kind).  A later build on the same
+    context supersedes it (using a stale one raises UsageError)."""
+
+    def __init__(self, ctx, generation, n_singular=0):
+        self.ctx = ctx
+        self.generation = generation
+        self.n_singular = n_singular
+
+    def current(self):
+        g = C.c_longlong()
+        L.check(self.ctx.lib.dg_bj_state(self.ctx.handle, None, None, C.byref(g)))
+        return g.value == self.generation
+
+    def __call__(self, v):
+        from .errors import UsageError
+        from .dgops import from_device, to_device
+        if not self.current():
+            raise UsageError("block-Jacobi preconditioner superseded by a later build")
+        ctx = self.ctx
+        x, host = to_device(v, ctx)
+        x = x.contiguous()
+        out = ctx.torch.empty_like(x)
+        L.check(ctx.lib.dg_bj_apply(ctx.bind_stream(), as_ptr(x), as_ptr(out)))
+        return from_device(out, host)
+
+
+def _set_coloring(ctx, colors):
+    colors = np.ascontiguousarray(np.asarray(colors, dtype=np.int64))
+    if getattr(ctx, "_bj_coloring", None) is not None and np.array_equal(ctx._bj_coloring,
+                                                                        colors):
+        return
+    n = colors.size
+    L.check(ctx.lib.dg_bj_set_coloring(ctx.handle, colors.ctypes.data, n))
+    ctx._bj_coloring = colors.copy()
+
+
+def block_jacobi_preconditioner(action, n_el, n_nodes, coloring=None):
+    """Inverse of the per-element diagonal blocks of the action (krylov.py:
+    143-178), probed colour by colour.  The Helmholtz action of
+    ``imex.build_helmholtz_action`` is probed and inverted in libdg; any
+    other device callable is probed from Python and inverted with
+    torch.linalg.inv."""
+    colors = (np.asarray(coloring, dtype=np.int64) if coloring is not None
+              else np.zeros(n_el, dtype=np.int64))
+    ctx = getattr(action, "ctx", None)
+    if getattr(action, "_native_gmres", None) is not None and ctx is not None:
+        _set_coloring(ctx, colors)
+        ns, gen = C.c_int(), C.c_longlong()
+        L.check(ctx.lib.dg_bj_build(ctx.bind_stream(), action.a_dt, as_ptr(action.h),
+                                    C.byref(ns), C.byref(gen)))
+        if ns.value:
+            warnings.warn(f"block Jacobi: {ns.value} singular blocks replaced by identity")
+        return BlockJacobi(ctx, gen.value, ns.value)
+    return _block_jacobi_torch(action, n_el, n_nodes, colors)
+
+
+def _block_jacobi_torch(action, n_el, n_nodes, colors):
+    import torch
+    if not torch.cuda.is_available():
+        raise DeviceError("block Jacobi runs on the device; no CUDA device visible")
+    dev = "cuda"
+    col = torch.as_tensor(colors, device=dev)
+    blocks = torch.empty((n_el, n_nodes, n_nodes), dtype=torch.float64, device=dev)
+    probe = torch.zeros((n_el, n_nodes), dtype=torch.float64, device=dev)
+    for c in np.unique(colors):
+        sel = col == int(c)
+        for i in range(n_nodes):
+            probe.zero_()
+            probe[sel, i] = 1.0
+            y = torch.as_tensor(action(probe.reshape(-1)), dtype=torch.float64,
+                                device=dev).reshape(n_el, n_nodes)
+            blocks[sel, :, i] = y[sel]
+    inv, info = torch.linalg.inv_ex(blocks)
+    bad = info != 0
+    if bool(bad.any()):
+        inv[bad] = torch.eye(n_nodes, dtype=torch.float64, device=dev)
+        warnings.warn(f"block Jacobi: {int(bad.sum())} singular blocks replaced by identity")
+
+    def apply(v):
+        host = not isinstance(v, torch.Tensor)
+        t = torch.as_tensor(np.asarray(v, dtype=np.float64) if host else v,
+                            dtype=torch.float64, device=dev).reshape(n_el, n_nodes)
+        out = torch.einsum("eij,ej->ei", inv, t).reshape(-1)
+        return out.cpu().numpy() if host else out
+
+    return apply
 
 
 def _gmres_torch(action, rhs, x0, tol_rel, restart, max_iter, preconditioner):
@@ -132,16 +248,16 @@ def _gmres_torch(action, rhs, x0, tol_rel, restart, max_iter, preconditioner):
     return (x.cpu().numpy() if host else x), st
 
 
-def native_gmres(ctx, a_dt, h, rhs, x0, tol_rel, restart, max_iter):
-    """dg_gmres_helmholtz on device tensors; returns (x tensor, KrylovStats)."""
+def native_gmres(ctx, a_dt, h, rhs, x0, tol_rel, restart, max_iter, precond=False):
+    """dg_gmres_helmholtz(_pc) on device tensors; returns (x tensor, KrylovStats)."""
     torch = ctx.torch
     x = (x0.clone() if x0 is not None else torch.zeros_like(rhs)).contiguous()
     cst = L.KrylovStatsC()
     cap = max_iter + 8 * (max_iter // max(restart, 1) + 2)
     hist = (C.c_double * cap)()
-    L.check(ctx.lib.dg_gmres_helmholtz(ctx.bind_stream(), a_dt, as_ptr(h), as_ptr(rhs),
-                                       as_ptr(x), tol_rel, restart, max_iter, C.byref(cst),
-                                       hist, cap))
+    L.check(ctx.lib.dg_gmres_helmholtz_pc(ctx.bind_stream(), a_dt, as_ptr(h), as_ptr(rhs),
+                                          as_ptr(x), tol_rel, restart, max_iter,
+                                          1 if precond else 0, C.byref(cst), hist, cap))
     st = KrylovStats(iterations=cst.iterations, residual=cst.residual, restarts=cst.restarts,
                      converged=bool(cst.converged), breakdown=bool(cst.breakdown),
                      residual_history=list(hist[:cst.n_history]))

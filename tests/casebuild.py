@@ -80,6 +80,8 @@ def build(name):
         return _bubble("cfg1", (32, 16), None, 2, 1e-8)
     if name == "cfg2":
         return _bubble("cfg2", (64, 32), 5.0e3, 4, 1e-10)
+    if name == "bjh":  # golden bj.npz, prefix h_: once-refined bubble, hanging faces
+        return _bubble("bjh", (16, 8), 5.0e3, 2, 1e-8)
     if name == "hang2d":
         ext = (60.0e3, 16.0e3)
         m = build_uniform_mesh(ext, (15, 4))

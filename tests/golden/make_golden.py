@@ -486,9 +486,58 @@ def case_cfg2ops():
     save("cfg2", rec)
 
 
+def _bj_record(prefix, mesh, split, U, a_dt, seed):
+    """Block-Jacobi preconditioner of the Helmholtz action at U
+    (krylov.py:118-178): the greedy element colouring, the preconditioner
+    applied to a seeded vector, and one right-preconditioned GMRES solve."""
+    colors = krylov.element_coloring(mesh)
+    d = split.dim
+    e_e = U[:, 1 + d]
+    action = imex.build_helmholtz_action(split, a_dt, U)
+    M = krylov.block_jacobi_preconditioner(action, e_e.shape[0], e_e.shape[1], colors)
+    v = np.random.default_rng(seed).standard_normal(e_e.shape)
+    h, K = split.frozen_coefficients(U)
+    F, _ = split.energy_affine_map(a_dt, h, K, U[:, 1:1 + d].copy(), e_e.copy())
+    F0 = F(np.zeros_like(e_e))
+    x0 = energy_like(U, seed + 1).ravel()
+    x, st = krylov.gmres(action, F0.ravel(), x0=x0, tol_rel=1e-8, restart=30, max_iter=1000,
+                         preconditioner=M)
+    return {prefix + "colors": colors, prefix + "a_dt": np.array(a_dt), prefix + "v": v,
+            prefix + "Mv": M(v.ravel()).reshape(e_e.shape), prefix + "rhs": F0,
+            prefix + "x0": x0.reshape(e_e.shape), prefix + "x": x.reshape(e_e.shape),
+            prefix + "iters": np.array(st.iterations),
+            prefix + "history": np.array(st.residual_history)}
+
+
+def case_bj():
+    """block_jacobi preconditioning: cfg1 mesh (colouring,
+    M v, preconditioned GMRES, 4 ARS(2,2,2) steps rebuilding every 3 solves)
+    and a once-refined bubble mesh with hanging faces (colouring, M v)."""
+    mesh, geom, ops, model, U0, bcs, split = bubble_case((32, 16), None, 2)
+    dt = 0.5
+    a_dt = dt * (1.0 - 1.0 / np.sqrt(2.0))
+    rec = {"case": np.array("bj")}
+    rec.update(_bj_record("c1_", mesh, split, U0, a_dt, 31))
+    scfg = imex.ImplicitSolveConfig(preconditioner="block_jacobi", precond_refresh=3)
+    tab = imex.ars222()
+    U = U0.copy()
+    pc = imex._PrecondCache()
+    fp, kr = [], []
+    for s in range(4):
+        U, st = imex.imex_step(U, s * dt, dt, tab, split, scfg, precond=pc)
+        fp.append(st.fp_iters)
+        kr.append(st.krylov_iters)
+        print(f"  bj step {s + 1}: fp {st.fp_iters} krylov {st.krylov_iters}", flush=True)
+    rec.update({"st_U_final": U, "st_fp_iters": _ragged(fp), "st_krylov_iters": _ragged(kr),
+                "st_refresh": np.array(3), "st_n_steps": np.array(4), "st_dt": np.array(dt)})
+    mesh2, geom2, ops2, model2, U2, bcs2, split2 = bubble_case((16, 8), 5.0e3, 2)
+    rec.update(_bj_record("h_", mesh2, split2, U2, a_dt, 32))
+    save("bj", rec)
+
+
 CASES = {"cfg2ops": case_cfg2ops, "cfg1": case_cfg1, "hang2d": case_hang2d, "hang3d": case_hang3d,
          "per3d": case_per3d, "cfg3s": case_cfg3s, "part": case_part,
-         "cfg2": case_cfg2}
+         "cfg2": case_cfg2, "bj": case_bj}
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(CASES)
