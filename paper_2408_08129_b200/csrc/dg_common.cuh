@@ -47,6 +47,7 @@ struct Model {
 struct GeoConst {
   double per_root[3];  // extents[a] / root_counts[a]
   double z_top;
+  double inv_ztop;     // 1 / z_top (warp-element kernel: multiply, no division)
   int terrain;         // 0: flat, column table unused
   int col_stride;
 };

@@ -749,6 +749,7 @@ int dg_ctx_create(const dg_ctx_desc* d, dg_ctx** out) {
   c->mesh.coarse_list = c->clist.p;
   for (int a = 0; a < 3; ++a) c->gc.per_root[a] = d->per_root[a];
   c->gc.z_top = d->z_top;
+  c->gc.inv_ztop = 1.0 / d->z_top;
   c->gc.terrain = d->terrain;
   c->gc.col_stride = d->col_stride;
   c->model = Model{d->gamma, d->gravity, d->inv_mach_sq, d->kinetic_factor};

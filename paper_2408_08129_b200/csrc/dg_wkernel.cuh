@@ -145,7 +145,7 @@ __device__ __forceinline__ void point_metric_ge(const GeoConst& gc, const Tab<N>
 #pragma unroll
   for (int a = 0; a < HD; ++a) det = det * g.s[a];
   det = det * zz;
-  const double decay = 1.0 - (g.lo[D - 1] + g.s[D - 1] * T.qx[qz]) / gc.z_top;
+  const double decay = 1.0 - (g.lo[D - 1] + g.s[D - 1] * T.qx[qz]) * gc.inv_ztop;
   double zg[2];
 #pragma unroll
   for (int a = 0; a < HD; ++a) zg[a] = GE[(1 + a) * NCs + c] * g.s[a] * decay;
@@ -192,7 +192,7 @@ __device__ __forceinline__ void face_metric_ge(const GeoConst& gc, const ElemGeo
       ws = fw * top;
       return;
     }
-    const double decay = 1.0 - (g.lo[D - 1] + g.s[D - 1] * (double)side) / gc.z_top;
+    const double decay = 1.0 - (g.lo[D - 1] + g.s[D - 1] * (double)side) * gc.inv_ztop;
     double nt[D];
     if constexpr (D == 2) {
       nt[0] = -GE[NCs + qf] * g.s[0] * decay;
@@ -205,8 +205,9 @@ __device__ __forceinline__ void face_metric_ge(const GeoConst& gc, const ElemGeo
 #pragma unroll
     for (int a = 0; a < D; ++a) m2 += nt[a] * nt[a];
     const double mag = sqrt(m2);
+    const double im = sgn / mag;
 #pragma unroll
-    for (int a = 0; a < D; ++a) n[a] = sgn * (nt[a] / mag);
+    for (int a = 0; a < D; ++a) n[a] = nt[a] * im;
     ws = fw * mag;
   }
 }
@@ -307,7 +308,7 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
     const double* src = reinterpret_cast<const double*>(&P.tab);
     for (int i = threadIdx.x; i < WL::TABD; i += blockDim.x) smem[i] = src[i];
   }
-  __syncthreads();  // the only CTA barrier: tables
+  // (the tables are first read at the face phase: the barrier is placed there)
   const Tab<N>& TS = *reinterpret_cast<const Tab<N>*>(smem);
   const Tab<N>& TC = P.tab;
   const MeshDev& mesh = P.mesh;
@@ -573,8 +574,11 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
         TN[cp] = t2v;
       }
       }  // nodal input
-      // own trace: lift contraction of the lane's pencil along AX
-      {
+      // own trace: lift contraction of the lane's pencil along AX (vertical
+      // faces of div(hV): only V_AX and h meet a non-zero normal component)
+      if (OPK == OP_DIVHV && AX < D - 1 && cp != AX && cp != D) {
+        TO[cp] = 0.0;
+      } else {
         double t = 0.0;
 #pragma unroll
         for (int k = 0; k < N; ++k) {
@@ -615,6 +619,7 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
     for (int k = 0; k < KOUT; ++k) fl[f][k] = fv[k] * sg;
   };
   // each lane reads back only the face slots it issued itself
+  __syncthreads();  // the CTA barrier: the tables copied at entry are visible
   if (WL::ASYNC) cp_async_wait_all();
   if constexpr (SMP) {
     if constexpr (OPK == OP_GRAD) {
