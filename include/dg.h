@@ -195,6 +195,10 @@ int dg_lincomb(dg_ctx* ctx, long long n, int m, const double* coefs, const doubl
                double* y);
 int dg_dots(dg_ctx* ctx, long long n, int nv, const double* V, long long vstride,
             const double* w, double* out_host /* nv+1: V_i.w, w.w */);
+/* Arnoldi update + normalisation dst = (w - sum_i c_i V_i) / na (krylov.py:69-72, 81);
+   w may be used as scratch */
+int dg_gs_update(dg_ctx* ctx, long long n, int nv, const double* V, long long vstride,
+                 const double* coefs_host, double* w, double na, double* dst);
 
 /* ---- multi-GPU (one process per GPU) ---- */
 int dg_nccl_unique_id(void* out128);

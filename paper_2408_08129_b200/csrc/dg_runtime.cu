@@ -421,26 +421,40 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const doubl
         happy = na <= 1e-14 * std::max(bn, nb);
         if (!happy) CK(axpy_div(c->stream, n, j + 1, Vb, vs, c->coef_dev.p, w, na, dst));
       } else {
-        CK(axpy_multi(c->stream, n, j + 1, Vb, vs, c->coef_dev.p, w, c->partial.p, c->redout.p));
-        double na2;
-        RET(reduce_read(c, c->redout.p, 1, &na2));
+        // update, |w|^2 and the re-orthogonalisation dots V^T w in ONE pass
+        // (the dots are only used when the norm test below asks for them)
+        CK(axpy_dots(c->stream, n, j + 1, Vb, vs, c->coef_dev.p, w, c->partial.p, c->redout.p));
+        RET(reduce_read(c, c->redout.p, j + 2, hc.data()));
+        const double na2 = hc[j + 1];
         na = std::sqrt(na2);
         if (na < 0.7071067811865476 * nb) {
           // one re-orthogonalisation pass (krylov.py:73-79)
-          CK(multidot(c->stream, n, j + 1, Vb, vs, w, c->partial.p, c->redout.p));
-          RET(reduce_read(c, c->redout.p, j + 2, hc.data()));
+          double s2r = 0.0;
           for (int i = 0; i <= j; ++i) {
             Hij(i, j) += hc[i];
             coefs[i] = hc[i];
+            s2r += hc[i] * hc[i];
           }
           CK(cudaMemcpyAsync(c->coef_dev.p, coefs, (j + 1) * sizeof(double),
                              cudaMemcpyHostToDevice, c->stream));
-          CK(axpy_multi(c->stream, n, j + 1, Vb, vs, c->coef_dev.p, w, c->partial.p, c->redout.p));
-          RET(reduce_read(c, c->redout.p, 1, &na2));
-          na = std::sqrt(na2);
+          const double nr2 = na2 - s2r;  // |w - V h2|^2, Pythagorean (h2 is a small correction)
+          if (nr2 > 0.5 * na2) {
+            na = std::sqrt(nr2);
+            happy = na <= 1e-14 * std::max(bn, nb);
+            if (!happy) CK(axpy_div(c->stream, n, j + 1, Vb, vs, c->coef_dev.p, w, na, dst));
+          } else {
+            double nr2x;
+            CK(axpy_multi(c->stream, n, j + 1, Vb, vs, c->coef_dev.p, w, c->partial.p,
+                          c->redout.p));
+            RET(reduce_read(c, c->redout.p, 1, &nr2x));
+            na = std::sqrt(nr2x);
+            happy = na <= 1e-14 * std::max(bn, nb);
+            if (!happy) CK(scale(c->stream, n, na, true, w, dst));
+          }
+        } else {
+          happy = na <= 1e-14 * std::max(bn, nb);
+          if (!happy) CK(scale(c->stream, n, na, true, w, dst));
         }
-        happy = na <= 1e-14 * std::max(bn, nb);
-        if (!happy) CK(scale(c->stream, n, na, true, w, dst));
       }
       Hij(j + 1, j) = na;
       st.iterations += 1;
@@ -1019,6 +1033,18 @@ int dg_dots(dg_ctx* c, long long n, int nv, const double* V, long long vstride, 
   if (nv < 0 || nv > 32) return fail(DG_ERR_USAGE, "dg_dots: 0..32 vectors");
   CK(multidot(c->stream, n, nv, V, vstride, w, c->partial.p, c->redout.p));
   return reduce_read(c, c->redout.p, nv + 1, out_host);
+}
+
+int dg_gs_update(dg_ctx* c, long long n, int nv, const double* V, long long vstride,
+                 const double* coefs_host, double* w, double na, double* dst) {
+  if (nv < 1 || nv > 32) return fail(DG_ERR_USAGE, "dg_gs_update: 1..32 vectors");
+  if (!(na != 0.0)) return fail(DG_ERR_USAGE, "dg_gs_update: zero norm");
+  CK(cudaStreamSynchronize(c->stream));  // the pinned staging slot is free
+  std::memcpy(c->pinned + 128, coefs_host, nv * sizeof(double));
+  CK(cudaMemcpyAsync(c->coef_dev.p, c->pinned + 128, nv * sizeof(double), cudaMemcpyHostToDevice,
+                     c->stream));
+  CK(axpy_div(c->stream, n, nv, V, vstride, c->coef_dev.p, w, na, dst));
+  return DG_OK;
 }
 
 int dg_nccl_unique_id(void* out128) {

@@ -8,6 +8,8 @@
 // per-CTA partials in a fixed traversal order, a second kernel combines
 // them with a fixed warp tree.  Results are bitwise reproducible run to run.
 #include <cstdint>
+#include <cstdlib>
+
 #include "dg_vector.cuh"
 #include "dg_prof.h"
 
@@ -407,10 +409,119 @@ cudaError_t axpy_multi(cudaStream_t st, long long n, int nv, const double* V, lo
   return cudaGetLastError();
 }
 
+// dst <- (w - sum_{i<NV} c_i V_i) / na in ONE pass over all NV <= 32 basis
+// vectors (no grouped re-read / re-write of w): NV is a template parameter,
+// so all NV + 1 loads of an element are issued back to back
+template <int NV>
+__global__ void __launch_bounds__(RED_THREADS)
+k_axpy_div_all(long long n, const double* __restrict__ V, long long vstride,
+               const double* __restrict__ coefs, const double* __restrict__ w, double na,
+               double* __restrict__ dst) {
+  __shared__ double c[NV];
+  for (int i = threadIdx.x; i < NV; i += blockDim.x) c[i] = coefs[i];
+  __syncthreads();
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    double a[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) a[i] = V[i * vstride + k];
+    const double wk = w[k];
+    double t = 0.0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) t = fma(c[i], a[i], t);
+    dst[k] = (wk - t) / na;
+  }
+}
+
+template <int NV>
+cudaError_t launch_axpy_div_all(cudaStream_t st, long long n, int nv, const double* V,
+                                long long vstride, const double* coefs, const double* w,
+                                double na, double* dst) {
+  if constexpr (NV > 1) {
+    if (nv < NV) return launch_axpy_div_all<NV - 1>(st, n, nv, V, vstride, coefs, w, na, dst);
+  }
+  k_axpy_div_all<NV><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, vstride, coefs, w, na, dst);
+  return cudaGetLastError();
+}
+
+// Gram-Schmidt update fused with the re-orthogonalisation dots: in one pass
+// w <- w - sum_i c_i V_i, then partials of V_i . w (new w) and |w|^2.  The
+// second use of V_i[k] re-reads the line the first loop just brought to L1.
+template <int NV>
+__global__ void __launch_bounds__(RED_THREADS)
+k_axpy_dots(long long n, const double* __restrict__ V, long long vstride,
+            const double* __restrict__ coefs, double* __restrict__ w,
+            double* __restrict__ partials) {
+  __shared__ double c[NV];
+  for (int i = threadIdx.x; i < NV; i += blockDim.x) c[i] = coefs[i];
+  __syncthreads();
+  double acc[NV + 1];
+#pragma unroll
+  for (int i = 0; i <= NV; ++i) acc[i] = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    double a[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) a[i] = V[i * vstride + k];
+    double t = 0.0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) t = fma(c[i], a[i], t);
+    const double wn = w[k] - t;
+    w[k] = wn;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc[i] = fma(V[i * vstride + k], wn, acc[i]);
+    acc[NV] = fma(wn, wn, acc[NV]);
+  }
+  __shared__ double red[RED_THREADS / 32][NV + 1];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i <= NV; ++i) {
+    const double v = warp_sum(acc[i]);
+    if (lane == 0) red[wid][i] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= NV; i += blockDim.x) {
+    double s = 0.0;
+    for (int w2 = 0; w2 < RED_THREADS / 32; ++w2) s += red[w2][i];
+    partials[(long long)blockIdx.x * (NV + 1) + i] = s;
+  }
+}
+
+template <int NV>
+cudaError_t launch_axpy_dots(cudaStream_t st, long long n, int nv, const double* V,
+                             long long vstride, const double* coefs, double* w,
+                             double* partials) {
+  if constexpr (NV > 1) {
+    if (nv < NV) return launch_axpy_dots<NV - 1>(st, n, nv, V, vstride, coefs, w, partials);
+  }
+  k_axpy_dots<NV><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, vstride, coefs, w, partials);
+  return cudaGetLastError();
+}
+
+cudaError_t axpy_dots(cudaStream_t st, long long n, int nv, const double* V, long long vstride,
+                      const double* coefs_dev, double* w, double* partials, double* out) {
+  if (nv > 32 || nv < 1) return cudaErrorInvalidValue;
+  prof_begin(st);
+  cudaError_t e = launch_axpy_dots<32>(st, n, nv, V, vstride, coefs_dev, w, partials);
+  if (e == cudaSuccess) {
+    k_reduce_cols<<<(nv + 1 + 7) / 8, 256, 0, st>>>(partials, RED_BLOCKS, nv + 1, out);
+    e = cudaGetLastError();
+  }
+  prof_end(st, P_AXPY, 8.0 * n * (nv + 2), 2);
+  return e;
+}
+
 cudaError_t axpy_div(cudaStream_t st, long long n, int nv, const double* V, long long vstride,
                      const double* coefs_dev, double* w, double na, double* dst) {
   // w is scratch: earlier groups update it in place, the last one divides
   if (nv > 32 || nv < 1) return cudaErrorInvalidValue;
+  static const bool grouped = getenv("DG_AXPY_GROUPED") != nullptr;
+  if (!grouped) {
+    prof_begin(st);
+    cudaError_t e = launch_axpy_div_all<32>(st, n, nv, V, vstride, coefs_dev, w, na, dst);
+    prof_end(st, P_AXPY, 8.0 * n * (nv + 2), 1);
+    return e;
+  }
   prof_begin(st);
   const int ng = (nv + GS - 1) / GS;
   for (int g = 0; g < ng; ++g) {

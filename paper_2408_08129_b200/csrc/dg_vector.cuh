@@ -11,6 +11,9 @@ cudaError_t lincomb(cudaStream_t st, long long n, int m, const double* c, const 
                     double* y);
 cudaError_t multidot(cudaStream_t st, long long n, int nv, const double* V, long long vstride,
                      const double* w, double* partials, double* out);
+// w <- w - sum c_i V_i, then out[0..nv-1] = V_i . w, out[nv] = |w|^2 (one pass)
+cudaError_t axpy_dots(cudaStream_t st, long long n, int nv, const double* V, long long vstride,
+                      const double* coefs_dev, double* w, double* partials, double* out);
 cudaError_t axpy_multi(cudaStream_t st, long long n, int nv, const double* V, long long vstride,
                        const double* coefs_dev, double* w, double* partials, double* norm2_out);
 cudaError_t axpy_div(cudaStream_t st, long long n, int nv, const double* V, long long vstride,

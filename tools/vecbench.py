@@ -1,6 +1,7 @@
-"""Gram-Schmidt multi-dot bandwidth vs the number of basis vectors.
+"""Gram-Schmidt multi-dot and update+normalise bandwidth vs the number of
+basis vectors (algorithmic bytes: dots 8 n (nv+1), update 8 n (nv+2)).
 
-    python tools/vecbench.py [--n 160358400] [--stride-pad 416]
+    python tools/vecbench.py [--n 160358400] [--pad 416] [--ops dots,update]
 """
 
 import argparse
@@ -18,6 +19,7 @@ def main():
     ap.add_argument("--n", type=int, default=160358400)
     ap.add_argument("--pad", type=int, default=416)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--ops", default="dots,update")
     a = ap.parse_args()
     import torch
 
@@ -34,19 +36,32 @@ def main():
     w = torch.randn(n, dtype=torch.float64, device="cuda")
     out = (C.c_double * 40)()
     ctx.bind_stream()
-    for nv in (1, 4, 8, 12, 16, 24, 31):
-        for _ in range(2):
-            lib.dg_dots(ctx.handle, n, nv, C.c_void_p(V.data_ptr()), vs, C.c_void_p(w.data_ptr()), out)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(a.reps):
-            lib.dg_dots(ctx.handle, n, nv, C.c_void_p(V.data_ptr()), vs, C.c_void_p(w.data_ptr()), out)
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / a.reps
-        gbs = 8.0 * n * (nv + 1) / (ms * 1e-3) / 1e9
-        print(json.dumps({"nv": nv, "ms": ms, "GB_s": gbs, "pad": a.pad}), flush=True)
+    dst = torch.empty_like(w)
+    coefs = (C.c_double * 32)(*([0.01] * 32))
+    vp, wp, dp = C.c_void_p(V.data_ptr()), C.c_void_p(w.data_ptr()), C.c_void_p(dst.data_ptr())
+
+    def dots(nv):
+        lib.dg_dots(ctx.handle, n, nv, vp, vs, wp, out)
+
+    def update(nv):
+        lib.dg_gs_update(ctx.handle, n, nv, vp, vs, coefs, wp, 1.0, dp)
+
+    for op in a.ops.split(","):
+        fn, extra = (dots, 1) if op == "dots" else (update, 2)
+        for nv in (1, 4, 8, 12, 16, 24, 31):
+            for _ in range(2):
+                fn(nv)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(a.reps):
+                fn(nv)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / a.reps
+            gbs = 8.0 * n * (nv + extra) / (ms * 1e-3) / 1e9
+            print(json.dumps({"op": op, "nv": nv, "ms": ms, "GB_s": gbs, "pad": a.pad}),
+                  flush=True)
 
 
 if __name__ == "__main__":
