@@ -398,6 +398,23 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
     for (int i = c; i < WL::GEE; i += NC)
       cp_async8(GEs + WL::GEON * NC + i, colp + NQH * D + i);
   }
+  if constexpr (OPK == OP_DIVHV && !IQ) {
+    // fused Gram-Schmidt dots: pull this element's slice of every basis
+    // vector into L2 now (one bulk TMA prefetch of n^d doubles per vector,
+    // spread over the element's lanes) so the epilogue's dot loads hit L2
+    if (P.gs_part != nullptr && act) {
+      for (int i = c; i < P.gs_nv; i += NC) {
+        const double* src = P.gsV + (long long)i * P.gs_vs + e * WL::NP;
+        // 16-byte aligned span covering the slice (odd n^d: 8-byte aligned)
+        const unsigned long long a0 = reinterpret_cast<unsigned long long>(src) & ~15ULL;
+        const unsigned long long a1 =
+            (reinterpret_cast<unsigned long long>(src + WL::NP) + 15ULL) & ~15ULL;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a0),
+                     "r"((unsigned)(a1 - a0))
+                     : "memory");
+      }
+    }
+  }
   // ---- 1. nodal column, z interpolation in registers -------------------
   // in_quad (H2 of the Helmholtz pair): inputs are already Gauss values
   constexpr bool iq = iq0;
