@@ -111,12 +111,17 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def traffic(workload, kernel_class):
-    """DRAM bytes per operator call of the dominant class from the committed
-    ncu --set full capture (profiles/r1_traffic.json), or None."""
+def traffic(workload, kernel_class, algorithmic_per_launch):
+    """DRAM bytes per operator call of the dominant class: the committed
+    ncu --set full capture (profiles/r1_traffic.json) gives the measured
+    excess over the algorithmic bytes of one call (neighbour gathers that miss
+    L2, the coarse-side pass); added to this run's per-launch algorithmic
+    bytes (the fused dots make the div(hV) bytes vary with the Arnoldi step).
+    None when no capture covers the class."""
     try:
         with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
-            return float(json.load(f)[workload][kernel_class])
+            t = json.load(f)[workload][kernel_class]
+        return algorithmic_per_launch + float(t["measured_bytes"]) - float(t["algorithmic_bytes"])
     except Exception:
         return None
 
@@ -312,7 +317,7 @@ def main():
             "roofline": {"bound": "hbm", "kernel": classes[k_dom], "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "peak_kind": peak_kind,
-                         "traffic": traffic(args.workload, classes[k_dom]),
+                         "traffic": traffic(args.workload, classes[k_dom], per_launch_bytes),
                          "bytes_per_launch": per_launch_bytes,
                          "ms_per_launch": per_launch_ms,
                          "share_of_step": ms_c[k_dom] / ms_total},

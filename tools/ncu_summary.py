@@ -5,6 +5,7 @@
 """
 
 import collections
+import re
 import csv
 import io
 import subprocess
@@ -25,6 +26,8 @@ def launches(path):
         except ValueError:
             continue
         name = r[ki].split("(")[0].replace("void ", "")
+        # one row per vector-kernel family (instantiated per basis count)
+        name = re.sub(r"^(k_\w+)<\d+>$", r"\1<nv>", name)
         tot[name] += v
         cnt[name] += 1
     T = sum(tot.values())

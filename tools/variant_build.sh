@@ -11,6 +11,6 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler
   -I$ROOT/include -I$ROOT/paper_2408_08129_b200/csrc "$@" \
   -c $ROOT/paper_2408_08129_b200/csrc/dg_ops_d3.cu -o $ROOT/_variants/d3_$NAME.o
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $ROOT/_variants/libdg_$NAME.so \
-  $B/dg_ops_d2.o $ROOT/_variants/d3_$NAME.o $B/dg_vector.o $B/dg_runtime.o $B/dg_comm.o \
+  $(ls $B/*.o | grep -v dg_ops_d3.o) $ROOT/_variants/d3_$NAME.o \
   -L/usr/lib/x86_64-linux-gnu -l:libnccl.so.2 -lcudart
 echo built _variants/libdg_$NAME.so
