@@ -192,13 +192,28 @@ k_pressure_dp(long long n, const double* __restrict__ x, const double* __restric
               double gm1, double kf, double* __restrict__ p_old, double* __restrict__ partials) {
   double a = 0.0, b = 0.0;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const double pn = gm1 * (x[i] - kf * K[i]);
-    const double po = p_old[i];
-    const double df = pn - po;
-    a = fma(df, df, a);
-    b = fma(po, po, b);
-    p_old[i] = pn;
+  // four elements per trip (fixed order per thread): 12 loads in flight
+  for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
+    double xv[4], kv[4], pv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long i = i0 + u * stride;
+      const bool ok = i < n;
+      xv[u] = ok ? x[i] : 0.0;
+      kv[u] = ok ? K[i] : 0.0;
+      pv[u] = ok ? p_old[i] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long i = i0 + u * stride;
+      if (i < n) {
+        const double pn = gm1 * (xv[u] - kf * kv[u]);
+        const double df = pn - pv[u];
+        a = fma(df, df, a);
+        b = fma(pv[u], pv[u], b);
+        p_old[i] = pn;
+      }
+    }
   }
   __shared__ double red[2][RED_THREADS / 32];
   a = warp_sum(a);
@@ -329,9 +344,11 @@ void prof_end(cudaStream_t st, int cls, double bytes, int nlaunch) {
 }
 
 // ------------------------------------------------------------ host wrappers
+// streaming kernels (no reduction): enough resident threads per SM to keep
+// the loads in flight (a 592-CTA grid leaves them latency-bound)
 static int grid_for(long long n) {
   long long g = (n + RED_THREADS - 1) / RED_THREADS;
-  if (g > RED_BLOCKS) g = RED_BLOCKS;
+  if (g > 148 * 32) g = 148 * 32;
   if (g < 1) g = 1;
   return (int)g;
 }
