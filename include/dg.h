@@ -133,6 +133,9 @@ int dg_divergence_advective(dg_ctx* ctx, const double* U, double* dual);
 int dg_gradient_scalar(dg_ctx* ctx, const double* p, int homogeneous, double* dual);
 int dg_divergence_hv(dg_ctx* ctx, const double* V, long long v_estride, const double* h,
                      int homogeneous, double* dual);
+/* full Euler flux divergence dual (DGOperators.divergence_full, orodg/dgops.py:298-328);
+   flux 1 = 'rusanov' (lambda = max |u.n| + c), 2 = 'centered' */
+int dg_divergence_full(dg_ctx* ctx, const double* U, int flux, double* dual);
 /* factorised mass inverse (orodg/geometry.py:372-396); ncomp comps per element */
 int dg_apply_mass_inverse(dg_ctx* ctx, const double* dual, int ncomp, double* out);
 
@@ -189,6 +192,13 @@ int dg_imex_step(dg_ctx* ctx, const double* U, double* U_out, double t, double d
 
 /* ---- reductions / vector ops ---- */
 int dg_integrate_conserved(dg_ctx* ctx, const double* U, double* out_host /* d+2 */);
+/* quadrature-weighted inner product of two (n_el, ncomp, n^d) fields
+   (DGOperators.global_inner_product, orodg/dgops.py:491-503) */
+int dg_global_inner_product(dg_ctx* ctx, const double* a, const double* b, int ncomp,
+                            double* out_host);
+/* Courant ingredients over the volume quadrature points (courant_numbers,
+   orodg/physics.py:255-272): max sound speed, max |u|, min rho, min p */
+int dg_courant_ingredients(dg_ctx* ctx, const double* U, double* out4);
 int dg_check_positivity(dg_ctx* ctx, const double* U, double* min_rho, long long* at_rho,
                         double* min_p, long long* at_p);
 int dg_lincomb(dg_ctx* ctx, long long n, int m, const double* coefs, const double* const* xs,

@@ -85,6 +85,9 @@ _SIGS = {
     "dg_check_positivity": ([P, P, C.POINTER(D), C.POINTER(LL), C.POINTER(D), C.POINTER(LL)], I),
     "dg_lincomb": ([P, LL, I, P, P, P], I),
     "dg_dots": ([P, LL, I, P, LL, P, P], I),
+    "dg_divergence_full": ([P, P, I, P], I),
+    "dg_global_inner_product": ([P, P, P, I, P], I),
+    "dg_courant_ingredients": ([P, P, P], I),
     "dg_gs_update": ([P, LL, I, P, LL, P, P, D, P], I),
     "dg_nccl_unique_id": ([P], I),
     "dg_ctx_set_comm": ([P, P, I, I, P, P, P], I),

@@ -15,6 +15,8 @@ struct AuxParams {
   int n_el;
   int ncomp;
   CView in;          // dual (mass inverse) or state (integrate)
+  CView in2;         // inner product: second field
+  Model model;       // Courant report
   MView out;         // nodal result (mass inverse)
   double* partial;   // integrate: (grid, ncomp)
   Tab<N> tab;
@@ -182,6 +184,145 @@ interp_kernel(const __grid_constant__ AuxParams<N> P) {
   }
 }
 
+// nodes -> Gauss points of KC comps staged in X (Y scratch); returns the
+// buffer holding the result (d ping-pong passes, CTA-synchronised)
+template <int D, int N, int KC>
+__device__ __forceinline__ const double* interp_inplace(const Tab<N>& T, double* X, double* Y,
+                                                        int q) {
+  constexpr int NP = ipow(N, D);
+  double* s = X;
+  double* d = Y;
+  for (int a = D - 1; a >= 0; --a) {
+    pass1d<D, N, KC, false>(&T.B[0][0], s, d, q, a, NP);
+    __syncthreads();
+    double* t = s;
+    s = d;
+    d = t;
+  }
+  return s;
+}
+
+// per-CTA partial of sum_{k,q} w det (B a)_k (B b)_k  (dgops.py:491-503)
+template <int D, int N>
+__global__ void __launch_bounds__(AuxLayout<D, N>::THREADS)
+inner_kernel(const __grid_constant__ AuxParams<N> P) {
+  using L = AuxLayout<D, N>;
+  constexpr int NP = L::NP;
+  extern __shared__ double smem[];
+  {
+    const double* src = reinterpret_cast<const double*>(&P.tab);
+    for (int i = threadIdx.x; i < L::TABD; i += blockDim.x) smem[i] = src[i];
+    __syncthreads();
+  }
+  const Tab<N>& T = *reinterpret_cast<const Tab<N>*>(smem);
+  double* red = smem + L::TABD;
+  const int el = threadIdx.x / NP, q = threadIdx.x - el * NP;
+  const long long e = (long long)blockIdx.x * L::EPB + el;
+  const bool valid = el < L::EPB && e < P.n_el;
+  const long long es = valid ? e : 0;
+  double* X = smem + L::TABD + 64 + el * 2 * L::KMAX * NP;
+  double* Y = X + L::KMAX * NP;
+  const double wd = wdet_at<D, N>(P.elem, P.col, P.gc, es, q, T);
+  double acc = 0.0;
+  for (int c0 = 0; c0 < P.ncomp; c0 += L::KMAX) {
+    const int kc = min(L::KMAX, P.ncomp - c0);
+    double va[L::KMAX];
+    // field a -> Gauss points, kept in registers
+    for (int c = 0; c < L::KMAX; ++c) X[c * NP + q] = c < kc ? P.in(es, c0 + c, q) : 0.0;
+    __syncthreads();
+    const double* ra = interp_inplace<D, N, L::KMAX>(T, X, Y, q);
+    for (int c = 0; c < L::KMAX; ++c) va[c] = ra[c * NP + q];
+    __syncthreads();
+    // field b -> Gauss points, products
+    for (int c = 0; c < L::KMAX; ++c) X[c * NP + q] = c < kc ? P.in2(es, c0 + c, q) : 0.0;
+    __syncthreads();
+    const double* rb = interp_inplace<D, N, L::KMAX>(T, X, Y, q);
+    for (int c = 0; c < kc; ++c) acc += va[c] * rb[c * NP + q] * wd;
+    __syncthreads();
+  }
+  double v = valid ? acc : 0.0;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    P.partial[blockIdx.x] = s;
+  }
+}
+
+// per-CTA (max sound speed, max |u|, min rho, min p) over the volume
+// quadrature points (physics.py:255-272)
+template <int D, int N>
+__global__ void __launch_bounds__(AuxLayout<D, N>::THREADS)
+courant_kernel(const __grid_constant__ AuxParams<N> P) {
+  using L = AuxLayout<D, N>;
+  constexpr int NP = L::NP;
+  static_assert(D + 2 <= L::KMAX, "state components");
+  extern __shared__ double smem[];
+  {
+    const double* src = reinterpret_cast<const double*>(&P.tab);
+    for (int i = threadIdx.x; i < L::TABD; i += blockDim.x) smem[i] = src[i];
+    __syncthreads();
+  }
+  const Tab<N>& T = *reinterpret_cast<const Tab<N>*>(smem);
+  double* red = smem + L::TABD;
+  const int el = threadIdx.x / NP, q = threadIdx.x - el * NP;
+  const long long e = (long long)blockIdx.x * L::EPB + el;
+  const bool valid = el < L::EPB && e < P.n_el;
+  const long long es = valid ? e : 0;
+  double* X = smem + L::TABD + 64 + el * 2 * L::KMAX * NP;
+  double* Y = X + L::KMAX * NP;
+  for (int c = 0; c < L::KMAX; ++c) X[c * NP + q] = c < D + 2 ? P.in(es, c, q) : 0.0;
+  __syncthreads();
+  double* s = X;
+  double* d = Y;
+  for (int a = D - 1; a >= 0; --a) {
+    pass1d<D, N, L::KMAX, false>(&T.B[0][0], s, d, q, a, NP);
+    __syncthreads();
+    double* t = s; s = d; d = t;
+  }
+  double cm = -INFINITY, um = -INFINITY, rmin = INFINITY, pmin = INFINITY;
+  if (valid) {
+    const double rho = s[q];
+    double u2 = 0.0;
+    for (int a = 0; a < D; ++a) {
+      const double ua = s[(1 + a) * NP + q] / rho;
+      u2 += ua * ua;
+    }
+    const double k = 0.5 * u2;
+    const Model& md = P.model;
+    const double p = (md.gamma - 1.0) * (s[(D + 1) * NP + q] - md.kinetic_factor * rho * k);
+    cm = sqrt(md.gamma * md.inv_mach_sq * p / rho);
+    um = sqrt(u2);
+    rmin = rho;
+    pmin = p;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+    um = fmax(um, __shfl_xor_sync(0xffffffffu, um, o));
+    rmin = fmin(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
+    pmin = fmin(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[(threadIdx.x >> 5) * 4 + 0] = cm;
+    red[(threadIdx.x >> 5) * 4 + 1] = um;
+    red[(threadIdx.x >> 5) * 4 + 2] = rmin;
+    red[(threadIdx.x >> 5) * 4 + 3] = pmin;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r[4] = {-INFINITY, -INFINITY, INFINITY, INFINITY};
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      r[0] = fmax(r[0], red[w * 4 + 0]);
+      r[1] = fmax(r[1], red[w * 4 + 1]);
+      r[2] = fmin(r[2], red[w * 4 + 2]);
+      r[3] = fmin(r[3], red[w * 4 + 3]);
+    }
+    for (int i = 0; i < 4; ++i) P.partial[(long long)blockIdx.x * 4 + i] = r[i];
+  }
+}
+
 template <int D, int N>
 cudaError_t launch_aux(int which, const AuxParams<N>& P, cudaStream_t st, int* grid_out) {
   using L = AuxLayout<D, N>;
@@ -194,9 +335,15 @@ cudaError_t launch_aux(int which, const AuxParams<N>& P, cudaStream_t st, int* g
   } else if (which == 1) {
     cudaFuncSetAttribute(integrate_kernel<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
     integrate_kernel<D, N><<<grid, L::THREADS, L::SMEM, st>>>(P);
-  } else {
+  } else if (which == 2) {
     cudaFuncSetAttribute(interp_kernel<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
     interp_kernel<D, N><<<grid, L::THREADS, L::SMEM, st>>>(P);
+  } else if (which == 3) {
+    cudaFuncSetAttribute(inner_kernel<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
+    inner_kernel<D, N><<<grid, L::THREADS, L::SMEM, st>>>(P);
+  } else {
+    cudaFuncSetAttribute(courant_kernel<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
+    courant_kernel<D, N><<<grid, L::THREADS, L::SMEM, st>>>(P);
   }
   return cudaGetLastError();
 }

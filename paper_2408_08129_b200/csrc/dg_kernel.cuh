@@ -221,10 +221,68 @@ __device__ __forceinline__ void face_metric_ax(const GeoConst& gc, const double*
 }
 
 // -------------------------------------------------------------- physics
+// full Euler flux tensor of one state, F[v][a] (physics.py:149-187: the
+// primitive variables and inviscid_flux, same operation order)
+template <int D>
+__device__ __forceinline__ void full_flux(const double* U, const Model& md, double F[][D],
+                                          double* un_speed = nullptr, const double* n = nullptr) {
+  const double rho = U[0];
+  double u[D];
+  double k = 0.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    u[a] = U[1 + a] / rho;
+    k += u[a] * u[a];
+  }
+  k = 0.5 * k;
+  const double gm1 = md.gamma - 1.0;
+  const double p = gm1 * (U[D + 1] - md.kinetic_factor * rho * k);
+  const double e = p / (gm1 * rho);
+  double ru[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) ru[a] = rho * u[a];
+#pragma unroll
+  for (int a = 0; a < D; ++a) F[0][a] = ru[a];
+#pragma unroll
+  for (int b = 0; b < D; ++b) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) F[1 + b][a] = ru[b] * u[a];
+    F[1 + b][b] += md.inv_mach_sq * p;
+  }
+  const double enth = rho * e + md.kinetic_factor * rho * k + p;
+#pragma unroll
+  for (int a = 0; a < D; ++a) F[D + 1][a] = enth * u[a];
+  if (un_speed) {
+    // |u . n| + c, c = sqrt(gamma / M^2 p / rho) (physics.py:127-129)
+    double un = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) un += u[a] * n[a];
+    *un_speed = fabs(un) + sqrt(md.gamma * md.inv_mach_sq * p / rho);
+  }
+}
+
 template <int D, int OPK, int KIN, int KOUT>
 __device__ __forceinline__ void num_flux(const double* TL, const double* TR, const double* n,
-                                         double kf, double* fl) {
+                                         double kf, double* fl, const Model* md = nullptr,
+                                         int full = 0) {
   if constexpr (OPK == OP_ADV) {
+    if (full) {
+      // divergence_full (dgops.py:298-328): centred full flux, Rusanov with
+      // lambda = max(|u.n| + c) when full == 1
+      double FL[D + 2][D], FR[D + 2][D], sL, sR;
+      full_flux<D>(TL, *md, FL, &sL, n);
+      full_flux<D>(TR, *md, FR, &sR, n);
+      const double lam = fmax(sL, sR);
+#pragma unroll
+      for (int c = 0; c < KOUT; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) s += (FL[c][a] + FR[c][a]) * n[a];
+        fl[c] = 0.5 * s;
+        if (full == 1) fl[c] -= 0.5 * lam * (TR[c] - TL[c]);
+      }
+      return;
+    }
     // Rusanov with the flow speed only (orodg/dgops.py:256-283)
     double mnL = 0.0, mnR = 0.0;
 #pragma unroll
@@ -445,7 +503,7 @@ __device__ __forceinline__ void face_flux_axis(const KParams<N>& P, const Tab<N>
       TRv[c] = minus ? TN[c] : TO[c];
     }
     double fl[KOUT];
-    num_flux<D, OPK, KIN, KOUT>(TLv, TRv, n, P.model.kinetic_factor, fl);
+    num_flux<D, OPK, KIN, KOUT>(TLv, TRv, n, P.model.kinetic_factor, fl, &P.model, P.full);
     const double sg = minus ? ws : -ws;
 #pragma unroll
     for (int k = 0; k < KOUT; ++k) Lf[k * NQF + qf] = fl[k] * sg;
@@ -530,6 +588,16 @@ elem_kernel(const __grid_constant__ KParams<N> P) {
   const double wq = point_weight<D, N>(TC, q);
   double F[D][KOUT];
   if constexpr (OPK == OP_ADV) {
+    if (P.full) {
+      double Uq[D + 2], Ff[D + 2][D];
+#pragma unroll
+      for (int c = 0; c < D + 2; ++c) Uq[c] = Q[c * NP + q];
+      full_flux<D>(Uq, P.model, Ff);
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int c = 0; c < D + 2; ++c) F[a][c] = Ff[c][a];
+    } else {
     const double rho = Q[q];
     double u[D];
     double k = 0.0;
@@ -546,6 +614,7 @@ elem_kernel(const __grid_constant__ KParams<N> P) {
 #pragma unroll
       for (int b = 0; b < D; ++b) F[a][1 + b] = Q[(1 + b) * NP + q] * u[a];
       F[a][D + 1] = kf * rho * k * u[a];
+    }
     }
   } else if constexpr (OPK == OP_DIVHV) {
     const double h = Q[D * NP + q];
@@ -844,7 +913,7 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
       TRv[c] = minus ? TN[c] : TO[c];
     }
     double fl[KOUT];
-    num_flux<D, OPK, KIN, KOUT>(TLv, TRv, n, P.model.kinetic_factor, fl);
+    num_flux<D, OPK, KIN, KOUT>(TLv, TRv, n, P.model.kinetic_factor, fl, &P.model, P.full);
     const double sg = minus ? ws : -ws;
 #pragma unroll
     for (int k = 0; k < KOUT; ++k) FW[((f * S + sub) * KOUT + k) * NQF + qf] = fl[k] * sg;

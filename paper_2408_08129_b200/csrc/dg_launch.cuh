@@ -22,6 +22,7 @@ struct OpArgs {
   int has_K, has_base, homogeneous, mode;
   int dbg;  // phase-skip flags for profiling experiments only (0 in production)
   int in_quad, out_quad;
+  int full;  // ADV: divergence_full flux (see KParams)
   double* mass_partial;
   const double* gsV;  // fused Gram-Schmidt dots (see KParams)
   long long gs_vs;
@@ -62,6 +63,7 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
   P.in_quad = a.in_quad;
   P.out_quad = a.out_quad;
   P.mass_partial = a.mass_partial;
+  P.full = a.full;
   P.gsV = a.gsV;
   P.gs_vs = a.gs_vs;
   P.gs_nv = a.gs_nv;
@@ -178,6 +180,8 @@ struct AuxArgs {
   int n_el;
   int ncomp;
   CView in;
+  CView in2;    // inner product: second field
+  Model model;  // Courant report
   MView out;
   double* partial;
   const double* tabs;

@@ -53,6 +53,7 @@ struct KParams {
   // points (out_quad), H2 reads V and h there (in_quad) -- B^-1 then B is
   // the identity, so the Helmholtz pair skips both transforms
   int in_quad, out_quad;
+  int full;              // ADV: 0 split advective flux, 1 full Euler Rusanov, 2 full centred
   double* mass_partial;  // ADV: per-CTA sum of the density dual (or null)
   // fused Gram-Schmidt dots of the result y (div(hV) MINV only, GMRES):
   // row (gs_row0 + CTA) of gs_part gets (V_0.y, .., V_{nv-1}.y, y.y) partials

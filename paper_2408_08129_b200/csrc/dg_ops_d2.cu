@@ -40,6 +40,8 @@ static cudaError_t aux_n(int which, const AuxArgs& a, cudaStream_t st, int* grid
   P.n_el = a.n_el;
   P.ncomp = a.ncomp;
   P.in = a.in;
+  P.in2 = a.in2;
+  P.model = a.model;
   P.out = a.out;
   P.partial = a.partial;
   std::memcpy(&P.tab, a.tabs, sizeof(Tab<N>));

@@ -169,8 +169,10 @@ CView cv(const double* p, long long es, long long cs) { return CView{p, es, cs};
 MView mv(double* p, long long es, long long cs) { return MView{p, es, cs}; }
 
 // ---------------------------------------------------------------- operators
-int op_advective(dg_ctx* c, const double* U, double* out, int mode, double* mass_rate_host) {
+int op_advective(dg_ctx* c, const double* U, double* out, int mode, double* mass_rate_host,
+                 int full = 0) {
   OpArgs a = base_args(c);
+  a.full = full;
   a.in = cv(U, (long long)c->V * c->NP, c->NP);
   a.out = mv(out, (long long)c->V * c->NP, c->NP);
   a.mode = mode;
@@ -812,6 +814,12 @@ int dg_divergence_advective(dg_ctx* c, const double* U, double* dual) {
   return op_advective(c, U, dual, OUT_DUAL, nullptr);
 }
 
+int dg_divergence_full(dg_ctx* c, const double* U, int flux, double* dual) {
+  if (flux != 1 && flux != 2) return fail(DG_ERR_CONFIG, "flux must be 1 (rusanov) or 2 (centered)");
+  RET(halo(c, const_cast<double*>(U), c->V));
+  return op_advective(c, U, dual, OUT_DUAL, nullptr, flux);
+}
+
 int dg_explicit_residual(dg_ctx* c, const double* U, double* R, double* mass_rate) {
   RET(halo(c, const_cast<double*>(U), c->V));
   return op_advective(c, U, R, OUT_MINV, mass_rate);
@@ -1007,6 +1015,68 @@ int dg_integrate_conserved(dg_ctx* c, const double* U, double* out_host) {
   }
   CK(reduce_cols(c->stream, c->partial.p, grid, c->V, c->redout.p));
   return reduce_read(c, c->redout.p, c->V, out_host);
+}
+
+int dg_global_inner_product(dg_ctx* c, const double* a, const double* b, int ncomp,
+                            double* out_host) {
+  AuxArgs x;
+  std::memset(&x, 0, sizeof x);
+  x.elem = c->elem.p;
+  x.col = c->col.p;
+  x.gc = c->gc;
+  x.n_el = c->n_el;
+  x.ncomp = ncomp;
+  x.in = cv(a, (long long)ncomp * c->NP, c->NP);
+  x.in2 = cv(b, (long long)ncomp * c->NP, c->NP);
+  x.partial = c->partial.p;
+  x.tabs = c->tabs.data();
+  int grid = 0;
+  cudaError_t e = c->dim == 2 ? launch_aux_d2(c->N, 3, x, c->stream, &grid)
+                              : launch_aux_d3(c->N, 3, x, c->stream, &grid);
+  CK(e);
+  if (grid == 0) CK(cudaMemsetAsync(c->redout.p, 0, sizeof(double), c->stream));
+  else CK(reduce_rows(c->stream, c->partial.p, grid, 1, c->partial.p + (size_t)grid, c->redout.p));
+  return reduce_read(c, c->redout.p, 1, out_host);  // (summed over ranks)
+}
+
+int dg_courant_ingredients(dg_ctx* c, const double* U, double* out4) {
+  AuxArgs x;
+  std::memset(&x, 0, sizeof x);
+  x.elem = c->elem.p;
+  x.col = c->col.p;
+  x.gc = c->gc;
+  x.n_el = c->n_el;
+  x.ncomp = c->V;
+  x.in = cv(U, (long long)c->V * c->NP, c->NP);
+  x.model = c->model;
+  x.partial = c->partial.p;
+  x.tabs = c->tabs.data();
+  int grid = 0;
+  cudaError_t e = c->dim == 2 ? launch_aux_d2(c->N, 4, x, c->stream, &grid)
+                              : launch_aux_d3(c->N, 4, x, c->stream, &grid);
+  CK(e);
+  std::vector<double> part((size_t)grid * 4);
+  CK(cudaStreamSynchronize(c->stream));
+  if (grid) CK(cudaMemcpy(part.data(), c->partial.p, part.size() * sizeof(double),
+                          cudaMemcpyDeviceToHost));
+  double r[4] = {-INFINITY, -INFINITY, INFINITY, INFINITY};
+  for (int b = 0; b < grid; ++b) {
+    r[0] = std::max(r[0], part[b * 4 + 0]);
+    r[1] = std::max(r[1], part[b * 4 + 1]);
+    r[2] = std::min(r[2], part[b * 4 + 2]);
+    r[3] = std::min(r[3], part[b * 4 + 3]);
+  }
+  if (c->comm.active()) {
+    // max of (c, |u|, -rho_min, -p_min) over ranks
+    double m[4] = {r[0], r[1], -r[2], -r[3]};
+    std::memcpy(c->pinned, m, sizeof m);
+    CK(cudaMemcpyAsync(c->redout.p, c->pinned, sizeof m, cudaMemcpyHostToDevice, c->stream));
+    if (!c->comm.allreduce_max(c->redout.p, 4, c->stream)) return fail(DG_ERR_COMM, c->comm.error());
+    RET(sync_read(c, c->redout.p, 4, m));
+    r[0] = m[0]; r[1] = m[1]; r[2] = -m[2]; r[3] = -m[3];
+  }
+  for (int i = 0; i < 4; ++i) out4[i] = r[i];
+  return DG_OK;
 }
 
 int dg_check_positivity(dg_ctx* c, const double* U, double* min_rho, long long* at_rho,

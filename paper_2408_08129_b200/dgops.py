@@ -83,6 +83,29 @@ class DGOperators:
         L.check(ctx.lib.dg_divergence_advective(ctx.bind_stream(), as_ptr(U), as_ptr(out)))
         return from_device(out, host)
 
+    def divergence_full(self, data, model=DIMENSIONAL, bcs=None, flux="rusanov", pool=None):
+        """Dual of the full Euler flux divergence (dgops.py:298-328); flux
+        'rusanov' (local max |u.n| + c) or 'centered'."""
+        codes = {"rusanov": 1, "centered": 2}
+        if flux not in codes:
+            from .errors import ConfigurationError
+            raise ConfigurationError(f"unknown flux {flux!r}")
+        ctx = self.context(model, bcs)
+        U, host = to_device(data, ctx)
+        self._shape_check(U, self.dim + 2)
+        out = ctx.empty(self.dim + 2, self.basis.n_nodes)
+        L.check(ctx.lib.dg_divergence_full(ctx.bind_stream(), as_ptr(U), codes[flux],
+                                           as_ptr(out)))
+        return from_device(out, host)
+
+    def apply_divergence(self, field, model=DIMENSIONAL, bcs=None, flux="rusanov", pool=None,
+                         mass_inverse=True):
+        """Divergence residual of the full flux for a StateField, optionally
+        mass-inverted to nodal (dgops.py:483-488)."""
+        self._check_field(field)
+        dual = self.divergence_full(field.data, model, bcs, flux, pool)
+        return self.apply_mass_inverse(dual) if mass_inverse else dual
+
     def gradient_scalar(self, p, model=DIMENSIONAL, bcs=None, pool=None):
         """Dual of the weak gradient, centred interface value (dgops.py:332-366)."""
         ctx = self.context(model, bcs)
@@ -126,6 +149,23 @@ class DGOperators:
         return from_device(out, host)
 
     # -------------------------------------------------------- reductions
+    def global_inner_product(self, a, b):
+        """Deterministic quadrature-weighted inner product (dgops.py:491-503)."""
+        if isinstance(a, StateField):
+            self._check_field(a)
+            a.check_compatible(b)
+            a, b = a.data, b.data
+        if tuple(a.shape) != tuple(b.shape):
+            raise UsageError(f"shape mismatch {tuple(a.shape)} vs {tuple(b.shape)}")
+        ctx = self.context()
+        at, _ = to_device(a, ctx)
+        bt, _ = to_device(b, ctx)
+        k = at.shape[1] if at.dim() == 3 else 1
+        out = C.c_double()
+        L.check(ctx.lib.dg_global_inner_product(ctx.bind_stream(), as_ptr(at), as_ptr(bt), k,
+                                                C.byref(out)))
+        return float(out.value)
+
     def integrate_conserved(self, field_or_data):
         """Per-variable domain integrals (dgops.py:505-511)."""
         ctx = self.context()

@@ -115,3 +115,50 @@ def gravity_source(W, out=None):
     S[d] = -m.gravity * W.rho
     S[d + 1] = -m.kinetic_factor * m.gravity * W.rho * W.u[d - 1]
     return S
+
+
+@dataclass(frozen=True)
+class CourantReport:
+    acoustic: float
+    advective: float
+    dt: float
+    degree: int
+    min_diameter: float
+    dim: int
+    max_sound_speed: float
+    max_speed: float
+
+    def __str__(self):
+        return (f"C={self.acoustic:.4g} C_u={self.advective:.4g} "
+                f"(dt={self.dt}, r={self.degree}, Hmin={self.min_diameter:.6g}, "
+                f"d={self.dim}, c_max={self.max_sound_speed:.6g}, "
+                f"|u|_max={self.max_speed:.6g})")
+
+
+def courant_numbers(field_data, geometry, dt, model=DIMENSIONAL):
+    """Acoustic and advective Courant numbers C = r c dt / (H sqrt(d))
+    (physics.py:255-272): the maxima over all volume quadrature points are
+    reduced on the device (libdg dg_courant_ingredients)."""
+    import ctypes as C
+
+    from . import _lib as L
+    from .dgops import to_device
+    from .device import DeviceContext, as_ptr
+    cache = geometry.__dict__.setdefault("_b200_courant_ctx", {})
+    ctx = cache.get(model)
+    if ctx is None:
+        ctx = cache[model] = DeviceContext(geometry, model)
+    U, _ = to_device(field_data, ctx)
+    out = (C.c_double * 4)()
+    L.check(ctx.lib.dg_courant_ingredients(ctx.bind_stream(), as_ptr(U), out))
+    c_max, u_max, rho_min, p_min = out[:]
+    if not (rho_min > 0.0):
+        raise PositivityError(f"non-positive density ({rho_min:.6e}) at a quadrature point")
+    if not (p_min > 0.0):
+        raise PositivityError(f"non-positive pressure ({p_min:.6e}) at a quadrature point")
+    h_min = geometry.min_diameter
+    d = geometry.mesh.dim
+    fac = geometry.basis.degree * dt / (h_min * np.sqrt(d))
+    return CourantReport(acoustic=fac * c_max, advective=fac * u_max, dt=dt,
+                         degree=geometry.basis.degree, min_diameter=h_min, dim=d,
+                         max_sound_speed=c_max, max_speed=u_max)

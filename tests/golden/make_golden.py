@@ -535,9 +535,57 @@ def case_bj():
     save("bj", rec)
 
 
+def case_full():
+    """DGOperators.divergence_full / apply_divergence (both fluxes),
+    global_inner_product and physics.courant_numbers (dgops.py:298-328,
+    483-503; physics.py:255-272) on the cfg1 bubble and the hang2d / hang3d
+    terrain + hanging + far-field meshes (inputs stored with the outputs)."""
+    from orodg.field import StateField
+    from orodg.physics import courant_numbers
+    rec = {"case": np.array("full")}
+    mesh, geom, ops, model, U, bcs, split = bubble_case((32, 16), None, 2)
+    builds = [("cfg1", geom, ops, model, U, bcs, U * (1.0 + 1e-3 * np.sin(U)))]
+    ext = (60.0e3, 16.0e3)
+    m = refine_region(build_uniform_mesh(ext, (15, 4)),
+                      lambda lf: abs(lf.center[0] - 30.0e3) < 6.0e3 and lf.center[1] < 6.0e3,
+                      times=2)
+    geom, ops, model, bg, U, bcs, split, sigma = _terrain_case(
+        m, 4, hill2d, cases.HillCaseConfig(domain=ext), cases.SpongeConfig(), (0,), 21, ext)
+    builds.append(("hang2d", geom, ops, model, U, bcs, bg))
+    ext = (20.0e3, 20.0e3, 10.0e3)
+    m = refine_region(build_uniform_mesh(ext, (4, 4, 2)),
+                      lambda lf: bool(np.all(np.abs(lf.center[:2] - 10.0e3) < 5.0e3)
+                                      and lf.center[2] < 5.0e3), times=1)
+    geom, ops, model, bg, U, bcs, split, sigma = _terrain_case(
+        m, 3, hill3d, cases.HillCaseConfig(domain=ext),
+        cases.SpongeConfig(top_depth=4.0e3, lateral_width=5.0e3), (0, 1), 31, ext)
+    builds.append(("hang3d", geom, ops, model, U, bcs, bg))
+    for name, geom, ops, model, U, bcs, U2 in builds:
+        p = name + "_"
+        rec[p + "U"] = U
+        rec[p + "U2"] = U2
+        # the reference's own 1-ulp input sensitivity (see noise_record)
+        rng = np.random.default_rng(4321)
+        Up = U * (1.0 + 2.0 ** -52 * rng.choice([-1.0, 1.0], size=U.shape))
+        for flux in ("rusanov", "centered"):
+            rec[p + "full_" + flux] = ops.divergence_full(U, model, bcs, flux)
+            rec["noise_" + p + "full_" + flux] = _per_var_noise(
+                ops.divergence_full(Up, model, bcs, flux), rec[p + "full_" + flux])
+        field = StateField(U, geom.mesh.fingerprint, geom.basis.degree)
+        rec[p + "apply_div"] = ops.apply_divergence(field, model, bcs, "rusanov")
+        rec["noise_" + p + "apply_div"] = _per_var_noise(
+            ops.apply_divergence(StateField(Up, geom.mesh.fingerprint, geom.basis.degree),
+                                 model, bcs, "rusanov"), rec[p + "apply_div"])
+        rec[p + "inner"] = np.array(ops.global_inner_product(U, U2))
+        cr = courant_numbers(U, geom, 0.5, model)
+        rec[p + "courant"] = np.array([cr.acoustic, cr.advective, cr.max_sound_speed,
+                                       cr.max_speed, cr.min_diameter])
+    save("full", rec)
+
+
 CASES = {"cfg2ops": case_cfg2ops, "cfg1": case_cfg1, "hang2d": case_hang2d, "hang3d": case_hang3d,
          "per3d": case_per3d, "cfg3s": case_cfg3s, "part": case_part,
-         "cfg2": case_cfg2, "bj": case_bj}
+         "cfg2": case_cfg2, "bj": case_bj, "full": case_full}
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(CASES)
