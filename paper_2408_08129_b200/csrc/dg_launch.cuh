@@ -29,6 +29,7 @@ struct OpArgs {
   int gs_nv;
   double* gs_part;
   const double* tabs;  // host pointer, Tab<N> layout
+  const double* tabs_dev;  // the same tables in device memory
 };
 
 struct LaunchInfo {
@@ -69,6 +70,7 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
   P.gs_nv = a.gs_nv;
   P.gs_part = a.gs_part;
   P.gs_row0 = 0;
+  P.tab_g = a.tabs_dev;
   std::memcpy(&P.tab, a.tabs, sizeof(Tab<N>));
   using WL = WLayout<D, N, OPK>;
   if constexpr (WL::OK) {
@@ -106,12 +108,12 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       if (a.mesh.n_coarse > 0) {
-        P.gs_row0 = wgrid;  // coarse elements' dot partials follow the CTA rows
+        P.gs_row0 = wgrid * WL::WPB;  // coarse elements' dot partials follow the warp rows
         coarse_kernel<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
             P, a.mesh.coarse_list, a.mesh.n_coarse, nullptr);
         e = cudaGetLastError();
       }
-      if (info) info->grid = wgrid + a.mesh.n_coarse;  // partial rows written
+      if (info) info->grid = wgrid * WL::WPB + a.mesh.n_coarse;  // dot partial rows written
       return e;
     }
   }

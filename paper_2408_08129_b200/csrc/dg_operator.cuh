@@ -61,6 +61,7 @@ struct KParams {
   long long gs_vs;
   int gs_nv, gs_row0;
   double* gs_part;
+  const double* tab_g;  // the Tab<N> tables in global memory (coalesced smem staging)
   Tab<N> tab;
 };
 

@@ -80,6 +80,7 @@ struct dg_ctx {
   GeoConst gc{};
   Model model{};
   std::vector<double> tabs;
+  DevBuf<double> tabs_dev;  // device copy of tabs (warp-element kernel staging)
   DevBuf<int> elem, nbr, hang, clist;
   DevBuf<uint8_t> kind;
   DevBuf<double> col, ffU, ffp, ffh, sigma, bg;
@@ -134,6 +135,7 @@ OpArgs base_args(dg_ctx* c) {
   a.gc = c->gc;
   a.model = c->model;
   a.tabs = c->tabs.data();
+  a.tabs_dev = c->tabs_dev.p;
   a.alpha = 1.0;
   a.coef = 1.0;
   static const int dbg = getenv("DG_DEBUG_SKIP") ? atoi(getenv("DG_DEBUG_SKIP")) : 0;
@@ -345,9 +347,9 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const doubl
   double* Vb = c->basis.p;
   const bool fuse = gs_fusable(c);
   if (fuse) {
-    // one row of <= m + 1 dot partials per element-kernel CTA (>= 4 elements
+    // one row of <= m + 1 dot partials per element-kernel warp (>= 1 element
     // each) and per coarse element
-    const long long rows = ((long long)c->n_el + 3) / 4 + c->mesh.n_coarse + 1;
+    const long long rows = (long long)c->n_el + 4 + c->mesh.n_coarse + 1;
     CK(c->gs_part.alloc((size_t)rows * 32));
   }
   double* coefs = c->pinned + 128;  // pinned staging for the coefficient uploads
@@ -711,6 +713,8 @@ int dg_ctx_create(const dg_ctx_desc* d, dg_ctx** out) {
     return fail(DG_ERR_USAGE, "basis table length mismatch");
   }
   c->tabs.assign(d->tabs, d->tabs + d->tabs_len);
+  if (c->tabs_dev.upload(c->tabs.data(), c->tabs.size()) != cudaSuccess)
+    return fail(DG_ERR_CUDA, "tables upload failed");
   auto up = [&](auto& buf, const auto* h, size_t cnt) -> cudaError_t { return buf.upload(h, cnt); };
   const size_t nf = (size_t)d->n_tot * 2 * d->dim;
   cudaError_t e = cudaSuccess;

@@ -228,8 +228,8 @@ __device__ __forceinline__ void mat_apply(const double (&M)[N][N], const double*
 }
 
 // Fused Gram-Schmidt dots (GMRES, krylov.py:69-72 with the classical
-// variant of DESIGN.md §4): the CTA's partial sums of V_i . y (i < nv) and
-// y . y over its elements' nodes, written as row (gs_row0 + CTA) of gs_part.
+// variant of DESIGN.md §4): each warp's partial sums of V_i . y (i < nv) and
+// y . y over its elements' nodes, written as row (gs_row0 + warp) of gs_part.
 // The lane's stored values wv[] are its x-pencil nodes (ii, c).  Elements
 // with a coarse-side hanging face are left to coarse_kernel, which adds to
 // their result afterwards.  Deterministic: fixed lane / warp / row order.
@@ -283,16 +283,10 @@ __device__ __forceinline__ void gs_dots(const KParams<N>& P, double* smem, const
     }
     __syncwarp();
   }
-  __syncthreads();  // every warp is done with its area: reuse the first one
-  double* red = smem + WL::TABD;
+  // one partial row per warp (no CTA barrier): row gs_row0 + global warp index
+  const long long row = (long long)P.gs_row0 + (long long)blockIdx.x * WL::WPB + wid;
   for (int i0 = 0, ch = 0; i0 < nvt; i0 += CH, ++ch)
-    if (lane < min(CH, nvt - i0)) red[wid * 32 + i0 + lane] = tot[ch];
-  __syncthreads();
-  if (wid == 0 && lane < nvt) {
-    double s = 0.0;
-    for (int w = 0; w < WL::WPB; ++w) s += red[w * 32 + lane];
-    P.gs_part[((long long)P.gs_row0 + blockIdx.x) * nvt + lane] = s;
-  }
+    if (lane < min(CH, nvt - i0)) P.gs_part[row * nvt + i0 + lane] = tot[ch];
 }
 
 // IQ: Gauss-point input (H2 of the Helmholtz pair in quad mode) -- a
@@ -304,10 +298,9 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
   constexpr int NC = WL::NC, EPW = WL::EPW, KIN = WL::KIN, KOUT = WL::KOUT;
   constexpr int KW = WL::KW, TSZ = WL::TSZ, NF = 2 * D;
   extern __shared__ double smem[];
-  {
-    const double* src = reinterpret_cast<const double*>(&P.tab);
-    for (int i = threadIdx.x; i < WL::TABD; i += blockDim.x) smem[i] = src[i];
-  }
+  // tables -> smem from their global copy (asynchronous, coalesced; the
+  // kernel-parameter copy would serialise on divergent constant-bank reads)
+  for (int i = threadIdx.x; i < WL::TABD; i += blockDim.x) cp_async8(smem + i, P.tab_g + i);
   // (the tables are first read at the face phase: the barrier is placed there)
   const Tab<N>& TS = *reinterpret_cast<const Tab<N>*>(smem);
   const Tab<N>& TC = P.tab;
@@ -636,8 +629,8 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
     for (int k = 0; k < KOUT; ++k) fl[f][k] = fv[k] * sg;
   };
   // each lane reads back only the face slots it issued itself
-  __syncthreads();  // the CTA barrier: the tables copied at entry are visible
-  if (WL::ASYNC) cp_async_wait_all();
+  cp_async_wait_all();  // this thread's staged copies (tables, face nodes) landed
+  __syncthreads();      // ... and every thread's: the tables are visible CTA-wide
   if constexpr (SMP) {
     if constexpr (OPK == OP_GRAD) {
       // p = alpha (x - beta K) at the staged nodes, in place (own slots)
