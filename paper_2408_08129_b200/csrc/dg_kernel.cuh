@@ -64,10 +64,11 @@ struct Layout {
   static constexpr int CTHREADS = ((NP + 31) / 32) * 32;
   static constexpr int C_A = 0;
   static constexpr int C_FW = C_A + KIN * NP;
-  static constexpr int C_Z = C_FW + NF * S * KOUT * NQF;
+  static constexpr int C_Z = C_FW + S * KOUT * NQF;  // one coarse face at a time
   static constexpr int C_T = C_Z + KOUT * NP;
-  static constexpr int C_CH = C_T + KOUT * NP;  // children's nodal face values
-  static constexpr int CELEM = C_CH + NF * S * KIN * NQF;
+  static constexpr int C_CH = C_T + KOUT * NP;  // children's nodal face values (one face)
+  static constexpr int C_GS = C_CH + S * KIN * NQF;  // fused-dot warp sums
+  static constexpr int CELEM = C_GS + CTHREADS;
   static constexpr size_t CSMEM = (size_t)(TABD + 64 + CELEM) * sizeof(double);
 };
 
@@ -520,8 +521,7 @@ elem_kernel(const __grid_constant__ KParams<N> P) {
   extern __shared__ double smem[];
   __shared__ short fnode[NF * NQF];  // volume node of face point j on face f
   {
-    const double* src = reinterpret_cast<const double*>(&P.tab);
-    for (int i = threadIdx.x; i < L::TABD; i += blockDim.x) smem[i] = src[i];
+    for (int i = threadIdx.x; i < L::TABD; i += blockDim.x) smem[i] = P.tab_g[i];
     for (int i = threadIdx.x; i < NF * NQF; i += blockDim.x)
       fnode[i] = (short)face_to_vol<D, N>((i / NQF) >> 1, (i / NQF) & 1, i % NQF);
   }
@@ -807,10 +807,9 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
   using L = Layout<D, N, OPK>;
   constexpr int NP = L::NP, NQF = L::NQF, NF = L::NF, S = L::S, KIN = L::KIN, KOUT = L::KOUT;
   extern __shared__ double smem[];
-  {
-    const double* src = reinterpret_cast<const double*>(&P.tab);
-    for (int i = threadIdx.x; i < L::TABD; i += blockDim.x) smem[i] = src[i];
-  }
+  // tables from their global copy (coalesced; the kernel-parameter copy
+  // serialises on divergent constant-bank reads)
+  for (int i = threadIdx.x; i < L::TABD; i += blockDim.x) smem[i] = P.tab_g[i];
   const Tab<N>& T = *reinterpret_cast<const Tab<N>*>(smem);
   double* red = smem + L::TABD;
   double* A = red + 64 + L::C_A;
@@ -824,110 +823,120 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
   if (act)
     for (int c = 0; c < KIN; ++c) A[c * NP + q] = load_input<D, N, OPK>(P, e, c, q);
   __syncthreads();
-  // stage the children's nodal face values (coalescing the L2 gathers)
   __shared__ short cfnode[NF * NQF];
   for (int i = threadIdx.x; i < NF * NQF; i += blockDim.x)
     cfnode[i] = (short)face_to_vol<D, N>((i / NQF) >> 1, (i / NQF) & 1, i % NQF);
   double* CH = red + 64 + L::C_CH;
-  for (int it = threadIdx.x; it < NF * S * KIN * NQF; it += blockDim.x) {
-    const int j = it % NQF;
-    int r = it / NQF;
-    const int cp = r % KIN;
-    r /= KIN;
-    const int sub = r % S;
-    const int f = r / S;
-    if ((mesh.kind[e * NF + f] & 15) != KIND_COARSE) continue;
-    const long long child = mesh.hang_children[(long long)mesh.nbr[e * NF + f] * S + sub];
-    if (OPK == OP_DIVHV && P.in_quad) {
-      // Gauss-point input: the child's trace at its face Gauss point j
-      const int ax = f >> 1, cs = 1 - (f & 1);
-      const int b = face_to_vol<D, N>(ax, 0, j), st = stride_of<D, N>(ax);
-      double t = 0.0;
-      for (int p = 0; p < N; ++p) t = fma(T.lift[cs][p], load_input<D, N, OPK>(P, child, cp, b + p * st), t);
-      CH[it] = t;
-    } else {
-      CH[it] = load_input<D, N, OPK>(P, child, cp, face_to_vol<D, N>(f >> 1, 1 - (f & 1), j));
-    }
-  }
+  // the element's face records and each coarse face's children, loaded once
+  __shared__ uint8_t s_kind[NF];
+  __shared__ int s_child[NF][S];
+  if (threadIdx.x < NF) s_kind[threadIdx.x] = mesh.kind[e * NF + threadIdx.x] & 15;
   __syncthreads();
-  // subface fluxes of every coarse face
-  for (int it = threadIdx.x; it < NF * S * NQF; it += blockDim.x) {
-    const int qf = it % NQF;
-    const int sub = (it / NQF) % S;
-    const int f = it / (NQF * S);
-    const int kd = mesh.kind[e * NF + f] & 15;
-    if (kd != KIND_COARSE) continue;
-    const int axis = f >> 1, side = f & 1;
-    const long long child = mesh.hang_children[(long long)mesh.nbr[e * NF + f] * S + sub];
-    const int qt0 = (D == 2) ? qf : qf / N;
-    const int qt1 = (D == 2) ? 0 : qf % N;
-    const int b0 = sub & 1, b1 = (sub >> 1) & 1;
-    double TO[KIN], TN[KIN];
-    const double* chv = CH + ((f * S + sub) * KIN) * NQF;
-    const bool iq = (OPK == OP_DIVHV) && P.in_quad;
-#pragma unroll
-    for (int c = 0; c < KIN; ++c) {
-      double ao = 0.0, an = 0.0;
-      if (iq) {
-        // own coarse-face Gauss trace (lift contraction) -> fine Gauss points
-        // through halfq (x) halfq; the child's trace was staged at qf
-        const int st = stride_of<D, N>(axis);
-        for (int j = 0; j < NQF; ++j) {
-          const int j0 = (D == 2) ? j : j / N;
-          const int j1 = (D == 2) ? 0 : j % N;
-          double mo = T.halfq[b0][qt0][j0];
-          if (D == 3) mo *= T.halfq[b1][qt1][j1];
-          const int bj = face_to_vol<D, N>(axis, 0, j);
-          double tg = 0.0;
-          for (int p = 0; p < N; ++p) tg = fma(T.lift[side][p], A[c * NP + bj + p * st], tg);
-          ao = fma(mo, tg, ao);
-        }
-        an = chv[c * NQF + qf];
-      } else {
-        for (int j = 0; j < NQF; ++j) {
-          const int j0 = (D == 2) ? j : j / N;
-          const int j1 = (D == 2) ? 0 : j % N;
-          double mo = T.half[b0][qt0][j0];
-          double mb = T.B[qt0][j0];
-          if (D == 3) {
-            mo *= T.half[b1][qt1][j1];
-            mb *= T.B[qt1][j1];
-          }
-          ao = fma(mo, A[c * NP + cfnode[f * NQF + j]], ao);
-          an = fma(mb, chv[c * NQF + j], an);
-        }
-      }
-      TO[c] = ao;
-      TN[c] = an;
-    }
-    const ElemGeo<D> og = elem_geo<D>(mesh.elem, P.gc, child);
-    double n[D], ws;
-    if (axis == 0) face_metric_ax<D, N, 0>(P.gc, mesh.col, og, 1 - side, false, qf, T, n, ws);
-    else if (axis == 1 || D == 2) face_metric_ax<D, N, (D == 2 ? 1 : 1)>(P.gc, mesh.col, og, 1 - side, false, qf, T, n, ws);
-    else face_metric_ax<D, N, D - 1>(P.gc, mesh.col, og, 1 - side, false, qf, T, n, ws);
-    const bool minus = side == 1;
-    double TLv[KIN], TRv[KIN];
-#pragma unroll
-    for (int c = 0; c < KIN; ++c) {
-      TLv[c] = minus ? TO[c] : TN[c];
-      TRv[c] = minus ? TN[c] : TO[c];
-    }
-    double fl[KOUT];
-    num_flux<D, OPK, KIN, KOUT>(TLv, TRv, n, P.model.kinetic_factor, fl, &P.model, P.full);
-    const double sg = minus ? ws : -ws;
-#pragma unroll
-    for (int k = 0; k < KOUT; ++k) FW[((f * S + sub) * KOUT + k) * NQF + qf] = fl[k] * sg;
+  if (threadIdx.x < NF * S) {
+    const int f = threadIdx.x / S, sub = threadIdx.x % S;
+    s_child[f][sub] = (s_kind[f] == KIND_COARSE)
+                          ? mesh.hang_children[(long long)mesh.nbr[e * NF + f] * S + sub]
+                          : 0;
   }
-  __syncthreads();
-  double wq = 1.0, det = 1.0;
-  if (act) {
-    int qi[D];
-#pragma unroll
-    for (int a = 0; a < D; ++a) qi[a] = digit<D, N>(q, a);
+  if (act)
 #pragma unroll
     for (int k = 0; k < KOUT; ++k) Z[k * NP + q] = 0.0;
-    for (int f = 0; f < NF; ++f) {
-      if ((mesh.kind[e * NF + f] & 15) != KIND_COARSE) continue;
+  // one coarse face at a time (the face kind is uniform over the CTA): stage
+  // the children's nodal face values, subface fluxes, lift into Z
+  for (int f = 0; f < NF; ++f) {
+    __syncthreads();  // face records staged; previous face's CH / FW consumed
+    if (s_kind[f] != KIND_COARSE) continue;
+    for (int it = threadIdx.x; it < S * KIN * NQF; it += blockDim.x) {
+      const int j = it % NQF;
+      int r = it / NQF;
+      const int cp = r % KIN;
+      const int sub = r / KIN;
+      const long long child = s_child[f][sub];
+      if (OPK == OP_DIVHV && P.in_quad) {
+        // Gauss-point input: the child's trace at its face Gauss point j
+        const int ax = f >> 1, cs = 1 - (f & 1);
+        const int b = face_to_vol<D, N>(ax, 0, j), st = stride_of<D, N>(ax);
+        double t = 0.0;
+        for (int p = 0; p < N; ++p)
+          t = fma(T.lift[cs][p], load_input<D, N, OPK>(P, child, cp, b + p * st), t);
+        CH[it] = t;
+      } else {
+        // the child's node on the opposite face of the same axis (f ^ 1)
+        CH[it] = load_input<D, N, OPK>(P, child, cp, cfnode[(f ^ 1) * NQF + j]);
+      }
+    }
+    __syncthreads();
+    // subface fluxes of this coarse face
+    for (int it = threadIdx.x; it < S * NQF; it += blockDim.x) {
+      const int qf = it % NQF;
+      const int sub = it / NQF;
+      const int axis = f >> 1, side = f & 1;
+      const long long child = s_child[f][sub];
+      const int qt0 = (D == 2) ? qf : qf / N;
+      const int qt1 = (D == 2) ? 0 : qf % N;
+      const int b0 = sub & 1, b1 = (sub >> 1) & 1;
+      double TO[KIN], TN[KIN];
+      const double* chv = CH + (sub * KIN) * NQF;
+      const bool iq = (OPK == OP_DIVHV) && P.in_quad;
+#pragma unroll
+      for (int c = 0; c < KIN; ++c) {
+        double ao = 0.0, an = 0.0;
+        if (iq) {
+          // own coarse-face Gauss trace (lift contraction) -> fine Gauss points
+          // through halfq (x) halfq; the child's trace was staged at qf
+          const int st = stride_of<D, N>(axis);
+          for (int j = 0; j < NQF; ++j) {
+            const int j0 = (D == 2) ? j : j / N;
+            const int j1 = (D == 2) ? 0 : j % N;
+            double mo = T.halfq[b0][qt0][j0];
+            if (D == 3) mo *= T.halfq[b1][qt1][j1];
+            const int bj = face_to_vol<D, N>(axis, 0, j);
+            double tg = 0.0;
+            for (int p = 0; p < N; ++p) tg = fma(T.lift[side][p], A[c * NP + bj + p * st], tg);
+            ao = fma(mo, tg, ao);
+          }
+          an = chv[c * NQF + qf];
+        } else {
+          for (int j = 0; j < NQF; ++j) {
+            const int j0 = (D == 2) ? j : j / N;
+            const int j1 = (D == 2) ? 0 : j % N;
+            double mo = T.half[b0][qt0][j0];
+            double mb = T.B[qt0][j0];
+            if (D == 3) {
+              mo *= T.half[b1][qt1][j1];
+              mb *= T.B[qt1][j1];
+            }
+            ao = fma(mo, A[c * NP + cfnode[f * NQF + j]], ao);
+            an = fma(mb, chv[c * NQF + j], an);
+          }
+        }
+        TO[c] = ao;
+        TN[c] = an;
+      }
+      const ElemGeo<D> og = elem_geo<D>(mesh.elem, P.gc, child);
+      double n[D], ws;
+      if (axis == 0) face_metric_ax<D, N, 0>(P.gc, mesh.col, og, 1 - side, false, qf, T, n, ws);
+      else if (axis == 1 || D == 2) face_metric_ax<D, N, (D == 2 ? 1 : 1)>(P.gc, mesh.col, og, 1 - side, false, qf, T, n, ws);
+      else face_metric_ax<D, N, D - 1>(P.gc, mesh.col, og, 1 - side, false, qf, T, n, ws);
+      const bool minus = side == 1;
+      double TLv[KIN], TRv[KIN];
+#pragma unroll
+      for (int c = 0; c < KIN; ++c) {
+        TLv[c] = minus ? TO[c] : TN[c];
+        TRv[c] = minus ? TN[c] : TO[c];
+      }
+      double fl[KOUT];
+      num_flux<D, OPK, KIN, KOUT>(TLv, TRv, n, P.model.kinetic_factor, fl, &P.model, P.full);
+      const double sg = minus ? ws : -ws;
+#pragma unroll
+      for (int k = 0; k < KOUT; ++k) FW[(sub * KOUT + k) * NQF + qf] = fl[k] * sg;
+    }
+    __syncthreads();
+    // lift: Z += lift[side] (x) (halfq^T (x) halfq^T) FW over the subfaces
+    if (act) {
+      int qi[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) qi[a] = digit<D, N>(q, a);
       const int a = f >> 1, side = f & 1;
       int qt0, qt1 = 0;
       if (D == 2) qt0 = qi[1 - a];
@@ -941,7 +950,7 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
         double acc = 0.0;
         for (int sub = 0; sub < S; ++sub) {
           const int b0 = sub & 1, b1 = (sub >> 1) & 1;
-          const double* fw = FW + ((f * S + sub) * KOUT + k) * NQF;
+          const double* fw = FW + (sub * KOUT + k) * NQF;
           for (int j = 0; j < NQF; ++j) {
             const int j0 = (D == 2) ? j : j / N;
             const int j1 = (D == 2) ? 0 : j % N;
@@ -953,6 +962,9 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
         Z[k * NP + q] += lw * acc;
       }
     }
+  }
+  double wq = 1.0, det = 1.0;
+  if (act) {
     const ElemGeo<D> g = elem_geo<D>(mesh.elem, P.gc, e);
     double ctrv[D][D];
     point_metric<D, N>(P, g, q, det, ctrv);
@@ -1036,8 +1048,7 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
       const int nvt = P.gs_nv + 1;
       const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
       constexpr int NW = L::CTHREADS / 32;
-      static_assert(L::CELEM - L::C_CH >= NW * 32, "coarse gs scratch");
-      double* wr = CH;  // children face values, free by now: NW x 32 warp sums
+      double* wr = red + 64 + L::C_GS;  // NW x 32 warp sums
       for (int col = 0; col < nvt; ++col) {
         double s = act ? (col < P.gs_nv ? P.gsV[(long long)col * P.gs_vs + e * NP + q] : yv) * yv
                        : 0.0;
