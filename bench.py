@@ -213,7 +213,16 @@ def main():
             return imex_step(U, t, case.dt, tab, split, cfg)
         n_dof_local = U.numel()
     setup_s = time.perf_counter() - t_setup
-    n_dof = n_dof_local * world
+    # whole-job DoF (the partition is uneven by up to one leaf per rank)
+    n_dof = case.mesh.n_leaves * case.geometry.basis.n_nodes * (case.mesh.dim + 2)
+
+    def max_over_ranks(v, op="max"):
+        if world == 1:
+            return v
+        import torch.distributed as dist
+        tt = torch.tensor([float(v)], dtype=torch.float64)  # gloo: host tensors
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        return float(tt)
 
     def barrier():
         if world > 1:
@@ -250,11 +259,7 @@ def main():
     cnt = (C.c_longlong * 6)()
     lib.dg_profile_read(ms_c, by_c, cnt)
     lib.dg_profile_enable(0)
-    if world > 1:
-        import torch.distributed as dist
-        tt = torch.tensor([ms_total], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms_total = float(tt)
+    ms_total = max_over_ranks(ms_total)
     ms_step = ms_total / args.steps
     value = n_dof * args.steps / (ms_total * 1e-3)
 
@@ -269,26 +274,27 @@ def main():
                               "GB_s": (by_c[k] / (ms_c[k] * 1e-3) / 1e9) if ms_c[k] else None}
                  for k in range(6)}
 
-    # e2e through the public API with host buffers (rank-local state)
-    e2e = None
-    if world == 1:
-        Uh = torch.empty(U.shape, dtype=torch.float64, pin_memory=True)
-        Uh.copy_(U)
-        barrier()
-        e0 = time.perf_counter()
-        ev0.record(stream)
-        for _ in range(max(1, min(args.steps, 3))):
-            Ud = Uh.to(dev, non_blocking=True)
-            Ud, _ = step(Ud, t)
-            Uh.copy_(Ud, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-        ev1.record(stream)
-        barrier()
-        ne = max(1, min(args.steps, 3))
-        ms_e2e = ev0.elapsed_time(ev1) / ne
-        e2e = {"value": n_dof / (ms_e2e * 1e-3), "unit": "DoF/s",
-               "h2d_bytes_per_step": int(U.numel() * 8), "d2h_bytes_per_step": int(U.numel() * 8),
-               "ms_per_step": ms_e2e, "wall_s_per_step": (time.perf_counter() - e0) / ne}
+    # e2e through the public API with host buffers (each rank: its local
+    # state copied host->device, the step, the result copied back)
+    Uh = torch.empty(U.shape, dtype=torch.float64, pin_memory=True)
+    Uh.copy_(U)
+    barrier()
+    e0 = time.perf_counter()
+    ev0.record(stream)
+    ne = max(1, min(args.steps, 3))
+    for _ in range(ne):
+        Ud = Uh.to(dev, non_blocking=True)
+        Ud, _ = step(Ud, t)
+        Uh.copy_(Ud, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    ev1.record(stream)
+    barrier()
+    ms_e2e = max_over_ranks(ev0.elapsed_time(ev1) / ne)
+    wall_e2e = max_over_ranks((time.perf_counter() - e0) / ne)
+    bytes_step = int(max_over_ranks(U.numel() * 8, op="sum"))
+    e2e = {"value": n_dof / (ms_e2e * 1e-3), "unit": "DoF/s",
+           "h2d_bytes_per_step": bytes_step, "d2h_bytes_per_step": bytes_step,
+           "ms_per_step": ms_e2e, "wall_s_per_step": wall_e2e}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
