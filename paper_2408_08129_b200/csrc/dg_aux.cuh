@@ -17,6 +17,7 @@ struct AuxParams {
   CView in;          // dual (mass inverse) or state (integrate)
   CView in2;         // inner product: second field
   Model model;       // Courant report
+  double* tr;        // interp (trace mode): face traces of component 0, (n_el, 2d, n^(d-1))
   MView out;         // nodal result (mass inverse)
   double* partial;   // integrate: (grid, ncomp)
   Tab<N> tab;
@@ -180,6 +181,18 @@ interp_kernel(const __grid_constant__ AuxParams<N> P) {
     if (valid)
       for (int c = 0; c < kc; ++c)
         P.out.p[e * P.out.estride + (c0 + c) * P.out.cstride + q] = s[c * NP + q];
+    if (P.tr != nullptr && c0 == 0 && valid) {
+      // trace mode: component 0's traces at the face Gauss points (lift
+      // contractions of the Gauss pencils, as the warp-element kernel)
+      constexpr int NQF = ipow(N, D - 1);
+      for (int it = q; it < 2 * D * NQF; it += NP) {
+        const int f = it / NQF, j = it - (it / NQF) * NQF;
+        double t = 0.0;
+        for (int p = 0; p < N; ++p)
+          t = fma(T.lift[f & 1][p], s[nbr_pencil_node<D, N>(f >> 1, p, j)], t);
+        P.tr[e * (2 * D * NQF) + it] = t;
+      }
+    }
     __syncthreads();
   }
 }

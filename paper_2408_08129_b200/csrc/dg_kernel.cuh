@@ -68,7 +68,8 @@ struct Layout {
   static constexpr int C_T = C_Z + KOUT * NP;
   static constexpr int C_CH = C_T + KOUT * NP;  // children's nodal face values (one face)
   static constexpr int C_GS = C_CH + S * KIN * NQF;  // fused-dot warp sums
-  static constexpr int CELEM = C_GS + CTHREADS;
+  static constexpr int C_OT = C_GS + CTHREADS;       // trace mode: own face traces (one face)
+  static constexpr int CELEM = C_OT + KIN * NQF;
   static constexpr size_t CSMEM = (size_t)(TABD + 64 + CELEM) * sizeof(double);
 };
 
@@ -816,11 +817,13 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
   double* FW = red + 64 + L::C_FW;
   double* Z = red + 64 + L::C_Z;
   double* Tm = red + 64 + L::C_T;
+  double* OT = red + 64 + L::C_OT;
   const MeshDev& mesh = P.mesh;
   const long long e = clist[blockIdx.x];
   const int q = threadIdx.x;
   const bool act = q < NP;
-  if (act)
+  // (trace mode: the own traces come from the trace buffers, no input tile)
+  if (act && !(OPK == OP_DIVHV && P.in_quad && P.trV != nullptr))
     for (int c = 0; c < KIN; ++c) A[c * NP + q] = load_input<D, N, OPK>(P, e, c, q);
   __syncthreads();
   __shared__ short cfnode[NF * NQF];
@@ -852,7 +855,16 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
       const int cp = r % KIN;
       const int sub = r / KIN;
       const long long child = s_child[f][sub];
-      if (OPK == OP_DIVHV && P.in_quad) {
+      if (OPK == OP_DIVHV && P.in_quad && P.trV != nullptr) {
+        // trace mode: the child's V / h traces on its face f ^ 1 at its face
+        // Gauss point j (vertical faces carry only the normal component)
+        const bool vert = (f >> 1) < D - 1;
+        constexpr int TSL = tr_slots<D>() * NQF, THL = 2 * D * NQF;
+        double t = 0.0;
+        if (cp == D) t = P.trH[child * THL + (f ^ 1) * NQF + j];
+        else if (!vert || cp == (f >> 1)) t = P.trV[child * TSL + tr_slot<D>(f ^ 1, cp) * NQF + j];
+        CH[it] = t;
+      } else if (OPK == OP_DIVHV && P.in_quad) {
         // Gauss-point input: the child's trace at its face Gauss point j
         const int ax = f >> 1, cs = 1 - (f & 1);
         const int b = face_to_vol<D, N>(ax, 0, j), st = stride_of<D, N>(ax);
@@ -863,6 +875,18 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
       } else {
         // the child's node on the opposite face of the same axis (f ^ 1)
         CH[it] = load_input<D, N, OPK>(P, child, cp, cfnode[(f ^ 1) * NQF + j]);
+      }
+    }
+    if (OPK == OP_DIVHV && P.in_quad && P.trV != nullptr) {
+      // trace mode: this element's own traces on face f (the coarse side)
+      const bool vert = (f >> 1) < D - 1;
+      constexpr int TSL = tr_slots<D>() * NQF, THL = 2 * D * NQF;
+      for (int it = threadIdx.x; it < KIN * NQF; it += blockDim.x) {
+        const int cp = it / NQF, j = it - (it / NQF) * NQF;
+        double t = 0.0;
+        if (cp == D) t = P.trH[e * THL + f * NQF + j];
+        else if (!vert || cp == (f >> 1)) t = P.trV[e * TSL + tr_slot<D>(f, cp) * NQF + j];
+        OT[it] = t;
       }
     }
     __syncthreads();
@@ -881,7 +905,18 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
 #pragma unroll
       for (int c = 0; c < KIN; ++c) {
         double ao = 0.0, an = 0.0;
-        if (iq) {
+        if (iq && P.trV != nullptr) {
+          // trace mode: own coarse-face Gauss trace (staged from the trace
+          // buffers) -> fine Gauss points through halfq (x) halfq
+          for (int j = 0; j < NQF; ++j) {
+            const int j0 = (D == 2) ? j : j / N;
+            const int j1 = (D == 2) ? 0 : j % N;
+            double mo = T.halfq[b0][qt0][j0];
+            if (D == 3) mo *= T.halfq[b1][qt1][j1];
+            ao = fma(mo, OT[c * NQF + j], ao);
+          }
+          an = chv[c * NQF + qf];
+        } else if (iq) {
           // own coarse-face Gauss trace (lift contraction) -> fine Gauss points
           // through halfq (x) halfq; the child's trace was staged at qf
           const int st = stride_of<D, N>(axis);
@@ -985,10 +1020,37 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
   const int qq = act ? q : 0;
   if (OPK == OP_GRAD && P.out_quad) {
     // Gauss-point output (Helmholtz H1): coef * Z / (w det), no B^-1
-    if (!act) return;
-    const double inv = 1.0 / (wq * det);
-    for (int k = 0; k < KOUT; ++k)
-      P.out.p[e * P.out.estride + k * P.out.cstride + q] += P.coef * (Z[k * NP + q] * inv);
+    if (act) {
+      const double inv = 1.0 / (wq * det);
+      for (int k = 0; k < KOUT; ++k) {
+        double* o = P.out.p + e * P.out.estride + k * P.out.cstride + q;
+        const double v = *o + P.coef * (Z[k * NP + q] * inv);
+        *o = v;
+        Tm[k * NP + q] = v;  // the final V of this coarse element
+      }
+    }
+    if (P.tr_out != nullptr) {
+      // trace mode: this element's V changed -- rewrite all its face traces
+      // (same lift contractions as the warp-element kernel)
+      __syncthreads();
+      constexpr int TSL = tr_slots<D>() * NQF;
+      for (int it = threadIdx.x; it < TSL; it += blockDim.x) {
+        const int slot = it / NQF, j = it - (it / NQF) * NQF;
+        int f, comp;
+        if (slot < 2 * (D - 1)) {
+          f = slot;
+          comp = slot >> 1;
+        } else {
+          f = 2 * (D - 1) + (slot - 2 * (D - 1)) / D;
+          comp = (slot - 2 * (D - 1)) % D;
+        }
+        const int ax = f >> 1, side = f & 1;
+        double t = 0.0;
+        for (int p = 0; p < N; ++p)
+          t = fma(T.lift[side][p], Tm[comp * NP + nbr_pencil_node<D, N>(ax, p, j)], t);
+        P.tr_out[e * TSL + it] = t;
+      }
+    }
     return;
   }
   if (P.mode == OUT_MINV) {

@@ -22,6 +22,9 @@ struct OpArgs {
   int has_K, has_base, homogeneous, mode;
   int dbg;  // phase-skip flags for profiling experiments only (0 in production)
   int in_quad, out_quad;
+  double* tr_out;      // trace mode (see KParams)
+  const double* trV;
+  const double* trH;
   int full;  // ADV: divergence_full flux (see KParams)
   double* mass_partial;
   const double* gsV;  // fused Gram-Schmidt dots (see KParams)
@@ -65,6 +68,9 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
   P.out_quad = a.out_quad;
   P.mass_partial = a.mass_partial;
   P.full = a.full;
+  P.tr_out = a.tr_out;
+  P.trV = a.trV;
+  P.trH = a.trH;
   P.gsV = a.gsV;
   P.gs_vs = a.gs_vs;
   P.gs_nv = a.gs_nv;
@@ -161,6 +167,24 @@ inline bool welem_enabled(int D, int N) {
   return nc <= 32 && !v2;
 }
 
+// can the warp-element div(hV) kernel stage face data asynchronously (and
+// with it run the face-trace mode) for this (dim, n)?
+template <int D>
+inline bool welem_async_divhv(int N) {
+  switch (N) {
+    case 2: return WLayout<D, 2, OP_DIVHV>::ASYNC;
+    case 3: return WLayout<D, 3, OP_DIVHV>::ASYNC;
+    case 4: return WLayout<D, 4, OP_DIVHV>::ASYNC;
+    case 5: return WLayout<D, 5, OP_DIVHV>::ASYNC;
+    case 6: return WLayout<D, 6, OP_DIVHV>::ASYNC;
+    case 7: return WLayout<D, 7, OP_DIVHV>::ASYNC;
+  }
+  return false;
+}
+inline bool welem_trace_ok(int D, int N) {
+  return D == 2 ? welem_async_divhv<2>(N) : welem_async_divhv<3>(N);
+}
+
 // grid size only (for sizing the per-CTA partial buffers)
 template <int D, int N, int OPK>
 int elem_grid(int n_el) {
@@ -184,6 +208,7 @@ struct AuxArgs {
   CView in;
   CView in2;    // inner product: second field
   Model model;  // Courant report
+  double* tr;   // interp: face traces (trace mode)
   MView out;
   double* partial;
   const double* tabs;

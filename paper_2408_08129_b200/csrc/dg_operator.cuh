@@ -53,6 +53,12 @@ struct KParams {
   // points (out_quad), H2 reads V and h there (in_quad) -- B^-1 then B is
   // the identity, so the Helmholtz pair skips both transforms
   int in_quad, out_quad;
+  // face-trace mode of the Helmholtz pair (Gauss-point storage): H1 writes
+  // the face traces of V at the face Gauss points (tr_out), H2 reads the
+  // neighbours' V and h traces (trV, trH) instead of their nodal face values
+  double* tr_out;
+  const double* trV;
+  const double* trH;
   int full;              // ADV: 0 split advective flux, 1 full Euler Rusanov, 2 full centred
   double* mass_partial;  // ADV: per-CTA sum of the density dual (or null)
   // fused Gram-Schmidt dots of the result y (div(hV) MINV only, GMRES):
@@ -64,6 +70,15 @@ struct KParams {
   const double* tab_g;  // the Tab<N> tables in global memory (coalesced smem staging)
   Tab<N> tab;
 };
+
+// face-trace slots of V per element (trace mode): vertical faces carry only
+// the normal component V_AX (their normal is exactly +-e_AX), z faces all d
+template <int D>
+__host__ __device__ constexpr int tr_slots() { return 2 * (D - 1) + 2 * D; }
+template <int D>
+__host__ __device__ constexpr int tr_slot(int f, int comp) {  // f: face, comp: V component
+  return (f < 2 * (D - 1)) ? f : 2 * (D - 1) + (f - 2 * (D - 1)) * D + comp;
+}
 
 template <int D, int OPK> struct OpDims;
 template <int D> struct OpDims<D, OP_ADV> { static constexpr int KIN = D + 2, KOUT = D + 2; };
@@ -105,6 +120,35 @@ __device__ __forceinline__ int face_to_vol(int a, int s, int j) {
     idx += (j / N) * stride_of<D, N>(t[0]) + (j % N) * stride_of<D, N>(t[1]);
   }
   return idx;
+}
+
+// nodal index of face point c (tangential C-order) on the NEIGHBOUR's face
+// (ax, 1 - side), i.e. the node this lane gathers for its face (ax, side)
+template <int D, int N>
+__device__ __forceinline__ int nbr_face_node(int ax, int side, int c) {
+  const int endn = (1 - side) ? N - 1 : 0;
+  if constexpr (D == 2) {
+    return (ax == 0) ? endn * N + c : c * N + endn;
+  } else {
+    const int fa = c / N, fb = c % N;
+    if (ax == 0) return (endn * N + fa) * N + fb;
+    if (ax == 1) return (fa * N + endn) * N + fb;
+    return (fa * N + fb) * N + endn;
+  }
+}
+
+// nodal/Gauss index of point p of the NEIGHBOUR's pencil along ax through
+// face point c (tangential C-order)
+template <int D, int N>
+__device__ __forceinline__ int nbr_pencil_node(int ax, int p, int c) {
+  if constexpr (D == 2) {
+    return (ax == 0) ? p * N + c : c * N + p;
+  } else {
+    const int fa = c / N, fb = c % N;
+    if (ax == 0) return (p * N + fa) * N + fb;
+    if (ax == 1) return (fa * N + p) * N + fb;
+    return (fa * N + fb) * N + p;
+  }
 }
 
 // shared-memory 1D pass: dst[c][q] = sum_j M(i_a, j) src[c][q(a->j)]

@@ -42,6 +42,7 @@ static cudaError_t aux_n(int which, const AuxArgs& a, cudaStream_t st, int* grid
   P.in = a.in;
   P.in2 = a.in2;
   P.model = a.model;
+  P.tr = a.tr;
   P.out = a.out;
   P.partial = a.partial;
   std::memcpy(&P.tab, a.tabs, sizeof(Tab<N>));

@@ -96,6 +96,7 @@ struct dg_ctx {
   DevBuf<int> bj_colors, bj_sing;
   int bj_ncolors = 0;
   DevBuf<double> bj_inv, sz, su;
+  DevBuf<double> trV, trH;  // trace mode: face traces of V (H1 output) and of h
   int bj_valid = 0, bj_age = 1 << 30;
   long long bj_gen = 0;
   LaunchInfo last{};
@@ -195,8 +196,10 @@ int op_advective(dg_ctx* c, const double* U, double* out, int mode, double* mass
 
 // V_k = base_k + coef * [Minv] G(alpha (x - beta K))
 int op_grad(dg_ctx* c, const double* x, const double* K, double alpha, double beta, int homog,
-            int mode, MView out, CView base, int has_base, double coef, int out_quad = 0) {
+            int mode, MView out, CView base, int has_base, double coef, int out_quad = 0,
+            double* tr_out = nullptr) {
   OpArgs a = base_args(c);
+  a.tr_out = tr_out;
   a.in = cv(x, c->NP, c->NP);
   if (K) {
     a.inK = cv(K, c->NP, c->NP);
@@ -223,8 +226,11 @@ struct GsFuse {  // fused Gram-Schmidt dots of the div(hV) result (gs_dots)
 };
 
 int op_divhv(dg_ctx* c, CView V, const double* h, int homog, int mode, MView out, CView base,
-             int has_base, double coef, int in_quad = 0, const GsFuse* gs = nullptr) {
+             int has_base, double coef, int in_quad = 0, const GsFuse* gs = nullptr,
+             const double* trV = nullptr, const double* trH = nullptr) {
   OpArgs a = base_args(c);
+  a.trV = trV;
+  a.trH = trH;
   if (gs) {
     a.gsV = gs->V;
     a.gs_vs = gs->vs;
@@ -243,15 +249,34 @@ int op_divhv(dg_ctx* c, CView V, const double* h, int homog, int mode, MView out
   return launch(c, OP_DIVHV, a);
 }
 
-bool quad_mode(dg_ctx* c) {
-  // Gauss-point storage of the Helmholtz intermediate: measured neutral on
-  // B200 (the removed B / B^-1 passes are paid back by n-deep neighbour
-  // gathers), so it is opt-in (DG_QUAD=1) and the nodal path is the default
-  static const bool on = getenv("DG_QUAD") != nullptr;
-  return on && welem_enabled(c->dim, c->N);
+// Face-trace mode of the Helmholtz pair: V and h live at the Gauss points,
+// H1 writes V's face traces, H2 takes its neighbours' traces from them (no
+// nodal interpolation, no tangential face passes for conforming faces)
+bool trace_mode(dg_ctx* c) {
+  // default on (the nodal path: DG_TRACE=0)
+  static const char* env = getenv("DG_TRACE");
+  static const bool on = env == nullptr || std::string(env) != "0";
+  return on && welem_enabled(c->dim, c->N) && welem_trace_ok(c->dim, c->N);
 }
 
-// frozen h at the Gauss points (once per fixed-point iterate)
+bool quad_mode(dg_ctx* c) {
+  // Gauss-point storage of the Helmholtz intermediate.  DG_QUAD=1 alone
+  // keeps the n-deep neighbour gathers of the first version (measured
+  // slower); the trace mode is its default form
+  static const bool on = getenv("DG_QUAD") != nullptr;
+  return (on && welem_enabled(c->dim, c->N)) || trace_mode(c);
+}
+
+int halo_elems(dg_ctx* c, double* field, int per_elem) {
+  if (!c->comm.active()) return DG_OK;
+  if (!c->comm.exchange(field, 1, per_elem, c->stream)) return fail(DG_ERR_COMM, c->comm.error());
+  return DG_OK;
+}
+
+int tr_len(dg_ctx* c) { return (2 * (c->dim - 1) + 2 * c->dim) * c->NQF; }  // V trace slots
+
+// frozen h at the Gauss points (once per fixed-point iterate), + its face
+// traces in trace mode
 int interp_h(dg_ctx* c, const double* h, double* hq) {
   AuxArgs a;
   std::memset(&a, 0, sizeof a);
@@ -263,13 +288,20 @@ int interp_h(dg_ctx* c, const double* h, double* hq) {
   a.in = cv(h, c->NP, c->NP);
   a.out = mv(hq, c->NP, c->NP);
   a.tabs = c->tabs.data();
+  const bool tm = trace_mode(c);
+  if (tm) {
+    CK(c->trH.alloc((size_t)c->n_tot * 2 * c->dim * c->NQF));
+    a.tr = c->trH.p;
+  }
   int grid = 0;
   prof_begin(c->stream);
   cudaError_t e = c->dim == 2 ? launch_aux_d2(c->N, 2, a, c->stream, &grid)
                               : launch_aux_d3(c->N, 2, a, c->stream, &grid);
   prof_end(c->stream, P_OTHER, 16.0 * c->n_el * c->NP, 1);
   CK(e);
-  return halo(c, hq, 1);
+  RET(halo(c, hq, 1));
+  if (tm) RET(halo_elems(c, c->trH.p, 2 * c->dim * c->NQF));
+  return DG_OK;
 }
 
 // homogeneous Helmholtz action y = x + a_dt Minv Div_h(V), V = -(a_dt/M^2)(g-1) Minv G(x).
@@ -280,18 +312,22 @@ int helm_apply(dg_ctx* c, double a_dt, const double* h, const double* hq, double
   RET(halo(c, x, 1));
   const double gm1 = c->model.gamma - 1.0;
   const int qd = hq != nullptr;
+  const bool tm = qd && trace_mode(c);
+  if (tm) CK(c->trV.alloc((size_t)c->n_tot * tr_len(c)));
   RET(op_grad(c, x, nullptr, gm1, 0.0, 1, OUT_MINV, mv(c->sV.p, (long long)d * c->NP, c->NP),
-              CView{}, 0, -(a_dt * c->model.inv_mach_sq), qd));
-  RET(halo(c, c->sV.p, d));
+              CView{}, 0, -(a_dt * c->model.inv_mach_sq), qd, tm ? c->trV.p : nullptr));
+  if (tm) RET(halo_elems(c, c->trV.p, tr_len(c)));  // H2 reads neighbours only through traces
+  else RET(halo(c, c->sV.p, d));
   RET(op_divhv(c, cv(c->sV.p, (long long)d * c->NP, c->NP), qd ? hq : h, 1, OUT_MINV,
-               mv(y, c->NP, c->NP), cv(x, c->NP, c->NP), 1, a_dt, qd, gs));
+               mv(y, c->NP, c->NP), cv(x, c->NP, c->NP), 1, a_dt, qd, gs,
+               tm ? c->trV.p : nullptr, tm ? c->trH.p : nullptr));
   return DG_OK;
 }
 
 // the warp-element div(hV) kernel can fuse the Gram-Schmidt dots
 bool gs_fusable(dg_ctx* c) {
   static const bool off = getenv("DG_GS_FUSE") && std::string(getenv("DG_GS_FUSE")) == "0";
-  return !off && welem_enabled(c->dim, c->N) && !quad_mode(c);
+  return !off && welem_enabled(c->dim, c->N) && (!quad_mode(c) || trace_mode(c));
 }
 
 // F(x) = e_e - a_dt Minv Div_h(m_e - a_dt/M^2 Minv G((g-1)(x - kf K)))   (imex.py:190-218)
@@ -781,7 +817,7 @@ int dg_ctx_destroy(dg_ctx* c) {
   if (!c) return DG_OK;
   cudaSetDevice(c->device);
   for (auto* b : {&c->col, &c->ffU, &c->ffp, &c->ffh, &c->sigma, &c->bg, &c->mass_partial,
-                  &c->partial, &c->redout, &c->coef_dev, &c->gs_part, &c->sV, &c->sh, &c->sK, &c->sx,
+                  &c->partial, &c->redout, &c->coef_dev, &c->gs_part, &c->trV, &c->trH, &c->sV, &c->sh, &c->sK, &c->sx,
                   &c->srhs, &c->spold, &c->sw, &c->sr, &c->sx2, &c->basis})
     b->release();
   for (auto& s : c->st) s.release();

@@ -88,35 +88,6 @@ __device__ __forceinline__ int yoff(int c, int jj) {  // 3D y-pencil of lane c, 
   return ((c / N) * N + jj) * (N + 1) + c % N;
 }
 
-// nodal index of face point c (tangential C-order) on the NEIGHBOUR's face
-// (ax, 1 - side), i.e. the node this lane gathers for its face (ax, side)
-template <int D, int N>
-__device__ __forceinline__ int nbr_face_node(int ax, int side, int c) {
-  const int endn = (1 - side) ? N - 1 : 0;
-  if constexpr (D == 2) {
-    return (ax == 0) ? endn * N + c : c * N + endn;
-  } else {
-    const int fa = c / N, fb = c % N;
-    if (ax == 0) return (endn * N + fa) * N + fb;
-    if (ax == 1) return (fa * N + endn) * N + fb;
-    return (fa * N + fb) * N + endn;
-  }
-}
-
-// nodal/Gauss index of point p of the NEIGHBOUR's pencil along ax through
-// face point c (tangential C-order)
-template <int D, int N>
-__device__ __forceinline__ int nbr_pencil_node(int ax, int p, int c) {
-  if constexpr (D == 2) {
-    return (ax == 0) ? p * N + c : c * N + p;
-  } else {
-    const int fa = c / N, fb = c % N;
-    if (ax == 0) return (p * N + fa) * N + fb;
-    if (ax == 1) return (fa * N + p) * N + fb;
-    return (fa * N + fb) * N + p;
-  }
-}
-
 __device__ __forceinline__ void cp_async8(void* smem_ptr, const void* gptr) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem_ptr);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gptr) : "memory");
@@ -355,7 +326,9 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
   double* FGs = X + WL::KX * TSZ;
   constexpr bool iq0 = (OPK == OP_DIVHV) && IQ;
   constexpr bool SMP = WL::ASYNC && !iq0;  // tangential passes through smem
-  if (WL::ASYNC && !iq0) {
+  constexpr bool TRM = WL::ASYNC && iq0;   // trace mode: neighbours' face traces staged
+  if (WL::ASYNC) {
+    constexpr int TSL = tr_slots<D>() * NC, THL = 2 * D * NC;  // trace floats / element
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
       const int kd = kf[f] & 15;
@@ -370,6 +343,13 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
           if constexpr (OPK == OP_GRAD) {
             if (r == 0 && P.in.p) src = P.in.p + nb * P.in.estride + node;
             if (r == 1 && P.has_K) src = P.inK.p + nb * P.inK.estride + node;
+          } else if constexpr (TRM) {
+            // the neighbour's traces on its face f ^ 1, at ITS face Gauss
+            // point c (the same point for a conforming neighbour)
+            const bool vert = (f >> 1) < D - 1;
+            const int comp = vert ? (r == 0 ? (f >> 1) : D) : r;
+            src = (comp < D) ? P.trV + nb * TSL + tr_slot<D>(f ^ 1, comp) * NC + c
+                             : P.trH + nb * THL + (f ^ 1) * NC + c;
           } else {
             // vertical face: (V_AX, h); z face: every component
             const int cin = (WL::fg_cnt(f) == KIN) ? r : (r == 0 ? (f >> 1) : D);
@@ -391,7 +371,7 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
     for (int i = c; i < WL::GEE; i += NC)
       cp_async8(GEs + WL::GEON * NC + i, colp + NQH * D + i);
   }
-  if constexpr (OPK == OP_DIVHV && !IQ) {
+  if constexpr (OPK == OP_DIVHV) {
     // fused Gram-Schmidt dots: pull this element's slice of every basis
     // vector into L2 now (one bulk TMA prefetch of n^d doubles per vector,
     // spread over the element's lanes) so the epilogue's dot loads hit L2
@@ -530,10 +510,54 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
         }
       }
     }
+    if constexpr (TRM) {
+      // trace mode: the neighbour's V / h traces at its face Gauss points
+      // are staged; a conforming neighbour's points coincide with ours, a
+      // fine leaf maps its coarse parent's through halfq (x) halfq in place
+      double* G0 = FGs + WL::fg_off(f);
+      constexpr int FC = (AX < D - 1) ? 2 : KIN;
+      auto slot_comp = [&](int r) { return (FC == KIN) ? r : (r == 0 ? AX : D); };
+#pragma unroll
+      for (int cp = 0; cp < KIN; ++cp) TN[cp] = 0.0;
+      if (!need_pass) {
+#pragma unroll
+        for (int r = 0; r < FC; ++r) TN[slot_comp(r)] = G0[r * NC + c];
+      } else {
+        const bool fine = kd == KIND_FINE;
+        double t1[FC];
+#pragma unroll
+        for (int r = 0; r < FC; ++r) {
+          double t1v = 0.0;
+          if constexpr (D == 2) {
+#pragma unroll
+            for (int j = 0; j < N; ++j) t1v = fma(Mq0[fa * N + j], G0[r * NC + j], t1v);
+            TN[slot_comp(r)] = fine ? t1v : G0[r * NC + c];
+          } else {
+#pragma unroll
+            for (int j = 0; j < N; ++j) t1v = fma(Mq0[fa * N + j], G0[r * NC + j * N + fb], t1v);
+            t1[r] = fine ? t1v : G0[r * NC + c];
+          }
+        }
+        if constexpr (D == 3) {
+          double* S = G0;
+          __syncwarp();
+#pragma unroll
+          for (int r = 0; r < FC; ++r) S[r * NC + c] = t1[r];
+          __syncwarp();
+#pragma unroll
+          for (int r = 0; r < FC; ++r) {
+            double t2v = 0.0;
+#pragma unroll
+            for (int j = 0; j < N; ++j) t2v = fma(Mq1[fb * N + j], S[r * NC + fa * N + j], t2v);
+            TN[slot_comp(r)] = fine ? t2v : S[r * NC + c];
+          }
+        }
+      }
+    }
 #pragma unroll
     for (int cp = 0; cp < KIN; ++cp) {
       double gval = 0.0;
-      if (iq) {
+      if constexpr (iq && !TRM) {
         if (act && inter) {
           double t = 0.0;
 #pragma unroll
@@ -563,7 +587,7 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
             TN[cp] = fine ? t2v : gval;
           }
         }
-      } else if constexpr (!SMP) {
+      } else if constexpr (!SMP && !TRM) {
       if (act && inter) {
         gval = load_input<D, N, OPK>(P, nb, cp, nbr_face_node<D, N>(AX, side, c));
       }
@@ -777,12 +801,52 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
   if (OPK == OP_GRAD && P.out_quad) {
     // H1 of the Helmholtz pair: V = coef * diag(1/(w det)) Z at the Gauss
     // points -- the B^-1 transform and H2's B interpolation cancel exactly
-    if (!act) return;
+    double Vg[KOUT][N];
 #pragma unroll
-    for (int k = 0; k < KOUT; ++k) {
-      double* out = P.out.p + e * P.out.estride + (long long)k * P.out.cstride + c * N;
+    for (int k = 0; k < KOUT; ++k)
 #pragma unroll
-      for (int kz = 0; kz < N; ++kz) out[kz] = P.coef * (Zc[k][kz] * (iwh * TC.iqw[kz]));
+      for (int kz = 0; kz < N; ++kz) Vg[k][kz] = P.coef * (Zc[k][kz] * (iwh * TC.iqw[kz]));
+    if (act) {
+#pragma unroll
+      for (int k = 0; k < KOUT; ++k) {
+        double* out = P.out.p + e * P.out.estride + (long long)k * P.out.cstride + c * N;
+#pragma unroll
+        for (int kz = 0; kz < N; ++kz) out[kz] = Vg[k][kz];
+      }
+    }
+    if (P.tr_out != nullptr) {
+      // trace mode: V's traces at the face Gauss points (lift contractions of
+      // the Gauss pencils): every component on the z faces from the lane's
+      // column, the normal component on the vertical faces through the tile
+      constexpr int TSL = tr_slots<D>() * NC;
+      double* tr = P.tr_out + es * TSL;
+#pragma unroll
+      for (int side = 0; side < 2; ++side)
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          double t = 0.0;
+#pragma unroll
+          for (int kz = 0; kz < N; ++kz) t = fma(TC.lift[side][kz], Vg[k][kz], t);
+          if (act) tr[tr_slot<D>(2 * (D - 1) + side, k) * NC + c] = t;
+        }
+      __syncwarp();  // every lane is done with the tile
+#pragma unroll
+      for (int a = 0; a < D - 1; ++a)
+#pragma unroll
+        for (int kz = 0; kz < N; ++kz) X[a * TSZ + c * (N + 1) + kz] = Vg[a][kz];
+      __syncwarp();
+#pragma unroll
+      for (int a = 0; a < D - 1; ++a)
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+          double t = 0.0;
+#pragma unroll
+          for (int p = 0; p < N; ++p) {
+            const int off = (a == 0) ? xoff<D, N>(c, p) : yoff<N>(c, p);
+            t = fma(TC.lift[side][p], X[a * TSZ + off], t);
+          }
+          if (act) tr[tr_slot<D>(2 * a + side, a) * NC + c] = t;
+        }
     }
     return;
   }
@@ -848,7 +912,7 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
       }
     }
   }
-  if constexpr (OPK == OP_DIVHV && !IQ) {
+  if constexpr (OPK == OP_DIVHV) {
     if (P.gs_part != nullptr) gs_dots<D, N, OPK>(P, smem, kf, act, e, c, wv);
   }
 }
