@@ -822,6 +822,12 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
   const long long e = clist[blockIdx.x];
   const int q = threadIdx.x;
   const bool act = q < NP;
+  // the Helmholtz H1 output at this Gauss point (read-modify-written at the
+  // end): issued first so the final update does not wait on it
+  double out_pre[KOUT];
+  if (OPK == OP_GRAD && P.out_quad && act)
+#pragma unroll
+    for (int k = 0; k < KOUT; ++k) out_pre[k] = P.out.p[e * P.out.estride + k * P.out.cstride + q];
   // (trace mode: the own traces come from the trace buffers, no input tile)
   if (act && !(OPK == OP_DIVHV && P.in_quad && P.trV != nullptr))
     for (int c = 0; c < KIN; ++c) A[c * NP + q] = load_input<D, N, OPK>(P, e, c, q);
@@ -1024,7 +1030,7 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
       const double inv = 1.0 / (wq * det);
       for (int k = 0; k < KOUT; ++k) {
         double* o = P.out.p + e * P.out.estride + k * P.out.cstride + q;
-        const double v = *o + P.coef * (Z[k * NP + q] * inv);
+        const double v = out_pre[k] + P.coef * (Z[k * NP + q] * inv);
         *o = v;
         Tm[k * NP + q] = v;  // the final V of this coarse element
       }
