@@ -801,8 +801,13 @@ elem_kernel(const __grid_constant__ KParams<N> P) {
 // subface fluxes (fine-side metric, mortar traces, dgops.py:159-206) lifted
 // through halfq^T, then the same epilogue as the main kernel, ADDED to the
 // main kernel's output (linear in the lift).
+#ifndef DG_CMINB_GRAD
+#define DG_CMINB_GRAD 8
+#endif
+template <int OPK>
+constexpr int coarse_minb() { return OPK == OP_GRAD ? DG_CMINB_GRAD : (OPK == OP_DIVHV ? 10 : 6); }
 template <int D, int N, int OPK>
-__global__ void __launch_bounds__(Layout<D, N, OPK>::CTHREADS)
+__global__ void __launch_bounds__(Layout<D, N, OPK>::CTHREADS, coarse_minb<OPK>())
 coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clist, int ncoarse,
               double* mass_partial) {
   using L = Layout<D, N, OPK>;
