@@ -1118,21 +1118,37 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
     // fused Gram-Schmidt dots of this (complete) coarse element, row
     // gs_row0 + CTA of gs_part (see gs_dots in dg_wkernel.cuh)
     if (P.gs_part != nullptr) {
-      const int nvt = P.gs_nv + 1;
+      // columns as gs_dots (dg_wkernel.cuh): single (V_i.y, y.y) or dual
+      // pairs (item.y, item.u) over the items V_i, y, u (u = the base)
+      const bool dual = P.gs_dual != 0;
+      const int nv = P.gs_nv;
+      const int nvt = dual ? 2 * (nv + 2) : nv + 1;
+      const double uq = (act && dual) ? P.base(e, 0, q) : 0.0;
       const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
       constexpr int NW = L::CTHREADS / 32;
       double* wr = red + 64 + L::C_GS;  // NW x 32 warp sums
-      for (int col = 0; col < nvt; ++col) {
-        double s = act ? (col < P.gs_nv ? P.gsV[(long long)col * P.gs_vs + e * NP + q] : yv) * yv
-                       : 0.0;
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) wr[wid * 32 + col] = s;
-      }
-      __syncthreads();
-      if (threadIdx.x < nvt) {
-        double s = 0.0;
-        for (int w = 0; w < NW; ++w) s += wr[w * 32 + threadIdx.x];
-        P.gs_part[((long long)P.gs_row0 + blockIdx.x) * nvt + threadIdx.x] = s;
+      for (int c0 = 0; c0 < nvt; c0 += 32) {
+        const int cnt = min(32, nvt - c0);
+        for (int cc = 0; cc < cnt; ++cc) {
+          const int col = c0 + cc;
+          const int item = dual ? col >> 1 : col;
+          const double other = (dual && (col & 1)) ? uq : yv;
+          double s = 0.0;
+          if (act) {
+            const double v = item < nv ? P.gsV[(long long)item * P.gs_vs + e * NP + q]
+                                       : (item == nv ? yv : uq);
+            s = v * other;
+          }
+          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+          if (lane == 0) wr[wid * 32 + cc] = s;
+        }
+        __syncthreads();
+        if (threadIdx.x < cnt) {
+          double s = 0.0;
+          for (int w = 0; w < NW; ++w) s += wr[w * 32 + threadIdx.x];
+          P.gs_part[((long long)P.gs_row0 + blockIdx.x) * nvt + c0 + threadIdx.x] = s;
+        }
+        __syncthreads();
       }
     }
   }

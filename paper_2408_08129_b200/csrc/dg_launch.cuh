@@ -29,7 +29,7 @@ struct OpArgs {
   double* mass_partial;
   const double* gsV;  // fused Gram-Schmidt dots (see KParams)
   long long gs_vs;
-  int gs_nv;
+  int gs_nv, gs_dual;
   double* gs_part;
   const double* tabs;  // host pointer, Tab<N> layout
   const double* tabs_dev;  // the same tables in device memory
@@ -75,6 +75,7 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
   P.gs_vs = a.gs_vs;
   P.gs_nv = a.gs_nv;
   P.gs_part = a.gs_part;
+  P.gs_dual = a.gs_dual;
   P.gs_row0 = 0;
   P.tab_g = a.tabs_dev;
   std::memcpy(&P.tab, a.tabs, sizeof(Tab<N>));

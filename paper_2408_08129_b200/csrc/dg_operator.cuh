@@ -63,9 +63,12 @@ struct KParams {
   double* mass_partial;  // ADV: per-CTA sum of the density dual (or null)
   // fused Gram-Schmidt dots of the result y (div(hV) MINV only, GMRES):
   // row (gs_row0 + CTA) of gs_part gets (V_0.y, .., V_{nv-1}.y, y.y) partials
+  // gs_dual (DCGS2 GMRES): the input u of the Helmholtz action
+  // is the epilogue's base; the row then holds 2 (nv + 2) partials, the pairs
+  // (V_i.y, V_i.u) for i < nv, then (y.y, y.u) and (u.y, u.u)
   const double* gsV;
   long long gs_vs;
-  int gs_nv, gs_row0;
+  int gs_nv, gs_row0, gs_dual;
   double* gs_part;
   const double* tab_g;  // the Tab<N> tables in global memory (coalesced smem staging)
   Tab<N> tab;

@@ -155,7 +155,7 @@ double op_bytes(dg_ctx* c, int opk, const OpArgs& a) {
   }
   if (opk == OP_GRAD) return n * (1 + (a.has_K ? 1 : 0) + d + (a.has_base ? d : 0));
   // V, h in, y out, base; + the basis vectors of fused Gram-Schmidt dots
-  return n * (d + 1 + 1 + (a.has_base ? 1 : 0) + (a.gs_part ? a.gs_nv : 0));
+  return n * (d + 1 + 1 + (a.has_base ? 1 : 0) + (a.gs_part ? a.gs_nv : 0));  // (dual: u = base)
 }
 
 int launch(dg_ctx* c, int opk, const OpArgs& a) {
@@ -223,6 +223,7 @@ struct GsFuse {  // fused Gram-Schmidt dots of the div(hV) result (gs_dots)
   long long vs = 0;
   int nv = 0;
   double* part = nullptr;
+  int dual = 0;  // DCGS2: also the dots with the action's input (gs_dots)
 };
 
 int op_divhv(dg_ctx* c, CView V, const double* h, int homog, int mode, MView out, CView base,
@@ -236,6 +237,7 @@ int op_divhv(dg_ctx* c, CView V, const double* h, int homog, int mode, MView out
     a.gs_vs = gs->vs;
     a.gs_nv = gs->nv;
     a.gs_part = gs->part;
+    a.gs_dual = gs->dual;
   }
   a.in = V;
   a.inH = cv(h, c->NP, c->NP);
@@ -366,6 +368,134 @@ int bj_apply_ctx(dg_ctx* c, const double* in, double* out) {
   return DG_OK;
 }
 
+// One restart cycle of GMRES with DCGS2 Arnoldi (classical Gram-Schmidt with
+// delayed re-orthogonalisation; Bielich et al. 2022).  Slot j of the basis
+// holds the lagged vector u_j (projected once, not yet re-orthogonalised nor
+// normalised) until iteration j finalises it.  Iteration j:
+//   z = A u_j, and in the epilogue of the kernel producing z the dots
+//   t = Q^T z, s = Q^T u_j, z.z, u_j.z, u_j.u_j  (Q = q_0..q_{j-1}, one read);
+//   alpha = |u_j - Q s| (Pythagorean: s is a rounding-level correction);
+//   column j-1 of Hbar gets += s, Hbar[j][j-1] = alpha (now final);
+//   A q_j = (z - Q_{j+1} Hbar s) / alpha (Arnoldi relation), so its
+//   projections h = (Q_{j+1}^T z - Hbar s) / alpha need no further pass;
+//   ONE update pass writes q_j (in place) and u_{j+1} = A q_j - Q_{j+1} h,
+//   with |u_{j+1}| as Hbar[j+1][j].
+// The same Krylov space and the same re-orthogonalised basis as CGS2 (and as
+// the reference's MGS + re-orthogonalisation, krylov.py:69-79, up to
+// rounding); per Arnoldi step the basis is read twice instead of three times.
+// Convergence, happy breakdown and max_iter tests as krylov.py:82-103 on the
+// running Givens estimate; the least-squares solve at the end of the cycle
+// re-factors the corrected Hbar.
+int dcgs2_cycle(dg_ctx* c, double a_dt, const double* h, const double* hq, int m, int max_iter,
+                double bn, double target, double beta, double* Vb, long long vs, Gm& st, std::vector<double>& g,
+                std::vector<double>& y, int& done) {
+  const long long n = (long long)c->n_el * c->NP;
+  double* coefs = c->pinned + 128;
+  double* z = c->sw.p;
+  std::vector<double> Hb((size_t)(m + 1) * m, 0.0), R((size_t)(m + 1) * m, 0.0);
+  std::vector<double> cs(m), sn(m), dots(2 * (m + 2)), sv(m), gv(m + 1), hv(m + 1);
+  auto HB = [&](int i, int j) -> double& { return Hb[(size_t)i * m + j]; };
+  auto RR = [&](int i, int j) -> double& { return R[(size_t)i * m + j]; };
+  done = 0;
+  for (int j = 0; j < m; ++j) {
+    double* u = Vb + (size_t)j * vs;
+    GsFuse gs{Vb, vs, j, c->gs_part.p, 1};
+    RET(helm_apply(c, a_dt, h, hq, u, z, &gs));
+    const int nvt = 2 * (j + 2);
+    CK(reduce_rows(c->stream, c->gs_part.p, c->last.grid, nvt, c->partial.p, c->redout.p));
+    RET(reduce_read(c, c->redout.p, nvt, dots.data()));
+    // dots: (Q_i.z, Q_i.u) pairs, then (z.z, z.u), then (u.z, u.u)
+    const double zz = dots[2 * j], uz = dots[2 * j + 1], uu = dots[2 * j + 3];
+    double alpha = 1.0, s2 = 0.0, st_ = 0.0;
+    for (int i = 0; i < j; ++i) {
+      sv[i] = dots[2 * i + 1];
+      s2 += sv[i] * sv[i];
+      st_ += sv[i] * dots[2 * i];
+    }
+    if (j > 0) {
+      // finalise u_j: q_j = (u_j - Q s) / alpha, and column j-1 of Hbar
+      alpha = std::sqrt(uu - s2);
+      for (int i = 0; i < j; ++i) HB(i, j - 1) += sv[i];
+      HB(j, j - 1) = alpha;
+    }
+    // g = Hbar[0:j+1, 0:j] s
+    for (int i = 0; i <= j; ++i) {
+      double t = 0.0;
+      for (int k = std::max(0, i - 1); k < j; ++k) t += HB(i, k) * sv[k];
+      gv[i] = t;
+    }
+    // h = (Q_{j+1}^T z - g) / alpha, Q_{j+1}^T z = [t; (u.z - s.t) / alpha]
+    for (int i = 0; i < j; ++i) hv[i] = (dots[2 * i] - gv[i]) / alpha;
+    hv[j] = ((uz - st_) / alpha - gv[j]) / alpha;
+    const double nb = std::sqrt(std::max(zz, 0.0)) / alpha;  // |A q_j| (breakdown scale)
+    for (int i = 0; i <= j; ++i) HB(i, j) = hv[i];
+    // one pass: q_j in place, u_{j+1}, |u_{j+1}|^2
+    for (int i = 0; i < j; ++i) coefs[i] = sv[i];
+    for (int i = 0; i <= j; ++i) coefs[j + i] = gv[i];
+    for (int i = 0; i <= j; ++i) coefs[2 * j + 1 + i] = hv[i];
+    coefs[3 * j + 2] = alpha;
+    CK(cudaMemcpyAsync(c->coef_dev.p, coefs, (3 * j + 3) * sizeof(double),
+                       cudaMemcpyHostToDevice, c->stream));
+    double* un = Vb + (size_t)(j + 1) * vs;
+    CK(dcgs2_update(c->stream, n, j, Vb, vs, c->coef_dev.p, u, z, un, c->partial.p,
+                    c->redout.p));
+    double na2;
+    RET(reduce_read(c, c->redout.p, 1, &na2));
+    const double na = std::sqrt(na2);
+    HB(j + 1, j) = na;
+    const bool happy = na <= 1e-14 * std::max(bn, nb);
+    st.iterations += 1;
+    // running Givens QR of the (provisional) column j
+    for (int i = 0; i <= j + 1; ++i) RR(i, j) = HB(i, j);
+    for (int i = 0; i < j; ++i) {
+      const double t = cs[i] * RR(i, j) + sn[i] * RR(i + 1, j);
+      RR(i + 1, j) = -sn[i] * RR(i, j) + cs[i] * RR(i + 1, j);
+      RR(i, j) = t;
+    }
+    const double den = std::hypot(RR(j, j), RR(j + 1, j));
+    cs[j] = den != 0.0 ? RR(j, j) / den : 1.0;
+    sn[j] = den != 0.0 ? RR(j + 1, j) / den : 0.0;
+    RR(j, j) = den;
+    RR(j + 1, j) = 0.0;
+    g[j + 1] = -sn[j] * g[j];
+    g[j] = cs[j] * g[j];
+    done = j + 1;
+    const double est = std::fabs(g[j + 1]);
+    st.hist.push_back(est / bn);
+    if (happy) {
+      st.breakdown = 1;
+      break;
+    }
+    if (est <= target || st.iterations >= max_iter) break;
+  }
+  if (!done) return DG_OK;
+  // least squares on the corrected Hbar (columns < done - 1 carry their
+  // re-orthogonalisation corrections): fresh Givens QR, then back-substitution
+  std::vector<double> gg(done + 1, 0.0);
+  gg[0] = beta;
+  for (int j = 0; j < done; ++j) {
+    for (int i = 0; i <= j + 1; ++i) RR(i, j) = HB(i, j);
+    for (int i = 0; i < j; ++i) {
+      const double t = cs[i] * RR(i, j) + sn[i] * RR(i + 1, j);
+      RR(i + 1, j) = -sn[i] * RR(i, j) + cs[i] * RR(i + 1, j);
+      RR(i, j) = t;
+    }
+    const double den = std::hypot(RR(j, j), RR(j + 1, j));
+    cs[j] = den != 0.0 ? RR(j, j) / den : 1.0;
+    sn[j] = den != 0.0 ? RR(j + 1, j) / den : 0.0;
+    RR(j, j) = den;
+    RR(j + 1, j) = 0.0;
+    gg[j + 1] = -sn[j] * gg[j];
+    gg[j] = cs[j] * gg[j];
+  }
+  for (int i = done - 1; i >= 0; --i) {
+    double t = gg[i];
+    for (int k = i + 1; k < done; ++k) t -= RR(i, k) * y[k];
+    y[i] = t / RR(i, i);
+  }
+  return DG_OK;
+}
+
 // right-preconditioned (pc: M = block-Jacobi inverse, krylov.py:56-66,105-109)
 int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const double* rhs, double* x,
           double tol, int restart, int max_iter, Gm& st, bool pc = false) {
@@ -382,11 +512,16 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const doubl
   CK(c->basis.alloc((size_t)(m + 1) * vs));
   double* Vb = c->basis.p;
   const bool fuse = gs_fusable(c);
+  // DCGS2 (delayed re-orthogonalisation) needs the fused dual
+  // dots and u = the action's input (no preconditioner); DG_GMRES=cgs2 keeps
+  // the CGS + selective re-orthogonalisation path
+  static const bool cgs_env = getenv("DG_GMRES") && std::string(getenv("DG_GMRES")) == "cgs2";
+  const bool dcgs2 = fuse && !pc && !cgs_env;
   if (fuse) {
     // one row of <= m + 1 dot partials per element-kernel warp (>= 1 element
     // each) and per coarse element
     const long long rows = (long long)c->n_el + 4 + c->mesh.n_coarse + 1;
-    CK(c->gs_part.alloc((size_t)rows * 32));
+    CK(c->gs_part.alloc((size_t)rows * 2 * (32 + 2)));
   }
   double* coefs = c->pinned + 128;  // pinned staging for the coefficient uploads
   double* w = c->sw.p;
@@ -422,7 +557,10 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const doubl
     std::fill(g.begin(), g.end(), 0.0);
     g[0] = beta;
     int done = 0;
-    for (int j = 0; j < m; ++j) {
+    if (dcgs2) {
+      RET(dcgs2_cycle(c, a_dt, h, hq, m, max_iter, bn, target, beta, Vb, vs, st, g, y, done));
+    }
+    for (int j = 0; j < m && !dcgs2; ++j) {
       // classical Gram-Schmidt: h_i = V_i . w and |w|^2 in one pass,
       // fused into the div(hV) kernel that produces w when it can
       double* src = Vb + (size_t)j * vs;
@@ -520,7 +658,7 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const doubl
       if (est <= target || st.iterations >= max_iter) break;
     }
     if (done) {
-      for (int i = done - 1; i >= 0; --i) {
+      for (int i = done - 1; i >= 0 && !dcgs2; --i) {  // (dcgs2_cycle solved for y)
         double s = g[i];
         for (int k = i + 1; k < done; ++k) s -= Hij(i, k) * y[k];
         y[i] = s / Hij(i, i);
@@ -785,9 +923,9 @@ int dg_ctx_create(const dg_ctx_desc* d, dg_ctx** out) {
   }
   const int max_grid = d->n_el + 1 + c->mesh.n_coarse;
   if (e == cudaSuccess) e = c->mass_partial.alloc(max_grid);
-  if (e == cudaSuccess) e = c->partial.alloc((size_t)RED_BLOCKS * 40 + (size_t)max_grid * 8);
+  if (e == cudaSuccess) e = c->partial.alloc((size_t)RED_BLOCKS * 72 + (size_t)max_grid * 8);
   if (e == cudaSuccess) e = c->redout.alloc(256);
-  if (e == cudaSuccess) e = c->coef_dev.alloc(64);
+  if (e == cudaSuccess) e = c->coef_dev.alloc(128);
   if (e == cudaSuccess) e = cudaMallocHost(&c->pinned, 256 * sizeof(double));
   if (e != cudaSuccess) {
     dg_ctx_destroy(c);

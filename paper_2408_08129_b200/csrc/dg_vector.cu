@@ -555,6 +555,85 @@ cudaError_t axpy_div(cudaStream_t st, long long n, int nv, const double* V, long
   return cudaGetLastError();
 }
 
+// DCGS2 Arnoldi update, ONE pass over the NV finalised basis
+// vectors Q_i, the lagged vector u (in/out) and z = A u:
+//   q  = (u - sum s_i Q_i) / alpha                       (re-orthogonalised u)
+//   w  = (z - sum_{i<NV} g_i Q_i - g_NV q) / alpha       (= A q, Arnoldi relation)
+//   u' = w - sum_{i<NV} h_i Q_i - h_NV q                 (next lagged vector)
+// u <- q, unext <- u', partials of |u'|^2.  coefs = [s (NV), g (NV+1),
+// h (NV+1), alpha].
+template <int NV>
+__global__ void __launch_bounds__(RED_THREADS)
+k_dcgs2_update(long long n, const double* __restrict__ Q, long long vstride,
+               const double* __restrict__ coefs, double* __restrict__ u,
+               const double* __restrict__ z, double* __restrict__ unext,
+               double* __restrict__ partials) {
+  __shared__ double cf[3 * NV + 3];
+  for (int i = threadIdx.x; i < 3 * NV + 3; i += blockDim.x) cf[i] = coefs[i];
+  __syncthreads();
+  const double* cs = cf;
+  const double* cg = cf + NV;
+  const double* ch = cf + 2 * NV + 1;
+  const double alpha = cf[3 * NV + 2];
+  double acc = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    double a[NV + 1];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) a[i] = Q[i * vstride + k];
+    const double uk = u[k], zk = z[k];
+    double t1 = 0.0, t2 = 0.0, t3 = 0.0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      t1 = fma(cs[i], a[i], t1);
+      t2 = fma(cg[i], a[i], t2);
+      t3 = fma(ch[i], a[i], t3);
+    }
+    const double q = (uk - t1) / alpha;
+    const double w = (zk - t2 - cg[NV] * q) / alpha;
+    const double un = w - t3 - ch[NV] * q;
+    u[k] = q;
+    unext[k] = un;
+    acc = fma(un, un, acc);
+  }
+  __shared__ double red[RED_THREADS / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  acc = warp_sum(acc);
+  if (lane == 0) red[wid] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w2 = 0; w2 < RED_THREADS / 32; ++w2) s += red[w2];
+    partials[blockIdx.x] = s;
+  }
+}
+
+template <int NV>
+cudaError_t launch_dcgs2(cudaStream_t st, long long n, int nv, const double* Q, long long vstride,
+                         const double* coefs, double* u, const double* z, double* unext,
+                         double* partials) {
+  if constexpr (NV > 0) {
+    if (nv < NV) return launch_dcgs2<NV - 1>(st, n, nv, Q, vstride, coefs, u, z, unext, partials);
+  }
+  k_dcgs2_update<NV><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, Q, vstride, coefs, u, z, unext,
+                                                         partials);
+  return cudaGetLastError();
+}
+
+cudaError_t dcgs2_update(cudaStream_t st, long long n, int nv, const double* Q, long long vstride,
+                         const double* coefs_dev, double* u, const double* z, double* unext,
+                         double* partials, double* out) {
+  if (nv > 31 || nv < 0) return cudaErrorInvalidValue;
+  prof_begin(st);
+  cudaError_t e = launch_dcgs2<31>(st, n, nv, Q, vstride, coefs_dev, u, z, unext, partials);
+  if (e == cudaSuccess) {
+    k_reduce_cols<<<1, 256, 0, st>>>(partials, RED_BLOCKS, 1, out);
+    e = cudaGetLastError();
+  }
+  prof_end(st, P_AXPY, 8.0 * n * (nv + 4), 2);
+  return e;
+}
+
 cudaError_t scale(cudaStream_t st, long long n, double a, bool divide, const double* x,
                   double* y) {
   prof_begin(st);
@@ -613,25 +692,30 @@ cudaError_t positivity(cudaStream_t st, long long n_el, int np, int d, const dou
   return cudaGetLastError();
 }
 
-// many rows (e.g. one per element-kernel CTA) x ncols <= 32: RED_BLOCKS CTAs
-// each sum a contiguous row range in order, then k_reduce_cols (deterministic)
+// many rows (e.g. one per element-kernel warp) x ncols (<= 96): RED_BLOCKS
+// CTAs each sum a contiguous row range in order, 32 columns at a time, then
+// k_reduce_cols (deterministic)
 __global__ void __launch_bounds__(RED_THREADS)
 k_reduce_rows(const double* __restrict__ partials, long long nrows, int ncols,
               double* __restrict__ out) {
   const long long per = (nrows + gridDim.x - 1) / gridDim.x;
   const long long r0 = (long long)blockIdx.x * per;
   const long long r1 = r0 + per < nrows ? r0 + per : nrows;
-  const int col = threadIdx.x & 31, grp = threadIdx.x >> 5;  // 8 row groups
-  double s = 0.0;
-  if (col < ncols)
-    for (long long r = r0 + grp; r < r1; r += RED_THREADS / 32) s += partials[r * ncols + col];
+  const int cl = threadIdx.x & 31, grp = threadIdx.x >> 5;  // 8 row groups
   __shared__ double red[RED_THREADS / 32][32];
-  red[grp][col] = s;
-  __syncthreads();
-  if (threadIdx.x < ncols) {
-    double t = 0.0;
-    for (int g = 0; g < RED_THREADS / 32; ++g) t += red[g][threadIdx.x];
-    out[(long long)blockIdx.x * ncols + threadIdx.x] = t;
+  for (int c0 = 0; c0 < ncols; c0 += 32) {
+    const int col = c0 + cl;
+    double s = 0.0;
+    if (col < ncols)
+      for (long long r = r0 + grp; r < r1; r += RED_THREADS / 32) s += partials[r * ncols + col];
+    red[grp][cl] = s;
+    __syncthreads();
+    if (threadIdx.x < 32 && c0 + threadIdx.x < ncols) {
+      double t = 0.0;
+      for (int g = 0; g < RED_THREADS / 32; ++g) t += red[g][threadIdx.x];
+      out[(long long)blockIdx.x * ncols + c0 + threadIdx.x] = t;
+    }
+    __syncthreads();
   }
 }
 

@@ -18,6 +18,10 @@ cudaError_t axpy_multi(cudaStream_t st, long long n, int nv, const double* V, lo
                        const double* coefs_dev, double* w, double* partials, double* norm2_out);
 cudaError_t axpy_div(cudaStream_t st, long long n, int nv, const double* V, long long vstride,
                      const double* coefs_dev, double* w, double na, double* dst);
+// DCGS2 Arnoldi update (see dg_vector.cu): u <- q, unext <- u', out[0] = |u'|^2
+cudaError_t dcgs2_update(cudaStream_t st, long long n, int nv, const double* Q, long long vstride,
+                         const double* coefs_dev, double* u, const double* z, double* unext,
+                         double* partials, double* out);
 cudaError_t scale(cudaStream_t st, long long n, double a, bool divide, const double* x,
                   double* y);
 cudaError_t frozen(cudaStream_t st, long long n_el, int np, int d, const double* U, double gm1,

@@ -201,12 +201,16 @@ __device__ __forceinline__ void mat_apply(const double (&M)[N][N], const double*
 // Fused Gram-Schmidt dots (GMRES, krylov.py:69-72 with the classical
 // variant of DESIGN.md §4): each warp's partial sums of V_i . y (i < nv) and
 // y . y over its elements' nodes, written as row (gs_row0 + warp) of gs_part.
+// Dual mode (P.gs_dual, DCGS2): also V_i . u, y . u and u . u, u = the
+// action's input (the epilogue's base values uv[]); items i = 0..nv+1 (V_i,
+// then y, then u) give the column pairs (item . y, item . u).
 // The lane's stored values wv[] are its x-pencil nodes (ii, c).  Elements
 // with a coarse-side hanging face are left to coarse_kernel, which adds to
 // their result afterwards.  Deterministic: fixed lane / warp / row order.
 template <int D, int N, int OPK>
 __device__ __forceinline__ void gs_dots(const KParams<N>& P, double* smem, const uint8_t* kf,
-                                        bool act, long long e, int c, const double* wv) {
+                                        bool act, long long e, int c, const double* wv,
+                                        const double* uv) {
   using WL = WLayout<D, N, OPK>;
   constexpr int NP = WL::NP, NF = 2 * D;
   constexpr int AREA = WL::NSLOT * WL::SLOT;  // this warp's element slots
@@ -218,46 +222,54 @@ __device__ __forceinline__ void gs_dots(const KParams<N>& P, double* smem, const
 #pragma unroll
   for (int f = 0; f < NF; ++f)
     if ((kf[f] & 15) == KIND_COARSE) own = false;
-  const int nvt = P.gs_nv + 1;
+  const bool dual = P.gs_dual != 0;
+  const int nv = P.gs_nv;
+  const int per = dual ? 2 : 1;              // columns per item
+  const int nit = nv + (dual ? 2 : 1);       // items
+  const int nvt = nit * per;                 // columns of the row
+  const int chi = dual ? CH / 2 : CH;        // items per chunk
   double* area = smem + WL::TABD + wid * AREA;
+  // one partial row per warp (no CTA barrier): row gs_row0 + global warp index
+  const long long row = (long long)P.gs_row0 + (long long)blockIdx.x * WL::WPB + wid;
   __syncwarp();  // every lane is done with this warp's tiles
-  double tot[2] = {0.0, 0.0};
-  for (int i0 = 0, ch = 0; i0 < nvt; i0 += CH, ++ch) {
-    const int cnt = min(CH, nvt - i0);
-    // four columns at a time: their 4 N loads are all in flight together
+  for (int i0 = 0; i0 < nit; i0 += chi) {
+    const int cnt = min(chi, nit - i0);
+    // four items at a time: their 4 N loads are all in flight together
     for (int i = 0; i < cnt; i += 4) {
       double vv[4][N];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int col = i0 + i + u;
-        const bool ld = own && (i + u < cnt) && col < P.gs_nv;
+        const bool ld = own && (i + u < cnt) && col < nv;
         const double* vp = P.gsV + (long long)col * P.gs_vs + e * NP;
 #pragma unroll
         for (int ii = 0; ii < N; ++ii) {
           const int node = (D == 3) ? ii * N * N + c : ii * N + c;
-          vv[u][ii] = ld ? vp[node] : wv[ii];
+          vv[u][ii] = ld ? vp[node] : (col == nv ? wv[ii] : uv[ii]);
         }
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        double s = 0.0;
+        double s = 0.0, s2 = 0.0;
 #pragma unroll
-        for (int ii = 0; ii < N; ++ii) s = fma(vv[u][ii], wv[ii], s);
-        if (i + u < cnt) area[(i + u) * 33 + lane] = own ? s : 0.0;
+        for (int ii = 0; ii < N; ++ii) {
+          s = fma(vv[u][ii], wv[ii], s);
+          s2 = fma(vv[u][ii], uv[ii], s2);
+        }
+        if (i + u < cnt) {
+          area[((i + u) * per) * 33 + lane] = own ? s : 0.0;
+          if (dual) area[((i + u) * 2 + 1) * 33 + lane] = own ? s2 : 0.0;
+        }
       }
     }
     __syncwarp();
-    if (lane < cnt) {
+    if (lane < cnt * per) {
       double t = 0.0;
       for (int l = 0; l < 32; ++l) t += area[lane * 33 + l];
-      tot[ch] = t;
+      P.gs_part[row * nvt + i0 * per + lane] = t;
     }
     __syncwarp();
   }
-  // one partial row per warp (no CTA barrier): row gs_row0 + global warp index
-  const long long row = (long long)P.gs_row0 + (long long)blockIdx.x * WL::WPB + wid;
-  for (int i0 = 0, ch = 0; i0 < nvt; i0 += CH, ++ch)
-    if (lane < min(CH, nvt - i0)) P.gs_part[row * nvt + i0 + lane] = tot[ch];
 }
 
 // IQ: Gauss-point input (H2 of the Helmholtz pair in quad mode) -- a
@@ -885,8 +897,9 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
   if (pre_base) cp_async_wait_all();
   // x pass and store from the x-pencil: points (ii, [j,] k) of lane c
   double wv[N];  // the stored values (KOUT == 1 when the dots are fused)
+  double uv[N];  // their base values (the Helmholtz action's input u)
 #pragma unroll
-  for (int ii = 0; ii < N; ++ii) wv[ii] = 0.0;
+  for (int ii = 0; ii < N; ++ii) wv[ii] = uv[ii] = 0.0;
   if (act) {
 #pragma unroll
     for (int k = 0; k < KOUT; ++k) {
@@ -904,8 +917,10 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
           val = o[ii];
         } else {
           const double r = __dmul_rn(P.coef, o[ii]);
-          if (pre_base) val = __dadd_rn(BSs[(k * N + ii) * NC + c], r);
-          else val = P.has_base ? __dadd_rn(P.base(e, k, node), r) : r;
+          const double bv = pre_base ? BSs[(k * N + ii) * NC + c]
+                                     : (P.has_base ? P.base(e, k, node) : 0.0);
+          val = (pre_base || P.has_base) ? __dadd_rn(bv, r) : r;
+          uv[ii] = bv;
         }
         *out = val;
         wv[ii] = val;
@@ -913,7 +928,7 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
     }
   }
   if constexpr (OPK == OP_DIVHV) {
-    if (P.gs_part != nullptr) gs_dots<D, N, OPK>(P, smem, kf, act, e, c, wv);
+    if (P.gs_part != nullptr) gs_dots<D, N, OPK>(P, smem, kf, act, e, c, wv, uv);
   }
 }
 
