@@ -209,6 +209,15 @@ int dg_dots(dg_ctx* ctx, long long n, int nv, const double* V, long long vstride
    w may be used as scratch */
 int dg_gs_update(dg_ctx* ctx, long long n, int nv, const double* V, long long vstride,
                  const double* coefs_host, double* w, double na, double* dst);
+/* DCGS2 Arnoldi update (one pass; the re-orthogonalised form of
+   krylov.py:69-81): with Q_i = V + i*vstride, i < nv, and coefs_host =
+   [s (nv), g (nv+1), h (nv+1), alpha]:
+     q = (u - sum s_i Q_i) / alpha,  w = (z - sum_{i<nv} g_i Q_i - g_nv q) / alpha,
+     u_next = w - sum_{i<nv} h_i Q_i - h_nv q;
+   u <- q (in place), *norm2_host = |u_next|^2.  0 <= nv <= 31. */
+int dg_dcgs2_update(dg_ctx* ctx, long long n, int nv, const double* V, long long vstride,
+                    const double* coefs_host, double* u, const double* z, double* u_next,
+                    double* norm2_host);
 
 /* ---- multi-GPU (one process per GPU) ---- */
 int dg_nccl_unique_id(void* out128);

@@ -89,6 +89,7 @@ _SIGS = {
     "dg_global_inner_product": ([P, P, P, I, P], I),
     "dg_courant_ingredients": ([P, P, P], I),
     "dg_gs_update": ([P, LL, I, P, LL, P, P, D, P], I),
+    "dg_dcgs2_update": ([P, LL, I, P, LL, P, P, P, P, P], I),
     "dg_nccl_unique_id": ([P], I),
     "dg_ctx_set_comm": ([P, P, I, I, P, P, P], I),
     "dg_halo_exchange": ([P, P, I], I),

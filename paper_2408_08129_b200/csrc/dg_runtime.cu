@@ -1295,6 +1295,20 @@ int dg_gs_update(dg_ctx* c, long long n, int nv, const double* V, long long vstr
   return DG_OK;
 }
 
+int dg_dcgs2_update(dg_ctx* c, long long n, int nv, const double* V, long long vstride,
+                    const double* coefs_host, double* u, const double* z, double* u_next,
+                    double* norm2_host) {
+  if (nv < 0 || nv > 31) return fail(DG_ERR_USAGE, "dg_dcgs2_update: 0..31 vectors");
+  if (!(coefs_host[3 * nv + 2] != 0.0)) return fail(DG_ERR_USAGE, "dg_dcgs2_update: zero alpha");
+  CK(cudaStreamSynchronize(c->stream));  // the pinned staging slot is free
+  std::memcpy(c->pinned + 128, coefs_host, (3 * nv + 3) * sizeof(double));
+  CK(cudaMemcpyAsync(c->coef_dev.p, c->pinned + 128, (3 * nv + 3) * sizeof(double),
+                     cudaMemcpyHostToDevice, c->stream));
+  CK(dcgs2_update(c->stream, n, nv, V, vstride, c->coef_dev.p, u, z, u_next, c->partial.p,
+                  c->redout.p));
+  return reduce_read(c, c->redout.p, 1, norm2_host);
+}
+
 int dg_nccl_unique_id(void* out128) {
   std::string err;
   if (!Comm::unique_id(out128, &err)) return fail(DG_ERR_COMM, err);

@@ -1,3 +1,4 @@
+#include <algorithm>
 // Streaming vector kernels of the implicit solver: IMEX stage linear
 // combinations (orodg/imex.py:267-298), GMRES Gram-Schmidt dots/updates
 // (orodg/krylov.py:69-80, 105-109), pressure fixed-point norms
@@ -562,19 +563,24 @@ cudaError_t axpy_div(cudaStream_t st, long long n, int nv, const double* V, long
 //   u' = w - sum_{i<NV} h_i Q_i - h_NV q                 (next lagged vector)
 // u <- q, unext <- u', partials of |u'|^2.  coefs = [s (NV), g (NV+1),
 // h (NV+1), alpha].
+#ifndef DG_DCGS2_MINB
+#define DG_DCGS2_MINB 1
+#endif
 template <int NV>
-__global__ void __launch_bounds__(RED_THREADS)
+__global__ void __launch_bounds__(RED_THREADS, DG_DCGS2_MINB)
 k_dcgs2_update(long long n, const double* __restrict__ Q, long long vstride,
                const double* __restrict__ coefs, double* __restrict__ u,
                const double* __restrict__ z, double* __restrict__ unext,
                double* __restrict__ partials) {
-  __shared__ double cf[3 * NV + 3];
-  for (int i = threadIdx.x; i < 3 * NV + 3; i += blockDim.x) cf[i] = coefs[i];
+  // u' = z / alpha - sum_{i<NV} c_i Q_i - c_NV q with c = g / alpha + h: two
+  // coefficient sets (s, c) instead of three
+  __shared__ double cs[NV + 1], cc[NV + 1];
+  const double alpha = coefs[3 * NV + 2];
+  for (int i = threadIdx.x; i <= NV; i += blockDim.x) {
+    cs[i] = i < NV ? coefs[i] : 0.0;
+    cc[i] = coefs[NV + i] / alpha + coefs[2 * NV + 1 + i];
+  }
   __syncthreads();
-  const double* cs = cf;
-  const double* cg = cf + NV;
-  const double* ch = cf + 2 * NV + 1;
-  const double alpha = cf[3 * NV + 2];
   double acc = 0.0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
@@ -582,16 +588,14 @@ k_dcgs2_update(long long n, const double* __restrict__ Q, long long vstride,
 #pragma unroll
     for (int i = 0; i < NV; ++i) a[i] = Q[i * vstride + k];
     const double uk = u[k], zk = z[k];
-    double t1 = 0.0, t2 = 0.0, t3 = 0.0;
+    double t1 = 0.0, t2 = 0.0;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       t1 = fma(cs[i], a[i], t1);
-      t2 = fma(cg[i], a[i], t2);
-      t3 = fma(ch[i], a[i], t3);
+      t2 = fma(cc[i], a[i], t2);
     }
     const double q = (uk - t1) / alpha;
-    const double w = (zk - t2 - cg[NV] * q) / alpha;
-    const double un = w - t3 - ch[NV] * q;
+    const double un = zk / alpha - t2 - cc[NV] * q;
     u[k] = q;
     unext[k] = un;
     acc = fma(un, un, acc);
@@ -611,12 +615,23 @@ k_dcgs2_update(long long n, const double* __restrict__ Q, long long vstride,
 template <int NV>
 cudaError_t launch_dcgs2(cudaStream_t st, long long n, int nv, const double* Q, long long vstride,
                          const double* coefs, double* u, const double* z, double* unext,
-                         double* partials) {
+                         double* partials, int* used_grid) {
   if constexpr (NV > 0) {
-    if (nv < NV) return launch_dcgs2<NV - 1>(st, n, nv, Q, vstride, coefs, u, z, unext, partials);
+    if (nv < NV)
+      return launch_dcgs2<NV - 1>(st, n, nv, Q, vstride, coefs, u, z, unext, partials, used_grid);
   }
-  k_dcgs2_update<NV><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, Q, vstride, coefs, u, z, unext,
-                                                         partials);
+  // one wave: every resident CTA slot once (the register footprint grows
+  // with NV; <= RED_BLOCKS partials for the deterministic column reduction)
+  static int grid = 0;
+  if (grid == 0) {
+    int dev = 0, nsm = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dcgs2_update<NV>, RED_THREADS, 0);
+    grid = std::min(RED_BLOCKS, std::max(1, nsm * std::max(occ, 1)));
+  }
+  *used_grid = grid;
+  k_dcgs2_update<NV><<<grid, RED_THREADS, 0, st>>>(n, Q, vstride, coefs, u, z, unext, partials);
   return cudaGetLastError();
 }
 
@@ -625,9 +640,10 @@ cudaError_t dcgs2_update(cudaStream_t st, long long n, int nv, const double* Q, 
                          double* partials, double* out) {
   if (nv > 31 || nv < 0) return cudaErrorInvalidValue;
   prof_begin(st);
-  cudaError_t e = launch_dcgs2<31>(st, n, nv, Q, vstride, coefs_dev, u, z, unext, partials);
+  int grid = RED_BLOCKS;
+  cudaError_t e = launch_dcgs2<31>(st, n, nv, Q, vstride, coefs_dev, u, z, unext, partials, &grid);
   if (e == cudaSuccess) {
-    k_reduce_cols<<<1, 256, 0, st>>>(partials, RED_BLOCKS, 1, out);
+    k_reduce_cols<<<1, 256, 0, st>>>(partials, grid, 1, out);
     e = cudaGetLastError();
   }
   prof_end(st, P_AXPY, 8.0 * n * (nv + 4), 2);

@@ -46,8 +46,17 @@ def main():
     def update(nv):
         lib.dg_gs_update(ctx.handle, n, nv, vp, vs, coefs, wp, 1.0, dp)
 
+    z = torch.randn(n, dtype=torch.float64, device="cuda")
+    un = torch.empty_like(w)
+    nrm = C.c_double()
+
+    def dcgs2(nv):
+        cf = (C.c_double * 96)(*([0.01] * (3 * nv + 2) + [1.0]))
+        lib.dg_dcgs2_update(ctx.handle, n, nv, vp, vs, cf, wp, C.c_void_p(z.data_ptr()),
+                            C.c_void_p(un.data_ptr()), C.byref(nrm))
+
     for op in a.ops.split(","):
-        fn, extra = (dots, 1) if op == "dots" else (update, 2)
+        fn, extra = {"dots": (dots, 1), "update": (update, 2), "dcgs2": (dcgs2, 4)}[op]
         for nv in (1, 4, 8, 12, 16, 24, 31):
             for _ in range(2):
                 fn(nv)
