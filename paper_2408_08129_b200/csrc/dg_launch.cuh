@@ -115,12 +115,12 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       if (a.mesh.n_coarse > 0) {
-        P.gs_row0 = wgrid * WL::WPB;  // coarse elements' dot partials follow the warp rows
+        P.gs_row0 = wgrid;  // coarse elements' dot partials follow the CTA rows
         coarse_kernel<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
             P, a.mesh.coarse_list, a.mesh.n_coarse, nullptr);
         e = cudaGetLastError();
       }
-      if (info) info->grid = wgrid * WL::WPB + a.mesh.n_coarse;  // dot partial rows written
+      if (info) info->grid = wgrid + a.mesh.n_coarse;  // dot partial rows written
       return e;
     }
   }

@@ -199,24 +199,71 @@ __device__ __forceinline__ void mat_apply(const double (&M)[N][N], const double*
 }
 
 // Fused Gram-Schmidt dots (GMRES, krylov.py:69-72 with the classical
-// variant of DESIGN.md §4): each warp's partial sums of V_i . y (i < nv) and
-// y . y over its elements' nodes, written as row (gs_row0 + warp) of gs_part.
+// variant of DESIGN.md §4): the CTA's partial sums of V_i . y (i < nv) and
+// y . y over its elements' nodes, written as row (gs_row0 + CTA) of gs_part.
 // Dual mode (P.gs_dual, DCGS2): also V_i . u, y . u and u . u, u = the
 // action's input (the epilogue's base values uv[]); items i = 0..nv+1 (V_i,
 // then y, then u) give the column pairs (item . y, item . u).
 // The lane's stored values wv[] are its x-pencil nodes (ii, c).  Elements
 // with a coarse-side hanging face are left to coarse_kernel, which adds to
-// their result afterwards.  Deterministic: fixed lane / warp / row order.
+// their result afterwards.  Per round of 16 columns each lane forms its
+// partials in registers and a butterfly transpose-reduction over the warp
+// (16 double shuffles) leaves one column total per lane pair; the warps'
+// totals meet in smem (one CTA barrier at the very end).  Deterministic:
+// fixed lane / warp / row order.
+template <int D, int N, int PER>
+__device__ __forceinline__ void gs_round(const KParams<N>& P, bool own, long long e, int c,
+                                         const double* wv, const double* uv, int c0, int nv,
+                                         int nvt, double* wtot) {
+  constexpr int NP = ipow(N, D), NI = 16 / PER;
+  const int lane = threadIdx.x & 31;
+  const int i0 = c0 / PER;
+  double sv[16];
+#pragma unroll
+  for (int t = 0; t < NI; ++t) {
+    const int it = i0 + t;
+    const bool ld = own && it < nv;
+    const double* vp = P.gsV + (long long)it * P.gs_vs + e * NP;
+    double v[N];
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii) {
+      const int node = (D == 3) ? ii * N * N + c : ii * N + c;
+      v[ii] = ld ? vp[node] : (it == nv ? wv[ii] : uv[ii]);
+    }
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii) {
+      s0 = fma(v[ii], wv[ii], s0);
+      if (PER == 2) s1 = fma(v[ii], uv[ii], s1);
+    }
+    sv[t * PER] = own ? s0 : 0.0;
+    if (PER == 2) sv[t * PER + 1] = own ? s1 : 0.0;
+  }
+  // butterfly: m values -> m/2 at offsets 16, 8, 4, 2; lane keeps the half
+  // selected by its offset bit, so column = (lane >> 1) & 15 at the end
+#pragma unroll
+  for (int o = 16, m = 16; o >= 2; o >>= 1, m >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int k = 0; k < m / 2; ++k) {
+      const double send = up ? sv[k] : sv[k + m / 2];
+      const double keep = up ? sv[k + m / 2] : sv[k];
+      sv[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  sv[0] += __shfl_xor_sync(0xffffffffu, sv[0], 1);
+  const int col = c0 + ((lane >> 1) & 15);
+  if ((lane & 1) == 0 && col < nvt) wtot[col] = sv[0];
+}
+
 template <int D, int N, int OPK>
 __device__ __forceinline__ void gs_dots(const KParams<N>& P, double* smem, const uint8_t* kf,
                                         bool act, long long e, int c, const double* wv,
                                         const double* uv) {
   using WL = WLayout<D, N, OPK>;
-  constexpr int NP = WL::NP, NF = 2 * D;
+  constexpr int NF = 2 * D;
   constexpr int AREA = WL::NSLOT * WL::SLOT;  // this warp's element slots
-  constexpr int CH0 = AREA / 33;
-  constexpr int CH = CH0 < 32 ? CH0 : 32;
-  static_assert(CH >= 16, "warp area too small for the fused dots");
+  static_assert(AREA >= 2 * (32 + 2), "warp area too small for the fused dots");
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   bool own = act;
 #pragma unroll
@@ -224,51 +271,22 @@ __device__ __forceinline__ void gs_dots(const KParams<N>& P, double* smem, const
     if ((kf[f] & 15) == KIND_COARSE) own = false;
   const bool dual = P.gs_dual != 0;
   const int nv = P.gs_nv;
-  const int per = dual ? 2 : 1;              // columns per item
-  const int nit = nv + (dual ? 2 : 1);       // items
-  const int nvt = nit * per;                 // columns of the row
-  const int chi = dual ? CH / 2 : CH;        // items per chunk
-  double* area = smem + WL::TABD + wid * AREA;
-  // one partial row per warp (no CTA barrier): row gs_row0 + global warp index
-  const long long row = (long long)P.gs_row0 + (long long)blockIdx.x * WL::WPB + wid;
+  const int nvt = dual ? 2 * (nv + 2) : nv + 1;  // columns of the row
+  double* wtot = smem + WL::TABD + wid * AREA;   // this warp's column totals
   __syncwarp();  // every lane is done with this warp's tiles
-  for (int i0 = 0; i0 < nit; i0 += chi) {
-    const int cnt = min(chi, nit - i0);
-    // four items at a time: their 4 N loads are all in flight together
-    for (int i = 0; i < cnt; i += 4) {
-      double vv[4][N];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int col = i0 + i + u;
-        const bool ld = own && (i + u < cnt) && col < nv;
-        const double* vp = P.gsV + (long long)col * P.gs_vs + e * NP;
-#pragma unroll
-        for (int ii = 0; ii < N; ++ii) {
-          const int node = (D == 3) ? ii * N * N + c : ii * N + c;
-          vv[u][ii] = ld ? vp[node] : (col == nv ? wv[ii] : uv[ii]);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        double s = 0.0, s2 = 0.0;
-#pragma unroll
-        for (int ii = 0; ii < N; ++ii) {
-          s = fma(vv[u][ii], wv[ii], s);
-          s2 = fma(vv[u][ii], uv[ii], s2);
-        }
-        if (i + u < cnt) {
-          area[((i + u) * per) * 33 + lane] = own ? s : 0.0;
-          if (dual) area[((i + u) * 2 + 1) * 33 + lane] = own ? s2 : 0.0;
-        }
-      }
-    }
-    __syncwarp();
-    if (lane < cnt * per) {
+  for (int c0 = 0; c0 < nvt; c0 += 16) {
+    if (dual) gs_round<D, N, 2>(P, own, e, c, wv, uv, c0, nv, nvt, wtot);
+    else gs_round<D, N, 1>(P, own, e, c, wv, uv, c0, nv, nvt, wtot);
+  }
+  __syncthreads();
+  if (wid == 0) {
+    const long long row = (long long)P.gs_row0 + blockIdx.x;
+    for (int col = lane; col < nvt; col += 32) {
       double t = 0.0;
-      for (int l = 0; l < 32; ++l) t += area[lane * 33 + l];
-      P.gs_part[row * nvt + i0 * per + lane] = t;
+#pragma unroll
+      for (int w = 0; w < WL::WPB; ++w) t += smem[WL::TABD + w * AREA + col];
+      P.gs_part[row * nvt + col] = t;
     }
-    __syncwarp();
   }
 }
 
@@ -387,7 +405,10 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
     // fused Gram-Schmidt dots: pull this element's slice of every basis
     // vector into L2 now (one bulk TMA prefetch of n^d doubles per vector,
     // spread over the element's lanes) so the epilogue's dot loads hit L2
-    if (P.gs_part != nullptr && act) {
+#ifndef DG_GS_PREFETCH
+#define DG_GS_PREFETCH 1
+#endif
+    if (DG_GS_PREFETCH && P.gs_part != nullptr && act) {
       for (int i = c; i < P.gs_nv; i += NC) {
         const double* src = P.gsV + (long long)i * P.gs_vs + e * WL::NP;
         // 16-byte aligned span covering the slice (odd n^d: 8-byte aligned)
