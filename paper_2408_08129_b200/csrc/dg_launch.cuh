@@ -5,7 +5,7 @@
 #include <cstdlib>
 #include <string>
 #include <type_traits>
-#include "dg_wkernel.cuh"
+#include "dg_xkernel.cuh"
 
 namespace dg {
 
@@ -121,6 +121,48 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
         e = cudaGetLastError();
       }
       if (info) info->grid = wgrid + a.mesh.n_coarse;  // dot partial rows written
+      return e;
+    }
+  }
+  if constexpr (OPK == OP_ADV && XLayout<D, N>::OK) {
+    // warp-element explicit kernel (dg_xkernel.cuh) unless DG_KERNEL=v2
+    using XL = XLayout<D, N>;
+    static const bool use_x = !(getenv("DG_KERNEL") && std::string(getenv("DG_KERNEL")) == "v2");
+    if (use_x) {
+      constexpr int EPC = XL::EPW * XL::WPB;
+      const int xgrid = (a.mesh.n_el + EPC - 1) / EPC;
+      if (info) {
+        info->epb = EPC;
+        info->threads = XL::THREADS;
+        info->smem = XL::SMEM;
+        info->grid = xgrid * XL::WPB;
+      }
+      if (xgrid == 0) return cudaSuccess;
+      static bool xconf = false;
+      if (!xconf) {
+        cudaError_t e = cudaFuncSetAttribute(xelem_kernel<D, N>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)XL::SMEM);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(xelem_kernel<D, N>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::CSMEM);
+        if (e != cudaSuccess) return e;
+        xconf = true;
+      }
+      xelem_kernel<D, N><<<xgrid, XL::THREADS, XL::SMEM, st>>>(P);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      const int rows = xgrid * XL::WPB;  // mass-rate partials: one per warp
+      if (a.mesh.n_coarse > 0) {
+        coarse_kernel<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
+            P, a.mesh.coarse_list, a.mesh.n_coarse,
+            a.mass_partial ? a.mass_partial + rows : nullptr);
+        e = cudaGetLastError();
+      }
+      if (info) info->grid = rows + a.mesh.n_coarse;  // partial slots written
       return e;
     }
   }
