@@ -293,12 +293,19 @@ __device__ __forceinline__ void num_flux(const double* TL, const double* TR, con
       mnR += TR[1 + a] * n[a];
     }
     const double rL = TL[0], rR = TR[0];
-    const double uL = mnL / rL, uR = mnR / rR;
+#ifndef DG_ADV_RCP
+#define DG_ADV_RCP 1
+#endif
+    // DG_ADV_RCP: one reciprocal per side instead of d + 1 divisions (a
+    // rounding-level change, inside the reference's own 1-ulp sensitivity)
+    const double irL = DG_ADV_RCP ? 1.0 / rL : 0.0, irR = DG_ADV_RCP ? 1.0 / rR : 0.0;
+    const double uL = DG_ADV_RCP ? mnL * irL : mnL / rL, uR = DG_ADV_RCP ? mnR * irR : mnR / rR;
     const double lam = fmax(fabs(uL), fabs(uR));
     double kL = 0.0, kR = 0.0;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      const double vl = TL[1 + a] / rL, vr = TR[1 + a] / rR;
+      const double vl = DG_ADV_RCP ? TL[1 + a] * irL : TL[1 + a] / rL;
+      const double vr = DG_ADV_RCP ? TR[1 + a] * irR : TR[1 + a] / rR;
       kL += vl * vl;
       kR += vr * vr;
     }

@@ -330,11 +330,12 @@ xelem_kernel(const __grid_constant__ KParams<N> P) {
       } else {
         // split advective flux (dgops.py:234-254)
         const double rho = Uq[0];
+        const double irho = DG_ADV_RCP ? 1.0 / rho : 0.0;
         double u[D];
         double k = 0.0;
 #pragma unroll
         for (int a = 0; a < D; ++a) {
-          u[a] = Uq[1 + a] / rho;
+          u[a] = DG_ADV_RCP ? Uq[1 + a] * irho : Uq[1 + a] / rho;
           k += u[a] * u[a];
         }
         k *= 0.5;
@@ -420,6 +421,21 @@ xelem_kernel(const __grid_constant__ KParams<N> P) {
 
   // ---- 4. epilogue: B^-1 diag(1/(w det)) (MINV) or B^T (DUAL) -----------
   const bool minv = (P.mode == OUT_MINV);
+  // the source terms' inputs at the lane's output nodes, loaded now so their
+  // latency hides under the B^-1 passes
+  double uin[V][N], bgv[V][N], sgm[N];
+  const bool src = act && minv;
+  const bool spg = src && P.sigma != nullptr;
+#pragma unroll
+  for (int ii = 0; ii < N; ++ii) {
+    const int node = (D == 3) ? ii * N * N + c : ii * N + c;
+#pragma unroll
+    for (int r = 0; r < V; ++r) {
+      uin[r][ii] = (src && (r == 0 || r == D || spg)) ? P.in(e, r, node) : 0.0;
+      bgv[r][ii] = (spg && r > 0) ? P.bg(e, r, node) : 0.0;
+    }
+    sgm[ii] = spg ? P.sigma[e * NP + node] : 0.0;
+  }
   double iwh = 1.0 / det_c;
   if constexpr (D == 3) iwh *= TC.iqw[c / N] * TC.iqw[c % N];
   else iwh *= TC.iqw[c];
@@ -479,13 +495,12 @@ xelem_kernel(const __grid_constant__ KParams<N> P) {
     double R[V];
 #pragma unroll
     for (int r = 0; r < V; ++r) R[r] = -res[r][ii];
-    const double rho = P.in(e, 0, node);
+    const double rho = uin[0][ii];
     R[D] += -md.gravity * rho;
-    R[D + 1] += -md.kinetic_factor * md.gravity * rho * (P.in(e, D, node) / rho);
-    if (P.sigma != nullptr) {
-      const double sgm = P.sigma[e * NP + node];
+    R[D + 1] += -md.kinetic_factor * md.gravity * rho * (uin[D][ii] / rho);
+    if (spg) {
 #pragma unroll
-      for (int r = 1; r < V; ++r) R[r] -= sgm * (P.in(e, r, node) - P.bg(e, r, node));
+      for (int r = 1; r < V; ++r) R[r] -= sgm[ii] * (uin[r][ii] - bgv[r][ii]);
     }
 #pragma unroll
     for (int r = 0; r < V; ++r) out[r * P.out.cstride] = R[r];
