@@ -140,19 +140,20 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
       if (xgrid == 0) return cudaSuccess;
       static bool xconf = false;
       if (!xconf) {
-        cudaError_t e = cudaFuncSetAttribute(xelem_kernel<D, N>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)XL::SMEM);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(xelem_kernel<D, N>,
-                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK>,
+        for (auto kfn : {xelem_kernel<D, N, false>, xelem_kernel<D, N, true>}) {
+          cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)XL::SMEM);
+          if (e != cudaSuccess) return e;
+          e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+          if (e != cudaSuccess) return e;
+        }
+        cudaError_t e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::CSMEM);
         if (e != cudaSuccess) return e;
         xconf = true;
       }
-      xelem_kernel<D, N><<<xgrid, XL::THREADS, XL::SMEM, st>>>(P);
+      if (a.full) xelem_kernel<D, N, true><<<xgrid, XL::THREADS, XL::SMEM, st>>>(P);
+      else xelem_kernel<D, N, false><<<xgrid, XL::THREADS, XL::SMEM, st>>>(P);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       const int rows = xgrid * XL::WPB;  // mass-rate partials: one per warp

@@ -59,6 +59,14 @@ __device__ __forceinline__ void point_metric_reg(const GeoConst& gc, const Tab<N
   }
 }
 
+// smem-only component loops are kept rolled (instruction-cache footprint of
+// the d+2-variable kernel); DG_XUNROLL=1 unrolls them
+#if defined(DG_XUNROLL) && DG_XUNROLL
+#define XROLL _Pragma("unroll")
+#else
+#define XROLL _Pragma("unroll 1")
+#endif
+
 template <int D, int N>
 struct XLayout {
   static constexpr int V = D + 2;
@@ -88,7 +96,9 @@ struct XLayout {
   static constexpr int MINB = DG_XMINB;
 };
 
-template <int D, int N>
+// FULL: divergence_full (P.full != 0) -- a separate instantiation keeps the
+// full Euler flux out of the explicit residual's code
+template <int D, int N, bool FULL>
 __global__ void __launch_bounds__(XLayout<D, N>::THREADS, XLayout<D, N>::MINB)
 xelem_kernel(const __grid_constant__ KParams<N> P) {
   using XL = XLayout<D, N>;
@@ -162,7 +172,7 @@ xelem_kernel(const __grid_constant__ KParams<N> P) {
   }
   __syncwarp();
   if constexpr (D == 3) {
-#pragma unroll
+XROLL
     for (int r = 0; r < V; ++r) {
       double v[N], o[N];
 #pragma unroll
@@ -173,7 +183,7 @@ xelem_kernel(const __grid_constant__ KParams<N> P) {
     }
     __syncwarp();
   }
-#pragma unroll
+XROLL
   for (int r = 0; r < V; ++r) {
     double v[N], o[N];
 #pragma unroll
@@ -254,28 +264,44 @@ xelem_kernel(const __grid_constant__ KParams<N> P) {
         TL[k] = minus ? TO[k] : TN[k];
         TR[k] = minus ? TN[k] : TO[k];
       }
-      num_flux<D, OP_ADV, V, V>(TL, TR, n, md.kinetic_factor, fv, &md, P.full);
+      num_flux<D, OP_ADV, V, V>(TL, TR, n, md.kinetic_factor, fv, &md, FULL ? P.full : 0);
       const double sg = minus ? ws : -ws;
 #pragma unroll
       for (int k = 0; k < V; ++k) fv[k] *= sg;
     }
     if constexpr (AX == D - 1) {
 #pragma unroll
-      for (int k = 0; k < V; ++k) flz[side][k] = fv[k];
+      for (int k = 0; k < V; ++k) {
+        if (side == 0) flz[0][k] = fv[k];
+        else flz[1][k] = fv[k];
+      }
     } else {
       __syncwarp();  // every lane is done reading this face's staged nodes
 #pragma unroll
       for (int k = 0; k < V; ++k) G0[k * NC + c] = fv[k];
     }
   };
-  face(std::integral_constant<int, 0>{}, 0);
-  face(std::integral_constant<int, 0>{}, 1);
+  // both sides unrolled (DG_XSIDEUNROLL=0: one code copy per axis, measured slower)
+#if !defined(DG_XSIDEUNROLL) || DG_XSIDEUNROLL
+#pragma unroll
+#else
+#pragma unroll 1
+#endif
+  for (int side = 0; side < 2; ++side) face(std::integral_constant<int, 0>{}, side);
   if constexpr (D == 3) {
-    face(std::integral_constant<int, 1>{}, 0);
-    face(std::integral_constant<int, 1>{}, 1);
+#if !defined(DG_XSIDEUNROLL) || DG_XSIDEUNROLL
+#pragma unroll
+#else
+#pragma unroll 1
+#endif
+    for (int side = 0; side < 2; ++side) face(std::integral_constant<int, 1>{}, side);
   }
-  face(std::integral_constant<int, D - 1>{}, 0);
-  face(std::integral_constant<int, D - 1>{}, 1);
+#if !defined(DG_XSIDEUNROLL) || DG_XSIDEUNROLL
+#pragma unroll
+#else
+#pragma unroll 1
+#endif
+  for (int side = 0; side < 2; ++side) face(std::integral_constant<int, D - 1>{}, side);
   __syncwarp();  // every lane is done reading the Gauss tile's pencils
 
   // ---- 3. volume: flux + metric per column point ------------------------
@@ -320,7 +346,7 @@ xelem_kernel(const __grid_constant__ KParams<N> P) {
 #pragma unroll
       for (int r = 0; r < V; ++r) Uq[r] = X[r * TSZ + c * CS + kz];
       double F[D][V];
-      if (P.full) {
+      if (FULL) {
         double Ff[V][D];
         full_flux<D>(Uq, md, Ff);
 #pragma unroll
@@ -377,7 +403,7 @@ xelem_kernel(const __grid_constant__ KParams<N> P) {
   }
   __syncwarp();
   // x (and y) directions on the lane's pencils, with that direction's lifts
-#pragma unroll
+XROLL
   for (int r = 0; r < V; ++r) {
     double v[N], o[N];
     const double f0 = FG[(0 * V + r) * NC + c], f1 = FG[(1 * V + r) * NC + c];
@@ -459,7 +485,7 @@ xelem_kernel(const __grid_constant__ KParams<N> P) {
     for (int kz = 0; kz < N; ++kz) X[r * TSZ + c * CS + kz] = Zc[r][kz];
   __syncwarp();
   if constexpr (D == 3) {
-#pragma unroll
+XROLL
     for (int r = 0; r < V; ++r) {
       double v[N], o[N];
 #pragma unroll
