@@ -803,6 +803,47 @@ elem_kernel(const __grid_constant__ KParams<N> P) {
   }
 }
 
+// fused Gram-Schmidt dots of one complete coarse element (CTHREADS threads,
+// thread q owns node q with final value yv), row gs_row0 + CTA of gs_part;
+// columns as gs_dots (dg_wkernel.cuh): single (V_i.y, y.y) or dual pairs
+// (item.y, item.u) over the items V_i, y, u (u = the base)
+template <int D, int N, int OPK>
+__device__ __forceinline__ void coarse_dots(const KParams<N>& P, long long e, int q, bool act,
+                                            double yv, double* wr /* NW x 32 */) {
+  using L = Layout<D, N, OPK>;
+  constexpr int NP = L::NP;
+  if (P.gs_part == nullptr) return;
+  const bool dual = P.gs_dual != 0;
+  const int nv = P.gs_nv;
+  const int nvt = dual ? 2 * (nv + 2) : nv + 1;
+  const double uq = (act && dual) ? P.base(e, 0, q) : 0.0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int NW = L::CTHREADS / 32;
+  for (int c0 = 0; c0 < nvt; c0 += 32) {
+    const int cnt = min(32, nvt - c0);
+    for (int cc = 0; cc < cnt; ++cc) {
+      const int col = c0 + cc;
+      const int item = dual ? col >> 1 : col;
+      const double other = (dual && (col & 1)) ? uq : yv;
+      double s = 0.0;
+      if (act) {
+        const double v = item < nv ? P.gsV[(long long)item * P.gs_vs + e * NP + q]
+                                   : (item == nv ? yv : uq);
+        s = v * other;
+      }
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) wr[wid * 32 + cc] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+      double s = 0.0;
+      for (int w = 0; w < NW; ++w) s += wr[w * 32 + threadIdx.x];
+      P.gs_part[((long long)P.gs_row0 + blockIdx.x) * nvt + c0 + threadIdx.x] = s;
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------- coarse-side fix-up
 // One CTA per element owning >= 1 coarse hanging face: the coarse side's
 // subface fluxes (fine-side metric, mortar traces, dgops.py:159-206) lifted
@@ -837,7 +878,8 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
   // the Helmholtz H1 output at this Gauss point (read-modify-written at the
   // end): issued first so the final update does not wait on it
   double out_pre[KOUT];
-  if (OPK == OP_GRAD && P.out_quad && act)
+  const bool side_mode = P.side_out != nullptr;
+  if (OPK == OP_GRAD && P.out_quad && act && !side_mode)
 #pragma unroll
     for (int k = 0; k < KOUT; ++k) out_pre[k] = P.out.p[e * P.out.estride + k * P.out.cstride + q];
   // (trace mode: the own traces come from the trace buffers, no input tile)
@@ -985,21 +1027,15 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
       for (int k = 0; k < KOUT; ++k) FW[(sub * KOUT + k) * NQF + qf] = fl[k] * sg;
     }
     __syncthreads();
-    // lift: Z += lift[side] (x) (halfq^T (x) halfq^T) FW over the subfaces
-    if (act) {
-      int qi[D];
-#pragma unroll
-      for (int a = 0; a < D; ++a) qi[a] = digit<D, N>(q, a);
-      const int a = f >> 1, side = f & 1;
-      int qt0, qt1 = 0;
-      if (D == 2) qt0 = qi[1 - a];
-      else {
-        qt0 = (a == 0) ? qi[1] : qi[0];
-        qt1 = (a == 2) ? qi[1] : qi[2];
-      }
-      const double lw = T.lift[side][qi[a]];
-#pragma unroll
-      for (int k = 0; k < KOUT; ++k) {
+    // coarse-face flux at the coarse face Gauss points, once per point:
+    // G[k][qt] = sum_sub (halfq^T (x) halfq^T) FW[sub][k]  (into the consumed
+    // children staging area CH)
+    {
+      double* G = CH;
+      for (int it = threadIdx.x; it < KOUT * NQF; it += blockDim.x) {
+        const int k = it / NQF, qt = it - (it / NQF) * NQF;
+        const int qt0 = (D == 2) ? qt : qt / N;
+        const int qt1 = (D == 2) ? 0 : qt % N;
         double acc = 0.0;
         for (int sub = 0; sub < S; ++sub) {
           const int b0 = sub & 1, b1 = (sub >> 1) & 1;
@@ -1012,8 +1048,26 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
             acc = fma(m, fw[j], acc);
           }
         }
-        Z[k * NP + q] += lw * acc;
+        G[it] = acc;
       }
+    }
+    __syncthreads();
+    // lift: Z += lift[side] (x) G
+    if (act) {
+      int qi[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) qi[a] = digit<D, N>(q, a);
+      const int a = f >> 1, side = f & 1;
+      int qt0, qt1 = 0;
+      if (D == 2) qt0 = qi[1 - a];
+      else {
+        qt0 = (a == 0) ? qi[1] : qi[0];
+        qt1 = (a == 2) ? qi[1] : qi[2];
+      }
+      const int qt = (D == 2) ? qt0 : qt0 * N + qt1;
+      const double lw = T.lift[side][qi[a]];
+#pragma unroll
+      for (int k = 0; k < KOUT; ++k) Z[k * NP + q] += lw * CH[k * NQF + qt];
     }
   }
   double wq = 1.0, det = 1.0;
@@ -1041,10 +1095,17 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
     if (act) {
       const double inv = 1.0 / (wq * det);
       for (int k = 0; k < KOUT; ++k) {
-        double* o = P.out.p + e * P.out.estride + k * P.out.cstride + q;
-        const double v = out_pre[k] + P.coef * (Z[k * NP + q] * inv);
-        *o = v;
-        Tm[k * NP + q] = v;  // the final V of this coarse element
+        if (side_mode) {
+          // the contribution alone (coarse_merge adds it to the main output)
+          const double v = P.coef * (Z[k * NP + q] * inv);
+          P.side_out[blockIdx.x * P.side_stride + k * NP + q] = v;
+          Tm[k * NP + q] = v;
+        } else {
+          double* o = P.out.p + e * P.out.estride + k * P.out.cstride + q;
+          const double v = out_pre[k] + P.coef * (Z[k * NP + q] * inv);
+          *o = v;
+          Tm[k * NP + q] = v;  // the final V of this coarse element
+        }
       }
     }
     if (P.tr_out != nullptr) {
@@ -1066,7 +1127,8 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
         double t = 0.0;
         for (int p = 0; p < N; ++p)
           t = fma(T.lift[side][p], Tm[comp * NP + nbr_pencil_node<D, N>(ax, p, j)], t);
-        P.tr_out[e * TSL + it] = t;
+        if (side_mode) P.side_tr[(long long)blockIdx.x * TSL + it] = t;  // traces are linear
+        else P.tr_out[e * TSL + it] = t;
       }
     }
     return;
@@ -1106,6 +1168,15 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
     }
   }
   __syncthreads();
+  if (side_mode) {
+    // H2 of the Helmholtz pair: the contribution alone; coarse_merge adds it
+    // and computes this element's fused dots
+    if (act)
+#pragma unroll
+      for (int k = 0; k < KOUT; ++k)
+        P.side_out[blockIdx.x * P.side_stride + k * NP + q] = __dmul_rn(P.coef, res[k * NP + q]);
+    return;
+  }
   double yv = 0.0;  // final value (KOUT == 1 when the Gram-Schmidt dots are fused)
   if (act) {
     double* out = P.out.p + e * P.out.estride + q;
@@ -1121,44 +1192,41 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
       yv = y;
     }
   }
-  if constexpr (OPK == OP_DIVHV) {
-    // fused Gram-Schmidt dots of this (complete) coarse element, row
-    // gs_row0 + CTA of gs_part (see gs_dots in dg_wkernel.cuh)
-    if (P.gs_part != nullptr) {
-      // columns as gs_dots (dg_wkernel.cuh): single (V_i.y, y.y) or dual
-      // pairs (item.y, item.u) over the items V_i, y, u (u = the base)
-      const bool dual = P.gs_dual != 0;
-      const int nv = P.gs_nv;
-      const int nvt = dual ? 2 * (nv + 2) : nv + 1;
-      const double uq = (act && dual) ? P.base(e, 0, q) : 0.0;
-      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-      constexpr int NW = L::CTHREADS / 32;
-      double* wr = red + 64 + L::C_GS;  // NW x 32 warp sums
-      for (int c0 = 0; c0 < nvt; c0 += 32) {
-        const int cnt = min(32, nvt - c0);
-        for (int cc = 0; cc < cnt; ++cc) {
-          const int col = c0 + cc;
-          const int item = dual ? col >> 1 : col;
-          const double other = (dual && (col & 1)) ? uq : yv;
-          double s = 0.0;
-          if (act) {
-            const double v = item < nv ? P.gsV[(long long)item * P.gs_vs + e * NP + q]
-                                       : (item == nv ? yv : uq);
-            s = v * other;
-          }
-          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-          if (lane == 0) wr[wid * 32 + cc] = s;
-        }
-        __syncthreads();
-        if (threadIdx.x < cnt) {
-          double s = 0.0;
-          for (int w = 0; w < NW; ++w) s += wr[w * 32 + threadIdx.x];
-          P.gs_part[((long long)P.gs_row0 + blockIdx.x) * nvt + c0 + threadIdx.x] = s;
-        }
-        __syncthreads();
-      }
+  if constexpr (OPK == OP_DIVHV) coarse_dots<D, N, OPK>(P, e, q, act, yv, red + 64 + L::C_GS);
+}
+
+
+// adds the side-mode contributions of coarse_kernel to the element kernel's
+// output (one CTA per coarse element): H1 -- V at the Gauss points and its
+// face traces; H2 -- y, then the element's fused dots
+template <int D, int N, int OPK>
+__global__ void __launch_bounds__(Layout<D, N, OPK>::CTHREADS)
+coarse_merge(const __grid_constant__ KParams<N> P, const int* __restrict__ clist) {
+  using L = Layout<D, N, OPK>;
+  constexpr int NP = L::NP, KOUT = L::KOUT, NQF = L::NQF;
+  __shared__ double wr[(L::CTHREADS / 32) * 32];
+  const long long e = clist[blockIdx.x];
+  const int q = threadIdx.x;
+  const bool act = q < NP;
+  const double* sv = P.side_out + blockIdx.x * P.side_stride;
+  double yv = 0.0;
+  if (act) {
+#pragma unroll
+    for (int k = 0; k < KOUT; ++k) {
+      double* o = P.out.p + e * P.out.estride + k * P.out.cstride + q;
+      const double y = *o + sv[k * NP + q];
+      *o = y;
+      yv = y;
     }
   }
+  if constexpr (OPK == OP_GRAD) {
+    if (P.tr_out != nullptr) {
+      constexpr int TSL = tr_slots<D>() * NQF;
+      for (int it = threadIdx.x; it < TSL; it += blockDim.x)
+        P.tr_out[e * TSL + it] += P.side_tr[(long long)blockIdx.x * TSL + it];
+    }
+  }
+  if constexpr (OPK == OP_DIVHV) coarse_dots<D, N, OPK>(P, e, q, act, yv, wr);
 }
 
 }  // namespace dg
