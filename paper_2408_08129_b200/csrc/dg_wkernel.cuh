@@ -23,6 +23,36 @@
 
 namespace dg {
 
+// per-element tile layout.  3D point (i, j, k) (z fastest; z-column
+// c = i*N + j): columns at a padded stride n+1, except for n = 4, where 16
+// lanes per element meet the 16 double-wide smem banks exactly: the
+// swizzle 16 k + 4 ((i + j) & 3) + ((j + k) & 3) maps every axis-aligned
+// plane (a column access, an x- or a y-pencil access across the element's
+// 16 lanes) onto 16 distinct banks, without padding.
+template <int D, int N>
+__host__ __device__ constexpr int tile_size() {
+  return (D == 3 && N == 4) ? 64 : ipow(N, D - 1) * (N + 1);
+}
+template <int D, int N>
+__device__ __forceinline__ int toff3(int i, int j, int k) {
+  if constexpr (D == 3 && N == 4) return 16 * k + 4 * ((i + j) & 3) + ((j + k) & 3);
+  else return (i * N + j) * (N + 1) + k;
+}
+template <int D, int N>
+__device__ __forceinline__ int coff(int c, int k) {  // own z-column c, point k
+  if constexpr (D == 3) return toff3<D, N>(c / N, c % N, k);
+  else return c * (N + 1) + k;
+}
+template <int D, int N>
+__device__ __forceinline__ int xoff(int c, int ii) {  // x-pencil of lane c, point ii
+  if constexpr (D == 3) return toff3<D, N>(ii, c / N, c % N);
+  else return ii * (N + 1) + c;
+}
+template <int N>
+__device__ __forceinline__ int yoff(int c, int jj) {  // 3D y-pencil of lane c, point jj
+  return toff3<3, N>(c / N, jj, c % N);
+}
+
 template <int D, int N, int OPK>
 struct WLayout {
   static constexpr int NP = ipow(N, D);
@@ -31,8 +61,7 @@ struct WLayout {
   static constexpr int KIN = OpDims<D, OPK>::KIN;
   static constexpr int KOUT = OpDims<D, OPK>::KOUT;
   static constexpr int KW = (OPK == OP_GRAD) ? 1 : KOUT;
-  static constexpr int CS = N + 1;             // padded column stride
-  static constexpr int TSZ = NC * CS;          // one tensor
+  static constexpr int TSZ = tile_size<D, N>();  // one tensor (tile layout: coff)
   static constexpr int KX0 = KIN > KOUT ? KIN : KOUT;
   static constexpr int KX1 = (D - 1) * KW;
   static constexpr int KX = KX0 > KX1 ? KX0 : KX1;
@@ -77,16 +106,6 @@ struct WLayout {
   static constexpr int MINB = (OPK == OP_GRAD) ? DG_WMINB_GRAD : DG_WMINB_DIVHV;
 };
 
-// pencil helpers on the per-element tile (3D: (i, j) column index c = i*N + j)
-template <int D, int N>
-__device__ __forceinline__ int xoff(int c, int ii) {  // x-pencil of lane c, point ii
-  if constexpr (D == 3) return (ii * N + c / N) * (N + 1) + c % N;
-  else return ii * (N + 1) + c;
-}
-template <int N>
-__device__ __forceinline__ int yoff(int c, int jj) {  // 3D y-pencil of lane c, point jj
-  return ((c / N) * N + jj) * (N + 1) + c % N;
-}
 
 __device__ __forceinline__ void cp_async8(void* smem_ptr, const void* gptr) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem_ptr);
@@ -446,7 +465,7 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
 #pragma unroll
   for (int cp = 0; cp < KIN; ++cp)
 #pragma unroll
-    for (int k = 0; k < N; ++k) X[cp * TSZ + c * (N + 1) + k] = q[cp][k];
+    for (int k = 0; k < N; ++k) X[cp * TSZ + coff<D, N>(c, k)] = q[cp][k];
   __syncwarp();
   if constexpr (D == 3) {
     if (!iq) {
@@ -649,7 +668,7 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
         double t = 0.0;
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-          const int off = (AX == D - 1) ? c * (N + 1) + k
+          const int off = (AX == D - 1) ? coff<D, N>(c, k)
                         : (AX == 0)     ? xoff<D, N>(c, k)
                                         : yoff<N>(c, k);
           t = fma(TC.lift[side][k], X[cp * TSZ + off], t);
@@ -756,11 +775,11 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
       double F[D][KOUT];
       if constexpr (OPK == OP_DIVHV) {
         // own column of the Gauss-point tile (read before G overwrites it)
-        const double h = X[D * TSZ + c * (N + 1) + kz];
+        const double h = X[D * TSZ + coff<D, N>(c, kz)];
 #pragma unroll
-        for (int a = 0; a < D; ++a) F[a][0] = h * X[a * TSZ + c * (N + 1) + kz];
+        for (int a = 0; a < D; ++a) F[a][0] = h * X[a * TSZ + coff<D, N>(c, kz)];
       } else {
-        const double p = X[c * (N + 1) + kz];
+        const double p = X[coff<D, N>(c, kz)];
 #pragma unroll
         for (int a = 0; a < D; ++a)
 #pragma unroll
@@ -784,9 +803,9 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
           if (bx == D - 1) {
             Gz[k][kz] = acc;
           } else if (OPK == OP_GRAD) {
-            if (k == bx) X[(bx * KW) * TSZ + c * (N + 1) + kz] = acc;
+            if (k == bx) X[(bx * KW) * TSZ + coff<D, N>(c, kz)] = acc;
           } else {
-            X[(bx * KW + k) * TSZ + c * (N + 1) + kz] = acc;
+            X[(bx * KW + k) * TSZ + coff<D, N>(c, kz)] = acc;
           }
         }
       }
@@ -830,13 +849,13 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
 #pragma unroll
   for (int kz = 0; kz < N; ++kz) {
     if constexpr (OPK == OP_GRAD) {
-      Zc[0][kz] += X[0 * TSZ + c * (N + 1) + kz];
-      if constexpr (D == 3) Zc[1][kz] += X[1 * TSZ + c * (N + 1) + kz];
+      Zc[0][kz] += X[0 * TSZ + coff<D, N>(c, kz)];
+      if constexpr (D == 3) Zc[1][kz] += X[1 * TSZ + coff<D, N>(c, kz)];
     } else {
 #pragma unroll
       for (int k = 0; k < KOUT; ++k) {
-        Zc[k][kz] += X[(0 * KW + k) * TSZ + c * (N + 1) + kz];
-        if constexpr (D == 3) Zc[k][kz] += X[(1 * KW + k) * TSZ + c * (N + 1) + kz];
+        Zc[k][kz] += X[(0 * KW + k) * TSZ + coff<D, N>(c, kz)];
+        if constexpr (D == 3) Zc[k][kz] += X[(1 * KW + k) * TSZ + coff<D, N>(c, kz)];
       }
     }
   }
@@ -881,7 +900,7 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
 #pragma unroll
       for (int a = 0; a < D - 1; ++a)
 #pragma unroll
-        for (int kz = 0; kz < N; ++kz) X[a * TSZ + c * (N + 1) + kz] = Vg[a][kz];
+        for (int kz = 0; kz < N; ++kz) X[a * TSZ + coff<D, N>(c, kz)] = Vg[a][kz];
       __syncwarp();
 #pragma unroll
       for (int a = 0; a < D - 1; ++a)
@@ -915,7 +934,7 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
 #pragma unroll
   for (int k = 0; k < KOUT; ++k)
 #pragma unroll
-    for (int kz = 0; kz < N; ++kz) X[k * TSZ + c * (N + 1) + kz] = Zc[k][kz];
+    for (int kz = 0; kz < N; ++kz) X[k * TSZ + coff<D, N>(c, kz)] = Zc[k][kz];
   __syncwarp();
   if constexpr (D == 3) {
 #pragma unroll

@@ -73,8 +73,7 @@ struct XLayout {
   static constexpr int NP = ipow(N, D);
   static constexpr int NC = ipow(N, D - 1);  // lanes per element
   static constexpr int EPW = 32 / NC;          // elements per warp
-  static constexpr int CS = N + 1;             // padded column stride
-  static constexpr int TSZ = NC * CS;          // one tensor
+  static constexpr int TSZ = tile_size<D, N>();  // one tensor (tile layout: coff)
   static constexpr int WPB = 2;                // warps per CTA
   static constexpr int THREADS = 32 * WPB;
   static constexpr int TABD = (int)(sizeof(Tab<N>) / sizeof(double));
@@ -103,7 +102,7 @@ __global__ void __launch_bounds__(XLayout<D, N>::THREADS, XLayout<D, N>::MINB)
 xelem_kernel(const __grid_constant__ KParams<N> P) {
   using XL = XLayout<D, N>;
   constexpr int NC = XL::NC, EPW = XL::EPW, V = XL::V, TSZ = XL::TSZ, NF = 2 * D;
-  constexpr int NP = XL::NP, CS = XL::CS;
+  constexpr int NP = XL::NP;
   extern __shared__ double smem[];
   for (int i = threadIdx.x; i < XL::TABD; i += blockDim.x) cp_async8(smem + i, P.tab_g + i);
   const Tab<N>& TS = *reinterpret_cast<const Tab<N>*>(smem);
@@ -168,7 +167,7 @@ xelem_kernel(const __grid_constant__ KParams<N> P) {
     double o[N];
     mat_apply<N, false>(TC.B, q[r], o);
 #pragma unroll
-    for (int k = 0; k < N; ++k) X[r * TSZ + c * CS + k] = o[k];
+    for (int k = 0; k < N; ++k) X[r * TSZ + coff<D, N>(c, k)] = o[k];
   }
   __syncwarp();
   if constexpr (D == 3) {
@@ -243,7 +242,7 @@ XROLL
       double t = 0.0;
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        const int off = (AX == D - 1) ? c * CS + k : (AX == 0) ? xoff<D, N>(c, k) : yoff<N>(c, k);
+        const int off = (AX == D - 1) ? coff<D, N>(c, k) : (AX == 0) ? xoff<D, N>(c, k) : yoff<N>(c, k);
         t = fma(TC.lift[side][k], X[r * TSZ + off], t);
       }
       TO[r] = t;
@@ -344,7 +343,7 @@ XROLL
       else wq *= TC.qw[c];
       double Uq[V];
 #pragma unroll
-      for (int r = 0; r < V; ++r) Uq[r] = X[r * TSZ + c * CS + kz];
+      for (int r = 0; r < V; ++r) Uq[r] = X[r * TSZ + coff<D, N>(c, kz)];
       double F[D][V];
       if (FULL) {
         double Ff[V][D];
@@ -387,8 +386,8 @@ XROLL
           }
           acc *= wq;
           if (bx == D - 1) Gz[r][kz] = acc;
-          else if (bx == 0) X[r * TSZ + c * CS + kz] = acc;  // own column, in place
-          else GY[r * TSZ + c * CS + kz] = acc;
+          else if (bx == 0) X[r * TSZ + coff<D, N>(c, kz)] = acc;  // own column, in place
+          else GY[r * TSZ + coff<D, N>(c, kz)] = acc;
         }
       }
     }
@@ -428,8 +427,8 @@ XROLL
   for (int r = 0; r < V; ++r)
 #pragma unroll
     for (int kz = 0; kz < N; ++kz) {
-      Zc[r][kz] += X[r * TSZ + c * CS + kz];
-      if constexpr (D == 3) Zc[r][kz] += GY[r * TSZ + c * CS + kz];
+      Zc[r][kz] += X[r * TSZ + coff<D, N>(c, kz)];
+      if constexpr (D == 3) Zc[r][kz] += GY[r * TSZ + coff<D, N>(c, kz)];
     }
 
   // mass rate: per-warp partial of the density dual (imex.py:148; the dual's
@@ -482,7 +481,7 @@ XROLL
 #pragma unroll
   for (int r = 0; r < V; ++r)
 #pragma unroll
-    for (int kz = 0; kz < N; ++kz) X[r * TSZ + c * CS + kz] = Zc[r][kz];
+    for (int kz = 0; kz < N; ++kz) X[r * TSZ + coff<D, N>(c, kz)] = Zc[r][kz];
   __syncwarp();
   if constexpr (D == 3) {
 XROLL
