@@ -74,7 +74,10 @@ struct XLayout {
   static constexpr int NC = ipow(N, D - 1);  // lanes per element
   static constexpr int EPW = 32 / NC;          // elements per warp
   static constexpr int TSZ = tile_size<D, N>();  // one tensor (tile layout: coff)
-  static constexpr int WPB = 2;                // warps per CTA
+#ifndef DG_XWPB
+#define DG_XWPB 1
+#endif
+  static constexpr int WPB = DG_XWPB;          // warps per CTA
   static constexpr int THREADS = 32 * WPB;
   static constexpr int TABD = (int)(sizeof(Tab<N>) / sizeof(double));
   static constexpr int NSLOT = EPW + ((32 % NC) ? 1 : 0);
@@ -90,7 +93,7 @@ struct XLayout {
   static constexpr size_t SMEM = (size_t)(TABD + WPB * NSLOT * SLOT) * sizeof(double);
   static constexpr bool OK = (NC <= 32) && (SMEM <= 200 * 1024);
 #ifndef DG_XMINB
-#define DG_XMINB 5
+#define DG_XMINB 11
 #endif
   static constexpr int MINB = DG_XMINB;
 };
