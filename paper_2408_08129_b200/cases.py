@@ -260,6 +260,30 @@ def baseline_case(name, root_scale=1.0, with_state=True):
                              with_state, 0.5,
                              "3D Gaussian hill 60x60x20 km, 120x120x20 root, refined z<6 km "
                              "and z<2 km (3 levels), r=3")
+    if name.startswith("cfg5"):
+        # "cfg5_r<degree>": the operator microbenchmark (BASELINE configs[4],
+        # SURVEY.md §8d): periodic (10 km)^3 box, a seeded 7% of the roots
+        # refined once (about 30% of the interior face rows hanging), state =
+        # hydrostatic background + seeded smooth 1e-3 perturbations; root
+        # count chosen for 1e8 total DoF x root_scale (n_el = 1.49 n_root)
+        r = int(name.split("_r")[1]) if "_r" in name else 3
+        n = r + 1
+        n_el = 1.0e8 * root_scale / (5 * n ** 3)
+        nr = max(2, int(round((n_el / 1.49) ** (1.0 / 3.0))))
+        ext = (10.0e3, 10.0e3, 10.0e3)
+        mesh = build_uniform_mesh(ext, (nr, nr, nr), periodic=(True, True, True))
+        pick = np.random.default_rng(5).random(mesh.n_leaves) < 0.07
+        mesh = refine_region(mesh, lambda i, l, o, lo, hi: pick[i], 1, vectorized=True)
+        geom = build_geometry(mesh, r)
+        U0 = None
+        if with_state:
+            bg = project_initial_data(
+                geom, hydrostatic_initial_state(HillCaseConfig(domain=ext))).data
+            U0 = perturbed_state(bg, geom.node_coords, ext, 41)
+        geom._memo.pop("nc", None)
+        return BaselineCase(name, mesh, geom, model, [], None, U0, 0.3, dict(),
+                            f"operator microbenchmark: periodic (10 km)^3, {nr}^3 roots, 7% "
+                            f"refined once, r={r}")
     raise ConfigurationError(f"unknown baseline case {name!r}")
 
 

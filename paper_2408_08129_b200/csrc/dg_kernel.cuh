@@ -55,7 +55,7 @@ struct Layout {
   static constexpr int EPB_S = (12288 - TABD - 64) / ELEM > 1 ? (12288 - TABD - 64) / ELEM : 1;
   static constexpr int EPB = EPB_T < EPB_S ? EPB_T : EPB_S;
   static constexpr int THREADS = ((EPB * NP + 31) / 32) * 32;
-  static constexpr int SLOTS = (THREADS + NP - 1) / NP;
+  static constexpr int SLOTS = EPB;  // padding threads shadow slot 0 (elem_kernel)
   static constexpr size_t SMEM = (size_t)(TABD + 64 + SLOTS * ELEM) * sizeof(double);
   static constexpr int REGCAP = (OPK == OP_ADV) ? 128 : 96;
   static constexpr int MINB0 = 65536 / (THREADS * REGCAP);
@@ -542,9 +542,13 @@ elem_kernel(const __grid_constant__ KParams<N> P) {
   const int tid = threadIdx.x;
   const long long e0 = (long long)blockIdx.x * L::EPB;
   const int nv = (int)min((long long)L::EPB, (long long)mesh.n_el - e0);
-  const int el = tid / NP;
-  const int q = tid - el * NP;
-  const bool act = el < nv;
+  const int el0 = tid / NP;
+  const bool act = el0 < nv;
+  // padding threads (EPB * NP not a multiple of 32) shadow slot 0: their
+  // per-point writes repeat the owner's identical values inside the same
+  // barrier phase, and every accumulation / store is guarded by act
+  const int el = el0 < L::EPB ? el0 : 0;
+  const int q = el0 < L::EPB ? tid - el0 * NP : (tid - L::EPB * NP) % NP;
   double* A = base + el * E + L::OFF_A;
   double* Q = base + el * E + L::OFF_Q;
   double* Z = base + el * E + L::OFF_Z;
@@ -726,7 +730,7 @@ elem_kernel(const __grid_constant__ KParams<N> P) {
       if ((tid & 31) == 0) red[tid >> 5] = v;
     }
   }
-  if (P.mode == OUT_MINV) {
+  if (P.mode == OUT_MINV && act) {
     const double inv = 1.0 / (wq * det);
 #pragma unroll
     for (int k = 0; k < KOUT; ++k) Z[k * NP + q] *= inv;

@@ -53,16 +53,31 @@ def main():
     lib.dg_frozen_coefficients(h, as_ptr(U), as_ptr(hh), as_ptr(K))
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
         peak = float(json.load(f)["hbm_gbs"])
+    # fp64 FMA peak measured on this box (tools/dfma_peak), else the spec
+    # figure at the max clock (SURVEY.md §8d placeholder)
+    fp64 = float(os.environ.get("DG_FP64_TFLOPS", "37.2"))
     N = n_el * nn
+    # SURVEY.md §8d models: algorithmic bytes and sum-factorised flops
+    n, V = c.geometry.basis.degree + 1, d + 2
+    top = c.mesh.topology
+    n_conf = sum(len(b.left) for b in top.conforming)
+    n_hrow = sum(len(b.coarse) for b in top.hanging)
+    n_bdry = top.n_boundary_faces()
+    Pv, Pf = 2.0 * n ** (d + 1), 2.0 * n ** d
+    Sf = 2 * n_conf + n_hrow + (d - 1) * n_hrow + n_bdry
+    nnz = d if not c.geometry.terrain else (3 if d == 2 else 5)
+    f_exp = V * (3 * d * n_el * Pv + 2 * Pf * Sf)
+    f_helm = n_el * (3 * d + nnz) * Pv + 2 * (d + 1) * Pf * Sf
+    b_exp = 8.0 * N * V * (3 if c.sponge is not None else 2)
     ops = {
         "explicit": (lambda: lib.dg_explicit_residual(h, as_ptr(U), as_ptr(R), None),
-                     N * (d + 2), 8.0 * N * ((d + 2) * 3)),
+                     N * (d + 2), b_exp, f_exp),
         "helmholtz": (lambda: lib.dg_helmholtz_apply(h, 0.3, as_ptr(hh), as_ptr(x), as_ptr(y)),
-                      N, 8.0 * N * (3 + 2 * d + 1)),
+                      N, 8.0 * N * (3 + 2 * d), f_helm),
         "grad": (lambda: lib.dg_gradient_scalar(h, as_ptr(x), 1, as_ptr(V)),
-                 N, 8.0 * N * (1 + d)),
+                 N, 8.0 * N * (1 + d), 0.0),
         "divhv": (lambda: lib.dg_divergence_hv(h, as_ptr(V), V.stride(0), as_ptr(hh), 1,
-                                               as_ptr(dv)), N, 8.0 * N * (d + 2)),
+                                               as_ptr(dv)), N, 8.0 * N * (d + 2), 0.0),
     }
     rhs = torch.empty_like(x)
     lib.dg_helmholtz_apply(h, 0.3, as_ptr(hh), as_ptr(x), as_ptr(rhs))
@@ -74,10 +89,10 @@ def main():
         st = L.KrylovStatsC()
         return lib.dg_gmres_helmholtz(h, 0.3, as_ptr(hh), as_ptr(rhs), as_ptr(x0), 1e-8, 30, 1000,
                                       C.byref(st), None, 0)
-    ops["gmres"] = (gm, N, 0.0)
+    ops["gmres"] = (gm, N, 0.0, 0.0)
     s = torch.cuda.current_stream()
     for name in a.ops.split(","):
-        fn, dofs, byts = ops[name]
+        fn, dofs, byts, flops = ops[name]
         for _ in range(3):
             L.check(fn())
         torch.cuda.synchronize()
@@ -89,9 +104,15 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.reps
         gbs = byts / (ms * 1e-3) / 1e9
+        tf = flops / (ms * 1e-3) / 1e12
+        # roofline: T_roof = max(B / BW, F / P_fp64)
+        t_roof = max(byts / (peak * 1e9), flops / (fp64 * 1e12)) * 1e3
         print(json.dumps({"op": name, "case": a.case, "n_el": n_el, "degree": c.geometry.basis.degree,
-                          "ms": ms, "dofs_per_s": dofs / (ms * 1e-3), "GB_s": gbs,
-                          "frac_hbm": gbs / peak, "launch": ctx.launch_info()}), flush=True)
+                          "dof": dofs, "ms": ms, "dofs_per_s": dofs / (ms * 1e-3), "GB_s": gbs,
+                          "frac_hbm": gbs / peak, "TFLOP_s": tf, "frac_fp64": tf / fp64,
+                          "bound": "hbm" if byts / (peak * 1e9) >= flops / (fp64 * 1e12) else "fp64",
+                          "roofline_ms": t_roof, "frac_roofline": t_roof / ms if ms else None,
+                          "launch": ctx.launch_info()}), flush=True)
 
 
 if __name__ == "__main__":
