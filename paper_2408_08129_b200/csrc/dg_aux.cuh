@@ -149,7 +149,8 @@ integrate_kernel(const __grid_constant__ AuxParams<N> P) {
 
 // nodes -> Gauss points for ncomp components (frozen h of the Helmholtz pair,
 // evaluated once per pressure fixed-point iterate)
-template <int D, int N>
+// KC: components per pass round (1 for the frozen h: no idle comps)
+template <int D, int N, int KC>
 __global__ void __launch_bounds__(AuxLayout<D, N>::THREADS)
 interp_kernel(const __grid_constant__ AuxParams<N> P) {
   using L = AuxLayout<D, N>;
@@ -167,14 +168,14 @@ interp_kernel(const __grid_constant__ AuxParams<N> P) {
   const long long es = valid ? e : 0;
   double* X = smem + L::TABD + 64 + el * 2 * L::KMAX * NP;
   double* Y = X + L::KMAX * NP;
-  for (int c0 = 0; c0 < P.ncomp; c0 += L::KMAX) {
-    const int kc = min(L::KMAX, P.ncomp - c0);
-    for (int c = 0; c < L::KMAX; ++c) X[c * NP + q] = c < kc ? P.in(es, c0 + c, q) : 0.0;
+  for (int c0 = 0; c0 < P.ncomp; c0 += KC) {
+    const int kc = min(KC, P.ncomp - c0);
+    for (int c = 0; c < KC; ++c) X[c * NP + q] = c < kc ? P.in(es, c0 + c, q) : 0.0;
     __syncthreads();
     double* s = X;
     double* d = Y;
     for (int a = D - 1; a >= 0; --a) {
-      pass1d<D, N, L::KMAX, false>(&T.B[0][0], s, d, q, a, NP);
+      pass1d<D, N, KC, false>(&T.B[0][0], s, d, q, a, NP);
       __syncthreads();
       double* t = s; s = d; d = t;
     }
@@ -349,8 +350,15 @@ cudaError_t launch_aux(int which, const AuxParams<N>& P, cudaStream_t st, int* g
     cudaFuncSetAttribute(integrate_kernel<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
     integrate_kernel<D, N><<<grid, L::THREADS, L::SMEM, st>>>(P);
   } else if (which == 2) {
-    cudaFuncSetAttribute(interp_kernel<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
-    interp_kernel<D, N><<<grid, L::THREADS, L::SMEM, st>>>(P);
+    if (P.ncomp == 1) {
+      cudaFuncSetAttribute(interp_kernel<D, N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)L::SMEM);
+      interp_kernel<D, N, 1><<<grid, L::THREADS, L::SMEM, st>>>(P);
+    } else {
+      cudaFuncSetAttribute(interp_kernel<D, N, L::KMAX>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
+      interp_kernel<D, N, L::KMAX><<<grid, L::THREADS, L::SMEM, st>>>(P);
+    }
   } else if (which == 3) {
     cudaFuncSetAttribute(inner_kernel<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
     inner_kernel<D, N><<<grid, L::THREADS, L::SMEM, st>>>(P);
