@@ -298,7 +298,7 @@ __device__ __forceinline__ void num_flux(const double* TL, const double* TR, con
 #endif
     // DG_ADV_RCP: one reciprocal per side instead of d + 1 divisions (a
     // rounding-level change, inside the reference's own 1-ulp sensitivity)
-    const double irL = DG_ADV_RCP ? 1.0 / rL : 0.0, irR = DG_ADV_RCP ? 1.0 / rR : 0.0;
+    const double irL = DG_ADV_RCP ? __drcp_rn(rL) : 0.0, irR = DG_ADV_RCP ? __drcp_rn(rR) : 0.0;
     const double uL = DG_ADV_RCP ? mnL * irL : mnL / rL, uR = DG_ADV_RCP ? mnR * irR : mnR / rR;
     const double lam = fmax(fabs(uL), fabs(uR));
     double kL = 0.0, kR = 0.0;

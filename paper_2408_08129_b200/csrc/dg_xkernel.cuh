@@ -358,7 +358,7 @@ XROLL
       } else {
         // split advective flux (dgops.py:234-254)
         const double rho = Uq[0];
-        const double irho = DG_ADV_RCP ? 1.0 / rho : 0.0;
+        const double irho = DG_ADV_RCP ? __drcp_rn(rho) : 0.0;
         double u[D];
         double k = 0.0;
 #pragma unroll
@@ -525,7 +525,7 @@ XROLL
     for (int r = 0; r < V; ++r) R[r] = -res[r][ii];
     const double rho = uin[0][ii];
     R[D] += -md.gravity * rho;
-    R[D + 1] += -md.kinetic_factor * md.gravity * rho * (uin[D][ii] / rho);
+    R[D + 1] += -md.kinetic_factor * md.gravity * rho * (uin[D][ii] * __drcp_rn(rho));
     if (spg) {
 #pragma unroll
       for (int r = 1; r < V; ++r) R[r] -= sgm[ii] * (uin[r][ii] - bgv[r][ii]);
