@@ -215,3 +215,40 @@ def test_partitioned_contexts_loopback(name, P):
         assert rel(vv[:pl.n_owned].cpu().numpy(), Vg[a:b].cpu().numpy()) <= 1e-14
         assert rel(dd[:pl.n_owned].cpu().numpy(), Dg[a:b].cpu().numpy()) <= 1e-14
     del y_ref
+
+
+@pytest.mark.parametrize("degree", [5, 6])
+def test_high_degree_periodic_vs_oracle(degree):
+    """n^(d-1) > 32 in 3D (r = 5, 6: the cfg5 sweep's top degrees) runs the
+    CTA-per-element kernels (incl. padding threads shadowing slot 0): the
+    explicit residual and the Helmholtz action against the CPU oracle on a
+    periodic box with hanging faces."""
+    from oracle import dg_oracle as O
+    from paper_2408_08129_b200 import cases
+    from paper_2408_08129_b200.field import project_initial_data
+    from paper_2408_08129_b200.geometry import build_geometry
+    from paper_2408_08129_b200.mesh import build_uniform_mesh, refine_region
+    from casebuild import Case
+    ext = (10.0e3, 10.0e3, 10.0e3)
+    m = build_uniform_mesh(ext, (2, 2, 2), periodic=(True, True, True))
+    m = refine_region(m, lambda lf: lf.index == 3, 1)
+    geom = build_geometry(m, degree)
+    bg = project_initial_data(
+        geom, cases.hydrostatic_initial_state(cases.HillCaseConfig(domain=ext))).data
+    U = cases.perturbed_state(bg, geom.node_coords, ext, 43)
+    c = Case(f"per3d_r{degree}", m, geom, [], None, U, 0.3)
+    ops, split = _split(c)
+    orc = O.Operators(geom, c.model, [], None)
+    R = split.explicit_residual(U)
+    Ro = orc.explicit_residual(U)
+    # per-variable gate as the golden cases (DESIGN.md §5): max(1e-12, 10 x
+    # the oracle's own sensitivity to a 1-ulp input perturbation)
+    U2 = U * (1.0 + 1e-16 * np.random.default_rng(1).standard_normal(U.shape))
+    sens = np.array(per_var_rel(orc.explicit_residual(U2), Ro))
+    errs = np.array(per_var_rel(R, Ro))
+    assert np.all(errs <= np.maximum(1e-12, 10.0 * sens)), (errs, sens)
+    h, _ = orc.frozen_coefficients(U)
+    x = cases.energy_like(U, 7)
+    from paper_2408_08129_b200.imex import build_helmholtz_action
+    y = build_helmholtz_action(split, c.a_dt, U)(x.ravel()).reshape(x.shape)
+    assert rel(y, orc.helmholtz_linear(c.a_dt, h, x)) <= 1e-12
