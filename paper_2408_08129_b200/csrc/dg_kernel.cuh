@@ -882,8 +882,7 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
   // the Helmholtz H1 output at this Gauss point (read-modify-written at the
   // end): issued first so the final update does not wait on it
   double out_pre[KOUT];
-  const bool side_mode = P.side_out != nullptr;
-  if (OPK == OP_GRAD && P.out_quad && act && !side_mode)
+  if (OPK == OP_GRAD && P.out_quad && act)
 #pragma unroll
     for (int k = 0; k < KOUT; ++k) out_pre[k] = P.out.p[e * P.out.estride + k * P.out.cstride + q];
   // (trace mode: the own traces come from the trace buffers, no input tile)
@@ -1099,17 +1098,10 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
     if (act) {
       const double inv = 1.0 / (wq * det);
       for (int k = 0; k < KOUT; ++k) {
-        if (side_mode) {
-          // the contribution alone (coarse_merge adds it to the main output)
-          const double v = P.coef * (Z[k * NP + q] * inv);
-          P.side_out[blockIdx.x * P.side_stride + k * NP + q] = v;
-          Tm[k * NP + q] = v;
-        } else {
-          double* o = P.out.p + e * P.out.estride + k * P.out.cstride + q;
-          const double v = out_pre[k] + P.coef * (Z[k * NP + q] * inv);
-          *o = v;
-          Tm[k * NP + q] = v;  // the final V of this coarse element
-        }
+        double* o = P.out.p + e * P.out.estride + k * P.out.cstride + q;
+        const double v = out_pre[k] + P.coef * (Z[k * NP + q] * inv);
+        *o = v;
+        Tm[k * NP + q] = v;  // the final V of this coarse element
       }
     }
     if (P.tr_out != nullptr) {
@@ -1131,8 +1123,7 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
         double t = 0.0;
         for (int p = 0; p < N; ++p)
           t = fma(T.lift[side][p], Tm[comp * NP + nbr_pencil_node<D, N>(ax, p, j)], t);
-        if (side_mode) P.side_tr[(long long)blockIdx.x * TSL + it] = t;  // traces are linear
-        else P.tr_out[e * TSL + it] = t;
+        P.tr_out[e * TSL + it] = t;
       }
     }
     return;
@@ -1172,15 +1163,6 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
     }
   }
   __syncthreads();
-  if (side_mode) {
-    // H2 of the Helmholtz pair: the contribution alone; coarse_merge adds it
-    // and computes this element's fused dots
-    if (act)
-#pragma unroll
-      for (int k = 0; k < KOUT; ++k)
-        P.side_out[blockIdx.x * P.side_stride + k * NP + q] = __dmul_rn(P.coef, res[k * NP + q]);
-    return;
-  }
   double yv = 0.0;  // final value (KOUT == 1 when the Gram-Schmidt dots are fused)
   if (act) {
     double* out = P.out.p + e * P.out.estride + q;
@@ -1199,38 +1181,5 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
   if constexpr (OPK == OP_DIVHV) coarse_dots<D, N, OPK>(P, e, q, act, yv, red + 64 + L::C_GS);
 }
 
-
-// adds the side-mode contributions of coarse_kernel to the element kernel's
-// output (one CTA per coarse element): H1 -- V at the Gauss points and its
-// face traces; H2 -- y, then the element's fused dots
-template <int D, int N, int OPK>
-__global__ void __launch_bounds__(Layout<D, N, OPK>::CTHREADS)
-coarse_merge(const __grid_constant__ KParams<N> P, const int* __restrict__ clist) {
-  using L = Layout<D, N, OPK>;
-  constexpr int NP = L::NP, KOUT = L::KOUT, NQF = L::NQF;
-  __shared__ double wr[(L::CTHREADS / 32) * 32];
-  const long long e = clist[blockIdx.x];
-  const int q = threadIdx.x;
-  const bool act = q < NP;
-  const double* sv = P.side_out + blockIdx.x * P.side_stride;
-  double yv = 0.0;
-  if (act) {
-#pragma unroll
-    for (int k = 0; k < KOUT; ++k) {
-      double* o = P.out.p + e * P.out.estride + k * P.out.cstride + q;
-      const double y = *o + sv[k * NP + q];
-      *o = y;
-      yv = y;
-    }
-  }
-  if constexpr (OPK == OP_GRAD) {
-    if (P.tr_out != nullptr) {
-      constexpr int TSL = tr_slots<D>() * NQF;
-      for (int it = threadIdx.x; it < TSL; it += blockDim.x)
-        P.tr_out[e * TSL + it] += P.side_tr[(long long)blockIdx.x * TSL + it];
-    }
-  }
-  if constexpr (OPK == OP_DIVHV) coarse_dots<D, N, OPK>(P, e, q, act, yv, wr);
-}
 
 }  // namespace dg

@@ -31,11 +31,6 @@ struct OpArgs {
   long long gs_vs;
   int gs_nv, gs_dual;
   double* gs_part;
-  // concurrent coarse-side kernel (see KParams::side_out): null = in-stream
-  cudaStream_t side_st;
-  cudaEvent_t ev_fork, ev_join;
-  double* side_buf;
-  double* side_tr;
   const double* tabs;  // host pointer, Tab<N> layout
   const double* tabs_dev;  // the same tables in device memory
 };
@@ -83,9 +78,6 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
   P.gs_dual = a.gs_dual;
   P.gs_row0 = 0;
   P.tab_g = a.tabs_dev;
-  P.side_out = nullptr;
-  P.side_tr = nullptr;
-  P.side_stride = 0;
   std::memcpy(&P.tab, a.tabs, sizeof(Tab<N>));
   using WL = WLayout<D, N, OPK>;
   if constexpr (WL::OK) {
@@ -101,9 +93,6 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
         info->grid = wgrid;
       }
       if (wgrid == 0) return cudaSuccess;
-      // coarse side concurrently (Helmholtz pair, MINV output)
-      const bool side = a.side_st != nullptr && a.mesh.n_coarse > 0 && a.mode == OUT_MINV &&
-                        (OPK == OP_DIVHV || a.out_quad);
       static bool wconf = false;
       if (!wconf) {
         for (auto kfn : {welem_kernel<D, N, OPK, false>, welem_kernel<D, N, OPK, OPK == OP_DIVHV>}) {
@@ -119,41 +108,13 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
         if (e != cudaSuccess) return e;
         wconf = true;
       }
-      if (side) {
-        // fork: the coarse side writes its contributions to the side
-        // buffers on the high-priority side stream, launched first so its
-        // latency-bound CTAs interleave with the element kernel's
-        KParams<N> Q = P;
-        Q.side_out = a.side_buf;
-        Q.side_tr = a.side_tr;
-        Q.side_stride = (long long)L::KOUT * L::NP;
-        cudaError_t e = cudaEventRecord(a.ev_fork, st);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(a.side_st, a.ev_fork, 0);
-        if (e != cudaSuccess) return e;
-        coarse_kernel<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, a.side_st>>>(
-            Q, a.mesh.coarse_list, a.mesh.n_coarse, nullptr);
-        e = cudaGetLastError();
-        if (e == cudaSuccess) e = cudaEventRecord(a.ev_join, a.side_st);
-        if (e != cudaSuccess) return e;
-      }
       if (OPK == OP_DIVHV && a.in_quad)
         welem_kernel<D, N, OPK, OPK == OP_DIVHV><<<wgrid, WL::THREADS, WL::SMEM, st>>>(P);
       else
         welem_kernel<D, N, OPK, false><<<wgrid, WL::THREADS, WL::SMEM, st>>>(P);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
-      if (side) {
-        // join, then add the contributions (+ the coarse elements' dots)
-        KParams<N> Q = P;
-        Q.side_out = a.side_buf;
-        Q.side_tr = a.side_tr;
-        Q.side_stride = (long long)L::KOUT * L::NP;
-        Q.gs_row0 = wgrid;
-        e = cudaStreamWaitEvent(st, a.ev_join, 0);
-        if (e != cudaSuccess) return e;
-        coarse_merge<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, 0, st>>>(Q, a.mesh.coarse_list);
-        e = cudaGetLastError();
-      } else if (a.mesh.n_coarse > 0) {
+      if (a.mesh.n_coarse > 0) {
         P.gs_row0 = wgrid;  // coarse elements' dot partials follow the CTA rows
         coarse_kernel<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
             P, a.mesh.coarse_list, a.mesh.n_coarse, nullptr);

@@ -70,13 +70,6 @@ struct KParams {
   long long gs_vs;
   int gs_nv, gs_row0, gs_dual;
   double* gs_part;
-  // side mode of coarse_kernel (Helmholtz pair): the coarse-side contribution
-  // of coarse element i is written to side_out[i * side_stride ...] (and its
-  // H1 trace contribution to side_tr) instead of being added to out, so the
-  // kernel can run concurrently with the element kernel; coarse_merge adds
-  double* side_out;
-  double* side_tr;
-  long long side_stride;
   const double* tab_g;  // the Tab<N> tables in global memory (coalesced smem staging)
   Tab<N> tab;
 };

@@ -97,11 +97,6 @@ struct dg_ctx {
   int bj_ncolors = 0;
   DevBuf<double> bj_inv, sz, su;
   DevBuf<double> trV, trH;  // trace mode: face traces of V (H1 output) and of h
-  // coarse-side kernels of the Helmholtz pair run concurrently with the
-  // element kernels on a high-priority side stream (side buffers + merge)
-  cudaStream_t side_st = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  DevBuf<double> side_buf, side_tr;
   int bj_valid = 0, bj_age = 1 << 30;
   long long bj_gen = 0;
   LaunchInfo last{};
@@ -146,13 +141,6 @@ OpArgs base_args(dg_ctx* c) {
   a.coef = 1.0;
   static const int dbg = getenv("DG_DEBUG_SKIP") ? atoi(getenv("DG_DEBUG_SKIP")) : 0;
   a.dbg = dbg;
-  if (c->side_st) {
-    a.side_st = c->side_st;
-    a.ev_fork = c->ev_fork;
-    a.ev_join = c->ev_join;
-    a.side_buf = c->side_buf.p;
-    a.side_tr = c->side_tr.p;
-  }
   return a;
 }
 
@@ -939,23 +927,6 @@ int dg_ctx_create(const dg_ctx_desc* d, dg_ctx** out) {
   if (e == cudaSuccess) e = c->redout.alloc(256);
   if (e == cudaSuccess) e = c->coef_dev.alloc(128);
   if (e == cudaSuccess) e = cudaMallocHost(&c->pinned, 256 * sizeof(double));
-  {
-    // concurrent coarse-side kernels, opt-in (DG_COARSE_SIDE=1): measured no
-    // gain -- the element kernels' register / smem footprint leaves no room
-    // for co-resident coarse CTAs, so the two grids still run one after the other
-    static const bool side_off =
-        !(getenv("DG_COARSE_SIDE") && std::string(getenv("DG_COARSE_SIDE")) == "1");
-    if (e == cudaSuccess && c->mesh.n_coarse > 0 && !side_off) {
-      int lo = 0, hi = 0;
-      e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
-      if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->side_st, cudaStreamNonBlocking, hi);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
-      const size_t tsl = (size_t)(2 * (d->dim - 1) + 2 * d->dim) * nqf;
-      if (e == cudaSuccess) e = c->side_buf.alloc((size_t)c->mesh.n_coarse * d->dim * np);
-      if (e == cudaSuccess) e = c->side_tr.alloc((size_t)c->mesh.n_coarse * tsl);
-    }
-  }
   if (e != cudaSuccess) {
     dg_ctx_destroy(c);
     return fail(DG_ERR_CUDA, std::string("context allocation: ") + cudaGetErrorString(e));
@@ -994,11 +965,6 @@ int dg_ctx_destroy(dg_ctx* c) {
   c->hang.release();
   c->kind.release();
   if (c->pinned) cudaFreeHost(c->pinned);
-  c->side_buf.release();
-  c->side_tr.release();
-  if (c->side_st) cudaStreamDestroy(c->side_st);
-  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
-  if (c->ev_join) cudaEventDestroy(c->ev_join);
   c->comm.shutdown();
   delete c;
   return DG_OK;

@@ -427,7 +427,7 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
 #ifndef DG_GS_PREFETCH
 #define DG_GS_PREFETCH 1
 #endif
-    if (DG_GS_PREFETCH == 1 && P.gs_part != nullptr && act) {
+    if (DG_GS_PREFETCH && P.gs_part != nullptr && act) {
       for (int i = c; i < P.gs_nv; i += NC) {
         const double* src = P.gsV + (long long)i * P.gs_vs + e * WL::NP;
         // 16-byte aligned span covering the slice (odd n^d: 8-byte aligned)
@@ -726,21 +726,6 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
   if constexpr (D == 3) {
     face(std::integral_constant<int, 2>{}, 0);
     face(std::integral_constant<int, 2>{}, 1);
-  }
-  if constexpr (OPK == OP_DIVHV) {
-    // (DG_GS_PREFETCH=2: the basis slices' L2 prefetch issued here, after
-    // the face phase, closer to their use in the epilogue)
-    if (DG_GS_PREFETCH == 2 && P.gs_part != nullptr && act) {
-      for (int i = c; i < P.gs_nv; i += NC) {
-        const double* src = P.gsV + (long long)i * P.gs_vs + e * WL::NP;
-        const unsigned long long a0 = reinterpret_cast<unsigned long long>(src) & ~15ULL;
-        const unsigned long long a1 =
-            (reinterpret_cast<unsigned long long>(src + WL::NP) + 15ULL) & ~15ULL;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a0),
-                     "r"((unsigned)(a1 - a0))
-                     : "memory");
-      }
-    }
   }
   // the epilogue's base values (the x-pencil nodes this lane stores) are
   // copied into the face-node area, now consumed, under the volume work
