@@ -270,9 +270,15 @@ def main():
     per_launch_ms = ms_c[k_dom] / max(cnt[k_dom], 1)
     per_launch_bytes = by_c[k_dom] / max(cnt[k_dom], 1)
     achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
-    breakdown = {classes[k]: {"ms": ms_c[k], "launches": int(cnt[k]),
-                              "GB_s": (by_c[k] / (ms_c[k] * 1e-3) / 1e9) if ms_c[k] else None}
-                 for k in range(6)}
+    # per class: algorithmic GB/s over the class's launches and its fraction
+    # of the HBM peak (explicit: the north-star explicit-operator figure;
+    # gradient + div_hv: the Helmholtz pair, div_hv incl. its fused dots)
+    breakdown = {}
+    for k in range(6):
+        gbs = (by_c[k] / (ms_c[k] * 1e-3) / 1e9) if ms_c[k] else None
+        breakdown[classes[k]] = {"ms": ms_c[k], "launches": int(cnt[k]), "GB_s": gbs,
+                                 "frac_hbm": (gbs / peak) if gbs else None,
+                                 "ms_per_launch": (ms_c[k] / cnt[k]) if cnt[k] else None}
 
     # e2e through the public API with host buffers (each rank: its local
     # state copied host->device, the step, the result copied back)
