@@ -63,7 +63,8 @@ struct MeshDev {
   const double* ff_p;       // (n_bface, nqf)
   const double* ff_h;       // (n_bface, nqf)
   int n_el;                 // owned elements processed by the kernels
-  const int* coarse_list;   // owned elements with >= 1 coarse hanging face
+  const int* coarse_list;   // per owned element with >= 1 coarse hanging face:
+                            // [element, (2d) x 2^(d-1) children or -1]
   int n_coarse;
 };
 

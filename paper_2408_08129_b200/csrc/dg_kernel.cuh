@@ -876,7 +876,8 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
   double* Tm = red + 64 + L::C_T;
   double* OT = red + 64 + L::C_OT;
   const MeshDev& mesh = P.mesh;
-  const long long e = clist[blockIdx.x];
+  const int* crec = clist + (long long)blockIdx.x * (1 + NF * S);  // coarse record
+  const long long e = crec[0];
   const int q = threadIdx.x;
   const bool act = q < NP;
   // the Helmholtz H1 output at this Gauss point (read-modify-written at the
@@ -896,13 +897,11 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
   // the element's face records and each coarse face's children, loaded once
   __shared__ uint8_t s_kind[NF];
   __shared__ int s_child[NF][S];
-  if (threadIdx.x < NF) s_kind[threadIdx.x] = mesh.kind[e * NF + threadIdx.x] & 15;
-  __syncthreads();
   if (threadIdx.x < NF * S) {
     const int f = threadIdx.x / S, sub = threadIdx.x % S;
-    s_child[f][sub] = (s_kind[f] == KIND_COARSE)
-                          ? mesh.hang_children[(long long)mesh.nbr[e * NF + f] * S + sub]
-                          : 0;
+    const int ch = crec[1 + threadIdx.x];
+    s_child[f][sub] = ch < 0 ? 0 : ch;
+    if (sub == 0) s_kind[f] = ch < 0 ? 0 : KIND_COARSE;
   }
   if (act)
 #pragma unroll

@@ -908,18 +908,29 @@ int dg_ctx_create(const dg_ctx_desc* d, dg_ctx** out) {
     e = up(c->sigma, d->sigma, (size_t)d->n_el * np);
     if (e == cudaSuccess) e = up(c->bg, d->background, (size_t)d->n_el * c->V * np);
   }
-  // owned elements with a coarse hanging face -> coarse fix-up kernel list
+  // owned elements with a coarse hanging face -> coarse fix-up kernel
+  // records (MeshDev::coarse_list): [element, then per face its 2^(d-1)
+  // children (fine leaves) or -1] -- the kernel reads one record instead of
+  // the dependent kind -> nbr -> hang_children chain
   {
     std::vector<int> cl;
-    const int nf = 2 * d->dim;
-    for (int e2 = 0; e2 < d->n_el; ++e2)
+    const int nf = 2 * d->dim, S = c->S;
+    int ncoarse = 0;
+    for (int e2 = 0; e2 < d->n_el; ++e2) {
+      bool has = false;
       for (int f = 0; f < nf; ++f)
-        if ((d->kind[(size_t)e2 * nf + f] & 15) == DG_FACE_COARSE) {
-          cl.push_back(e2);
-          break;
-        }
+        if ((d->kind[(size_t)e2 * nf + f] & 15) == DG_FACE_COARSE) has = true;
+      if (!has) continue;
+      ++ncoarse;
+      cl.push_back(e2);
+      for (int f = 0; f < nf; ++f)
+        for (int sub = 0; sub < S; ++sub)
+          cl.push_back((d->kind[(size_t)e2 * nf + f] & 15) == DG_FACE_COARSE
+                           ? d->hang_children[(size_t)d->nbr[(size_t)e2 * nf + f] * S + sub]
+                           : -1);
+    }
     if (e == cudaSuccess && !cl.empty()) e = c->clist.upload(cl.data(), cl.size());
-    c->mesh.n_coarse = (int)cl.size();
+    c->mesh.n_coarse = ncoarse;
   }
   const int max_grid = d->n_el + 1 + c->mesh.n_coarse;
   if (e == cudaSuccess) e = c->mass_partial.alloc(max_grid);
