@@ -64,8 +64,13 @@ struct MeshDev {
   const double* ff_h;       // (n_bface, nqf)
   int n_el;                 // owned elements processed by the kernels
   const int* coarse_list;   // per owned element with >= 1 coarse hanging face:
-                            // [element, (2d) x 2^(d-1) children or -1]
+                            // [element, (2d) hanging groups or -1,
+                            //  (2d) x 2^(d-1) children or -1]
   int n_coarse;
+  // coarse-face fluxes (flux mode): the coarse side's lifted numerical flux
+  // at the coarse face's Gauss points, (n_groups, KOUT, n^(d-1)) per hanging
+  // group, written by coarse_kernel before the element kernel reads them
+  double* cflux;
 };
 
 // Strided component view: comp c of element e at p + e*estride + c*cstride

@@ -474,8 +474,12 @@ __device__ __forceinline__ void face_flux_axis(const KParams<N>& P, const Tab<N>
     const int kd = kraw & 15;
     double* Lf = base + e * L::ELEM + L::OFF_L + f * KOUT * NQF;
     if (kd == KIND_COARSE) {
+      // precomputed coarse-face flux (flux mode), else added by coarse_kernel
+      const double* cf = mesh.cflux;
+      const long long grp = mesh.nbr[ge * NF + f];
 #pragma unroll
-      for (int k = 0; k < KOUT; ++k) Lf[k * NQF + qf] = 0.0;
+      for (int k = 0; k < KOUT; ++k)
+        Lf[k * NQF + qf] = cf ? cf[(grp * KOUT + k) * NQF + qf] : 0.0;
       continue;
     }
     // own trace: nodal value at the face = lift[side] . Gauss column
@@ -876,14 +880,17 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
   double* Tm = red + 64 + L::C_T;
   double* OT = red + 64 + L::C_OT;
   const MeshDev& mesh = P.mesh;
-  const int* crec = clist + (long long)blockIdx.x * (1 + NF * S);  // coarse record
+  const int* crec = clist + (long long)blockIdx.x * (1 + NF + NF * S);  // coarse record
   const long long e = crec[0];
+  // flux mode: only the coarse faces' lifted fluxes, into mesh.cflux (the
+  // element kernel lifts them with the rest of its faces)
+  const bool fmode = P.mesh.cflux != nullptr;
   const int q = threadIdx.x;
   const bool act = q < NP;
   // the Helmholtz H1 output at this Gauss point (read-modify-written at the
   // end): issued first so the final update does not wait on it
   double out_pre[KOUT];
-  if (OPK == OP_GRAD && P.out_quad && act)
+  if (OPK == OP_GRAD && P.out_quad && act && !fmode)
 #pragma unroll
     for (int k = 0; k < KOUT; ++k) out_pre[k] = P.out.p[e * P.out.estride + k * P.out.cstride + q];
   // (trace mode: the own traces come from the trace buffers, no input tile)
@@ -897,11 +904,15 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
   // the element's face records and each coarse face's children, loaded once
   __shared__ uint8_t s_kind[NF];
   __shared__ int s_child[NF][S];
+  __shared__ int s_grp[NF];
   if (threadIdx.x < NF * S) {
     const int f = threadIdx.x / S, sub = threadIdx.x % S;
-    const int ch = crec[1 + threadIdx.x];
+    const int ch = crec[1 + NF + threadIdx.x];
     s_child[f][sub] = ch < 0 ? 0 : ch;
-    if (sub == 0) s_kind[f] = ch < 0 ? 0 : KIND_COARSE;
+    if (sub == 0) {
+      s_kind[f] = ch < 0 ? 0 : KIND_COARSE;
+      s_grp[f] = crec[1 + f];
+    }
   }
   if (act)
 #pragma unroll
@@ -1054,6 +1065,13 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
       }
     }
     __syncthreads();
+    if (fmode) {
+      // flux mode: hand the coarse face's flux to the element kernel
+      const long long grp = s_grp[f];
+      for (int it = threadIdx.x; it < KOUT * NQF; it += blockDim.x)
+        P.mesh.cflux[grp * KOUT * NQF + it] = CH[it];
+      continue;
+    }
     // lift: Z += lift[side] (x) G
     if (act) {
       int qi[D];
@@ -1072,6 +1090,7 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
       for (int k = 0; k < KOUT; ++k) Z[k * NP + q] += lw * CH[k * NQF + qt];
     }
   }
+  if (fmode) return;
   double wq = 1.0, det = 1.0;
   if (act) {
     const ElemGeo<D> g = elem_geo<D>(mesh.elem, P.gc, e);

@@ -108,19 +108,28 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
         if (e != cudaSuccess) return e;
         wconf = true;
       }
+      const bool fmode = a.mesh.n_coarse > 0 && a.mesh.cflux != nullptr;
+      if (fmode) {
+        // the coarse faces' fluxes first; the element kernel lifts them
+        coarse_kernel<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
+            P, a.mesh.coarse_list, a.mesh.n_coarse, nullptr);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+      }
       if (OPK == OP_DIVHV && a.in_quad)
         welem_kernel<D, N, OPK, OPK == OP_DIVHV><<<wgrid, WL::THREADS, WL::SMEM, st>>>(P);
       else
         welem_kernel<D, N, OPK, false><<<wgrid, WL::THREADS, WL::SMEM, st>>>(P);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
-      if (a.mesh.n_coarse > 0) {
+      if (a.mesh.n_coarse > 0 && !fmode) {
         P.gs_row0 = wgrid;  // coarse elements' dot partials follow the CTA rows
         coarse_kernel<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
             P, a.mesh.coarse_list, a.mesh.n_coarse, nullptr);
         e = cudaGetLastError();
       }
-      if (info) info->grid = wgrid + a.mesh.n_coarse;  // dot partial rows written
+      // dot partial rows written
+      if (info) info->grid = wgrid + (fmode ? 0 : a.mesh.n_coarse);
       return e;
     }
   }
@@ -152,11 +161,22 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
         if (e != cudaSuccess) return e;
         xconf = true;
       }
+      const bool fmode = a.mesh.n_coarse > 0 && a.mesh.cflux != nullptr;
+      if (fmode) {
+        coarse_kernel<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
+            P, a.mesh.coarse_list, a.mesh.n_coarse, nullptr);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+      }
       if (a.full) xelem_kernel<D, N, true><<<xgrid, XL::THREADS, XL::SMEM, st>>>(P);
       else xelem_kernel<D, N, false><<<xgrid, XL::THREADS, XL::SMEM, st>>>(P);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       const int rows = xgrid * XL::WPB;  // mass-rate partials: one per warp
+      if (fmode) {
+        if (info) info->grid = rows;
+        return e;
+      }
       if (a.mesh.n_coarse > 0) {
         coarse_kernel<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
             P, a.mesh.coarse_list, a.mesh.n_coarse,
@@ -189,9 +209,20 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  const bool fmode = a.mesh.n_coarse > 0 && a.mesh.cflux != nullptr;
+  if (fmode) {
+    coarse_kernel<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
+        P, a.mesh.coarse_list, a.mesh.n_coarse, nullptr);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   elem_kernel<D, N, OPK><<<grid, L::THREADS, L::SMEM, st>>>(P);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (fmode) {
+    if (info) info->grid = grid;
+    return e;
+  }
   if (a.mesh.n_coarse > 0) {
     coarse_kernel<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
         P, a.mesh.coarse_list, a.mesh.n_coarse,

@@ -82,6 +82,7 @@ struct dg_ctx {
   std::vector<double> tabs;
   DevBuf<double> tabs_dev;  // device copy of tabs (warp-element kernel staging)
   DevBuf<int> elem, nbr, hang, clist;
+  DevBuf<double> cflux;  // coarse-face fluxes (MeshDev::cflux)
   DevBuf<uint8_t> kind;
   DevBuf<double> col, ffU, ffp, ffh, sigma, bg;
   // scratch
@@ -924,6 +925,10 @@ int dg_ctx_create(const dg_ctx_desc* d, dg_ctx** out) {
       ++ncoarse;
       cl.push_back(e2);
       for (int f = 0; f < nf; ++f)
+        cl.push_back((d->kind[(size_t)e2 * nf + f] & 15) == DG_FACE_COARSE
+                         ? d->nbr[(size_t)e2 * nf + f]
+                         : -1);
+      for (int f = 0; f < nf; ++f)
         for (int sub = 0; sub < S; ++sub)
           cl.push_back((d->kind[(size_t)e2 * nf + f] & 15) == DG_FACE_COARSE
                            ? d->hang_children[(size_t)d->nbr[(size_t)e2 * nf + f] * S + sub]
@@ -931,6 +936,12 @@ int dg_ctx_create(const dg_ctx_desc* d, dg_ctx** out) {
     }
     if (e == cudaSuccess && !cl.empty()) e = c->clist.upload(cl.data(), cl.size());
     c->mesh.n_coarse = ncoarse;
+    // coarse-face flux buffer (flux mode; DG_COARSE_FLUX=0: the coarse side
+    // is added afterwards by the fix-up epilogue instead)
+    static const bool cf_off =
+        getenv("DG_COARSE_FLUX") && std::string(getenv("DG_COARSE_FLUX")) == "0";
+    if (e == cudaSuccess && ncoarse > 0 && !cf_off)
+      e = c->cflux.alloc((size_t)d->n_hang_groups * c->V * nqf);
   }
   const int max_grid = d->n_el + 1 + c->mesh.n_coarse;
   if (e == cudaSuccess) e = c->mass_partial.alloc(max_grid);
@@ -952,6 +963,7 @@ int dg_ctx_create(const dg_ctx_desc* d, dg_ctx** out) {
   c->mesh.ff_h = c->ffh.p;
   c->mesh.n_el = d->n_el;
   c->mesh.coarse_list = c->clist.p;
+  c->mesh.cflux = c->cflux.p;
   for (int a = 0; a < 3; ++a) c->gc.per_root[a] = d->per_root[a];
   c->gc.z_top = d->z_top;
   c->gc.inv_ztop = 1.0 / d->z_top;
@@ -972,6 +984,7 @@ int dg_ctx_destroy(dg_ctx* c) {
   for (auto& s : c->st) s.release();
   c->elem.release();
   c->clist.release();
+  c->cflux.release();
   c->nbr.release();
   c->hang.release();
   c->kind.release();

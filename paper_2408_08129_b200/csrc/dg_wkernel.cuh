@@ -285,9 +285,11 @@ __device__ __forceinline__ void gs_dots(const KParams<N>& P, double* smem, const
   static_assert(AREA >= 2 * (32 + 2), "warp area too small for the fused dots");
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   bool own = act;
+  if (P.mesh.cflux == nullptr) {  // (flux mode: coarse elements are complete here)
 #pragma unroll
-  for (int f = 0; f < NF; ++f)
-    if ((kf[f] & 15) == KIND_COARSE) own = false;
+    for (int f = 0; f < NF; ++f)
+      if ((kf[f] & 15) == KIND_COARSE) own = false;
+  }
   const bool dual = P.gs_dual != 0;
   const int nv = P.gs_nv;
   const int nvt = dual ? 2 * (nv + 2) : nv + 1;  // columns of the row
@@ -677,8 +679,12 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
       }
     }
     if (kd == KIND_COARSE || !act) {
+      // coarse side of a hanging face: its lifted flux was precomputed by
+      // coarse_kernel (flux mode, mesh.cflux), else added afterwards
+      const bool cf = act && kd == KIND_COARSE && mesh.cflux != nullptr;
 #pragma unroll
-      for (int k = 0; k < KOUT; ++k) fl[f][k] = 0.0;
+      for (int k = 0; k < KOUT; ++k)
+        fl[f][k] = cf ? mesh.cflux[(nb * KOUT + k) * NC + c] : 0.0;
       return;
     }
     const bool outward = (kd == KIND_WALL || kd == KIND_FARFIELD);

@@ -252,8 +252,11 @@ XROLL
     }
     double fv[V];
     if (kd == KIND_COARSE || !act) {
+      // coarse side of a hanging face: precomputed by coarse_kernel (flux mode)
+      const bool cf = act && kd == KIND_COARSE && mesh.cflux != nullptr;
 #pragma unroll
-      for (int k = 0; k < V; ++k) fv[k] = 0.0;
+      for (int k = 0; k < V; ++k)
+        fv[k] = cf ? mesh.cflux[((long long)nf[f] * V + k) * NC + c] : 0.0;
     } else {
       const bool outward = (kd == KIND_WALL || kd == KIND_FARFIELD);
       double n[D], ws;
