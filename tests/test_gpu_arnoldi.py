@@ -93,3 +93,43 @@ def test_gmres_arnoldi_variants(mode):
         assert conv, name
         assert it == int(z["gm_iters"]), (name, it, int(z["gm_iters"]))
         assert d <= 1e-10, (name, d)
+
+
+_CHILD_OPS = r"""
+import json, sys
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import numpy as np
+from casebuild import build, golden, per_var_rel, rel
+from paper_2408_08129_b200.dgops import DGOperators
+from paper_2408_08129_b200.imex import SplitOperators, build_helmholtz_action
+out = {}
+for name in ("hang2d", "hang3d", "per3d"):
+    c, z = build(name), golden(name)
+    ops = DGOperators(c.geom)
+    split = SplitOperators(ops, c.model, c.bcs, c.sponge)
+    R = split.explicit_residual(c.U)
+    y = build_helmholtz_action(split, float(z["a_dt"]), c.U)(z["x"].ravel()).reshape(z["x"].shape)
+    out[name] = [max(per_var_rel(R, z["explicit_residual"])), rel(y, z["helm_x"])]
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("mode", ["flux", "fixup"])
+def test_coarse_face_modes(mode):
+    """The coarse side of hanging faces as precomputed fluxes (default) and
+    as the fix-up epilogue (DG_COARSE_FLUX=0) give the same operators on the
+    hanging-face golden cases."""
+    env = dict(os.environ)
+    if mode == "fixup":
+        env["DG_COARSE_FLUX"] = "0"
+    else:
+        env.pop("DG_COARSE_FLUX", None)
+    code = _CHILD_OPS % (ROOT, os.path.join(ROOT, "tests"))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    for name, (e_exp, e_helm) in res.items():
+        # explicit: the golden gate's sensitivity floor of these cases (<= 1e-9)
+        assert e_exp <= 1e-9, (name, e_exp)
+        assert e_helm <= 1e-12, (name, e_helm)
