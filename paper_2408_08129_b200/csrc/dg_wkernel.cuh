@@ -752,6 +752,9 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
   __syncwarp();  // every lane is done reading Q from the tile
   double Zc[KOUT][N];
   double det_c = 1.0;  // det J is z-independent: one value per column
+  // the column's horizontal quadrature weight, from the smem tables (a
+  // lane-dependent index into the parameter bank would serialise the warp)
+  const double wcol = (D == 3) ? TS.qw[c / N] * TS.qw[c % N] : TS.qw[c];
   {
     double Gz[KOUT][N];
 #pragma unroll
@@ -762,7 +765,7 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
         point_metric_ge<D, N>(P.gc, TC, g, kz, GEs, NC, c, det, ctrv);
       else
         point_metric<D, N>(P, g, qp, det, ctrv);
-      const double wq = point_weight<D, N>(TC, qp);
+      const double wq = wcol * TC.qw[kz];  // = point_weight(qp), same product order
       double F[D][KOUT];
       if constexpr (OPK == OP_DIVHV) {
         // own column of the Gauss-point tile (read before G overwrites it)
@@ -854,8 +857,8 @@ welem_kernel(const __grid_constant__ KParams<N> P) {
   const bool minv = (P.mode == OUT_MINV);
   // 1/(w det): det is z-independent, 1/w a product of 1D reciprocals
   double iwh = 1.0 / det_c;
-  if constexpr (D == 3) iwh *= TC.iqw[c / N] * TC.iqw[c % N];
-  else iwh *= TC.iqw[c];
+  if constexpr (D == 3) iwh *= TS.iqw[c / N] * TS.iqw[c % N];
+  else iwh *= TS.iqw[c];
   if (OPK == OP_GRAD && P.out_quad) {
     // H1 of the Helmholtz pair: V = coef * diag(1/(w det)) Z at the Gauss
     // points -- the B^-1 transform and H2's B interpolation cancel exactly

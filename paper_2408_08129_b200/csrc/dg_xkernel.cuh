@@ -345,8 +345,8 @@ XROLL
       }
       det_c = det;
       double wq = TC.qw[kz];
-      if constexpr (D == 3) wq *= TC.qw[c / N] * TC.qw[c % N];
-      else wq *= TC.qw[c];
+      if constexpr (D == 3) wq *= TS.qw[c / N] * TS.qw[c % N];  // smem: lane-dependent index
+      else wq *= TS.qw[c];
       double Uq[V];
 #pragma unroll
       for (int r = 0; r < V; ++r) Uq[r] = X[r * TSZ + coff<D, N>(c, kz)];
@@ -468,8 +468,8 @@ XROLL
     sgm[ii] = spg ? P.sigma[e * NP + node] : 0.0;
   }
   double iwh = 1.0 / det_c;
-  if constexpr (D == 3) iwh *= TC.iqw[c / N] * TC.iqw[c % N];
-  else iwh *= TC.iqw[c];
+  if constexpr (D == 3) iwh *= TS.iqw[c / N] * TS.iqw[c % N];
+  else iwh *= TS.iqw[c];
 #pragma unroll
   for (int r = 0; r < V; ++r) {
     double t[N];
