@@ -193,3 +193,19 @@ def test_mortar_exact(dim, r):
         exact = f(*np.meshgrid(*pts, indexing="ij")).ravel()
         assert np.abs(b.mortar_interp[sf] @ vals - exact).max() < 1e-12
     assert np.allclose(lagrange_eval_matrix(nodes, nodes), np.eye(r + 1))
+
+
+def test_cfg5_recipe():
+    """BASELINE configs[4]: periodic box, a seeded 7% of the
+    roots refined once -> about 30% of the interior face rows hanging;
+    hydrostatic state + smooth 1e-3 perturbations."""
+    from paper_2408_08129_b200.cases import baseline_case
+    c = baseline_case("cfg5_r3", root_scale=0.05)
+    top = c.mesh.topology
+    assert all(c.mesh.periodic) and c.geometry.basis.degree == 3
+    assert top.n_boundary_faces() == 0
+    n_conf = sum(len(b.left) for b in top.conforming)
+    n_rows = sum(len(b.coarse) for b in top.hanging)
+    frac = n_rows / (n_conf + n_rows)
+    assert 0.2 < frac < 0.4, frac
+    assert np.isfinite(c.U0).all() and c.U0.shape == (c.mesh.n_leaves, 5, 64)
