@@ -67,6 +67,13 @@ __device__ __forceinline__ void point_metric_reg(const GeoConst& gc, const Tab<N
 #define XROLL _Pragma("unroll 1")
 #endif
 
+// staging area of face f's neighbour nodes (see XLayout::NFG)
+template <int D, int V, int NC>
+__device__ __forceinline__ double* fstage(double* FG, double* GY, int f) {
+  if (D == 3 && f >= 2 * (D - 1)) return GY + (f - 2 * (D - 1)) * V * NC;
+  return FG + f * V * NC;
+}
+
 template <int D, int N>
 struct XLayout {
   static constexpr int V = D + 2;
@@ -87,7 +94,10 @@ struct XLayout {
   static constexpr int OFF_X = 0;
   static constexpr int OFF_GY = OFF_X + V * TSZ;
   static constexpr int OFF_FG = OFF_GY + (D == 3 ? V * TSZ : 0);
-  static constexpr int OFF_GE = OFF_FG + 2 * D * V * NC;
+  // 3D: the z faces' staged nodes live in the GY tile, free until the
+  // volume phase (FG keeps the x / y faces, later their fluxes)
+  static constexpr int NFG = (D == 3) ? 2 * (D - 1) : 2 * D;
+  static constexpr int OFF_GE = OFF_FG + NFG * V * NC;
   static constexpr int SLOT0 = OFF_GE + GEON * NC + GEE;
   static constexpr int SLOT = (SLOT0 % 2 == 0) ? SLOT0 + 1 : SLOT0;  // bank shift
   static constexpr size_t SMEM = (size_t)(TABD + WPB * NSLOT * SLOT) * sizeof(double);
@@ -151,7 +161,7 @@ xelem_kernel(const __grid_constant__ KParams<N> P) {
     const int node = nbr_face_node<D, N>(f >> 1, f & 1, c);
 #pragma unroll
     for (int r = 0; r < V; ++r) {
-      double* dst = FG + (f * V + r) * NC + c;
+      double* dst = fstage<D, V, NC>(FG, GY, f) + r * NC + c;
       if (inter) cp_async8(dst, P.in.p + nb * P.in.estride + r * P.in.cstride + node);
       else *dst = 0.0;
     }
@@ -209,7 +219,7 @@ XROLL
     const int sf = (kraw >> 4) & 3;
     const double* M0 = (kd == KIND_FINE) ? &TS.half[sf & 1][0][0] : &TS.B[0][0];
     const double* M1 = (kd == KIND_FINE) ? &TS.half[(sf >> 1) & 1][0][0] : &TS.B[0][0];
-    double* G0 = FG + f * V * NC;
+    double* G0 = fstage<D, V, NC>(FG, GY, f);
     double TN[V], TO[V];
     // neighbour trace: tangential passes straight from the staged nodes
     double t1[V];
