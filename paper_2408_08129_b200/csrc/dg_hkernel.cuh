@@ -1,0 +1,773 @@
+// Lean warp-element kernels of the homogeneous pressure-Helmholtz action in
+// flux-trace mode (fp64, sm_100a): the GMRES hot path.
+//
+//   H1 (hgrad_kernel):  V = coef diag(1/(w detJ)) G(alpha x)   at the Gauss
+//                       points (the weak gradient, dgops.py:332-366, with the
+//                       homogeneous ghosts of imex.py:221-242), and for every
+//                       face f of the element, at its face Gauss point c,
+//                           psi[e][f][c] = 1/2 ws h (V . n+)
+//                       with n+ the +axis-oriented unit normal and ws the
+//                       face weight of the element's own face metric
+//                       (geometry.py:305-357); elements with a coarse hanging
+//                       face also write their V face traces (trV) for the
+//                       mortar of the fine side.
+//   H2 (hdiv_kernel):   y = x + coef Minv Div_h(V)  (dgops.py:368-479).  The
+//                       centred face flux 1/2 (h_L V_L.n + h_R V_R.n) ws of a
+//                       conforming face is psi_own + psi_neighbour: the
+//                       kernel reads two 128-byte rows per face instead of
+//                       staging traces, evaluating metrics and ghosts.  Wall:
+//                       the mirrored ghost cancels the flux (0); far field
+//                       (homogeneous): V ghost 0, flux psi_own; fine side of
+//                       a hanging face: the coarse parent's traces through the
+//                       Gauss-point mortar (halfq), own metric; coarse side:
+//                       precomputed by coarse_kernel (psi mode).
+//
+// Lane layout as the general warp-element kernel (dg_wkernel.cuh): an element
+// is owned by n^(d-1) consecutive lanes, lane c holds z-column c in registers
+// and face point c of every face; x / y passes go through a per-element smem
+// tile under __syncwarp() only.  The 1D tables are brought into shared memory
+// by one bulk copy (cp.async.bulk + mbarrier) per CTA.
+#pragma once
+#include "dg_wkernel.cuh"
+
+namespace dg {
+
+template <int D, int N>
+struct HLayout {
+  static constexpr int NP = ipow(N, D);
+  static constexpr int NC = ipow(N, D - 1);   // lanes per element
+  static constexpr int EPW = 32 / NC;         // elements per warp
+  static constexpr int NSLOT = EPW + ((32 % NC) ? 1 : 0);
+  static constexpr int WPB = 4;
+  static constexpr int THREADS = 32 * WPB;
+  static constexpr int NF = 2 * D;
+  static constexpr int TSZ = tile_size<D, N>();
+  static constexpr int TABD = (int)(sizeof(Tab<N>) / sizeof(double));
+  static constexpr int TABP = (TABD + 1) & ~1;  // element slots 16-byte aligned
+  static constexpr int KX = (D - 1) > 1 ? (D - 1) : 1;  // tile comps
+  static constexpr int NHW = 2 * (D - 1) + 2 * D;       // 1/2 ws n+ values per face point
+  static constexpr int odd(int s) { return (s % 2 == 0) ? s + 1 : s; }
+  // H1 slot: tile | neighbour face nodes (NF x NC) | 1/2 ws n+ (NHW x NC)
+  static constexpr int GSLOT = odd(KX * TSZ + NF * NC + NHW * NC);
+  // H2 slot: tile (the fine-face staging (d+1) x NC and the fused dots'
+  // warp totals reuse it)
+  static constexpr int DRAW = KX * TSZ > (D + 1) * NC ? KX * TSZ : (D + 1) * NC;
+  static constexpr int DSLOT = odd(DRAW > 40 ? DRAW : 40);
+  static constexpr size_t GSMEM = (size_t)(TABP + WPB * NSLOT * GSLOT) * sizeof(double);
+  static constexpr size_t DSMEM = (size_t)(TABP + WPB * NSLOT * DSLOT) * sizeof(double);
+  static constexpr bool OK = NC <= 32;
+};
+
+#ifndef DG_HK1_MINB
+#define DG_HK1_MINB 6
+#endif
+#ifndef DG_HK2_MINB
+#define DG_HK2_MINB 6
+#endif
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+// the Tab<N> tables (global copy) -> smem by one bulk copy issued by thread 0;
+// every thread waits on the mbarrier (phase 0) before its first table read
+__device__ __forceinline__ void tab_bulk_issue(double* dst, const double* src, unsigned bytes,
+                                               unsigned long long* bar) {
+  if (threadIdx.x == 0) {
+    const unsigned b = smem_u32(bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(b) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(b)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tab_bulk_wait(unsigned long long* bar) {
+  const unsigned b = smem_u32(bar);
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      "HK_WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+      " @P1 bra HK_DONE;\n"
+      " bra HK_WAIT;\n"
+      "HK_DONE:\n}\n" ::"r"(b)
+      : "memory");
+}
+
+// own-geometry face metric at face point c of face (AX, side): the
+// +axis-oriented unit normal n+ and the face weight ws (geometry.py:305-357;
+// vertical faces have the exact normal e_AX, terrain z faces pay the sqrt)
+template <int D, int N, int AX>
+__device__ __forceinline__ void face_nplus(const GeoConst& gc, const ElemGeo<D>& g, int side, int c,
+                                           const Tab<N>& TS, double omh_edge, const double* dh,
+                                           double n[D], double& ws) {
+  const double fw = (D == 2) ? TS.qw[c] : TS.qw[c / N] * TS.qw[c % N];
+#pragma unroll
+  for (int a = 0; a < D; ++a) n[a] = 0.0;
+  if constexpr (AX < D - 1) {
+    const double zzv = g.s[D - 1] * omh_edge;
+    const double mag = (D == 2) ? zzv : g.s[1 - AX] * zzv;
+    n[AX] = 1.0;
+    ws = fw * fabs(mag);
+  } else {
+    const double top = (D == 2) ? g.s[0] : g.s[0] * g.s[1];
+    if (!gc.terrain) {
+      n[D - 1] = 1.0;
+      ws = fw * top;
+      return;
+    }
+    const double decay = 1.0 - (g.lo[D - 1] + g.s[D - 1] * (double)side) * gc.inv_ztop;
+    double nt[D];
+    if constexpr (D == 2) {
+      nt[0] = -dh[0] * g.s[0] * decay;
+    } else {
+      nt[0] = -g.s[1] * dh[0] * g.s[0] * decay;
+      nt[1] = -g.s[0] * dh[1] * g.s[1] * decay;
+    }
+    nt[D - 1] = top;
+    double m2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) m2 += nt[a] * nt[a];
+    const double mag = sqrt(m2);
+    const double im = 1.0 / mag;
+#pragma unroll
+    for (int a = 0; a < D; ++a) n[a] = nt[a] * im;
+    ws = fw * mag;
+  }
+}
+
+// the contravariant metric rows of a Gauss point of the lane's column
+// (geometry.py:204-238): c[bx][a] = ctrv[bx][a]; det is z-independent
+template <int D, int N>
+__device__ __forceinline__ void col_metric(const GeoConst& gc, const ElemGeo<D>& g, double omh,
+                                           const double* dh, double qxz, double ct[D][D]) {
+#pragma unroll
+  for (int b = 0; b < D; ++b)
+#pragma unroll
+    for (int a = 0; a < D; ++a) ct[b][a] = 0.0;
+  const double zz = g.s[D - 1] * omh;
+  const double decay = 1.0 - (g.lo[D - 1] + g.s[D - 1] * qxz) * gc.inv_ztop;
+  if constexpr (D == 2) {
+    ct[0][0] = zz;
+    ct[1][0] = gc.terrain ? -(dh[0] * g.s[0] * decay) : 0.0;
+    ct[1][1] = g.s[0];
+  } else {
+    ct[0][0] = g.s[1] * zz;
+    ct[1][1] = g.s[0] * zz;
+    ct[2][0] = gc.terrain ? -g.s[1] * (dh[0] * g.s[0] * decay) : 0.0;
+    ct[2][1] = gc.terrain ? -g.s[0] * (dh[1] * g.s[1] * decay) : 0.0;
+    ct[2][2] = g.s[0] * g.s[1];
+  }
+}
+
+template <int D>
+__device__ __forceinline__ double col_det(const ElemGeo<D>& g, double omh) {
+  double det = 1.0;
+#pragma unroll
+  for (int a = 0; a < D - 1; ++a) det = det * g.s[a];
+  return det * (g.s[D - 1] * omh);
+}
+
+// pencil offset of lane c's pencil along axis AX, point k
+template <int D, int N, int AX>
+__device__ __forceinline__ int poff(int c, int k) {
+  if constexpr (AX == D - 1) return coff<D, N>(c, k);
+  else if constexpr (AX == 0) return xoff<D, N>(c, k);
+  else return yoff<N>(c, k);
+}
+
+// the element's terrain scalars at the lane's column / face points
+template <int D, int N>
+struct ColData {
+  double omh;          // 1 - h/z_top at the column's horizontal Gauss point
+  double dh[2];        // grad h there (also the z faces' point-c values)
+};
+
+template <int D, int N>
+__device__ __forceinline__ ColData<D, N> col_data(const GeoConst& gc, const double* col,
+                                                  const ElemGeo<D>& g, int c, bool act) {
+  ColData<D, N> cd;
+  cd.omh = 1.0;
+  cd.dh[0] = cd.dh[1] = 0.0;
+  if (gc.terrain && act) {
+    constexpr int NQH = ipow(N, D - 1);
+    const double* colp = col + (long long)g.col * gc.col_stride;
+    cd.omh = colp[c];
+#pragma unroll
+    for (int a = 0; a < D - 1; ++a) cd.dh[a] = colp[NQH * (1 + a) + c];
+  }
+  return cd;
+}
+
+// 1 - h_edge/z_top along vertical face (AX, side) at the lane's point
+template <int D, int N>
+__device__ __forceinline__ double edge_omh(const GeoConst& gc, const double* col,
+                                          const ElemGeo<D>& g, int f, int c, bool act) {
+  if (!(gc.terrain && act)) return 1.0;
+  constexpr int NQH = ipow(N, D - 1), NE = ipow(N, D - 2);
+  return col[(long long)g.col * gc.col_stride + NQH * D + f * NE + ((D == 2) ? 0 : c / N)];
+}
+
+// ---------------------------------------------------------------------- H1
+template <int D, int N>
+__global__ void __launch_bounds__(HLayout<D, N>::THREADS, DG_HK1_MINB)
+hgrad_kernel(const __grid_constant__ KParams<N> P) {
+  using HL = HLayout<D, N>;
+  constexpr int NC = HL::NC, EPW = HL::EPW, NF = HL::NF, TSZ = HL::TSZ;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ unsigned long long tbar;
+  tab_bulk_issue(smem, P.tab_g, HL::TABD * 8, &tbar);
+  const Tab<N>& TS = *reinterpret_cast<const Tab<N>*>(smem);
+  const Tab<N>& TC = P.tab;
+  const MeshDev& mesh = P.mesh;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int eiw = lane / NC, c = lane - eiw * NC;
+  const bool slot_ok = eiw < EPW;
+  const long long e = ((long long)blockIdx.x * HL::WPB + wid) * EPW + eiw;
+  const bool act = slot_ok && e < mesh.n_el;
+  const long long es = act ? e : 0;
+  double* X = smem + HL::TABP + (wid * HL::NSLOT + (slot_ok ? eiw : EPW)) * HL::GSLOT;
+  double* FG = X + HL::KX * TSZ;
+  double* HW = FG + NF * NC;
+
+  uint8_t kf[NF];
+  int nf[NF];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    kf[f] = act ? mesh.kind[es * NF + f] : (uint8_t)KIND_WALL;
+    nf[f] = act ? mesh.nbr[es * NF + f] : 0;
+  }
+  // own nodal column and the neighbours' face nodes, all loads in flight
+  double xc[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) xc[k] = act ? P.in.p[es * P.in.estride + c * N + k] : 0.0;
+  double gn[NF];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    const int kd = kf[f] & 15;
+    const bool inter = act && (kd == KIND_CONF || kd == KIND_FINE);
+    gn[f] = inter ? P.in.p[(long long)nf[f] * P.in.estride + nbr_face_node<D, N>(f >> 1, f & 1, c)]
+                  : 0.0;
+  }
+  const ElemGeo<D> g = elem_geo<D>(mesh.elem, P.gc, es);
+  const ColData<D, N> cd = col_data<D, N>(P.gc, mesh.col, g, c, act);
+  __syncthreads();  // the table barrier is initialised
+
+  // ---- p = alpha x to the Gauss points (z in registers, y / x via the tile)
+  {
+    double col[N], q[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) col[k] = P.alpha * xc[k];
+    mat_apply<N, false>(TC.B, col, q);
+#pragma unroll
+    for (int k = 0; k < N; ++k) X[coff<D, N>(c, k)] = q[k];
+  }
+#pragma unroll
+  for (int f = 0; f < NF; ++f) FG[f * NC + c] = P.alpha * gn[f];
+  __syncwarp();
+  if constexpr (D == 3) {
+    double v[N], o[N];
+#pragma unroll
+    for (int jj = 0; jj < N; ++jj) v[jj] = X[yoff<N>(c, jj)];
+    mat_apply<N, false>(TC.B, v, o);
+#pragma unroll
+    for (int jj = 0; jj < N; ++jj) X[yoff<N>(c, jj)] = o[jj];
+    __syncwarp();
+  }
+  {
+    double v[N], o[N];
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii) v[ii] = X[xoff<D, N>(c, ii)];
+    mat_apply<N, false>(TC.B, v, o);
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii) X[xoff<D, N>(c, ii)] = o[ii];
+  }
+  tab_bulk_wait(&tbar);
+  // ---- neighbour traces at face point c: tangential passes over the staged
+  // face nodes (B, or the mortar halves for a fine leaf's coarse parent)
+  const int fa = (D == 2) ? c : c / N;
+  const int fb = (D == 2) ? 0 : c % N;
+  double tn[NF];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    const int kd = kf[f] & 15;
+    const int sf = (kf[f] >> 4) & 3;
+    const double* M0 = (kd == KIND_FINE) ? &TS.half[sf & 1][0][0] : &TS.B[0][0];
+    double t = 0.0;
+    if constexpr (D == 2) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) t = fma(M0[fa * N + j], FG[f * NC + j], t);
+    } else {
+#pragma unroll
+      for (int j = 0; j < N; ++j) t = fma(M0[fa * N + j], FG[f * NC + j * N + fb], t);
+    }
+    tn[f] = t;
+  }
+  if constexpr (D == 3) {
+    __syncwarp();
+#pragma unroll
+    for (int f = 0; f < NF; ++f) FG[f * NC + c] = tn[f];
+    __syncwarp();
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      const int kd = kf[f] & 15;
+      const int sf = (kf[f] >> 4) & 3;
+      const double* M1 = (kd == KIND_FINE) ? &TS.half[(sf >> 1) & 1][0][0] : &TS.B[0][0];
+      double t = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) t = fma(M1[fb * N + j], FG[f * NC + fa * N + j], t);
+      tn[f] = t;
+    }
+  }
+  __syncwarp();  // the tile holds p at the Gauss points of every lane
+  // ---- face fluxes  sg 1/2 ws n+ (p_own + p_x): p_x = neighbour (interior),
+  // p_own (wall), 0 (far field, homogeneous); coarse side precomputed
+  double flv[2 * (D - 1)];  // vertical faces: the AX component only
+  double flz[2][D];         // z faces
+  auto face = [&](auto ax_c, int side) {
+    constexpr int AX = decltype(ax_c)::value;
+    const int f = 2 * AX + side;
+    const int kd = kf[f] & 15;
+    double to = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) to = fma(TC.lift[side][k], X[poff<D, N, AX>(c, k)], to);
+    double fl[D];
+    double hw[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) hw[a] = 0.0;
+    if (kd == KIND_COARSE || !act) {
+      const bool cf = act && mesh.cflux != nullptr;
+#pragma unroll
+      for (int a = 0; a < D; ++a) fl[a] = cf ? mesh.cflux[((long long)nf[f] * D + a) * NC + c] : 0.0;
+    } else {
+      double n[D], ws;
+      const double oe = (AX < D - 1) ? edge_omh<D, N>(P.gc, mesh.col, g, f, c, act) : 1.0;
+      face_nplus<D, N, AX>(P.gc, g, side, c, TS, oe, cd.dh, n, ws);
+      const double px = (kd == KIND_WALL) ? to : (kd == KIND_FARFIELD ? 0.0 : tn[f]);
+      const double ph = to + px;
+      const double sg = side ? 1.0 : -1.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        hw[a] = (0.5 * ws) * n[a];
+        fl[a] = sg * (hw[a] * ph);
+      }
+    }
+    if constexpr (AX < D - 1) {
+      flv[f] = fl[AX];
+      HW[f * NC + c] = hw[AX];
+    } else {
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        flz[side][a] = fl[a];
+        HW[(2 * (D - 1) + side * D + a) * NC + c] = hw[a];
+      }
+    }
+  };
+  face(std::integral_constant<int, 0>{}, 0);
+  face(std::integral_constant<int, 0>{}, 1);
+  if constexpr (D == 3) {
+    face(std::integral_constant<int, 1>{}, 0);
+    face(std::integral_constant<int, 1>{}, 1);
+  }
+  face(std::integral_constant<int, D - 1>{}, 0);
+  face(std::integral_constant<int, D - 1>{}, 1);
+  // own h traces at the face points (frozen per fixed-point iterate)
+  double hf[NF];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) hf[f] = act ? P.trH[es * (NF * NC) + f * NC + c] : 0.0;
+
+  // ---- volume: G_bx,k = ctrv[bx][k] p wq; bx < d-1 through the tile
+  double Zc[D][N];
+  const double det = col_det<D>(g, cd.omh);
+  const double wcol = (D == 3) ? TS.qw[c / N] * TS.qw[c % N] : TS.qw[c];
+  {
+    double Gz[D][N];
+#pragma unroll
+    for (int kz = 0; kz < N; ++kz) {
+      double ct[D][D];
+      col_metric<D, N>(P.gc, g, cd.omh, cd.dh, TC.qx[kz], ct);
+      const double wq = wcol * TC.qw[kz];
+      const double p = X[coff<D, N>(c, kz)];
+      X[coff<D, N>(c, kz)] = (p * ct[0][0]) * wq;
+      if constexpr (D == 3) X[TSZ + coff<D, N>(c, kz)] = (p * ct[1][1]) * wq;
+#pragma unroll
+      for (int k = 0; k < D; ++k) Gz[k][kz] = (p * ct[D - 1][k]) * wq;
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      mat_apply<N, true>(TC.Dhat, Gz[k], Zc[k]);
+#pragma unroll
+      for (int kz = 0; kz < N; ++kz)
+        Zc[k][kz] = TC.lift[0][kz] * flz[0][k] + TC.lift[1][kz] * flz[1][k] - Zc[k][kz];
+    }
+  }
+  __syncwarp();
+  {
+    double v[N], o[N];
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii) v[ii] = X[xoff<D, N>(c, ii)];
+    mat_apply<N, true>(TC.Dhat, v, o);
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii)
+      X[xoff<D, N>(c, ii)] = TC.lift[0][ii] * flv[0] + TC.lift[1][ii] * flv[1] - o[ii];
+    if constexpr (D == 3) {
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj) v[jj] = X[TSZ + yoff<N>(c, jj)];
+      mat_apply<N, true>(TC.Dhat, v, o);
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj)
+        X[TSZ + yoff<N>(c, jj)] = TC.lift[0][jj] * flv[2] + TC.lift[1][jj] * flv[3] - o[jj];
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int kz = 0; kz < N; ++kz) {
+    Zc[0][kz] += X[coff<D, N>(c, kz)];
+    if constexpr (D == 3) Zc[1][kz] += X[TSZ + coff<D, N>(c, kz)];
+  }
+  // ---- epilogue: V = coef Z / (w det) at the Gauss points
+  double iwh = 1.0 / det;
+  if constexpr (D == 3) iwh *= TS.iqw[c / N] * TS.iqw[c % N];
+  else iwh *= TS.iqw[c];
+  double Vg[D][N];
+#pragma unroll
+  for (int k = 0; k < D; ++k)
+#pragma unroll
+    for (int kz = 0; kz < N; ++kz) Vg[k][kz] = P.coef * (Zc[k][kz] * (iwh * TC.iqw[kz]));
+  if (act) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      double* out = P.out.p + e * P.out.estride + (long long)k * P.out.cstride + c * N;
+#pragma unroll
+      for (int kz = 0; kz < N; ++kz) out[kz] = Vg[k][kz];
+    }
+  }
+  // ---- face traces of V and psi = 1/2 ws h (V . n+)
+  double tz[2][D];
+#pragma unroll
+  for (int side = 0; side < 2; ++side)
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      double t = 0.0;
+#pragma unroll
+      for (int kz = 0; kz < N; ++kz) t = fma(TC.lift[side][kz], Vg[k][kz], t);
+      tz[side][k] = t;
+    }
+  __syncwarp();  // every lane is done with the tile
+#pragma unroll
+  for (int a = 0; a < D - 1; ++a)
+#pragma unroll
+    for (int kz = 0; kz < N; ++kz) X[a * TSZ + coff<D, N>(c, kz)] = Vg[a][kz];
+  __syncwarp();
+  double tv[2 * (D - 1)];
+#pragma unroll
+  for (int a = 0; a < D - 1; ++a)
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      double t = 0.0;
+#pragma unroll
+      for (int p = 0; p < N; ++p) {
+        const int off = (a == 0) ? xoff<D, N>(c, p) : yoff<N>(c, p);
+        t = fma(TC.lift[side][p], X[a * TSZ + off], t);
+      }
+      tv[2 * a + side] = t;
+    }
+  if (act) {
+    double* ps = P.psi_out + e * (NF * NC);
+#pragma unroll
+    for (int f = 0; f < 2 * (D - 1); ++f) ps[f * NC + c] = hf[f] * (HW[f * NC + c] * tv[f]);
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      double vn = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) vn = fma(HW[(2 * (D - 1) + side * D + a) * NC + c], tz[side][a], vn);
+      ps[(2 * (D - 1) + side) * NC + c] = hf[2 * (D - 1) + side] * vn;
+    }
+    bool coarse = false;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) coarse |= (kf[f] & 15) == KIND_COARSE;
+    if (coarse && P.tr_out != nullptr) {
+      // the mortar of the fine neighbours (hdiv_kernel) and the coarse-side
+      // fluxes (coarse_kernel) read this element's V traces
+      constexpr int TSL = tr_slots<D>() * NC;
+      double* tr = P.tr_out + e * TSL;
+#pragma unroll
+      for (int f = 0; f < 2 * (D - 1); ++f) tr[tr_slot<D>(f, f >> 1) * NC + c] = tv[f];
+#pragma unroll
+      for (int side = 0; side < 2; ++side)
+#pragma unroll
+        for (int k = 0; k < D; ++k) tr[tr_slot<D>(2 * (D - 1) + side, k) * NC + c] = tz[side][k];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------- H2
+template <int D, int N>
+__global__ void __launch_bounds__(HLayout<D, N>::THREADS, DG_HK2_MINB)
+hdiv_kernel(const __grid_constant__ KParams<N> P) {
+  using HL = HLayout<D, N>;
+  constexpr int NC = HL::NC, EPW = HL::EPW, NF = HL::NF, TSZ = HL::TSZ;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ unsigned long long tbar;
+  tab_bulk_issue(smem, P.tab_g, HL::TABD * 8, &tbar);
+  const Tab<N>& TS = *reinterpret_cast<const Tab<N>*>(smem);
+  const Tab<N>& TC = P.tab;
+  const MeshDev& mesh = P.mesh;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int eiw = lane / NC, c = lane - eiw * NC;
+  const bool slot_ok = eiw < EPW;
+  const long long e = ((long long)blockIdx.x * HL::WPB + wid) * EPW + eiw;
+  const bool act = slot_ok && e < mesh.n_el;
+  const long long es = act ? e : 0;
+  double* X = smem + HL::TABP + (wid * HL::NSLOT + (slot_ok ? eiw : EPW)) * HL::DSLOT;
+
+  uint8_t kf[NF];
+  int nf[NF];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    kf[f] = act ? mesh.kind[es * NF + f] : (uint8_t)KIND_WALL;
+    nf[f] = act ? mesh.nbr[es * NF + f] : 0;
+  }
+  // face fluxes first (their loads are the dependent ones)
+  double fl[NF];
+  {
+    const double* ps = P.psi + es * (NF * NC) + c;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      const int kd = kf[f] & 15;
+      const double po = act ? ps[f * NC] : 0.0;
+      const double pn = (act && kd == KIND_CONF)
+                            ? P.psi[(long long)nf[f] * (NF * NC) + (f ^ 1) * NC + c] : 0.0;
+      const double sg = (f & 1) ? 1.0 : -1.0;
+      double v = 0.0;
+      if (kd == KIND_CONF) v = sg * (po + pn);
+      else if (kd == KIND_FARFIELD || kd == KIND_FINE) v = sg * po;  // (fine: + the mortar part)
+      else if (kd == KIND_COARSE && mesh.cflux != nullptr && act)
+        v = mesh.cflux[(long long)nf[f] * NC + c];
+      fl[f] = act ? v : 0.0;
+    }
+  }
+  double Vq[D][N], hq[N], bv[N];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int kz = 0; kz < N; ++kz)
+      Vq[a][kz] = act ? P.in.p[es * P.in.estride + (long long)a * P.in.cstride + c * N + kz] : 0.0;
+#pragma unroll
+  for (int kz = 0; kz < N; ++kz) hq[kz] = act ? P.inH.p[es * P.inH.estride + c * N + kz] : 0.0;
+#pragma unroll
+  for (int ii = 0; ii < N; ++ii) {
+    const int node = (D == 3) ? ii * N * N + c : ii * N + c;
+    bv[ii] = (act && P.has_base) ? P.base.p[es * P.base.estride + node] : 0.0;
+  }
+  const ElemGeo<D> g = elem_geo<D>(mesh.elem, P.gc, es);
+  const ColData<D, N> cd = col_data<D, N>(P.gc, mesh.col, g, c, act);
+  __syncthreads();  // the table barrier is initialised
+  tab_bulk_wait(&tbar);
+
+  // ---- fine side of hanging faces: the coarse parent's V / h traces at its
+  // face Gauss points through halfq (x) halfq, flux with the own metric
+  const int fa = (D == 2) ? c : c / N;
+  const int fb = (D == 2) ? 0 : c % N;
+  auto fine_face = [&](auto ax_c, int side) {
+    constexpr int AX = decltype(ax_c)::value;
+    const int f = 2 * AX + side;
+    const int kd = kf[f] & 15;
+    const bool fine = act && kd == KIND_FINE;
+    if (!__any_sync(0xffffffffu, fine)) return;
+    constexpr int FC = (AX < D - 1) ? 2 : D + 1;  // (V_AX, h) or (V, h)
+    constexpr int TSL = tr_slots<D>() * NC, THL = 2 * D * NC;
+    const long long pe = nf[f];
+#pragma unroll
+    for (int r = 0; r < FC; ++r) {
+      double v = 0.0;
+      if (fine) {
+        const bool isv = r < FC - 1;
+        const int comp = (AX < D - 1) ? AX : r;
+        v = isv ? P.trV[pe * TSL + tr_slot<D>(f ^ 1, comp) * NC + c]
+                : P.trH[pe * THL + (f ^ 1) * NC + c];
+      }
+      X[r * NC + c] = v;
+    }
+    __syncwarp();
+    const int sf = (kf[f] >> 4) & 3;
+    const double* Mq0 = &TS.halfq[sf & 1][0][0];
+    const double* Mq1 = &TS.halfq[(sf >> 1) & 1][0][0];
+    double tr[FC];
+#pragma unroll
+    for (int r = 0; r < FC; ++r) {
+      double t = 0.0;
+      if constexpr (D == 2) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) t = fma(Mq0[fa * N + j], X[r * NC + j], t);
+      } else {
+#pragma unroll
+        for (int j = 0; j < N; ++j) t = fma(Mq0[fa * N + j], X[r * NC + j * N + fb], t);
+      }
+      tr[r] = t;
+    }
+    if constexpr (D == 3) {
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < FC; ++r) X[r * NC + c] = tr[r];
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < FC; ++r) {
+        double t = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) t = fma(Mq1[fb * N + j], X[r * NC + fa * N + j], t);
+        tr[r] = t;
+      }
+    }
+    __syncwarp();  // the staging area is reused by the next face
+    if (fine) {
+      double n[D], ws;
+      const double oe = (AX < D - 1) ? edge_omh<D, N>(P.gc, mesh.col, g, f, c, act) : 1.0;
+      face_nplus<D, N, AX>(P.gc, g, side, c, TS, oe, cd.dh, n, ws);
+      double vn;
+      if constexpr (AX < D - 1) {
+        vn = tr[0] * n[AX];
+      } else {
+        vn = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) vn = fma(tr[a], n[a], vn);
+      }
+      const double sg = side ? 1.0 : -1.0;
+      fl[f] += sg * ((0.5 * ws) * (tr[FC - 1] * vn));
+    }
+  };
+  if (mesh.n_coarse > 0) {
+    fine_face(std::integral_constant<int, 0>{}, 0);
+    fine_face(std::integral_constant<int, 0>{}, 1);
+    if constexpr (D == 3) {
+      fine_face(std::integral_constant<int, 1>{}, 0);
+      fine_face(std::integral_constant<int, 1>{}, 1);
+    }
+    fine_face(std::integral_constant<int, D - 1>{}, 0);
+    fine_face(std::integral_constant<int, D - 1>{}, 1);
+  }
+
+  // ---- volume: G_bx = (sum_a ctrv[bx][a] h V_a) wq; bx < d-1 via the tile
+  double Zc[N];
+  const double det = col_det<D>(g, cd.omh);
+  const double wcol = (D == 3) ? TS.qw[c / N] * TS.qw[c % N] : TS.qw[c];
+  {
+    double Gz[N];
+#pragma unroll
+    for (int kz = 0; kz < N; ++kz) {
+      double ct[D][D];
+      col_metric<D, N>(P.gc, g, cd.omh, cd.dh, TC.qx[kz], ct);
+      const double wq = wcol * TC.qw[kz];
+      double F[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) F[a] = hq[kz] * Vq[a][kz];
+      X[coff<D, N>(c, kz)] = (F[0] * ct[0][0]) * wq;
+      if constexpr (D == 3) X[TSZ + coff<D, N>(c, kz)] = (F[1] * ct[1][1]) * wq;
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) acc += F[a] * ct[D - 1][a];
+      Gz[kz] = acc * wq;
+    }
+    mat_apply<N, true>(TC.Dhat, Gz, Zc);
+    const int zf = 2 * (D - 1);
+#pragma unroll
+    for (int kz = 0; kz < N; ++kz)
+      Zc[kz] = TC.lift[0][kz] * fl[zf] + TC.lift[1][kz] * fl[zf + 1] - Zc[kz];
+  }
+  __syncwarp();
+  {
+    double v[N], o[N];
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii) v[ii] = X[xoff<D, N>(c, ii)];
+    mat_apply<N, true>(TC.Dhat, v, o);
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii)
+      X[xoff<D, N>(c, ii)] = TC.lift[0][ii] * fl[0] + TC.lift[1][ii] * fl[1] - o[ii];
+    if constexpr (D == 3) {
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj) v[jj] = X[TSZ + yoff<N>(c, jj)];
+      mat_apply<N, true>(TC.Dhat, v, o);
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj)
+        X[TSZ + yoff<N>(c, jj)] = TC.lift[0][jj] * fl[2] + TC.lift[1][jj] * fl[3] - o[jj];
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int kz = 0; kz < N; ++kz) {
+    Zc[kz] += X[coff<D, N>(c, kz)];
+    if constexpr (D == 3) Zc[kz] += X[TSZ + coff<D, N>(c, kz)];
+  }
+  // ---- epilogue: y = base + coef B^-1 diag(1/(w det)) Z, + fused dots
+  double iwh = 1.0 / det;
+  if constexpr (D == 3) iwh *= TS.iqw[c / N] * TS.iqw[c % N];
+  else iwh *= TS.iqw[c];
+  {
+    double t[N];
+#pragma unroll
+    for (int kz = 0; kz < N; ++kz) t[kz] = Zc[kz] * (iwh * TC.iqw[kz]);
+    mat_apply<N, false>(TC.Binv, t, Zc);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int kz = 0; kz < N; ++kz) X[coff<D, N>(c, kz)] = Zc[kz];
+  __syncwarp();
+  if constexpr (D == 3) {
+    double v[N], o[N];
+#pragma unroll
+    for (int jj = 0; jj < N; ++jj) v[jj] = X[yoff<N>(c, jj)];
+    mat_apply<N, false>(TC.Binv, v, o);
+#pragma unroll
+    for (int jj = 0; jj < N; ++jj) X[yoff<N>(c, jj)] = o[jj];
+    __syncwarp();
+  }
+  double wv[N], uv[N];
+  {
+    double v[N], o[N];
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii) v[ii] = X[xoff<D, N>(c, ii)];
+    mat_apply<N, false>(TC.Binv, v, o);
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii) {
+      const double r = __dmul_rn(P.coef, o[ii]);
+      const double val = P.has_base ? __dadd_rn(bv[ii], r) : r;
+      wv[ii] = act ? val : 0.0;
+      uv[ii] = act ? bv[ii] : 0.0;
+      if (act) {
+        const int node = (D == 3) ? ii * N * N + c : ii * N + c;
+        P.out.p[e * P.out.estride + node] = val;
+      }
+    }
+  }
+  if (P.gs_part != nullptr) {
+    // fused Gram-Schmidt dots (as gs_dots, dg_wkernel.cuh): every element is
+    // complete here (coarse faces in flux mode)
+    constexpr int AREA = HL::NSLOT * HL::DSLOT;
+    static_assert(AREA >= 2 * (32 + 2), "warp area too small for the fused dots");
+    const bool dual = P.gs_dual != 0;
+    const int nv = P.gs_nv;
+    const int nvt = dual ? 2 * (nv + 2) : nv + 1;
+    double* wtot = smem + HL::TABP + wid * AREA;
+    __syncwarp();
+    for (int c0 = 0; c0 < nvt; c0 += 16) {
+      if (dual) gs_round<D, N, 2>(P, act, e, c, wv, uv, c0, nv, nvt, wtot);
+      else gs_round<D, N, 1>(P, act, e, c, wv, uv, c0, nv, nvt, wtot);
+    }
+    __syncthreads();
+    if (wid == 0) {
+      const long long row = (long long)P.gs_row0 + blockIdx.x;
+      for (int col = lane; col < nvt; col += 32) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < HL::WPB; ++w) t += smem[HL::TABP + w * AREA + col];
+        P.gs_part[row * nvt + col] = t;
+      }
+    }
+  }
+}
+
+}  // namespace dg

@@ -87,7 +87,11 @@ struct dg_ctx {
   DevBuf<double> col, ffU, ffp, ffh, sigma, bg;
   // scratch
   DevBuf<double> mass_partial, partial, redout, coef_dev, gs_part;
-  double* pinned = nullptr;  // 256 doubles
+  double* pinned = nullptr;  // 2 * pin_half doubles: reads at [0, pin_half), coefs above
+  int pin_half = 128;
+  int kcap = 31;             // restart length the Krylov scratch is sized for
+  int max_grid = 0;
+  double* pin_coef() const { return pinned + pin_half; }
   DevBuf<double> sV;         // vector field (n_tot, d, NP)
   DevBuf<double> sh, sK, sx, srhs, spold, sw, sr, sx2, shq;  // scalar fields
   DevBuf<double> basis;      // (m+1) x (n_tot NP)
@@ -369,6 +373,27 @@ int bj_apply_ctx(dg_ctx* c, const double* in, double* out) {
   return DG_OK;
 }
 
+// Krylov scratch for restart length m: the reduction partials (groups of 8
+// dots per pass), the read-back and coefficient slots and the pinned staging
+// are sized for m <= 31 at context creation and grown here for longer
+// restarts (imex.py:96-114 accepts any krylov_restart >= 1)
+int ensure_krylov_cap(dg_ctx* c, int m) {
+  if (m <= c->kcap) return DG_OK;
+  CK(cudaStreamSynchronize(c->stream));
+  const size_t cols = (size_t)2 * (m + 4) + 9 * (size_t)((m + 9) / 8);
+  CK(c->partial.alloc((size_t)RED_BLOCKS * cols + (size_t)c->max_grid * 8));
+  CK(c->redout.alloc(2 * (size_t)(m + 8)));
+  CK(c->coef_dev.alloc(3 * (size_t)(m + 8)));
+  const int half = 3 * (m + 8);
+  double* pin = nullptr;
+  CK(cudaMallocHost(&pin, 2 * (size_t)half * sizeof(double)));
+  cudaFreeHost(c->pinned);
+  c->pinned = pin;
+  c->pin_half = half;
+  c->kcap = m;
+  return DG_OK;
+}
+
 // One restart cycle of GMRES with DCGS2 Arnoldi (classical Gram-Schmidt with
 // delayed re-orthogonalisation; Bielich et al. 2022).  Slot j of the basis
 // holds the lagged vector u_j (projected once, not yet re-orthogonalised nor
@@ -391,7 +416,7 @@ int dcgs2_cycle(dg_ctx* c, double a_dt, const double* h, const double* hq, int m
                 double bn, double target, double beta, double* Vb, long long vs, Gm& st, std::vector<double>& g,
                 std::vector<double>& y, int& done) {
   const long long n = (long long)c->n_el * c->NP;
-  double* coefs = c->pinned + 128;
+  double* coefs = c->pin_coef();
   double* z = c->sw.p;
   std::vector<double> Hb((size_t)(m + 1) * m, 0.0), R((size_t)(m + 1) * m, 0.0);
   std::vector<double> cs(m), sn(m), dots(2 * (m + 2)), sv(m), gv(m + 1), hv(m + 1);
@@ -415,8 +440,18 @@ int dcgs2_cycle(dg_ctx* c, double a_dt, const double* h, const double* hq, int m
     }
     if (j > 0) {
       // finalise u_j: q_j = (u_j - Q s) / alpha, and column j-1 of Hbar
-      alpha = std::sqrt(uu - s2);
+      const double a2 = uu - s2;
       for (int i = 0; i < j; ++i) HB(i, j - 1) += sv[i];
+      if (!(a2 > 1e-20 * uu) || !std::isfinite(a2)) {
+        // u_j lies in span(Q) to rounding (or the dots are not finite): the
+        // re-orthogonalised norm is the breakdown of column j-1 -- stop with
+        // the j finished columns (krylov.py:82 happy-breakdown rule) instead
+        // of dividing by a vanishing alpha
+        HB(j, j - 1) = (a2 > 0.0 && std::isfinite(a2)) ? std::sqrt(a2) : 0.0;
+        st.breakdown = 1;
+        break;
+      }
+      alpha = std::sqrt(a2);
       HB(j, j - 1) = alpha;
     }
     // g = Hbar[0:j+1, 0:j] s
@@ -506,13 +541,15 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const doubl
   int m = restart < 1 ? 1 : restart;
   if (m > c->n_global) m = (int)c->n_global;
   if (m < 1) m = 1;
-  if (m > 31) return fail(DG_ERR_USAGE, "krylov_restart > 31 not supported on the device path");
+  RET(ensure_krylov_cap(c, m));
   // basis vectors at a padded stride: a power-of-two-rich stride makes the
   // j+1 streams of one Gram-Schmidt pass collide in the same DRAM channels
   const long long vs = ((ns + 31) / 32) * 32 + 32 * 13;
   CK(c->basis.alloc((size_t)(m + 1) * vs));
   double* Vb = c->basis.p;
-  const bool fuse = gs_fusable(c);
+  // (the fused dots' partial rows hold <= 32 + 2 column pairs: longer
+  // restarts take the unfused CGS passes)
+  const bool fuse = gs_fusable(c) && m <= 31;
   // DCGS2 (delayed re-orthogonalisation) needs the fused dual
   // dots and u = the action's input (no preconditioner); DG_GMRES=cgs2 keeps
   // the CGS + selective re-orthogonalisation path
@@ -524,7 +561,7 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const doubl
     const long long rows = (long long)c->n_el + 4 + c->mesh.n_coarse + 1;
     CK(c->gs_part.alloc((size_t)rows * 2 * (32 + 2)));
   }
-  double* coefs = c->pinned + 128;  // pinned staging for the coefficient uploads
+  double* coefs = c->pin_coef();  // pinned staging for the coefficient uploads
   double* w = c->sw.p;
   double* r = c->sr.p;
   double bn2;
@@ -944,6 +981,7 @@ int dg_ctx_create(const dg_ctx_desc* d, dg_ctx** out) {
       e = c->cflux.alloc((size_t)d->n_hang_groups * c->V * nqf);
   }
   const int max_grid = d->n_el + 1 + c->mesh.n_coarse;
+  c->max_grid = max_grid;
   if (e == cudaSuccess) e = c->mass_partial.alloc(max_grid);
   if (e == cudaSuccess) e = c->partial.alloc((size_t)RED_BLOCKS * 72 + (size_t)max_grid * 8);
   if (e == cudaSuccess) e = c->redout.alloc(256);
@@ -1312,8 +1350,8 @@ int dg_gs_update(dg_ctx* c, long long n, int nv, const double* V, long long vstr
   if (nv < 1 || nv > 32) return fail(DG_ERR_USAGE, "dg_gs_update: 1..32 vectors");
   if (!(na != 0.0)) return fail(DG_ERR_USAGE, "dg_gs_update: zero norm");
   CK(cudaStreamSynchronize(c->stream));  // the pinned staging slot is free
-  std::memcpy(c->pinned + 128, coefs_host, nv * sizeof(double));
-  CK(cudaMemcpyAsync(c->coef_dev.p, c->pinned + 128, nv * sizeof(double), cudaMemcpyHostToDevice,
+  std::memcpy(c->pin_coef(), coefs_host, nv * sizeof(double));
+  CK(cudaMemcpyAsync(c->coef_dev.p, c->pin_coef(), nv * sizeof(double), cudaMemcpyHostToDevice,
                      c->stream));
   CK(axpy_div(c->stream, n, nv, V, vstride, c->coef_dev.p, w, na, dst));
   return DG_OK;
@@ -1325,8 +1363,8 @@ int dg_dcgs2_update(dg_ctx* c, long long n, int nv, const double* V, long long v
   if (nv < 0 || nv > 31) return fail(DG_ERR_USAGE, "dg_dcgs2_update: 0..31 vectors");
   if (!(coefs_host[3 * nv + 2] != 0.0)) return fail(DG_ERR_USAGE, "dg_dcgs2_update: zero alpha");
   CK(cudaStreamSynchronize(c->stream));  // the pinned staging slot is free
-  std::memcpy(c->pinned + 128, coefs_host, (3 * nv + 3) * sizeof(double));
-  CK(cudaMemcpyAsync(c->coef_dev.p, c->pinned + 128, (3 * nv + 3) * sizeof(double),
+  std::memcpy(c->pin_coef(), coefs_host, (3 * nv + 3) * sizeof(double));
+  CK(cudaMemcpyAsync(c->coef_dev.p, c->pin_coef(), (3 * nv + 3) * sizeof(double),
                      cudaMemcpyHostToDevice, c->stream));
   CK(dcgs2_update(c->stream, n, nv, V, vstride, c->coef_dev.p, u, z, u_next, c->partial.p,
                   c->redout.p));

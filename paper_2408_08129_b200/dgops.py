@@ -72,6 +72,19 @@ class DGOperators:
         if tuple(t.shape) != want:
             raise UsageError(f"array shape {tuple(t.shape)}, expected {want}")
 
+    # ------------------------------------------------------------ engine
+    def weak_form(self, data, k_out, vol_flux, face_flux, bc_ghost, pool=None):
+        """The reference's generic weak-form engine (dgops.py:87-230) takes
+        numpy flux callbacks evaluated batch by batch on the host; the device
+        path has no generic callback engine, only the fused operators below
+        (divergence_advective / divergence_full / gradient_scalar /
+        divergence_hv), so this raises instead of silently running on the
+        CPU."""
+        raise UsageError(
+            "DGOperators.weak_form with host flux callbacks is not available on the B200 "
+            "path; use divergence_advective, divergence_full, gradient_scalar or "
+            "divergence_hv (fused device operators)")
+
     # ------------------------------------------------------------ duals
     def divergence_advective(self, data, model=DIMENSIONAL, bcs=None, pool=None):
         """Dual of the advective flux divergence, Rusanov with the flow speed
@@ -140,7 +153,8 @@ class DGOperators:
         return apply
 
     def apply_mass_inverse(self, dual):
-        """Factorised mass inverse (geometry.py:372-396)."""
+        """Factorised mass inverse (geometry.py:372-396); the reference's
+        entry point is ``MeshGeometry.apply_mass_inverse`` (same kernel)."""
         ctx = self.context()
         dt, host = to_device(dual, ctx)
         k = dt.shape[1] if dt.dim() == 3 else 1

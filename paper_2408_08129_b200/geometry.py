@@ -135,6 +135,52 @@ class MeshGeometry:
         self._cols = _Columns(surface, mesh) if self.terrain else None
         self._memo = {}
 
+    # ------------------------------------------------------------ mass inverse
+    def apply_mass_inverse(self, dual, out=None, elements=slice(None)):
+        """Nodal coefficients from a dual vector (geometry.py:372-396), on the
+        device: the factorised inverse B^-1 diag(1/(w detJ)) B^-T per element
+        (libdg dg_apply_mass_inverse).  dual: (n_sel, ..., n_nodes) for the
+        selected elements; numpy in -> numpy out (or into ``out``), CUDA
+        tensors stay on the device."""
+        from .dgops import from_device, to_device
+        from .physics import DIMENSIONAL
+        from . import _lib as L
+        from .device import DeviceContext, as_ptr
+        ctx = self._memo.get("mass_ctx")
+        if ctx is None:
+            ctx = DeviceContext(self, DIMENSIONAL)
+            self._memo["mass_ctx"] = ctx
+        t, host = to_device(dual, ctx)
+        shape = tuple(t.shape)
+        nn = self.basis.n_nodes
+        if shape[-1] != nn:
+            from .errors import UsageError
+            raise UsageError(f"dual has {shape[-1]} nodes per element, expected {nn}")
+        full = isinstance(elements, slice) and elements == slice(None)
+        n_el = self.mesh.n_leaves
+        k = 1
+        for s_ in shape[1:-1]:
+            k *= s_
+        if full:
+            src = t.reshape(shape[0], k, nn).contiguous()
+        else:
+            # block-diagonal inverse: embed the selected elements, apply, take
+            src = ctx.torch.zeros((n_el, k, nn), dtype=t.dtype, device=t.device)
+            idx = ctx.torch.as_tensor(np.arange(n_el)[elements], device=t.device)
+            src[idx] = t.reshape(shape[0], k, nn)
+        res = ctx.empty(k, nn, rows=src.shape[0])
+        L.check(ctx.lib.dg_apply_mass_inverse(ctx.bind_stream(), as_ptr(src), k, as_ptr(res)))
+        if not full:
+            res = res[idx]
+        res = res.reshape(shape)
+        if out is not None:
+            if isinstance(out, np.ndarray):
+                out[...] = res.cpu().numpy()
+            else:
+                out.copy_(res)
+            return out
+        return from_device(res, host)
+
     # ------------------------------------------------------------ column data
     def _colq(self):
         """h and grad h at the horizontal Gauss grid per column."""

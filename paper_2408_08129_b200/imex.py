@@ -20,6 +20,7 @@ from .device import as_ptr
 from .dgops import from_device, to_device
 from .errors import ConfigurationError, UsageError
 from .krylov import native_gmres
+from .timing import NullTimer, credit
 
 
 @dataclass(frozen=True)
@@ -197,6 +198,32 @@ class SplitOperators:
             R += to_device(self.forcing(t), ctx)[0]
         return from_device(R, host)
 
+    def implicit_residual(self, data):
+        """Pressure-gradient and enthalpy-divergence terms at the given state
+        (imex.py:161-175): R[momentum] = -M^-2 Minv Grad(p), R[energy] =
+        -Minv Div(h m), density row zero; device operators throughout."""
+        ctx = self.ctx
+        U, host = to_device(data, ctx)
+        d = self.dim
+        nn = self.geometry.basis.n_nodes
+        h = ctx.empty(nn)
+        K = ctx.empty(nn)
+        L.check(ctx.lib.dg_frozen_coefficients(ctx.bind_stream(), as_ptr(U), as_ptr(h), as_ptr(K)))
+        gm1 = self.model.gamma - 1.0
+        # p = (gamma - 1)(rho E - kf rho k)  (physics.py pressure, imex.py:203)
+        p = (U[:, 1 + d] - self.model.kinetic_factor * K) * gm1
+        R = ctx.torch.zeros_like(U)
+        gd = self.ops.gradient_scalar(p.contiguous(), self.model, self.bcs)
+        R[:, 1:1 + d] = -self.model.inv_mach_sq * self.ops.apply_mass_inverse(gd)
+        dv = self.ops.divergence_hv(U[:, 1:1 + d].contiguous(), h, self.model, self.bcs)
+        R[:, 1 + d] = -self.ops.apply_mass_inverse(dv)[:, 0]
+        return from_device(R, host)
+
+    def full_residual(self, data, t=0.0):
+        """explicit_residual + implicit_residual (imex.py:177-178)."""
+        E = self.explicit_residual(data, t)
+        return E + self.implicit_residual(data)
+
     def frozen_coefficients(self, data):
         ctx = self.ctx
         U, host = to_device(data, ctx)
@@ -284,22 +311,69 @@ def _step_error_info(cs):
                 values=float(cs.fail_value))
 
 
+def _solve_cfg(cfg, pc):
+    """The C struct of a solver config: the drop-in's own
+    ImplicitSolveConfig, or any object with the reference's fields (e.g.
+    orodg.imex.ImplicitSolveConfig, which has no ``c()``)."""
+    if hasattr(cfg, "c"):
+        return cfg.c(pc)
+    return ImplicitSolveConfig(
+        fp_tol=cfg.fp_tol, fp_max_iter=cfg.fp_max_iter, krylov_tol=cfg.krylov_tol,
+        krylov_restart=cfg.krylov_restart, krylov_max_iter=cfg.krylov_max_iter,
+        preconditioner=getattr(cfg, "preconditioner", "none"),
+        precond_refresh=getattr(cfg, "precond_refresh", 20)).c(pc)
+
+
+# libdg profiler classes -> the reference's timer blocks (timing.py:12-13):
+# the explicit operator is "explicit_residual", the Helmholtz applies and the
+# Gram-Schmidt passes inside GMRES are "krylov"; the rest of the native step
+# (stage combinations, F0, back-substitution, positivity) stays in
+# "implicit_fixed_point"
+_BLOCK_OF_CLASS = {0: "explicit_residual", 1: "krylov", 2: "krylov", 3: "krylov", 4: "krylov"}
+
+
+def _profiled(ctx, timer, fn):
+    """Run a native call inside timer.block("implicit_fixed_point") and move
+    the CUDA-event time of its explicit / Krylov kernels to their blocks."""
+    if timer is None or isinstance(timer, NullTimer):
+        return fn()
+    lib = ctx.lib
+    lib.dg_profile_enable(1)
+    try:
+        with timer.block("implicit_fixed_point"):
+            out = fn()
+            ms, by, cnt = (C.c_double * 6)(), (C.c_double * 6)(), (C.c_longlong * 6)()
+            lib.dg_profile_read(ms, by, cnt)
+    finally:
+        lib.dg_profile_enable(0)
+    for k, name in _BLOCK_OF_CLASS.items():
+        credit(timer, name, ms[k] * 1e-3, source="implicit_fixed_point")
+    return out
+
+
 def imex_step(data, t, dt, tableau, split, cfg, timer=None, precond=None):
-    """One IMEX-RK step (imex.py:252-299); returns (new_data, StepStats)."""
+    """One IMEX-RK step (imex.py:252-299); returns (new_data, StepStats).
+
+    ARS(2,2,2) without forcing runs as one native call (dg_imex_step); other
+    tableaux, or a SplitOperators with a forcing callable, run the
+    reference's stage loop over the device operators with the forcing added
+    to every explicit residual at t + c_ex[l] dt (imex.py:157-158, 286)."""
     ctx = split.ctx
     U, host = to_device(data, ctx)
     st = StepStats()
     pc = _bj_enter(split, cfg, precond)
     try:
-        if _is_ars222(tableau):
+        if _is_ars222(tableau) and split.forcing is None:
             out = ctx.empty(split.dim + 2, split.geometry.basis.n_nodes)
             cs = L.StepStatsC()
-            code = ctx.lib.dg_imex_step(ctx.bind_stream(), as_ptr(U), as_ptr(out), float(t),
-                                        float(dt), C.byref(cfg.c(pc)), C.byref(cs))
+            ccfg = _solve_cfg(cfg, pc)
+            code = _profiled(ctx, timer, lambda: ctx.lib.dg_imex_step(
+                ctx.bind_stream(), as_ptr(U), as_ptr(out), float(t), float(dt), C.byref(ccfg),
+                C.byref(cs)))
             st.absorb(cs)
             L.check(code, stats=st, **_step_error_info(cs))
             return from_device(out, host), st
-        return _generic_step(U, host, t, dt, tableau, split, cfg, st, pc)
+        return _generic_step(U, host, t, dt, tableau, split, cfg, st, pc, timer)
     finally:
         if pc:
             _bj_exit(split, precond)
@@ -312,8 +386,9 @@ def _lincomb(ctx, coefs, xs, out):
     L.check(ctx.lib.dg_lincomb(ctx.handle, n, len(xs), arr, ptrs, as_ptr(out)))
 
 
-def _generic_step(U, host, t, dt, tab, split, cfg, st, pc=False):
+def _generic_step(U, host, t, dt, tab, split, cfg, st, pc=False, timer=None):
     """Arbitrary tableau: the reference's stage loop over device operators."""
+    timer = timer or NullTimer()
     ctx = split.ctx
     ctx.bind_stream()
     s = tab.stages
@@ -334,9 +409,10 @@ def _generic_step(U, host, t, dt, tab, split, cfg, st, pc=False):
         else:
             it = ctx.empty(*acc.shape[1:])
             cs = L.StepStatsC()
-            code = ctx.lib.dg_solve_implicit_stage(ctx.handle, as_ptr(acc), as_ptr(U_stage),
-                                                   dt * a_ll, C.byref(cfg.c(pc)), as_ptr(it),
-                                                   C.byref(cs))
+            ccfg = _solve_cfg(cfg, pc)
+            code = _profiled(ctx, timer, lambda: ctx.lib.dg_solve_implicit_stage(
+                ctx.handle, as_ptr(acc), as_ptr(U_stage), dt * a_ll, C.byref(ccfg), as_ptr(it),
+                C.byref(cs)))
             st.absorb(cs)
             L.check(code, stats=st, **_step_error_info(cs))
             KI[l] = ctx.empty(*acc.shape[1:])
@@ -346,8 +422,15 @@ def _generic_step(U, host, t, dt, tab, split, cfg, st, pc=False):
         if tab.b_ex[l] != 0.0 or np.any(tab.a_ex[l + 1:, l] != 0.0):
             KE[l] = ctx.empty(*acc.shape[1:])
             mr = C.c_double()
-            L.check(ctx.lib.dg_explicit_residual(ctx.handle, as_ptr(U_stage), as_ptr(KE[l]),
-                                                 C.byref(mr)))
+            with timer.block("explicit_residual"):
+                L.check(ctx.lib.dg_explicit_residual(ctx.handle, as_ptr(U_stage), as_ptr(KE[l]),
+                                                     C.byref(mr)))
+                if split.forcing is not None:
+                    # imex.py:157-158: R += forcing(t) at the stage time
+                    f, _ = to_device(split.forcing(t + tab.c_ex[l] * dt), ctx)
+                    KE[l] += f.reshape(KE[l].shape)
+                if timer is not None and not isinstance(timer, NullTimer):
+                    ctx.torch.cuda.current_stream().synchronize()
             st.mass_rate += tab.b_ex[l] * mr.value
     if tab.stiffly_accurate:
         return from_device(U_stage, host), st
@@ -376,9 +459,10 @@ def _solve_implicit_stage(acc, guess, a_dt, split, cfg, stats, timer=None, preco
     cs = L.StepStatsC()
     pc = _bj_enter(split, cfg, precond)
     try:
-        code = ctx.lib.dg_solve_implicit_stage(ctx.bind_stream(), as_ptr(At), as_ptr(Gt),
-                                               float(a_dt), C.byref(cfg.c(pc)), as_ptr(it),
-                                               C.byref(cs))
+        ccfg = _solve_cfg(cfg, pc)
+        code = _profiled(ctx, timer, lambda: ctx.lib.dg_solve_implicit_stage(
+            ctx.bind_stream(), as_ptr(At), as_ptr(Gt), float(a_dt), C.byref(ccfg), as_ptr(it),
+            C.byref(cs)))
     finally:
         if pc:
             _bj_exit(split, precond)
@@ -390,13 +474,18 @@ def _solve_implicit_stage(acc, guess, a_dt, split, cfg, stats, timer=None, preco
 
 
 def run_time_loop(data, dt, t_final, stepper, callbacks=(), timer=None, t0=0.0):
-    """Fixed-dt driver landing exactly on t_final (imex.py:373-404)."""
+    """Fixed-dt driver landing exactly on t_final (imex.py:373-404): the
+    callbacks run inside timer.block("output"), one timer.step_snapshot()
+    per step, returns (data, timer.report(per_step))."""
     from .errors import SolverError
     if dt <= 0 or t_final <= t0:
         raise ConfigurationError("need dt > 0 and t_final > t0")
+    timer = timer or NullTimer()
+    per_step = []
     t = t0
-    for cb in callbacks:
-        cb(0, t, data, None)
+    with timer.block("output"):
+        for cb in callbacks:
+            cb(0, t, data, None)
     n_full = int(np.floor((t_final - t0) / dt + 1e-12))
     rem = (t_final - t0) - n_full * dt
     if rem < 1e-12 * dt:
@@ -409,6 +498,8 @@ def run_time_loop(data, dt, t_final, stepper, callbacks=(), timer=None, t0=0.0):
         except Exception as err:
             raise SolverError(f"step {step} at t={t:.6g} failed: {err}") from err
         t = t0 + step * dt if step < n_steps else t_final
-        for cb in callbacks:
-            cb(step, t, data, stats)
-    return data, None
+        with timer.block("output"):
+            for cb in callbacks:
+                cb(step, t, data, stats)
+        per_step.append(timer.step_snapshot())
+    return data, timer.report(per_step)

@@ -7,8 +7,10 @@ on the GPU:
   native solver loop of libdg (dg_gmres_helmholtz): basis, Gram-Schmidt
   dots/updates and the operator all on the device, Givens rotations on the
   host from one small read-back per Arnoldi step;
-* any other linear callable is driven from Python over torch CUDA tensors
-  (the callable receives and must return a CUDA float64 vector).
+* any other linear callable is driven from Python over torch CUDA tensors:
+  a device callable receives and returns CUDA float64 vectors, a host
+  callable in the reference's numpy convention is detected and fed host
+  copies (``_Operand``).
 
 Orthogonalisation is classical Gram-Schmidt with the reference's selective
 re-orthogonalisation test (norm drop below 1/sqrt 2 => one more pass) --
@@ -161,11 +163,45 @@ def _block_jacobi_torch(action, n_el, n_nodes, colors):
     return apply
 
 
+class _Operand:
+    """Adapter for a user callable in the generic path: device callables get
+    and return CUDA float64 vectors; a host callable in the reference's
+    convention (numpy in, numpy out, krylov.py:27) is detected on first use
+    -- it rejects the CUDA tensor or returns a numpy array -- and from then
+    on gets a host copy, its result is moved to the device.  The Krylov
+    basis, Gram-Schmidt passes and updates stay on the device either way."""
+
+    def __init__(self, fn, dev):
+        self.fn = fn
+        self.dev = dev
+        self.host = None
+
+    def __call__(self, v):
+        import torch
+        if self.host is None:
+            try:
+                out = self.fn(v)
+                self.host = not isinstance(out, torch.Tensor)
+            except (TypeError, RuntimeError, AttributeError, ValueError):
+                self.host = True
+                out = self.fn(v.detach().cpu().numpy())
+        elif self.host:
+            out = self.fn(v.detach().cpu().numpy())
+        else:
+            out = self.fn(v)
+        if not isinstance(out, torch.Tensor):
+            out = torch.as_tensor(np.asarray(out, dtype=np.float64), device=self.dev)
+        return out.reshape(-1).to(device=self.dev, dtype=torch.float64)
+
+
 def _gmres_torch(action, rhs, x0, tol_rel, restart, max_iter, preconditioner):
     import torch
     if not torch.cuda.is_available():
         raise DeviceError("gmres runs on the device; no CUDA device visible")
     dev = "cuda"
+    action = _Operand(action, dev)
+    if preconditioner is not None:
+        preconditioner = _Operand(preconditioner, dev)
     host = not isinstance(rhs, torch.Tensor)
     b = torch.as_tensor(np.asarray(rhs, dtype=np.float64).ravel() if host else rhs,
                         dtype=torch.float64, device=dev).reshape(-1)

@@ -96,15 +96,26 @@ def build(name):
         return _terrain(name, m, 3, hill3d, ext,
                         cases.SpongeConfig(top_depth=4.0e3, lateral_width=5.0e3),
                         (0, 1), 31, 0.3, dt=0.5)
-    if name == "per3d":
+    if name == "hang3d_r4":
+        ext = (20.0e3, 20.0e3, 10.0e3)
+        m = build_uniform_mesh(ext, (4, 4, 2))
+        m = refine_region(m, lambda lf: bool(np.all(np.abs(lf.center[:2] - 10.0e3) < 5.0e3)
+                                             and lf.center[2] < 5.0e3), times=1)
+        return _terrain(name, m, 4, hill3d, ext,
+                        cases.SpongeConfig(top_depth=4.0e3, lateral_width=5.0e3),
+                        (0, 1), 37, 0.3, dt=0.5)
+    if name in ("per3d", "per3d_r4", "cfg5s"):
         ext = (10.0e3, 10.0e3, 10.0e3)
-        m = build_uniform_mesh(ext, (4, 4, 4), periodic=(True, True, True))
-        pick = np.random.default_rng(5).random(m.n_leaves) < 0.3
+        root, pseed, frac, deg, useed = {
+            "per3d": (4, 5, 0.3, 2, 41), "per3d_r4": (3, 7, 0.3, 4, 43),
+            "cfg5s": (6, 5, 0.07, 3, 41)}[name]
+        m = build_uniform_mesh(ext, (root,) * 3, periodic=(True, True, True))
+        pick = np.random.default_rng(pseed).random(m.n_leaves) < frac
         m = refine_region(m, lambda lf: bool(pick[lf.index]), 1)
-        geom = build_geometry(m, 2)
+        geom = build_geometry(m, deg)
         bg = project_initial_data(
             geom, cases.hydrostatic_initial_state(cases.HillCaseConfig(domain=ext))).data
-        U = cases.perturbed_state(bg, geom.node_coords, ext, 41)
+        U = cases.perturbed_state(bg, geom.node_coords, ext, useed)
         return Case(name, m, geom, [], None, U, 0.3)
     if name == "cfg3s":
         ext = (50.0e3, 21.0e3)
@@ -143,6 +154,20 @@ def parity_tols(z, key, floor=1e-12, factor=10.0):
     return np.maximum(floor, factor * np.asarray(z[nk]))
 
 
+# achieved errors of every parity check of the session, written by
+# conftest.pytest_sessionfinish to $DG_PARITY_LOG (profiles/r2_parity.json)
+PARITY_LOG = []
+
+
+def record(case, key, errs, tols, **extra):
+    import os as _os
+    rec = {"test": _os.environ.get("PYTEST_CURRENT_TEST", "").split(" ")[0], "case": case,
+           "key": key, "err": [float(e) for e in np.atleast_1d(errs)],
+           "tol": [float(t) for t in np.atleast_1d(tols)]}
+    rec.update(extra)
+    PARITY_LOG.append(rec)
+
+
 def assert_parity(got, z, key, floor=1e-12, factor=10.0):
     ref = z[key]
     got = np.asarray(got)
@@ -152,5 +177,14 @@ def assert_parity(got, z, key, floor=1e-12, factor=10.0):
     tols = parity_tols(z, key, floor, factor)
     if tols is None:
         tols = np.full(len(errs), floor)
+    record(str(z.get("case", "?")), key, errs, tols)
     assert np.all(errs <= tols), f"{key}: per-var err {errs} > tol {tols}"
     return errs
+
+
+def check_rel(case, key, got, ref, tol, floor=0.0):
+    """Whole-array relative L2 gate, logged with its achieved value."""
+    e = rel(got, ref, floor)
+    record(case, key, [e], [tol])
+    assert e <= tol, f"{case} {key}: rel err {e:.3e} > {tol:.1e}"
+    return e

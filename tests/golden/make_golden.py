@@ -20,6 +20,11 @@ Cases (inputs built only through the reference's public API):
   cfg3s    scaled-down Schar case (terrain, sponge, far-field, 2 refinement
            levels near the ground), r=4, 3 steps
   part     partition_leaves on the cfg2 mesh, P=1..8, unit and seeded weights
+  hang3d_r4  hang3d's mesh at r=4 (25-lane elements on the device)
+  per3d_r4   periodic seeded-refined box at r=4
+  cfg5s    BASELINE configs[4] recipe at 6^3 roots, r=3
+  dropin   implicit/full residual, forced step, subset mass inverse, host
+           gmres with restart 40
 
 Warm-bubble recipe (harness choice, recorded here and mirrored by
 paper_2408_08129_b200.cases.warm_bubble_state): constant theta0 = 300 K
@@ -583,9 +588,116 @@ def case_full():
     save("full", rec)
 
 
+def case_hang3d_r4():
+    """hang3d's terrain + hanging + far-field + sponge mesh at r=4 (n^(d-1)
+    = 25 lanes per element on the device): every operator, one GMRES solve,
+    one step."""
+    ext = (20.0e3, 20.0e3, 10.0e3)
+    m = build_uniform_mesh(ext, (4, 4, 2))
+    mesh = refine_region(
+        m, lambda lf: bool(np.all(np.abs(lf.center[:2] - 10.0e3) < 5.0e3)
+                           and lf.center[2] < 5.0e3), times=1)
+    geom, ops, model, bg, U, bcs, split, sigma = _terrain_case(
+        mesh, 4, hill3d, cases.HillCaseConfig(domain=ext),
+        cases.SpongeConfig(top_depth=4.0e3, lateral_width=5.0e3), (0, 1), 37, ext)
+    rec = {"case": np.array("hang3d_r4"), "degree": np.array(4), "background": bg,
+           "sigma": sigma}
+    rec.update(mesh_record(mesh))
+    rec.update(operator_record(ops, split, U, model, bcs, 37, 0.3))
+    rec.update(gmres_record(split, U, 0.3, 1e-8, 37))
+    rec.update(steps_record(split, U, 0.5, 1, imex.ImplicitSolveConfig()))
+    save("hang3d_r4", rec)
+
+
+def case_per3d_r4():
+    """per3d's triply-periodic seeded-refined box at r=4."""
+    ext = (10.0e3, 10.0e3, 10.0e3)
+    m = build_uniform_mesh(ext, (3, 3, 3), periodic=(True, True, True))
+    pick = np.random.default_rng(7).random(m.n_leaves) < 0.3
+    mesh = refine_region(m, lambda lf: bool(pick[lf.index]), 1)
+    geom = build_geometry(mesh, 4)
+    ops = DGOperators(geom)
+    model = FlowModel.dimensional()
+    bg = project_initial_data(
+        geom, cases.hydrostatic_initial_state(cases.HillCaseConfig(domain=ext))).data
+    U = perturbed(bg, geom.node_coords, ext, 43)
+    split = imex.SplitOperators(ops, model, [])
+    rec = {"case": np.array("per3d_r4"), "degree": np.array(4), "pick": pick}
+    rec.update(mesh_record(mesh))
+    rec.update(operator_record(ops, split, U, model, [], 43, 0.3))
+    save("per3d_r4", rec)
+
+
+def case_cfg5s():
+    """BASELINE configs[4] recipe at a reduced root count:
+    periodic (10 km)^3, 6^3 roots, a seeded 7% refined once, r=3,
+    hydrostatic background + seeded smooth 1e-3 perturbations."""
+    ext = (10.0e3, 10.0e3, 10.0e3)
+    m = build_uniform_mesh(ext, (6, 6, 6), periodic=(True, True, True))
+    pick = np.random.default_rng(5).random(m.n_leaves) < 0.07
+    mesh = refine_region(m, lambda lf: bool(pick[lf.index]), 1)
+    geom = build_geometry(mesh, 3)
+    ops = DGOperators(geom)
+    model = FlowModel.dimensional()
+    bg = project_initial_data(
+        geom, cases.hydrostatic_initial_state(cases.HillCaseConfig(domain=ext))).data
+    U = perturbed(bg, geom.node_coords, ext, 41)
+    split = imex.SplitOperators(ops, model, [])
+    rec = {"case": np.array("cfg5s"), "degree": np.array(3), "pick": pick}
+    rec.update(mesh_record(mesh))
+    rec.update(operator_record(ops, split, U, model, [], 41, 0.3))
+    rec.update(gmres_record(split, U, 0.3, 1e-8, 41))
+    save("cfg5s", rec)
+
+
+def case_dropin():
+    """Drop-in API surface beyond the hot operators, on hang3d's mesh (r=3):
+    implicit_residual / full_residual (imex.py:161-178), a forced ARS(2,2,2)
+    step (imex.py:157-158; forcing(t) = (1 + t/10) S, S a seeded smooth
+    field), MeshGeometry.apply_mass_inverse on an element subset
+    (geometry.py:372-396), and gmres on a host (numpy) operator with
+    restart 40 > 31 (krylov.py:27-115)."""
+    ext = (20.0e3, 20.0e3, 10.0e3)
+    m = build_uniform_mesh(ext, (4, 4, 2))
+    mesh = refine_region(
+        m, lambda lf: bool(np.all(np.abs(lf.center[:2] - 10.0e3) < 5.0e3)
+                           and lf.center[2] < 5.0e3), times=1)
+    geom, ops, model, bg, U, bcs, split, sigma = _terrain_case(
+        mesh, 3, hill3d, cases.HillCaseConfig(domain=ext),
+        cases.SpongeConfig(top_depth=4.0e3, lateral_width=5.0e3), (0, 1), 31, ext)
+    rec = {"case": np.array("dropin"), "U": U}
+    rec["implicit_residual"] = split.implicit_residual(U)
+    rec["full_residual"] = split.full_residual(U, 0.0)
+    rng = np.random.default_rng(99)
+    S = np.zeros_like(U)
+    for v in range(U.shape[1]):
+        S[:, v] = 1e-4 * np.abs(U[:, v]).max() * smooth_noise(geom.node_coords, ext, rng)
+    rec["forcing_S"] = S
+    fsplit = imex.SplitOperators(ops, model, bcs, sponge=(sigma, bg),
+                                 forcing=lambda t: (1.0 + t / 10.0) * S)
+    Uf, st = imex.imex_step(U, 0.25, 0.5, imex.ars222(), fsplit, imex.ImplicitSolveConfig())
+    rec["forced_U1"] = Uf
+    rec["forced_krylov"] = np.array(st.krylov_iters)
+    rec["forced_fp"] = np.array(st.fp_iters)
+    sel = np.arange(0, mesh.n_leaves, 3)
+    dual = ops.divergence_advective(U, model, bcs)[sel]
+    rec["minv_sel"] = sel
+    rec["minv_sel_dual"] = dual
+    rec["minv_sel_out"] = geom.apply_mass_inverse(dual, elements=sel)
+    n = 120
+    A = np.eye(n) + 0.3 * rng.standard_normal((n, n)) / np.sqrt(n)
+    b = rng.standard_normal(n)
+    x, kst = krylov.gmres(lambda v: A @ v, b, tol_rel=1e-10, restart=40, max_iter=500)
+    rec["gm_A"], rec["gm_b"], rec["gm_x"] = A, b, x
+    rec["gm_iters"] = np.array(kst.iterations)
+    rec["gm_history"] = np.array(kst.residual_history)
+    save("dropin", rec)
+
+
 CASES = {"cfg2ops": case_cfg2ops, "cfg1": case_cfg1, "hang2d": case_hang2d, "hang3d": case_hang3d,
          "per3d": case_per3d, "cfg3s": case_cfg3s, "part": case_part,
-         "cfg2": case_cfg2, "bj": case_bj, "full": case_full}
+         "cfg2": case_cfg2, "bj": case_bj, "full": case_full, "hang3d_r4": case_hang3d_r4,
+         "per3d_r4": case_per3d_r4, "cfg5s": case_cfg5s, "dropin": case_dropin}
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(CASES)

@@ -8,7 +8,7 @@ import pytest
 from casebuild import assert_parity, build, golden, per_var_rel, rel
 from oracle import dg_oracle as O
 
-OP_CASES = ["cfg1", "hang2d", "hang3d", "per3d", "cfg3s"]
+OP_CASES = ["cfg1", "hang2d", "hang3d", "per3d", "cfg3s", "hang3d_r4", "per3d_r4", "cfg5s"]
 
 
 def _ops(c):
@@ -58,7 +58,7 @@ def test_oracle_linear_operators_match_reference(name):
     assert rel(ops.integrate_conserved(c.U), z["integrate_conserved"]) <= 1e-13
 
 
-@pytest.mark.parametrize("name", ["cfg1", "hang2d", "hang3d"])
+@pytest.mark.parametrize("name", ["cfg1", "hang2d", "hang3d", "hang3d_r4", "cfg5s"])
 def test_oracle_gmres_matches_reference(name):
     c, z = build(name), golden(name)
     ops = _ops(c)
