@@ -12,9 +12,13 @@ value = whole-job throughput with the state resident in HBM; e2e = the same
 through the public imex_step API with the state copied host->device and
 back every step.  The state is 6.4 GB >> 126 MB L2, so no flush is needed.
 
---impl reference times the reference algorithm on the host CPU (the numpy
-oracle port, oracle/dg_oracle.py, all host threads) on a bounded sample of
-the same recipe (a smaller root grid), reported in the same unit.
+--impl reference times the REAL reference (orodg from baseline/_ref, its own
+public API, WorkerPool over the physical cores, BLAS single-threaded as its
+CLI sets it) on a bounded sample of the same recipe: a central 6x6x20-root
+window of the cfg4 mesh around the hill (6,264 cells, 2.0 M DoF).  The B200
+line carries the same sample timed on one host core (cpu_baseline, kind
+"reference") and on the GPU (same_problem: same inputs, same first step,
+both sides' iteration counts).
 """
 
 import argparse
@@ -127,51 +131,194 @@ def traffic(workload, kernel_class, algorithmic_per_launch):
 
 
 # ------------------------------------------------------------ CPU baseline
-def cpu_step_sample(workload, threads, budget_s=30.0):
-    """Reference algorithm (numpy oracle port) on a bounded sample of the
-    workload recipe: one IMEX step on a shrunken root grid."""
-    from threadpoolctl import threadpool_limits
+# The like-for-like sample: a central n x n x 20-root window of the cfg4
+# recipe (cases.baseline_case("cfg4w<n>")), built and stepped by the REAL
+# reference (orodg, installed in baseline/_ref; /root/reference/pkg/src in
+# the build container) through its own public API -- build_uniform_mesh,
+# refine_region, build_geometry, project_initial_data, farfield_bcs,
+# sponge_sigma, DGOperators(geometry, WorkerPool(P)), SplitOperators,
+# imex_step -- and by the B200 path on the same inputs.  The oracle port
+# (oracle/dg_oracle.py) is the fallback only when orodg is not importable.
+WINDOW = {"cfg4": 6, "cfg3": None, "cfg2": None, "cfg1": None}
 
+
+def _import_reference():
+    for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(p, "orodg")):
+            if p not in sys.path:
+                sys.path.insert(0, p)
+            import orodg  # noqa: F401
+            return p
+    return None
+
+
+def physical_cores():
+    try:
+        from orodg.parallel import physical_cores as pc
+        return pc()
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def reference_case(workload, workers):
+    """(split, U0, dt, dof, desc) of the workload's bounded sample, built
+    with the reference's own API."""
+    import numpy as np
+    from orodg import cases as rc
+    from orodg import imex as ri
+    from orodg.boundary import wall_everywhere
+    from orodg.dgops import DGOperators
+    from orodg.field import project_initial_data
+    from orodg.geometry import build_geometry
+    from orodg.mesh import build_uniform_mesh, refine_region
+    from orodg.parallel import WorkerPool
+    from orodg.physics import FlowModel
+    model = FlowModel.dimensional()
+    pool = WorkerPool(workers)
+    if workload == "cfg4":
+        n = WINDOW["cfg4"]
+        ext = (500.0 * n, 500.0 * n, 20.0e3)
+        mesh = build_uniform_mesh(ext, (n, n, 20))
+        mesh = refine_region(mesh, lambda lf: lf.center[2] < 6.0e3, 1)
+        mesh = refine_region(mesh, lambda lf: lf.center[2] < 2.0e3, 1)
+        xc, yc = ext[0] / 2, ext[1] / 2
+
+        def hill(x, y):  # BASELINE configs[3] hill (cases.gaussian_hill)
+            return 400.0 * np.exp(-(((x - xc) ** 2 + (y - yc) ** 2) / 3.0e3 ** 2))
+
+        geom = build_geometry(mesh, 3, terrain=hill)
+        hc = rc.HillCaseConfig(domain=ext, x_c=xc, y_c=yc)
+        bg = project_initial_data(geom, rc.hydrostatic_initial_state(hc)).data
+        bcs = rc.farfield_bcs(geom, bg)
+        sigma = rc.sponge_sigma(geom, rc.SpongeConfig(), ext, lateral_axes=())
+        split = ri.SplitOperators(DGOperators(geom, pool), model, bcs, sponge=(sigma, bg))
+        U0, dt = bg.copy(), 0.5
+        desc = (f"central {n}x{n}x20-root window of the cfg4 recipe ({mesh.n_leaves} cells, "
+                f"r=3, top sponge; the lateral sponge lies outside the window)")
+        cfg = ri.ImplicitSolveConfig()
+    elif workload in ("cfg1", "cfg2"):
+        root = (32, 16) if workload == "cfg1" else (64, 32)
+        mesh = build_uniform_mesh((20.0e3, 10.0e3), root)
+        if workload == "cfg2":
+            mesh = refine_region(mesh, lambda lf: lf.center[1] < 5.0e3, 1)
+        geom = build_geometry(mesh, 2 if workload == "cfg1" else 4)
+        from paper_2408_08129_b200.cases import warm_bubble_state
+        U0 = project_initial_data(geom, warm_bubble_state()).data
+        split = ri.SplitOperators(DGOperators(geom, pool), model, wall_everywhere(mesh))
+        dt = 0.5
+        desc = f"{workload} (full size)"
+        cfg = ri.ImplicitSolveConfig(krylov_tol=1e-8 if workload == "cfg1" else 1e-10)
+    else:
+        raise ValueError(f"no reference sample for {workload}")
+    dof = U0.size
+    return split, U0, dt, dof, desc, cfg, pool
+
+
+def reference_steps(workload, workers, n_steps, warmup=0):
+    """Time n_steps ARS(2,2,2) steps of the real reference on the sample."""
+    import time as _t
+    from orodg import imex as ri
+    split, U, dt, dof, desc, cfg, pool = reference_case(workload, workers)
+    tab = ri.ars222()
+    t = 0.0
+    for _ in range(warmup):
+        U, st = ri.imex_step(U, t, dt, tab, split, cfg)
+        t += dt
+    secs, kry = [], []
+    for _ in range(n_steps):
+        t0 = _t.perf_counter()
+        U, st = ri.imex_step(U, t, dt, tab, split, cfg)
+        secs.append(_t.perf_counter() - t0)
+        kry.append((list(st.fp_iters), list(st.krylov_iters)))
+        t += dt
+    pool.close()
+    return {"seconds": secs, "dof": dof, "desc": desc, "iterations": kry}
+
+
+def port_step_sample(workload, budget_s=30.0):
+    """Fallback when orodg is not importable: the numpy oracle port on the
+    same sample (one step, one thread)."""
     from oracle import dg_oracle as O
     from paper_2408_08129_b200.cases import baseline_case
-    scale = {"cfg4": 3.0 / 120.0, "cfg3": 20.0 / 400.0, "cfg2": 1.0, "cfg1": 1.0}[workload]
-    c = baseline_case(workload, root_scale=scale)
+    name = f"cfg4w{WINDOW['cfg4']}" if workload == "cfg4" else workload
+    c = baseline_case(name)
     ops = O.Operators(c.geometry, c.model, c.bcs, c.sponge)
-    d = c.mesh.dim
-    nn = c.geometry.basis.n_nodes
-    dofs = c.mesh.n_leaves * nn * (d + 2)
-    with threadpool_limits(threads):
-        t0 = time.perf_counter()
-        U, st = O.imex_step(ops, c.U0, 0.0, c.dt, **{k: v for k, v in c.solve.items()})
-        t = time.perf_counter() - t0
-    return {"value": dofs / t, "unit": "DoF/s", "cores": threads, "kind": "port",
-            "seconds_per_step": t,
-            "sample": f"1 ARS(2,2,2) step of the {workload} recipe on a "
-                      f"{'x'.join(map(str, c.mesh.root_counts))} root grid "
-                      f"({c.mesh.n_leaves} cells, {dofs} DoF), krylov {st.krylov_iters}"}
+    t0 = time.perf_counter()
+    U, st = O.imex_step(ops, c.U0, 0.0, c.dt, **{k: v for k, v in c.solve.items()})
+    t = time.perf_counter() - t0
+    return {"seconds": [t], "dof": c.U0.size, "desc": c.description,
+            "iterations": [(list(st.fp_iters), list(st.krylov_iters))]}
+
+
+def cpu_sample(workload, workers, n_steps=1, warmup=0):
+    """(result dict, kind) -- the real reference when importable, else the port."""
+    if _import_reference() is not None:
+        return reference_steps(workload, workers, n_steps, warmup), "reference"
+    return port_step_sample(workload), "port"
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
-    vals = []
-    last = None
-    for _ in range(args.steps):
-        last = cpu_step_sample(args.workload, threads)
-        vals.append(last["seconds_per_step"])
-    ms = 1e3 * sum(vals) / len(vals)
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from threadpoolctl import threadpool_limits
+    _import_reference()
+    workers = physical_cores()
+    with threadpool_limits(1):  # the reference's own setting (cli.py:7-8)
+        res, kind = cpu_sample(args.workload, workers, args.steps, args.warmup)
+    secs = res["seconds"]
+    ms = 1e3 * sum(secs) / len(secs)
+    value = res["dof"] * len(secs) / sum(secs)
     line = {"metric": "fp64 DoF/s per ARS(2,2,2) IMEX-RK step (all variables)",
-            "value": last["value"], "unit": "DoF/s", "n_gpus": args.gpus, "steps": args.steps,
+            "value": value, "unit": "DoF/s", "n_gpus": args.gpus, "steps": len(secs),
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": args.workload, "description": DESC[args.workload]},
-            "cpu_baseline": {k: last[k] for k in ("value", "unit", "cores", "kind", "sample")},
-            "e2e": {"value": last["value"], "unit": "DoF/s", "h2d_bytes_per_step": 0,
+            "config": {"workload": args.workload, "description": DESC[args.workload],
+                       "sample": res["desc"], "iterations": res["iterations"]},
+            "cpu_baseline": {"value": value, "unit": "DoF/s", "cores": workers, "kind": kind,
+                             "sample": res["desc"] + f"; {len(secs)} timed steps, WorkerPool("
+                                                     f"{workers}) threads, BLAS 1 thread"},
+            "e2e": {"value": value, "unit": "DoF/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def same_problem(workload, dev, cpu):
+    """The B200 path on the CPU baseline's own sample (same recipe, same
+    inputs, same first step through the public imex_step with host buffers):
+    the like-for-like ratio, with both sides' iteration counts."""
+    import numpy as np
+    import torch
+    from paper_2408_08129_b200.cases import baseline_case
+    from paper_2408_08129_b200.dgops import DGOperators
+    from paper_2408_08129_b200.imex import ImplicitSolveConfig, SplitOperators, ars222, imex_step
+    name = f"cfg4w{WINDOW['cfg4']}" if workload == "cfg4" else workload
+    c = baseline_case(name)
+    split = SplitOperators(DGOperators(c.geometry), c.model, c.bcs, c.sponge)
+    cfg = ImplicitSolveConfig(**c.solve)
+    U0 = np.ascontiguousarray(c.U0)
+    # first step (the one the CPU timed), repeated from the same host state
+    U1, st = imex_step(U0, 0.0, c.dt, ars222(), split, cfg)
+    torch.cuda.synchronize()
+    reps = 5
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        U1, st = imex_step(U0, 0.0, c.dt, ars222(), split, cfg)
+    torch.cuda.synchronize()
+    t = (time.perf_counter() - t0) / reps
+    gpu = U0.size / t
+    return {"workload": name, "description": c.description, "dof": int(U0.size),
+            "gpu_e2e_dofs_per_s": gpu, "gpu_seconds_per_step": t,
+            "gpu_iterations": [list(st.fp_iters), list(st.krylov_iters)],
+            "cpu_dofs_per_s": cpu["value"], "cpu_kind": cpu["kind"], "cpu_cores": cpu["cores"],
+            "cpu_iterations": cpu["iterations"][0] if cpu.get("iterations") else None,
+            "speedup_vs_1_core": gpu / cpu["value"],
+            "note": "one GPU vs one host core, both stepping the same first ARS(2,2,2) step "
+                    "of the same sample through their public imex_step (GPU: numpy in, numpy "
+                    "out, host<->device copies included)"}
 
 
 # ------------------------------------------------------------------ B200
@@ -303,10 +450,20 @@ def main():
            "ms_per_step": ms_e2e, "wall_s_per_step": wall_e2e}
 
     cpu = None
+    same = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_step_sample(args.workload, 1)
-            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            from threadpoolctl import threadpool_limits
+            _import_reference()
+            with threadpool_limits(1):
+                res, kind = cpu_sample(args.workload, 1, 1)
+            v = res["dof"] * len(res["seconds"]) / sum(res["seconds"])
+            cpu = {"value": v, "unit": "DoF/s", "cores": 1, "kind": kind,
+                   "sample": res["desc"] + "; 1 ARS(2,2,2) step from the initial state, "
+                             "WorkerPool(1), BLAS 1 thread",
+                   "seconds_per_step": sum(res["seconds"]) / len(res["seconds"]),
+                   "iterations": res["iterations"]}
+            same = same_problem(args.workload, dev, cpu)
         except Exception as err:  # pragma: no cover
             cpu = {"error": str(err)}
 
@@ -335,6 +492,7 @@ def main():
                          "share_of_step": ms_c[k_dom] / ms_total},
             "kernel_breakdown": breakdown,
             "cpu_baseline": cpu,
+            "same_problem": same,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),

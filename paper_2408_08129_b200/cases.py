@@ -260,6 +260,24 @@ def baseline_case(name, root_scale=1.0, with_state=True):
                              with_state, 0.5,
                              "3D Gaussian hill 60x60x20 km, 120x120x20 root, refined z<6 km "
                              "and z<2 km (3 levels), r=3")
+    if name.startswith("cfg4w"):
+        # "cfg4w<n>": an n x n x 20 root window of the cfg4 recipe centred on
+        # the hill -- the same 500 m roots, refinement (z < 6 km, z < 2 km),
+        # hill, dt, far-field / wall boundaries and top sponge; the 10 km
+        # lateral sponge of the full 60 km box lies outside a central window
+        # (<= 40 km), so it is absent.  The like-for-like sample on which the
+        # CPU reference and the GPU are timed side by side (bench.py)
+        n = int(name[5:]) if len(name) > 5 else 6
+        ext = (500.0 * n, 500.0 * n, 20.0e3)
+        mesh = build_uniform_mesh(ext, (n, n, 20))
+        zc = lambda lo, hi: 0.5 * (lo[:, -1] + hi[:, -1])  # noqa: E731
+        mesh = refine_region(mesh, lambda i, l, o, lo, hi: zc(lo, hi) < 6.0e3, 1, vectorized=True)
+        mesh = refine_region(mesh, lambda i, l, o, lo, hi: zc(lo, hi) < 2.0e3, 1, vectorized=True)
+        hc = HillCaseConfig(domain=ext, x_c=ext[0] / 2, y_c=ext[1] / 2)
+        geom = build_geometry(mesh, 3, terrain=gaussian_hill(xc=ext[0] / 2, yc=ext[1] / 2))
+        return _terrain_case(name, mesh, geom, model, hc, SpongeConfig(), (), with_state, 0.5,
+                             f"cfg4 recipe, central {n}x{n}x20-root window (lateral sponge "
+                             "outside the window), r=3")
     if name.startswith("cfg5"):
         # "cfg5_r<degree>": the operator microbenchmark (BASELINE configs[4],
         # SURVEY.md §8d): periodic (10 km)^3 box, a seeded 7% of the roots

@@ -59,10 +59,10 @@ struct HLayout {
 };
 
 #ifndef DG_HK1_MINB
-#define DG_HK1_MINB 6
+#define DG_HK1_MINB 5
 #endif
 #ifndef DG_HK2_MINB
-#define DG_HK2_MINB 6
+#define DG_HK2_MINB 4
 #endif
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -328,9 +328,10 @@ hgrad_kernel(const __grid_constant__ KParams<N> P) {
   // p_own (wall), 0 (far field, homogeneous); coarse side precomputed
   double flv[2 * (D - 1)];  // vertical faces: the AX component only
   double flz[2][D];         // z faces
-  auto face = [&](auto ax_c, int side) {
+  auto face = [&](auto ax_c, auto side_c) {
     constexpr int AX = decltype(ax_c)::value;
-    const int f = 2 * AX + side;
+    constexpr int side = decltype(side_c)::value;
+    constexpr int f = 2 * AX + side;
     const int kd = kf[f] & 15;
     double to = 0.0;
 #pragma unroll
@@ -356,25 +357,28 @@ hgrad_kernel(const __grid_constant__ KParams<N> P) {
         fl[a] = sg * (hw[a] * ph);
       }
     }
+    // (a wall's mirrored ghost cancels the div(hV) flux: psi = 0 there, so
+    // H2 sums psi + pin uniformly over conforming, wall and far-field faces)
+    const double keep = (kd == KIND_WALL) ? 0.0 : 1.0;
     if constexpr (AX < D - 1) {
       flv[f] = fl[AX];
-      HW[f * NC + c] = hw[AX];
+      HW[f * NC + c] = keep * hw[AX];
     } else {
 #pragma unroll
       for (int a = 0; a < D; ++a) {
         flz[side][a] = fl[a];
-        HW[(2 * (D - 1) + side * D + a) * NC + c] = hw[a];
+        HW[(2 * (D - 1) + side * D + a) * NC + c] = keep * hw[a];
       }
     }
   };
-  face(std::integral_constant<int, 0>{}, 0);
-  face(std::integral_constant<int, 0>{}, 1);
+  face(std::integral_constant<int, 0>{}, std::integral_constant<int, 0>{});
+  face(std::integral_constant<int, 0>{}, std::integral_constant<int, 1>{});
   if constexpr (D == 3) {
-    face(std::integral_constant<int, 1>{}, 0);
-    face(std::integral_constant<int, 1>{}, 1);
+    face(std::integral_constant<int, 1>{}, std::integral_constant<int, 0>{});
+    face(std::integral_constant<int, 1>{}, std::integral_constant<int, 1>{});
   }
-  face(std::integral_constant<int, D - 1>{}, 0);
-  face(std::integral_constant<int, D - 1>{}, 1);
+  face(std::integral_constant<int, D - 1>{}, std::integral_constant<int, 0>{});
+  face(std::integral_constant<int, D - 1>{}, std::integral_constant<int, 1>{});
   // own h traces at the face points (frozen per fixed-point iterate)
   double hf[NF];
 #pragma unroll
@@ -478,14 +482,24 @@ hgrad_kernel(const __grid_constant__ KParams<N> P) {
     }
   if (act) {
     double* ps = P.psi_out + e * (NF * NC);
+    double pv[NF];
 #pragma unroll
-    for (int f = 0; f < 2 * (D - 1); ++f) ps[f * NC + c] = hf[f] * (HW[f * NC + c] * tv[f]);
+    for (int f = 0; f < 2 * (D - 1); ++f) pv[f] = hf[f] * (HW[f * NC + c] * tv[f]);
 #pragma unroll
     for (int side = 0; side < 2; ++side) {
       double vn = 0.0;
 #pragma unroll
       for (int a = 0; a < D; ++a) vn = fma(HW[(2 * (D - 1) + side * D + a) * NC + c], tz[side][a], vn);
-      ps[(2 * (D - 1) + side) * NC + c] = hf[2 * (D - 1) + side] * vn;
+      pv[2 * (D - 1) + side] = hf[2 * (D - 1) + side] * vn;
+    }
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      ps[f * NC + c] = pv[f];
+      // the conforming neighbour's incoming slot (its face f ^ 1): H2 then
+      // reads only its own contiguous rows (ghost neighbours: hk_pin_fixup
+      // after the halo exchange)
+      if (P.pin_out != nullptr && (kf[f] & 15) == KIND_CONF && nf[f] < mesh.n_el)
+        P.pin_out[(long long)nf[f] * (NF * NC) + (f ^ 1) * NC + c] = pv[f];
     }
     bool coarse = false;
 #pragma unroll
@@ -573,9 +587,10 @@ hdiv_kernel(const __grid_constant__ KParams<N> P) {
   // face Gauss points through halfq (x) halfq, flux with the own metric
   const int fa = (D == 2) ? c : c / N;
   const int fb = (D == 2) ? 0 : c % N;
-  auto fine_face = [&](auto ax_c, int side) {
+  auto fine_face = [&](auto ax_c, auto side_c) {
     constexpr int AX = decltype(ax_c)::value;
-    const int f = 2 * AX + side;
+    constexpr int side = decltype(side_c)::value;
+    constexpr int f = 2 * AX + side;
     const int kd = kf[f] & 15;
     const bool fine = act && kd == KIND_FINE;
     if (!__any_sync(0xffffffffu, fine)) return;
@@ -641,14 +656,14 @@ hdiv_kernel(const __grid_constant__ KParams<N> P) {
     }
   };
   if (mesh.n_coarse > 0) {
-    fine_face(std::integral_constant<int, 0>{}, 0);
-    fine_face(std::integral_constant<int, 0>{}, 1);
+    fine_face(std::integral_constant<int, 0>{}, std::integral_constant<int, 0>{});
+    fine_face(std::integral_constant<int, 0>{}, std::integral_constant<int, 1>{});
     if constexpr (D == 3) {
-      fine_face(std::integral_constant<int, 1>{}, 0);
-      fine_face(std::integral_constant<int, 1>{}, 1);
+      fine_face(std::integral_constant<int, 1>{}, std::integral_constant<int, 0>{});
+      fine_face(std::integral_constant<int, 1>{}, std::integral_constant<int, 1>{});
     }
-    fine_face(std::integral_constant<int, D - 1>{}, 0);
-    fine_face(std::integral_constant<int, D - 1>{}, 1);
+    fine_face(std::integral_constant<int, D - 1>{}, std::integral_constant<int, 0>{});
+    fine_face(std::integral_constant<int, D - 1>{}, std::integral_constant<int, 1>{});
   }
 
   // ---- volume: G_bx = (sum_a ctrv[bx][a] h V_a) wq; bx < d-1 via the tile
@@ -768,6 +783,426 @@ hdiv_kernel(const __grid_constant__ KParams<N> P) {
       }
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// H2, pipelined (hdiv2_kernel): persistent warps, each owning a strided
+// sequence of element groups (the EPW elements of one warp); every group's
+// inputs are contiguous per-element blocks -- V and h at the Gauss points,
+// the own psi rows and the incoming pin rows written by the neighbours' H1,
+// the base (the action's input), the 32-byte face records -- brought into a
+// two-stage shared-memory ring by cp.async.bulk (TMA) issued by one lane, so
+// the next group's loads are in flight while this one is computed and the
+// memory parallelism no longer depends on registers or occupancy.  Same
+// arithmetic as hdiv_kernel.  Even n^d only (16-byte aligned element blocks).
+template <int D, int N>
+struct H2Pipe {
+  using HL = HLayout<D, N>;
+  static constexpr int NP = HL::NP, NC = HL::NC, NF = HL::NF, EPW = HL::EPW;
+  static constexpr bool OK = HL::OK && (NP % 2 == 0) && ((NF * NC) % 2 == 0);
+  // stage sub-arrays (doubles, all even offsets)
+  static constexpr int OV = 0;
+  static constexpr int OH = OV + EPW * D * NP;
+  static constexpr int OP = OH + EPW * NP;
+  static constexpr int OI = OP + EPW * NF * NC;
+  static constexpr int OB = OI + EPW * NF * NC;
+  static constexpr int OR = OB + EPW * NP;
+  static constexpr int STG = OR + EPW * 4;  // + 32-byte records
+  static constexpr int TSLOT = HL::odd(HL::DRAW);
+  static constexpr int WT = 2 * (32 + 2);
+  static constexpr int WREG = ((2 * STG + HL::NSLOT * TSLOT + WT) + 1) & ~1;  // per warp
+  static constexpr int WPB = 4;
+  static constexpr size_t SMEM = (size_t)(HL::TABP + WPB * WREG) * sizeof(double);
+};
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      "HK2_WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @P1 bra HK2_DONE;\n"
+      " bra HK2_WAIT;\n"
+      "HK2_DONE:\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// the fused Gram-Schmidt dots accumulated over the groups of a warp
+// (gs_round with += into the warp's column totals)
+template <int D, int N, int PER>
+__device__ __forceinline__ void gs_round_acc(const KParams<N>& P, bool own, long long e, int c,
+                                             const double* wv, const double* uv, int c0, int nv,
+                                             int nvt, double* wtot) {
+  constexpr int NP = ipow(N, D), NI = 16 / PER;
+  const int lane = threadIdx.x & 31;
+  const int i0 = c0 / PER;
+  double sv[16];
+#pragma unroll
+  for (int t = 0; t < NI; ++t) {
+    const int it = i0 + t;
+    const bool ld = own && it < nv;
+    const double* vp = P.gsV + (long long)it * P.gs_vs + e * NP;
+    double v[N];
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii) {
+      const int node = (D == 3) ? ii * N * N + c : ii * N + c;
+      v[ii] = ld ? vp[node] : (it == nv ? wv[ii] : uv[ii]);
+    }
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int ii = 0; ii < N; ++ii) {
+      s0 = fma(v[ii], wv[ii], s0);
+      if (PER == 2) s1 = fma(v[ii], uv[ii], s1);
+    }
+    sv[t * PER] = own ? s0 : 0.0;
+    if (PER == 2) sv[t * PER + 1] = own ? s1 : 0.0;
+  }
+#pragma unroll
+  for (int o = 16, m = 16; o >= 2; o >>= 1, m >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int k = 0; k < m / 2; ++k) {
+      const double send = up ? sv[k] : sv[k + m / 2];
+      const double keep = up ? sv[k + m / 2] : sv[k];
+      sv[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  sv[0] += __shfl_xor_sync(0xffffffffu, sv[0], 1);
+  const int col = c0 + ((lane >> 1) & 15);
+  if ((lane & 1) == 0 && col < nvt) wtot[col] += sv[0];
+}
+
+#ifndef DG_HK2P_MINB
+#define DG_HK2P_MINB 2
+#endif
+
+template <int D, int N>
+__global__ void __launch_bounds__(128, DG_HK2P_MINB)
+hdiv2_kernel(const __grid_constant__ KParams<N> P) {
+  using HL = HLayout<D, N>;
+  using PL = H2Pipe<D, N>;
+  constexpr int NC = HL::NC, EPW = HL::EPW, NF = HL::NF, TSZ = HL::TSZ, NP = HL::NP;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ unsigned long long tbar;
+  __shared__ unsigned long long sbar[PL::WPB][2];
+  tab_bulk_issue(smem, P.tab_g, HL::TABD * 8, &tbar);
+  const Tab<N>& TS = *reinterpret_cast<const Tab<N>*>(smem);
+  const Tab<N>& TC = P.tab;
+  const MeshDev& mesh = P.mesh;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int eiw = lane / NC, c = lane - eiw * NC;
+  const bool slot_ok = eiw < EPW;
+  double* W = smem + HL::TABP + wid * PL::WREG;
+  double* STG0 = W;
+  double* X = W + 2 * PL::STG + (slot_ok ? eiw : EPW) * PL::TSLOT;
+  double* wtot = W + 2 * PL::STG + HL::NSLOT * PL::TSLOT;
+  const unsigned bar0 = smem_u32(&sbar[wid][0]), bar1 = smem_u32(&sbar[wid][1]);
+  const long long ngroups = ((long long)mesh.n_el + EPW - 1) / EPW;
+  const long long gw = (long long)blockIdx.x * PL::WPB + wid;
+  const long long GW = (long long)gridDim.x * PL::WPB;
+  const bool dots = P.gs_part != nullptr;
+  const bool dual = P.gs_dual != 0;
+  const int nv = P.gs_nv;
+  const int nvt = dual ? 2 * (nv + 2) : nv + 1;
+  for (int i = lane; i < PL::WT; i += 32) wtot[i] = 0.0;
+
+  // lane 0: bring group g into stage s
+  auto issue = [&](long long g, int s) {
+    const long long e0 = g * EPW;
+    const int ne = (int)min((long long)EPW, (long long)mesh.n_el - e0);
+    double* st = STG0 + s * PL::STG;
+    const unsigned b = s ? bar1 : bar0;
+    const unsigned bytes = 8u * ne * (D * NP + NP + 2 * NF * NC + (P.has_base ? NP : 0) + 4);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes)
+                 : "memory");
+    bulk_g2s(st + PL::OV, P.in.p + e0 * P.in.estride, 8u * ne * D * NP, b);
+    bulk_g2s(st + PL::OH, P.inH.p + e0 * P.inH.estride, 8u * ne * NP, b);
+    bulk_g2s(st + PL::OP, P.psi + e0 * (NF * NC), 8u * ne * NF * NC, b);
+    bulk_g2s(st + PL::OI, P.pin + e0 * (NF * NC), 8u * ne * NF * NC, b);
+    if (P.has_base) bulk_g2s(st + PL::OB, P.base.p + e0 * P.base.estride, 8u * ne * NP, b);
+    bulk_g2s(st + PL::OR, P.frec + e0 * 8, 32u * ne, b);
+    if (dots) {
+      // the fused dots' basis slices of this group into L2
+      for (int i = 0; i < nv; ++i) {
+        const double* src = P.gsV + (long long)i * P.gs_vs + e0 * NP;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src),
+                     "r"(8u * ne * NP)
+                     : "memory");
+      }
+    }
+  };
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar1) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    if (gw < ngroups) issue(gw, 0);
+    if (gw + GW < ngroups) issue(gw + GW, 1);
+  }
+  __syncthreads();  // the table barrier is initialised (and every stage barrier)
+  tab_bulk_wait(&tbar);
+  const int fa = (D == 2) ? c : c / N;
+  const int fb = (D == 2) ? 0 : c % N;
+  const double wcol = (D == 3) ? TS.qw[c / N] * TS.qw[c % N] : TS.qw[c];
+  double iwq = (D == 3) ? TS.iqw[c / N] * TS.iqw[c % N] : TS.iqw[c];
+
+  int k = 0;
+  for (long long g = gw; g < ngroups; g += GW, ++k) {
+    const int s = k & 1;
+    mbar_wait(s ? bar1 : bar0, (unsigned)((k >> 1) & 1));
+    const double* st = STG0 + s * PL::STG;
+    const long long e = g * EPW + eiw;
+    const bool act = slot_ok && e < mesh.n_el;
+    const int esl = act ? eiw : 0;
+    const int* rec = reinterpret_cast<const int*>(st + PL::OR) + esl * 8;
+    const uint8_t* rk = reinterpret_cast<const uint8_t*>(rec + 6);
+    uint8_t kf[NF];
+    int nf[NF];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      kf[f] = act ? rk[f] : (uint8_t)KIND_WALL;
+      nf[f] = rec[f];
+    }
+    // face fluxes: psi + pin (conforming, wall, far field, fine), coarse side
+    // precomputed
+    double fl[NF];
+    {
+      const double* ps = st + PL::OP + esl * (NF * NC) + c;
+      const double* pi = st + PL::OI + esl * (NF * NC) + c;
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+        const int kd = kf[f] & 15;
+        const double sg = (f & 1) ? 1.0 : -1.0;
+        double v = sg * (ps[f * NC] + pi[f * NC]);
+        if (kd == KIND_COARSE) v = (mesh.cflux != nullptr) ? mesh.cflux[(long long)nf[f] * NC + c] : 0.0;
+        fl[f] = act ? v : 0.0;
+      }
+    }
+    const long long es = act ? e : 0;
+    const ElemGeo<D> g3 = elem_geo<D>(mesh.elem, P.gc, es);
+    const ColData<D, N> cd = col_data<D, N>(P.gc, mesh.col, g3, c, act);
+    // fine side of hanging faces (as hdiv_kernel)
+    auto fine_face = [&](auto ax_c, auto side_c) {
+      constexpr int AX = decltype(ax_c)::value;
+      constexpr int side = decltype(side_c)::value;
+      constexpr int f = 2 * AX + side;
+      const int kd = kf[f] & 15;
+      const bool fine = act && kd == KIND_FINE;
+      if (!__any_sync(0xffffffffu, fine)) return;
+      constexpr int FC = (AX < D - 1) ? 2 : D + 1;
+      constexpr int TSL = tr_slots<D>() * NC, THL = 2 * D * NC;
+      const long long pe = nf[f];
+#pragma unroll
+      for (int r = 0; r < FC; ++r) {
+        double v = 0.0;
+        if (fine) {
+          const bool isv = r < FC - 1;
+          const int comp = (AX < D - 1) ? AX : r;
+          v = isv ? P.trV[pe * TSL + tr_slot<D>(f ^ 1, comp) * NC + c]
+                  : P.trH[pe * THL + (f ^ 1) * NC + c];
+        }
+        X[r * NC + c] = v;
+      }
+      __syncwarp();
+      const int sf = (kf[f] >> 4) & 3;
+      const double* Mq0 = &TS.halfq[sf & 1][0][0];
+      const double* Mq1 = &TS.halfq[(sf >> 1) & 1][0][0];
+      double tr[FC];
+#pragma unroll
+      for (int r = 0; r < FC; ++r) {
+        double t = 0.0;
+        if constexpr (D == 2) {
+#pragma unroll
+          for (int j = 0; j < N; ++j) t = fma(Mq0[fa * N + j], X[r * NC + j], t);
+        } else {
+#pragma unroll
+          for (int j = 0; j < N; ++j) t = fma(Mq0[fa * N + j], X[r * NC + j * N + fb], t);
+        }
+        tr[r] = t;
+      }
+      if constexpr (D == 3) {
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < FC; ++r) X[r * NC + c] = tr[r];
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < FC; ++r) {
+          double t = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) t = fma(Mq1[fb * N + j], X[r * NC + fa * N + j], t);
+          tr[r] = t;
+        }
+      }
+      __syncwarp();
+      if (fine) {
+        double n[D], ws;
+        const double oe = (AX < D - 1) ? edge_omh<D, N>(P.gc, mesh.col, g3, f, c, act) : 1.0;
+        face_nplus<D, N, AX>(P.gc, g3, side, c, TS, oe, cd.dh, n, ws);
+        double vn;
+        if constexpr (AX < D - 1) {
+          vn = tr[0] * n[AX];
+        } else {
+          vn = 0.0;
+#pragma unroll
+          for (int a = 0; a < D; ++a) vn = fma(tr[a], n[a], vn);
+        }
+        const double sg = side ? 1.0 : -1.0;
+        fl[f] += sg * ((0.5 * ws) * (tr[FC - 1] * vn));
+      }
+    };
+    if (mesh.n_coarse > 0) {
+      fine_face(std::integral_constant<int, 0>{}, std::integral_constant<int, 0>{});
+      fine_face(std::integral_constant<int, 0>{}, std::integral_constant<int, 1>{});
+      if constexpr (D == 3) {
+        fine_face(std::integral_constant<int, 1>{}, std::integral_constant<int, 0>{});
+        fine_face(std::integral_constant<int, 1>{}, std::integral_constant<int, 1>{});
+      }
+      fine_face(std::integral_constant<int, D - 1>{}, std::integral_constant<int, 0>{});
+      fine_face(std::integral_constant<int, D - 1>{}, std::integral_constant<int, 1>{});
+    }
+    // volume
+    double Zc[N];
+    const double det = col_det<D>(g3, cd.omh);
+    {
+      const double* Vs = st + PL::OV + esl * (D * NP) + c * N;
+      const double* Hs = st + PL::OH + esl * NP + c * N;
+      double Gz[N];
+#pragma unroll
+      for (int kz = 0; kz < N; ++kz) {
+        double ct[D][D];
+        col_metric<D, N>(P.gc, g3, cd.omh, cd.dh, TC.qx[kz], ct);
+        const double wq = wcol * TC.qw[kz];
+        const double h = Hs[kz];
+        double F[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) F[a] = h * Vs[a * NP + kz];
+        X[coff<D, N>(c, kz)] = (F[0] * ct[0][0]) * wq;
+        if constexpr (D == 3) X[TSZ + coff<D, N>(c, kz)] = (F[1] * ct[1][1]) * wq;
+        double acc = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) acc += F[a] * ct[D - 1][a];
+        Gz[kz] = acc * wq;
+      }
+      mat_apply<N, true>(TC.Dhat, Gz, Zc);
+      const int zf = 2 * (D - 1);
+#pragma unroll
+      for (int kz = 0; kz < N; ++kz)
+        Zc[kz] = TC.lift[0][kz] * fl[zf] + TC.lift[1][kz] * fl[zf + 1] - Zc[kz];
+    }
+    __syncwarp();
+    {
+      double v[N], o[N];
+#pragma unroll
+      for (int ii = 0; ii < N; ++ii) v[ii] = X[xoff<D, N>(c, ii)];
+      mat_apply<N, true>(TC.Dhat, v, o);
+#pragma unroll
+      for (int ii = 0; ii < N; ++ii)
+        X[xoff<D, N>(c, ii)] = TC.lift[0][ii] * fl[0] + TC.lift[1][ii] * fl[1] - o[ii];
+      if constexpr (D == 3) {
+#pragma unroll
+        for (int jj = 0; jj < N; ++jj) v[jj] = X[TSZ + yoff<N>(c, jj)];
+        mat_apply<N, true>(TC.Dhat, v, o);
+#pragma unroll
+        for (int jj = 0; jj < N; ++jj)
+          X[TSZ + yoff<N>(c, jj)] = TC.lift[0][jj] * fl[2] + TC.lift[1][jj] * fl[3] - o[jj];
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int kz = 0; kz < N; ++kz) {
+      Zc[kz] += X[coff<D, N>(c, kz)];
+      if constexpr (D == 3) Zc[kz] += X[TSZ + coff<D, N>(c, kz)];
+    }
+    // epilogue
+    const double iwh = (1.0 / det) * iwq;
+    {
+      double t[N];
+#pragma unroll
+      for (int kz = 0; kz < N; ++kz) t[kz] = Zc[kz] * (iwh * TC.iqw[kz]);
+      mat_apply<N, false>(TC.Binv, t, Zc);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int kz = 0; kz < N; ++kz) X[coff<D, N>(c, kz)] = Zc[kz];
+    __syncwarp();
+    if constexpr (D == 3) {
+      double v[N], o[N];
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj) v[jj] = X[yoff<N>(c, jj)];
+      mat_apply<N, false>(TC.Binv, v, o);
+#pragma unroll
+      for (int jj = 0; jj < N; ++jj) X[yoff<N>(c, jj)] = o[jj];
+      __syncwarp();
+    }
+    double wv[N], uv[N];
+    {
+      const double* Bs = st + PL::OB + esl * NP;
+      double v[N], o[N];
+#pragma unroll
+      for (int ii = 0; ii < N; ++ii) v[ii] = X[xoff<D, N>(c, ii)];
+      mat_apply<N, false>(TC.Binv, v, o);
+#pragma unroll
+      for (int ii = 0; ii < N; ++ii) {
+        const int node = (D == 3) ? ii * N * N + c : ii * N + c;
+        const double bv = P.has_base ? Bs[node] : 0.0;
+        const double r = __dmul_rn(P.coef, o[ii]);
+        const double val = P.has_base ? __dadd_rn(bv, r) : r;
+        wv[ii] = act ? val : 0.0;
+        uv[ii] = act ? bv : 0.0;
+        if (act) P.out.p[e * P.out.estride + node] = val;
+      }
+    }
+    __syncwarp();  // every lane is done with this stage and the tile
+    if (lane == 0 && g + 2 * GW < ngroups) issue(g + 2 * GW, s);
+    if (dots) {
+      for (int c0 = 0; c0 < nvt; c0 += 16) {
+        if (dual) gs_round_acc<D, N, 2>(P, act, e, c, wv, uv, c0, nv, nvt, wtot);
+        else gs_round_acc<D, N, 1>(P, act, e, c, wv, uv, c0, nv, nvt, wtot);
+      }
+    }
+  }
+  if (dots) {
+    __syncthreads();
+    if (wid == 0) {
+      for (int col = lane; col < nvt; col += 32) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < PL::WPB; ++w) t += smem[HL::TABP + w * PL::WREG + 2 * PL::STG + HL::NSLOT * PL::TSLOT + col];
+        P.gs_part[((long long)P.gs_row0 + blockIdx.x) * nvt + col] = t;
+      }
+    }
+  }
+}
+
+// 32-byte face records for the pipelined H2: int32 nbr[2d] | uint8 kind[2d]
+template <int D>
+__global__ void hk_face_records(const int* __restrict__ nbr, const uint8_t* __restrict__ kind,
+                                int n, int* __restrict__ rec) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  int r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int f = 0; f < 2 * D; ++f) r[f] = nbr[(long long)e * 2 * D + f];
+  uint8_t* kb = reinterpret_cast<uint8_t*>(r + 6);
+  for (int f = 0; f < 2 * D; ++f) kb[f] = kind[(long long)e * 2 * D + f];
+  for (int i = 0; i < 8; ++i) rec[(long long)e * 8 + i] = r[i];
+}
+
+// pin rows of owned elements whose conforming neighbour is a ghost (another
+// rank's element): copied from the ghost's exchanged psi after the halo
+// exchange; fix = (element, face, ghost) triples
+static __global__ void hk_pin_fixup(const int* __restrict__ fix, int nfix, int nc, int nf,
+                             const double* __restrict__ psi, double* __restrict__ pin) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)nfix * nc) return;
+  const int t = (int)(i / nc), c = (int)(i % nc);
+  const int e = fix[3 * t], f = fix[3 * t + 1], gh = fix[3 * t + 2];
+  pin[((long long)e * nf + f) * nc + c] = psi[((long long)gh * nf + (f ^ 1)) * nc + c];
 }
 
 }  // namespace dg

@@ -928,7 +928,12 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
       const int cp = r % KIN;
       const int sub = r / KIN;
       const long long child = s_child[f][sub];
-      if (OPK == OP_DIVHV && P.in_quad && P.trV != nullptr) {
+      if (OPK == OP_DIVHV && P.psi != nullptr) {
+        // flux-trace mode: the child's psi = 1/2 ws h (V . n+) on its face
+        // f ^ 1 at its face Gauss point j (dg_hkernel.cuh)
+        constexpr int PSL = NF * NQF;
+        CH[it] = (cp == 0) ? P.psi[child * PSL + (f ^ 1) * NQF + j] : 0.0;
+      } else if (OPK == OP_DIVHV && P.in_quad && P.trV != nullptr) {
         // trace mode: the child's V / h traces on its face f ^ 1 at its face
         // Gauss point j (vertical faces carry only the normal component)
         const bool vert = (f >> 1) < D - 1;
@@ -1034,10 +1039,22 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
         TRv[c] = minus ? TN[c] : TO[c];
       }
       double fl[KOUT];
+      if (OPK == OP_DIVHV && P.psi != nullptr) {
+        // flux-trace mode: the child's half is its psi (fine-side metric,
+        // the same n+ and ws as below), the coarse half 1/2 ws h (V . n+)
+        // from the mortar-interpolated own traces
+        double vn = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) vn = fma(TO[a], n[a], vn);
+        fl[0] = (minus ? 1.0 : -1.0) * (TN[0] + (0.5 * ws) * (TO[D] * vn));
+#pragma unroll
+        for (int k = 0; k < KOUT; ++k) FW[(sub * KOUT + k) * NQF + qf] = fl[k];
+      } else {
       num_flux<D, OPK, KIN, KOUT>(TLv, TRv, n, P.model.kinetic_factor, fl, &P.model, P.full);
       const double sg = minus ? ws : -ws;
 #pragma unroll
       for (int k = 0; k < KOUT; ++k) FW[(sub * KOUT + k) * NQF + qf] = fl[k] * sg;
+      }
     }
     __syncthreads();
     // coarse-face flux at the coarse face Gauss points, once per point:

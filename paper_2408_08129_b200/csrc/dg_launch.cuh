@@ -1,11 +1,13 @@
 // Host-side launcher for the templated element kernels (one translation
 // unit per dimension instantiates N = 2..7 and the three operator kinds).
 #pragma once
+#include <algorithm>
 #include <cstring>
 #include <cstdlib>
 #include <string>
 #include <type_traits>
 #include "dg_xkernel.cuh"
+#include "dg_hkernel.cuh"
 
 namespace dg {
 
@@ -25,6 +27,11 @@ struct OpArgs {
   double* tr_out;      // trace mode (see KParams)
   const double* trV;
   const double* trH;
+  double* psi_out;     // flux-trace mode (see KParams)
+  const double* psi;
+  double* pin_out;
+  const double* pin;
+  const int* frec;
   int full;  // ADV: divergence_full flux (see KParams)
   double* mass_partial;
   const double* gsV;  // fused Gram-Schmidt dots (see KParams)
@@ -71,6 +78,11 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
   P.tr_out = a.tr_out;
   P.trV = a.trV;
   P.trH = a.trH;
+  P.psi_out = a.psi_out;
+  P.psi = a.psi;
+  P.pin_out = a.pin_out;
+  P.pin = a.pin;
+  P.frec = a.frec;
   P.gsV = a.gsV;
   P.gs_vs = a.gs_vs;
   P.gs_nv = a.gs_nv;
@@ -79,6 +91,78 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
   P.gs_row0 = 0;
   P.tab_g = a.tabs_dev;
   std::memcpy(&P.tab, a.tabs, sizeof(Tab<N>));
+  using HL = HLayout<D, N>;
+  if constexpr (HL::OK && OPK != OP_ADV) {
+    // flux-trace mode of the Helmholtz pair (dg_hkernel.cuh)
+    const bool hk = (OPK == OP_GRAD) ? a.psi_out != nullptr : a.psi != nullptr;
+    if (hk) {
+      constexpr int EPC = HL::EPW * HL::WPB;
+      const int hgrid = (a.mesh.n_el + EPC - 1) / EPC;
+      const size_t hsm = (OPK == OP_GRAD) ? HL::GSMEM : HL::DSMEM;
+      if (info) {
+        info->epb = EPC;
+        info->threads = HL::THREADS;
+        info->smem = hsm;
+        info->grid = hgrid;
+      }
+      if (hgrid == 0) return cudaSuccess;
+      static bool hconf = false;
+      if (!hconf) {
+        cudaError_t e = (OPK == OP_GRAD)
+            ? cudaFuncSetAttribute(hgrad_kernel<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)HL::GSMEM)
+            : cudaFuncSetAttribute(hdiv_kernel<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)HL::DSMEM);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::CSMEM);
+        if (e != cudaSuccess) return e;
+        hconf = true;
+      }
+      if (a.mesh.n_coarse > 0) {
+        if (a.mesh.cflux == nullptr) return cudaErrorInvalidValue;  // flux mode required
+        coarse_kernel<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
+            P, a.mesh.coarse_list, a.mesh.n_coarse, nullptr);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+      }
+      if constexpr (OPK == OP_GRAD) {
+        hgrad_kernel<D, N><<<hgrid, HL::THREADS, HL::GSMEM, st>>>(P);
+      } else {
+        using PL = H2Pipe<D, N>;
+        if constexpr (PL::OK) {
+          if (a.pin != nullptr && a.frec != nullptr) {
+            // persistent pipelined H2: every SM's resident CTAs, the groups
+            // strided over the warps
+            static int pgrid = 0;
+            if (pgrid == 0) {
+              cudaError_t e = cudaFuncSetAttribute(
+                  hdiv2_kernel<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PL::SMEM);
+              if (e != cudaSuccess) return e;
+              int dev = 0, sms = 0, occ = 0;
+              cudaGetDevice(&dev);
+              cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+              e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hdiv2_kernel<D, N>, 128,
+                                                                PL::SMEM);
+              if (e != cudaSuccess) return e;
+              pgrid = sms * (occ > 0 ? occ : 1);
+            }
+            const long long groups = (a.mesh.n_el + HL::EPW - 1) / HL::EPW;
+            const int g = (int)std::min<long long>(pgrid, (groups + PL::WPB - 1) / PL::WPB);
+            if (info) {
+              info->threads = 128;
+              info->smem = PL::SMEM;
+              info->grid = g;  // one dot-partial row per CTA
+            }
+            hdiv2_kernel<D, N><<<g, 128, PL::SMEM, st>>>(P);
+            return cudaGetLastError();
+          }
+        }
+        hdiv_kernel<D, N><<<hgrid, HL::THREADS, HL::DSMEM, st>>>(P);
+      }
+      return cudaGetLastError();
+    }
+  }
   using WL = WLayout<D, N, OPK>;
   if constexpr (WL::OK) {
     // warp-element kernel (v3) for the Helmholtz pair unless DG_KERNEL=v2

@@ -59,6 +59,14 @@ struct KParams {
   double* tr_out;
   const double* trV;
   const double* trH;
+  // flux-trace (psi) mode of the Helmholtz pair (dg_hkernel.cuh): H1 writes
+  // psi = 1/2 ws h (V . n+) per face point (n_el, 2d, n^(d-1)), H2 and the
+  // coarse-side kernel read it
+  double* psi_out;
+  const double* psi;
+  double* pin_out;      // H1: the conforming neighbours' incoming psi slots
+  const double* pin;    // H2 (pipelined): own incoming slots
+  const int* frec;      // H2 (pipelined): 32-byte face records (hk_face_records)
   int full;              // ADV: 0 split advective flux, 1 full Euler Rusanov, 2 full centred
   double* mass_partial;  // ADV: per-CTA sum of the density dual (or null)
   // fused Gram-Schmidt dots of the result y (div(hV) MINV only, GMRES):

@@ -102,6 +102,11 @@ struct dg_ctx {
   int bj_ncolors = 0;
   DevBuf<double> bj_inv, sz, su;
   DevBuf<double> trV, trH;  // trace mode: face traces of V (H1 output) and of h
+  DevBuf<double> psi;       // flux-trace mode: 1/2 ws h (V . n+) per face point (H1 output)
+  DevBuf<double> pin;       // ... and the conforming neighbours' values, scattered by H1
+  DevBuf<int> frec;         // 32-byte face records of the pipelined H2
+  DevBuf<int> pinfix;       // (element, face, ghost) triples: pin rows fed by a ghost
+  int n_pinfix = 0;
   int bj_valid = 0, bj_age = 1 << 30;
   long long bj_gen = 0;
   LaunchInfo last{};
@@ -202,9 +207,12 @@ int op_advective(dg_ctx* c, const double* U, double* out, int mode, double* mass
 // V_k = base_k + coef * [Minv] G(alpha (x - beta K))
 int op_grad(dg_ctx* c, const double* x, const double* K, double alpha, double beta, int homog,
             int mode, MView out, CView base, int has_base, double coef, int out_quad = 0,
-            double* tr_out = nullptr) {
+            double* tr_out = nullptr, double* psi_out = nullptr, double* pin_out = nullptr) {
   OpArgs a = base_args(c);
   a.tr_out = tr_out;
+  a.psi_out = psi_out;
+  a.pin_out = pin_out;
+  if (psi_out) a.trH = c->trH.p;  // psi = 1/2 ws h (V . n+): the own h traces
   a.in = cv(x, c->NP, c->NP);
   if (K) {
     a.inK = cv(K, c->NP, c->NP);
@@ -233,10 +241,14 @@ struct GsFuse {  // fused Gram-Schmidt dots of the div(hV) result (gs_dots)
 
 int op_divhv(dg_ctx* c, CView V, const double* h, int homog, int mode, MView out, CView base,
              int has_base, double coef, int in_quad = 0, const GsFuse* gs = nullptr,
-             const double* trV = nullptr, const double* trH = nullptr) {
+             const double* trV = nullptr, const double* trH = nullptr,
+             const double* psi = nullptr, const double* pin = nullptr) {
   OpArgs a = base_args(c);
   a.trV = trV;
   a.trH = trH;
+  a.psi = psi;
+  a.pin = pin;
+  a.frec = pin ? c->frec.p : nullptr;
   if (gs) {
     a.gsV = gs->V;
     a.gs_vs = gs->vs;
@@ -264,6 +276,48 @@ bool trace_mode(dg_ctx* c) {
   static const char* env = getenv("DG_TRACE");
   static const bool on = env == nullptr || std::string(env) != "0";
   return on && welem_enabled(c->dim, c->N) && welem_trace_ok(c->dim, c->N);
+}
+
+// Flux-trace (psi) mode of the trace-mode pair (dg_hkernel.cuh): H1 writes
+// 1/2 ws h (V . n+) per face point, H2 sums its own and its neighbours'
+// values instead of evaluating face traces, metrics and ghosts.  Needs the
+// coarse faces in flux mode.  Default on (DG_PSI=0: the trace-mode pair)
+bool psi_mode(dg_ctx* c) {
+  static const char* env = getenv("DG_PSI");
+  static const bool on = env == nullptr || std::string(env) != "0";
+  return on && trace_mode(c) && (c->mesh.n_coarse == 0 || c->cflux.p != nullptr);
+}
+
+// Pipelined H2 (hdiv2_kernel: persistent warps fed by cp.async.bulk): needs
+// 16-byte aligned element blocks (even n^d).  Default on (DG_PIPE=0: hdiv)
+bool pipe_mode(dg_ctx* c) {
+  static const char* env = getenv("DG_PIPE");
+  static const bool on = env == nullptr || std::string(env) != "0";
+  return on && (c->NP % 2 == 0);
+}
+
+// DCGS2 with the pipelined H2: the Gram-Schmidt dots in their own streaming
+// pass instead of the div(hV) epilogue (DG_SEPDOTS=0 keeps them fused)
+bool sep_dots(dg_ctx* c) {
+  static const char* env = getenv("DG_SEPDOTS");
+  static const bool on = env == nullptr || std::string(env) != "0";
+  return on && trace_mode(c) && psi_mode(c) && pipe_mode(c);
+}
+
+// the pin buffer (zero: boundary, fine and coarse faces are never written)
+// and the 32-byte face records of the pipelined H2
+int setup_pin(dg_ctx* c, int psl) {
+  CK(c->pin.alloc((size_t)c->n_tot * psl));
+  CK(cudaMemsetAsync(c->pin.p, 0, (size_t)c->n_tot * psl * sizeof(double), c->stream));
+  CK(c->frec.alloc((size_t)c->n_tot * 8));
+  if (c->dim == 2)
+    hk_face_records<2><<<(c->n_tot + 255) / 256, 256, 0, c->stream>>>(c->nbr.p, c->kind.p, c->n_tot,
+                                                                      c->frec.p);
+  else
+    hk_face_records<3><<<(c->n_tot + 255) / 256, 256, 0, c->stream>>>(c->nbr.p, c->kind.p, c->n_tot,
+                                                                      c->frec.p);
+  CK(cudaGetLastError());
+  return DG_OK;
 }
 
 bool quad_mode(dg_ctx* c) {
@@ -320,14 +374,28 @@ int helm_apply(dg_ctx* c, double a_dt, const double* h, const double* hq, double
   const double gm1 = c->model.gamma - 1.0;
   const int qd = hq != nullptr;
   const bool tm = qd && trace_mode(c);
+  const bool pm = tm && psi_mode(c);
   if (tm) CK(c->trV.alloc((size_t)c->n_tot * tr_len(c)));
+  const int psl = 2 * d * c->NQF;  // psi values per element
+  const bool pp = pm && pipe_mode(c);
+  if (pm) CK(c->psi.alloc((size_t)c->n_tot * psl));
+  if (pp && c->pin.p == nullptr) RET(setup_pin(c, psl));
   RET(op_grad(c, x, nullptr, gm1, 0.0, 1, OUT_MINV, mv(c->sV.p, (long long)d * c->NP, c->NP),
-              CView{}, 0, -(a_dt * c->model.inv_mach_sq), qd, tm ? c->trV.p : nullptr));
-  if (tm) RET(halo_elems(c, c->trV.p, tr_len(c)));  // H2 reads neighbours only through traces
+              CView{}, 0, -(a_dt * c->model.inv_mach_sq), qd, tm ? c->trV.p : nullptr,
+              pm ? c->psi.p : nullptr, pp ? c->pin.p : nullptr));
+  if (pm) RET(halo_elems(c, c->psi.p, psl));        // H2 reads its neighbours' psi
+  if (pp && c->n_pinfix > 0) {
+    const long long nt = (long long)c->n_pinfix * c->NQF;
+    hk_pin_fixup<<<(unsigned)((nt + 255) / 256), 256, 0, c->stream>>>(
+        c->pinfix.p, c->n_pinfix, c->NQF, 2 * d, c->psi.p, c->pin.p);
+    CK(cudaGetLastError());
+  }
+  if (tm) RET(halo_elems(c, c->trV.p, tr_len(c)));  // (and the coarse parents' traces)
   else RET(halo(c, c->sV.p, d));
   RET(op_divhv(c, cv(c->sV.p, (long long)d * c->NP, c->NP), qd ? hq : h, 1, OUT_MINV,
                mv(y, c->NP, c->NP), cv(x, c->NP, c->NP), 1, a_dt, qd, gs,
-               tm ? c->trV.p : nullptr, tm ? c->trH.p : nullptr));
+               tm ? c->trV.p : nullptr, tm ? c->trH.p : nullptr, pm ? c->psi.p : nullptr,
+               pp ? c->pin.p : nullptr));
   return DG_OK;
 }
 
@@ -425,10 +493,19 @@ int dcgs2_cycle(dg_ctx* c, double a_dt, const double* h, const double* hq, int m
   done = 0;
   for (int j = 0; j < m; ++j) {
     double* u = Vb + (size_t)j * vs;
-    GsFuse gs{Vb, vs, j, c->gs_part.p, 1};
-    RET(helm_apply(c, a_dt, h, hq, u, z, &gs));
     const int nvt = 2 * (j + 2);
-    CK(reduce_rows(c->stream, c->gs_part.p, c->last.grid, nvt, c->partial.p, c->redout.p));
+    if (sep_dots(c)) {
+      // the pipelined div(hV) kernel streams without the dots; one dual-dot
+      // pass over Q, z and u follows (dg_vector.cu k_dual_dots)
+      RET(helm_apply(c, a_dt, h, hq, u, z));
+      int rows = 0;
+      CK(dual_dots(c->stream, n, j, Vb, vs, z, u, c->gs_part.p, &rows));
+      CK(reduce_rows(c->stream, c->gs_part.p, rows, nvt, c->partial.p, c->redout.p));
+    } else {
+      GsFuse gs{Vb, vs, j, c->gs_part.p, 1};
+      RET(helm_apply(c, a_dt, h, hq, u, z, &gs));
+      CK(reduce_rows(c->stream, c->gs_part.p, c->last.grid, nvt, c->partial.p, c->redout.p));
+    }
     RET(reduce_read(c, c->redout.p, nvt, dots.data()));
     // dots: (Q_i.z, Q_i.u) pairs, then (z.z, z.u), then (u.z, u.u)
     const double zz = dots[2 * j], uz = dots[2 * j + 1], uu = dots[2 * j + 3];
@@ -973,6 +1050,18 @@ int dg_ctx_create(const dg_ctx_desc* d, dg_ctx** out) {
     }
     if (e == cudaSuccess && !cl.empty()) e = c->clist.upload(cl.data(), cl.size());
     c->mesh.n_coarse = ncoarse;
+    // owned conforming faces whose neighbour is a ghost (partitioned runs):
+    // their incoming psi rows come from the halo (hk_pin_fixup)
+    std::vector<int> pf;
+    for (int e2 = 0; e2 < d->n_el; ++e2)
+      for (int f = 0; f < nf; ++f)
+        if ((d->kind[(size_t)e2 * nf + f] & 15) == DG_FACE_CONF && d->nbr[(size_t)e2 * nf + f] >= d->n_el) {
+          pf.push_back(e2);
+          pf.push_back(f);
+          pf.push_back(d->nbr[(size_t)e2 * nf + f]);
+        }
+    if (e == cudaSuccess && !pf.empty()) e = c->pinfix.upload(pf.data(), pf.size());
+    c->n_pinfix = (int)(pf.size() / 3);
     // coarse-face flux buffer (flux mode; DG_COARSE_FLUX=0: the coarse side
     // is added afterwards by the fix-up epilogue instead)
     static const bool cf_off =
@@ -1016,11 +1105,13 @@ int dg_ctx_destroy(dg_ctx* c) {
   if (!c) return DG_OK;
   cudaSetDevice(c->device);
   for (auto* b : {&c->col, &c->ffU, &c->ffp, &c->ffh, &c->sigma, &c->bg, &c->mass_partial,
-                  &c->partial, &c->redout, &c->coef_dev, &c->gs_part, &c->trV, &c->trH, &c->sV, &c->sh, &c->sK, &c->sx,
+                  &c->partial, &c->redout, &c->coef_dev, &c->gs_part, &c->trV, &c->trH, &c->psi, &c->pin, &c->sV, &c->sh, &c->sK, &c->sx,
                   &c->srhs, &c->spold, &c->sw, &c->sr, &c->sx2, &c->basis})
     b->release();
   for (auto& s : c->st) s.release();
   c->elem.release();
+  c->frec.release();
+  c->pinfix.release();
   c->clist.release();
   c->cflux.release();
   c->nbr.release();

@@ -635,6 +635,85 @@ cudaError_t launch_dcgs2(cudaStream_t st, long long n, int nv, const double* Q, 
   return cudaGetLastError();
 }
 
+// DCGS2 dual Gram-Schmidt dots in one streaming pass (the unfused form of
+// the dots the div(hV) kernel can fuse, dg_wkernel.cuh gs_dots): row b of
+// rows = block b's partials of (Q_i.z, Q_i.u) for i < NV, then (z.z, z.u),
+// then (u.z, u.u) -- 2 (NV + 2) columns, reduced over the fixed grid by
+// reduce_rows (deterministic)
+template <int NV>
+__global__ void __launch_bounds__(RED_THREADS)
+k_dual_dots(long long n, const double* __restrict__ Q, long long vstride,
+            const double* __restrict__ z, const double* __restrict__ u, double* __restrict__ rows) {
+  constexpr int NA = NV > 0 ? NV : 1;
+  constexpr int NT = 2 * (NV + 2);
+  double pz[NA], pu[NA];
+#pragma unroll
+  for (int i = 0; i < NA; ++i) pz[i] = pu[i] = 0.0;
+  double zz = 0.0, zu = 0.0, uu = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    double a[NA];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) a[i] = Q[i * vstride + k];
+    const double zk = z[k], uk = u[k];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      pz[i] = fma(a[i], zk, pz[i]);
+      pu[i] = fma(a[i], uk, pu[i]);
+    }
+    zz = fma(zk, zk, zz);
+    zu = fma(zk, uk, zu);
+    uu = fma(uk, uk, uu);
+  }
+  __shared__ double red[RED_THREADS / 32][NT];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int col = 0; col < NT; ++col) {
+    double v;
+    if (col < 2 * NV) v = (col & 1) ? pu[col >> 1] : pz[col >> 1];
+    else if (col == 2 * NV) v = zz;
+    else if (col == 2 * NV + 1 || col == 2 * NV + 2) v = zu;
+    else v = uu;
+    v = warp_sum(v);
+    if (lane == 0) red[wid][col] = v;
+  }
+  __syncthreads();
+  for (int col = threadIdx.x; col < NT; col += blockDim.x) {
+    double t = 0.0;
+    for (int w2 = 0; w2 < RED_THREADS / 32; ++w2) t += red[w2][col];
+    rows[(long long)blockIdx.x * NT + col] = t;
+  }
+}
+
+template <int NV>
+cudaError_t launch_dual_dots(cudaStream_t st, long long n, int nv, const double* Q,
+                             long long vstride, const double* z, const double* u, double* rows,
+                             int* used_grid) {
+  if constexpr (NV > 0) {
+    if (nv < NV) return launch_dual_dots<NV - 1>(st, n, nv, Q, vstride, z, u, rows, used_grid);
+  }
+  static int grid = 0;
+  if (grid == 0) {
+    int dev = 0, nsm = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dual_dots<NV>, RED_THREADS, 0);
+    grid = std::min(RED_BLOCKS, std::max(1, nsm * std::max(occ, 1)));
+  }
+  *used_grid = grid;
+  k_dual_dots<NV><<<grid, RED_THREADS, 0, st>>>(n, Q, vstride, z, u, rows);
+  return cudaGetLastError();
+}
+
+cudaError_t dual_dots(cudaStream_t st, long long n, int nv, const double* Q, long long vstride,
+                      const double* z, const double* u, double* rows, int* nrows) {
+  if (nv > 31 || nv < 0) return cudaErrorInvalidValue;
+  prof_begin(st);
+  cudaError_t e = launch_dual_dots<31>(st, n, nv, Q, vstride, z, u, rows, nrows);
+  prof_end(st, P_DOT, 8.0 * n * (nv + 2), 1);
+  return e;
+}
+
 cudaError_t dcgs2_update(cudaStream_t st, long long n, int nv, const double* Q, long long vstride,
                          const double* coefs_dev, double* u, const double* z, double* unext,
                          double* partials, double* out) {

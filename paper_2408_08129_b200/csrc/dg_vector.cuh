@@ -22,6 +22,9 @@ cudaError_t axpy_div(cudaStream_t st, long long n, int nv, const double* V, long
 cudaError_t dcgs2_update(cudaStream_t st, long long n, int nv, const double* Q, long long vstride,
                          const double* coefs_dev, double* u, const double* z, double* unext,
                          double* partials, double* out);
+// DCGS2 dual dots (Q_i.z, Q_i.u, z.z, z.u, u.z, u.u) as per-block rows
+cudaError_t dual_dots(cudaStream_t st, long long n, int nv, const double* Q, long long vstride,
+                      const double* z, const double* u, double* rows, int* nrows);
 cudaError_t scale(cudaStream_t st, long long n, double a, bool divide, const double* x,
                   double* y);
 cudaError_t frozen(cudaStream_t st, long long n_el, int np, int d, const double* U, double gm1,

@@ -668,6 +668,13 @@ def case_dropin():
     rec = {"case": np.array("dropin"), "U": U}
     rec["implicit_residual"] = split.implicit_residual(U)
     rec["full_residual"] = split.full_residual(U, 0.0)
+    # the reference's own 1-ulp input sensitivity (noise_record)
+    rp = np.random.default_rng(1234)
+    Up = U * (1.0 + 2.0 ** -52 * rp.choice([-1.0, 1.0], size=U.shape))
+    rec["noise_implicit_residual"] = _per_var_noise(split.implicit_residual(Up),
+                                                    rec["implicit_residual"])
+    rec["noise_full_residual"] = _per_var_noise(split.full_residual(Up, 0.0),
+                                                rec["full_residual"])
     rng = np.random.default_rng(99)
     S = np.zeros_like(U)
     for v in range(U.shape[1]):
