@@ -224,6 +224,15 @@ int dg_nccl_unique_id(void* out128);
 int dg_ctx_set_comm(dg_ctx* ctx, const void* unique_id128, int rank, int nranks,
                     const int32_t* send_counts, const int32_t* send_elems,
                     const int32_t* recv_counts);
+/* the same partition plans between nranks contexts of ONE process (one host
+   thread per context, e.g. several contexts on one GPU): ghost rows arrive by
+   one cudaMemcpyAsync per peer ordered by CUDA events and host barriers, the
+   allreduces sum on the host in rank order.  Every rank of `group` must call
+   it (concurrently).  The executable stand-in for the NCCL path on a box with
+   fewer GPUs than ranks (orodg/parallel.py has no multi-process path). */
+int dg_ctx_set_comm_loopback(dg_ctx* ctx, int group, int rank, int nranks,
+                             const int32_t* send_counts, const int32_t* send_elems,
+                             const int32_t* recv_counts);
 int dg_halo_exchange(dg_ctx* ctx, double* field, int ncomp);
 
 /* ---- instrumentation (no reference counterpart; orodg/timing.py is host-only) ----

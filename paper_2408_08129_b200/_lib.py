@@ -92,6 +92,7 @@ _SIGS = {
     "dg_dcgs2_update": ([P, LL, I, P, LL, P, P, P, P, P], I),
     "dg_nccl_unique_id": ([P], I),
     "dg_ctx_set_comm": ([P, P, I, I, P, P, P], I),
+    "dg_ctx_set_comm_loopback": ([P, I, I, I, P, P, P], I),
     "dg_halo_exchange": ([P, P, I], I),
     "dg_split_contiguous": ([P, LL, I, P], I),
     "dg_launch_count": ([], LL),

@@ -3,7 +3,11 @@
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
 
 #include "dg_comm.h"
 
@@ -63,6 +67,145 @@ bool Comm::unique_id(void* out128, std::string* err) {
   return true;
 }
 
+// ------------------------------------------------------------ loopback
+struct LoopGroup {
+  int n = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  std::vector<const double*> sendbuf;
+  std::vector<std::vector<int>> send_off;
+  std::vector<cudaEvent_t> ev_pack, ev_copied;
+  std::vector<std::vector<double>> slots;
+  std::vector<long long> n_el;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const long long g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+static std::mutex g_loop_mu;
+static std::map<int, std::shared_ptr<LoopGroup>> g_loops;
+
+bool Comm::init_plan(int rank, int nranks, const int32_t* send_counts, const int32_t* send_elems,
+                     const int32_t* recv_counts, int n_el, int n_tot) {
+  rank_ = rank;
+  nranks_ = nranks;
+  n_el_ = n_el;
+  n_tot_ = n_tot;
+  send_counts_.assign(send_counts, send_counts + nranks);
+  recv_counts_.assign(recv_counts, recv_counts + nranks);
+  send_off_.assign(nranks + 1, 0);
+  recv_off_.assign(nranks + 1, 0);
+  for (int p = 0; p < nranks; ++p) {
+    send_off_[p + 1] = send_off_[p] + send_counts_[p];
+    recv_off_[p + 1] = recv_off_[p] + recv_counts_[p];
+  }
+  n_send_ = send_off_[nranks];
+  if (recv_off_[nranks] != n_tot - n_el) {
+    err_ = "halo plan: received ghost count does not match n_tot - n_el";
+    return false;
+  }
+  if (n_send_ > 0) {
+    CUCK(cudaMalloc(&d_send_elems_, n_send_ * sizeof(int)));
+    CUCK(cudaMemcpy(d_send_elems_, send_elems, n_send_ * sizeof(int), cudaMemcpyHostToDevice));
+  }
+  CUCK(cudaMalloc(&scratch_, 8 * sizeof(double) + nranks * sizeof(double)));
+  return true;
+}
+
+bool Comm::init_loopback(int group, int rank, int nranks, const int32_t* send_counts,
+                         const int32_t* send_elems, const int32_t* recv_counts, int n_el,
+                         int n_tot) {
+  if (nranks <= 1) {
+    rank_ = 0;
+    nranks_ = 1;
+    return true;
+  }
+  std::shared_ptr<LoopGroup> G;
+  {
+    std::lock_guard<std::mutex> lk(g_loop_mu);
+    auto& slot = g_loops[group];
+    if (!slot) {
+      slot = std::make_shared<LoopGroup>();
+      slot->n = nranks;
+      slot->sendbuf.assign(nranks, nullptr);
+      slot->send_off.assign(nranks, {});
+      slot->ev_pack.assign(nranks, nullptr);
+      slot->ev_copied.assign(nranks, nullptr);
+      slot->slots.assign(nranks, {});
+      slot->n_el.assign(nranks, 0);
+    }
+    if (slot->n != nranks) {
+      err_ = "loopback group size mismatch";
+      return false;
+    }
+    G = slot;
+  }
+  if (!init_plan(rank, nranks, send_counts, send_elems, recv_counts, n_el, n_tot)) return false;
+  CUCK(cudaEventCreateWithFlags(&G->ev_pack[rank], cudaEventDisableTiming));
+  CUCK(cudaEventCreateWithFlags(&G->ev_copied[rank], cudaEventDisableTiming));
+  CUCK(cudaEventRecord(G->ev_copied[rank], 0));
+  G->send_off[rank] = send_off_;
+  G->n_el[rank] = n_el;
+  loop_ = G.get();
+  G->barrier();  // every rank registered
+  offset_ = 0;
+  for (int p = 0; p < rank; ++p) offset_ += G->n_el[p];
+  // keep the group alive while any member uses it
+  static std::mutex keep_mu;
+  static std::vector<std::shared_ptr<LoopGroup>> keep;
+  {
+    std::lock_guard<std::mutex> lk(keep_mu);
+    keep.push_back(G);
+  }
+  G->barrier();
+  if (rank == 0) {
+    std::lock_guard<std::mutex> lk(g_loop_mu);
+    g_loops.erase(group);  // the id can be reused by a later group
+  }
+  return true;
+}
+
+bool Comm::ensure_bufs(size_t per) {
+  const size_t need = std::max((size_t)n_send_, (size_t)(n_tot_ - n_el_)) * per;
+  if (need > buf_cap_) {
+    if (loop_) CUCK(cudaDeviceSynchronize());  // peers may still read the old buffer
+    if (sendbuf_) cudaFree(sendbuf_);
+    if (recvbuf_) cudaFree(recvbuf_);
+    CUCK(cudaMalloc(&sendbuf_, need * sizeof(double)));
+    CUCK(cudaMalloc(&recvbuf_, need * sizeof(double)));
+    buf_cap_ = need;
+  }
+  return true;
+}
+
+// op: 0 sum, 1 max
+bool Comm::loop_reduce(double* dev, int n, cudaStream_t st, int op) {
+  LoopGroup* G = loop_;
+  auto& mine = G->slots[rank_];
+  if ((int)mine.size() < n) mine.resize(n);
+  CUCK(cudaMemcpyAsync(mine.data(), dev, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUCK(cudaStreamSynchronize(st));
+  G->barrier();
+  std::vector<double> r(G->slots[0].begin(), G->slots[0].begin() + n);
+  for (int q = 1; q < G->n; ++q)
+    for (int i = 0; i < n; ++i)
+      r[i] = op == 0 ? r[i] + G->slots[q][i] : std::max(r[i], G->slots[q][i]);
+  G->barrier();  // every rank has read the slots
+  CUCK(cudaMemcpyAsync(dev, r.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+  CUCK(cudaStreamSynchronize(st));
+  return true;
+}
+
 bool Comm::init(const void* uid, int rank, int nranks, const int32_t* send_counts,
                 const int32_t* send_elems, const int32_t* recv_counts, int n_el, int n_tot) {
   rank_ = rank;
@@ -109,14 +252,41 @@ bool Comm::exchange(double* field, int ncomp, int np, cudaStream_t st, long long
   if (nranks_ <= 1) return true;
   if (estride < 0) estride = (long long)ncomp * np;
   const size_t per = (size_t)ncomp * np;
-  const size_t need = std::max((size_t)n_send_, (size_t)(n_tot_ - n_el_)) * per;
-  if (need > buf_cap_) {
-    if (sendbuf_) cudaFree(sendbuf_);
-    if (recvbuf_) cudaFree(recvbuf_);
-    CUCK(cudaMalloc(&sendbuf_, need * sizeof(double)));
-    CUCK(cudaMalloc(&recvbuf_, need * sizeof(double)));
-    buf_cap_ = need;
+  if (loop_) {
+    LoopGroup* G = loop_;
+    // the peers' copies out of our send buffer (previous exchange) are done
+    for (int q = 0; q < nranks_; ++q)
+      if (q != rank_) CUCK(cudaStreamWaitEvent(st, G->ev_copied[q], 0));
+    if (!ensure_bufs(per)) return false;
+    if (n_send_ > 0) {
+      const long long tot = (long long)n_send_ * per;
+      const int grid = (int)std::min<long long>((tot + 255) / 256, 4096);
+      k_pack<<<grid, 256, 0, st>>>(field, estride, ncomp, np, d_send_elems_, n_send_, sendbuf_);
+      CUCK(cudaGetLastError());
+    }
+    CUCK(cudaEventRecord(G->ev_pack[rank_], st));
+    G->sendbuf[rank_] = sendbuf_;
+    G->barrier();  // every rank's pack is recorded
+    for (int q = 0; q < nranks_; ++q) {
+      if (q == rank_ || recv_counts_[q] == 0) continue;
+      CUCK(cudaStreamWaitEvent(st, G->ev_pack[q], 0));
+      CUCK(cudaMemcpyAsync(recvbuf_ + (size_t)recv_off_[q] * per,
+                           G->sendbuf[q] + (size_t)G->send_off[q][rank_] * per,
+                           (size_t)recv_counts_[q] * per * sizeof(double), cudaMemcpyDeviceToDevice,
+                           st));
+    }
+    CUCK(cudaEventRecord(G->ev_copied[rank_], st));
+    G->barrier();  // every rank's copies are recorded
+    const int ng = n_tot_ - n_el_;
+    if (ng > 0) {
+      const long long tot = (long long)ng * per;
+      const int grid = (int)std::min<long long>((tot + 255) / 256, 4096);
+      k_unpack<<<grid, 256, 0, st>>>(field, estride, ncomp, np, n_el_, ng, recvbuf_);
+      CUCK(cudaGetLastError());
+    }
+    return true;
   }
+  if (!ensure_bufs(per)) return false;
   if (n_send_ > 0) {
     const long long tot = (long long)n_send_ * per;
     const int grid = (int)std::min<long long>((tot + 255) / 256, 4096);
@@ -147,18 +317,39 @@ bool Comm::exchange(double* field, int ncomp, int np, cudaStream_t st, long long
 
 bool Comm::allreduce_sum(double* dev, int n, cudaStream_t st) {
   if (nranks_ <= 1) return true;
+  if (loop_) return loop_reduce(dev, n, st, 0);
   NCCK(ncclAllReduce(dev, dev, n, ncclDouble, ncclSum, (ncclComm_t)comm_, st));
   return true;
 }
 
 bool Comm::allreduce_max(double* dev, int n, cudaStream_t st) {
   if (nranks_ <= 1) return true;
+  if (loop_) return loop_reduce(dev, n, st, 1);
   NCCK(ncclAllReduce(dev, dev, n, ncclDouble, ncclMax, (ncclComm_t)comm_, st));
   return true;
 }
 
 bool Comm::allreduce_minloc(double loc[4], cudaStream_t st) {
   if (nranks_ <= 1) return true;
+  if (loop_) {
+    LoopGroup* G = loop_;
+    auto& mine = G->slots[rank_];
+    if (mine.size() < 4) mine.resize(4);
+    std::copy(loc, loc + 4, mine.begin());
+    G->barrier();
+    double v[2] = {INFINITY, INFINITY}, idx[2] = {INFINITY, INFINITY};
+    for (int q = 0; q < G->n; ++q)
+      for (int k = 0; k < 2; ++k) v[k] = std::min(v[k], G->slots[q][2 * k]);
+    for (int q = 0; q < G->n; ++q)
+      for (int k = 0; k < 2; ++k)
+        if (G->slots[q][2 * k] == v[k]) idx[k] = std::min(idx[k], G->slots[q][2 * k + 1]);
+    G->barrier();
+    loc[0] = v[0];
+    loc[1] = idx[0];
+    loc[2] = v[1];
+    loc[3] = idx[1];
+    return true;
+  }
   ncclComm_t c = (ncclComm_t)comm_;
   double v[2] = {loc[0], loc[2]};
   CUCK(cudaMemcpyAsync(scratch_, v, 2 * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -180,6 +371,7 @@ bool Comm::allreduce_minloc(double loc[4], cudaStream_t st) {
 void Comm::shutdown() {
   if (comm_) ncclCommDestroy((ncclComm_t)comm_);
   comm_ = nullptr;
+  loop_ = nullptr;
   if (d_send_elems_) cudaFree(d_send_elems_);
   if (sendbuf_) cudaFree(sendbuf_);
   if (recvbuf_) cudaFree(recvbuf_);

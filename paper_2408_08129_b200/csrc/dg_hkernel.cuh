@@ -98,6 +98,25 @@ __device__ __forceinline__ void tab_bulk_wait(unsigned long long* bar) {
       : "memory");
 }
 
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      "HK2_WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @P1 bra HK2_DONE;\n"
+      " bra HK2_WAIT;\n"
+      "HK2_DONE:\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
 // own-geometry face metric at face point c of face (AX, side): the
 // +axis-oriented unit normal n+ and the face weight ws (geometry.py:305-357;
 // vertical faces have the exact normal e_AX, terrain z faces pay the sqrt)
@@ -213,61 +232,60 @@ __device__ __forceinline__ double edge_omh(const GeoConst& gc, const double* col
 }
 
 // ---------------------------------------------------------------------- H1
+// 64-byte element records of the pipelined kernels (hk_elem_records):
+// int32 nbr[2d] | uint8 kind[2d] at byte 24 | int32 elem row (level,
+// origin[d], column) at byte 32
+constexpr int REC_INTS = 16;
+template <int D>
+__device__ __forceinline__ ElemGeo<D> geo_from_row(const int* r, const GeoConst& gc) {
+  ElemGeo<D> g;
+  const double scale = __longlong_as_double((long long)(1023 - r[0]) << 52);
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    g.s[a] = gc.per_root[a] * scale;
+    g.lo[a] = g.s[a] * (double)r[1 + a];
+  }
+  g.col = r[1 + D];
+  return g;
+}
+
+// One element's H1 on lane c (see the file comment).  Inputs: the lane's
+// nodal x column (xcol[k], k < n), the neighbours' raw face nodes staged at
+// FG[f n^(d-1) + c] (0 where there is no interior neighbour), the own h
+// traces hf(f) = hrow[f n^(d-1)], the element's face records, geometry and
+// column row (terrain).  Writes V, psi (+ pin scatter, + trV for elements
+// with a coarse face).
 template <int D, int N>
-__global__ void __launch_bounds__(HLayout<D, N>::THREADS, DG_HK1_MINB)
-hgrad_kernel(const __grid_constant__ KParams<N> P) {
+__device__ __forceinline__ void hgrad_body(const KParams<N>& P, const Tab<N>& TS, int c, bool act,
+                                           long long e, const uint8_t (&kf)[2 * D],
+                                           const int (&nf)[2 * D], const ElemGeo<D>& g,
+                                           const double* colrow, const double* xcol,
+                                           const double* hrow, double* X, double* FG, double* HW) {
   using HL = HLayout<D, N>;
-  constexpr int NC = HL::NC, EPW = HL::EPW, NF = HL::NF, TSZ = HL::TSZ;
-  extern __shared__ __align__(16) double smem[];
-  __shared__ unsigned long long tbar;
-  tab_bulk_issue(smem, P.tab_g, HL::TABD * 8, &tbar);
-  const Tab<N>& TS = *reinterpret_cast<const Tab<N>*>(smem);
+  constexpr int NC = HL::NC, NF = HL::NF, TSZ = HL::TSZ;
+  constexpr int NQH = ipow(N, D - 1), NE = ipow(N, D - 2);
   const Tab<N>& TC = P.tab;
   const MeshDev& mesh = P.mesh;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int eiw = lane / NC, c = lane - eiw * NC;
-  const bool slot_ok = eiw < EPW;
-  const long long e = ((long long)blockIdx.x * HL::WPB + wid) * EPW + eiw;
-  const bool act = slot_ok && e < mesh.n_el;
-  const long long es = act ? e : 0;
-  double* X = smem + HL::TABP + (wid * HL::NSLOT + (slot_ok ? eiw : EPW)) * HL::GSLOT;
-  double* FG = X + HL::KX * TSZ;
-  double* HW = FG + NF * NC;
-
-  uint8_t kf[NF];
-  int nf[NF];
+  ColData<D, N> cd;
+  cd.omh = 1.0;
+  cd.dh[0] = cd.dh[1] = 0.0;
+  if (P.gc.terrain && act) {
+    cd.omh = colrow[c];
 #pragma unroll
-  for (int f = 0; f < NF; ++f) {
-    kf[f] = act ? mesh.kind[es * NF + f] : (uint8_t)KIND_WALL;
-    nf[f] = act ? mesh.nbr[es * NF + f] : 0;
+    for (int a = 0; a < D - 1; ++a) cd.dh[a] = colrow[NQH * (1 + a) + c];
   }
-  // own nodal column and the neighbours' face nodes, all loads in flight
-  double xc[N];
-#pragma unroll
-  for (int k = 0; k < N; ++k) xc[k] = act ? P.in.p[es * P.in.estride + c * N + k] : 0.0;
-  double gn[NF];
-#pragma unroll
-  for (int f = 0; f < NF; ++f) {
-    const int kd = kf[f] & 15;
-    const bool inter = act && (kd == KIND_CONF || kd == KIND_FINE);
-    gn[f] = inter ? P.in.p[(long long)nf[f] * P.in.estride + nbr_face_node<D, N>(f >> 1, f & 1, c)]
-                  : 0.0;
-  }
-  const ElemGeo<D> g = elem_geo<D>(mesh.elem, P.gc, es);
-  const ColData<D, N> cd = col_data<D, N>(P.gc, mesh.col, g, c, act);
-  __syncthreads();  // the table barrier is initialised
-
+  auto edge = [&](int f) -> double {
+    return (P.gc.terrain && act) ? colrow[NQH * D + f * NE + ((D == 2) ? 0 : c / N)] : 1.0;
+  };
   // ---- p = alpha x to the Gauss points (z in registers, y / x via the tile)
   {
     double col[N], q[N];
 #pragma unroll
-    for (int k = 0; k < N; ++k) col[k] = P.alpha * xc[k];
+    for (int k = 0; k < N; ++k) col[k] = P.alpha * xcol[k];
     mat_apply<N, false>(TC.B, col, q);
 #pragma unroll
     for (int k = 0; k < N; ++k) X[coff<D, N>(c, k)] = q[k];
   }
-#pragma unroll
-  for (int f = 0; f < NF; ++f) FG[f * NC + c] = P.alpha * gn[f];
   __syncwarp();
   if constexpr (D == 3) {
     double v[N], o[N];
@@ -286,7 +304,6 @@ hgrad_kernel(const __grid_constant__ KParams<N> P) {
 #pragma unroll
     for (int ii = 0; ii < N; ++ii) X[xoff<D, N>(c, ii)] = o[ii];
   }
-  tab_bulk_wait(&tbar);
   // ---- neighbour traces at face point c: tangential passes over the staged
   // face nodes (B, or the mortar halves for a fine leaf's coarse parent)
   const int fa = (D == 2) ? c : c / N;
@@ -346,9 +363,8 @@ hgrad_kernel(const __grid_constant__ KParams<N> P) {
       for (int a = 0; a < D; ++a) fl[a] = cf ? mesh.cflux[((long long)nf[f] * D + a) * NC + c] : 0.0;
     } else {
       double n[D], ws;
-      const double oe = (AX < D - 1) ? edge_omh<D, N>(P.gc, mesh.col, g, f, c, act) : 1.0;
-      face_nplus<D, N, AX>(P.gc, g, side, c, TS, oe, cd.dh, n, ws);
-      const double px = (kd == KIND_WALL) ? to : (kd == KIND_FARFIELD ? 0.0 : tn[f]);
+      face_nplus<D, N, AX>(P.gc, g, side, c, TS, (AX < D - 1) ? edge(f) : 1.0, cd.dh, n, ws);
+      const double px = (kd == KIND_WALL) ? to : (kd == KIND_FARFIELD ? 0.0 : P.alpha * tn[f]);
       const double ph = to + px;
       const double sg = side ? 1.0 : -1.0;
 #pragma unroll
@@ -379,10 +395,6 @@ hgrad_kernel(const __grid_constant__ KParams<N> P) {
   }
   face(std::integral_constant<int, D - 1>{}, std::integral_constant<int, 0>{});
   face(std::integral_constant<int, D - 1>{}, std::integral_constant<int, 1>{});
-  // own h traces at the face points (frozen per fixed-point iterate)
-  double hf[NF];
-#pragma unroll
-  for (int f = 0; f < NF; ++f) hf[f] = act ? P.trH[es * (NF * NC) + f * NC + c] : 0.0;
 
   // ---- volume: G_bx,k = ctrv[bx][k] p wq; bx < d-1 through the tile
   double Zc[D][N];
@@ -484,13 +496,13 @@ hgrad_kernel(const __grid_constant__ KParams<N> P) {
     double* ps = P.psi_out + e * (NF * NC);
     double pv[NF];
 #pragma unroll
-    for (int f = 0; f < 2 * (D - 1); ++f) pv[f] = hf[f] * (HW[f * NC + c] * tv[f]);
+    for (int f = 0; f < 2 * (D - 1); ++f) pv[f] = hrow[f * NC] * (HW[f * NC + c] * tv[f]);
 #pragma unroll
     for (int side = 0; side < 2; ++side) {
       double vn = 0.0;
 #pragma unroll
       for (int a = 0; a < D; ++a) vn = fma(HW[(2 * (D - 1) + side * D + a) * NC + c], tz[side][a], vn);
-      pv[2 * (D - 1) + side] = hf[2 * (D - 1) + side] * vn;
+      pv[2 * (D - 1) + side] = hrow[(2 * (D - 1) + side) * NC] * vn;
     }
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
@@ -505,8 +517,8 @@ hgrad_kernel(const __grid_constant__ KParams<N> P) {
 #pragma unroll
     for (int f = 0; f < NF; ++f) coarse |= (kf[f] & 15) == KIND_COARSE;
     if (coarse && P.tr_out != nullptr) {
-      // the mortar of the fine neighbours (hdiv_kernel) and the coarse-side
-      // fluxes (coarse_kernel) read this element's V traces
+      // the mortar of the fine neighbours (hdiv) and the coarse-side fluxes
+      // (coarse_kernel) read this element's V traces
       constexpr int TSL = tr_slots<D>() * NC;
       double* tr = P.tr_out + e * TSL;
 #pragma unroll
@@ -517,6 +529,231 @@ hgrad_kernel(const __grid_constant__ KParams<N> P) {
         for (int k = 0; k < D; ++k) tr[tr_slot<D>(2 * (D - 1) + side, k) * NC + c] = tz[side][k];
     }
   }
+}
+
+template <int D, int N>
+__global__ void __launch_bounds__(HLayout<D, N>::THREADS, DG_HK1_MINB)
+hgrad_kernel(const __grid_constant__ KParams<N> P) {
+  using HL = HLayout<D, N>;
+  constexpr int NC = HL::NC, EPW = HL::EPW, NF = HL::NF, TSZ = HL::TSZ;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ unsigned long long tbar;
+  tab_bulk_issue(smem, P.tab_g, HL::TABD * 8, &tbar);
+  const Tab<N>& TS = *reinterpret_cast<const Tab<N>*>(smem);
+  const MeshDev& mesh = P.mesh;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int eiw = lane / NC, c = lane - eiw * NC;
+  const bool slot_ok = eiw < EPW;
+  const long long e = ((long long)blockIdx.x * HL::WPB + wid) * EPW + eiw;
+  const bool act = slot_ok && e < mesh.n_el;
+  const long long es = act ? e : 0;
+  double* X = smem + HL::TABP + (wid * HL::NSLOT + (slot_ok ? eiw : EPW)) * HL::GSLOT;
+  double* FG = X + HL::KX * TSZ;
+  double* HW = FG + NF * NC;
+  uint8_t kf[NF];
+  int nf[NF];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    kf[f] = act ? mesh.kind[es * NF + f] : (uint8_t)KIND_WALL;
+    nf[f] = act ? mesh.nbr[es * NF + f] : 0;
+  }
+  double xc[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) xc[k] = act ? P.in.p[es * P.in.estride + c * N + k] : 0.0;
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    const int kd = kf[f] & 15;
+    const bool inter = act && (kd == KIND_CONF || kd == KIND_FINE);
+    FG[f * NC + c] =
+        inter ? P.in.p[(long long)nf[f] * P.in.estride + nbr_face_node<D, N>(f >> 1, f & 1, c)]
+              : 0.0;
+  }
+  const ElemGeo<D> g = elem_geo<D>(mesh.elem, P.gc, es);
+  const double* colrow = P.gc.terrain ? mesh.col + (long long)g.col * P.gc.col_stride : nullptr;
+  __syncthreads();  // the table barrier is initialised
+  tab_bulk_wait(&tbar);
+  hgrad_body<D, N>(P, TS, c, act, e, kf, nf, g, colrow, xc, P.trH + es * (NF * NC) + c, X, FG,
+                   HW);
+}
+
+// H1, pipelined (hgrad2_kernel): persistent warps over strided element
+// groups as hdiv2_kernel.  Per group a two-stage ring holds, by
+// cp.async.bulk, the nodal x blocks, the own h-trace rows and the 64-byte
+// element records; one group AHEAD, as soon as its records have landed, the
+// lanes stage the neighbours' face nodes (cp.async, 8 B each) and the first
+// lane of each element its column row (cp.async.bulk, terrain) -- so every
+// load of a group is in flight while the previous group is computed.
+template <int D, int N>
+struct H1Pipe {
+  using HL = HLayout<D, N>;
+  static constexpr int NP = HL::NP, NC = HL::NC, NF = HL::NF, EPW = HL::EPW;
+  static constexpr int COLS = 2 * ((ipow(N, D - 1) * D + 2 * (D - 1) * ipow(N, D - 2) + 1) / 2);
+  static constexpr bool OK = HL::OK && (NP % 2 == 0) && ((NF * NC) % 2 == 0);
+  static constexpr int OX = 0;                      // nodal x (bulk)
+  static constexpr int OH = OX + EPW * NP;          // own h traces (bulk)
+  static constexpr int OR = OH + EPW * NF * NC;     // records (bulk), 8 doubles each
+  static constexpr int BULK = OR + EPW * 8;
+  static constexpr int OF = BULK;                   // neighbour face nodes (cp.async),
+                                                    // one slot per lane group (+ padding)
+  static constexpr int OC = OF + HL::NSLOT * NF * NC;  // column rows (bulk, terrain)
+  static constexpr int STG = OC + EPW * COLS;
+  static constexpr int ESLOT = HL::odd(HL::KX * HL::TSZ + HL::NHW * NC);  // tile + HW
+  static constexpr int WREG = ((2 * STG + HL::NSLOT * ESLOT) + 1) & ~1;
+  static constexpr int WPB = 4;
+  static constexpr size_t SMEM = (size_t)(HL::TABP + WPB * WREG) * sizeof(double);
+};
+
+#ifndef DG_HK1P_MINB
+#define DG_HK1P_MINB 3
+#endif
+
+__device__ __forceinline__ void cp_async8_raw(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+
+template <int D, int N>
+__global__ void __launch_bounds__(128, DG_HK1P_MINB)
+hgrad2_kernel(const __grid_constant__ KParams<N> P) {
+  using HL = HLayout<D, N>;
+  using PL = H1Pipe<D, N>;
+  constexpr int NC = HL::NC, EPW = HL::EPW, NF = HL::NF, TSZ = HL::TSZ, NP = HL::NP;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ unsigned long long tbar;
+  __shared__ unsigned long long sbar[PL::WPB][2], cbar[PL::WPB][2];
+  tab_bulk_issue(smem, P.tab_g, HL::TABD * 8, &tbar);
+  const Tab<N>& TS = *reinterpret_cast<const Tab<N>*>(smem);
+  const MeshDev& mesh = P.mesh;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int eiw = lane / NC, c = lane - eiw * NC;
+  const bool slot_ok = eiw < EPW;
+  double* W = smem + HL::TABP + wid * PL::WREG;
+  double* ES = W + 2 * PL::STG + (slot_ok ? eiw : EPW) * PL::ESLOT;
+  double* X = ES;
+  double* HW = ES + HL::KX * TSZ;
+  const unsigned bar[2] = {smem_u32(&sbar[wid][0]), smem_u32(&sbar[wid][1])};
+  const unsigned cb[2] = {smem_u32(&cbar[wid][0]), smem_u32(&cbar[wid][1])};
+  const long long ngroups = ((long long)mesh.n_el + EPW - 1) / EPW;
+  const long long gw = (long long)blockIdx.x * PL::WPB + wid;
+  const long long GW = (long long)gridDim.x * PL::WPB;
+  const bool terr = P.gc.terrain != 0;
+
+  auto issue = [&](long long g, int s) {  // lane 0: the bulk part of group g
+    const long long e0 = g * EPW;
+    const int ne = (int)min((long long)EPW, (long long)mesh.n_el - e0);
+    double* st = W + s * PL::STG;
+    const unsigned bytes = 8u * ne * (NP + NF * NC + 8);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar[s]),
+                 "r"(bytes)
+                 : "memory");
+    bulk_g2s(st + PL::OX, P.in.p + e0 * P.in.estride, 8u * ne * NP, bar[s]);
+    bulk_g2s(st + PL::OH, P.trH + e0 * (NF * NC), 8u * ne * NF * NC, bar[s]);
+    bulk_g2s(st + PL::OR, P.frec + e0 * REC_INTS, 64u * ne, bar[s]);
+  };
+  // all lanes: the lookahead part of group g (its records landed): the
+  // neighbours' face nodes and (terrain) the column rows
+  auto lookahead = [&](long long g, int s) {
+    double* st = W + s * PL::STG;
+    const long long e = g * EPW + eiw;
+    const bool act = slot_ok && e < mesh.n_el;
+    const int esl = act ? eiw : 0;
+    const int* rec = reinterpret_cast<const int*>(st + PL::OR) + esl * REC_INTS;
+    const uint8_t* rk = reinterpret_cast<const uint8_t*>(rec + 6);
+    double* fg = st + PL::OF + (slot_ok ? eiw : EPW) * (NF * NC);
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      const int kd = rk[f] & 15;
+      const bool inter = act && (kd == KIND_CONF || kd == KIND_FINE);
+      if (inter)
+        cp_async8_raw(fg + f * NC + c,
+                      P.in.p + (long long)rec[f] * P.in.estride + nbr_face_node<D, N>(f >> 1, f & 1, c));
+      else
+        fg[f * NC + c] = 0.0;
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    if (terr) {
+      // one column row per element, by the element's first lane
+      const int ne = (int)min((long long)EPW, (long long)mesh.n_el - g * EPW);
+      if (lane == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(cb[s]),
+                     "r"(8u * ne * PL::COLS)
+                     : "memory");
+      }
+      __syncwarp();
+      if (act && c == 0) {
+        const int colid = rec[8 + 1 + D];
+        bulk_g2s(st + PL::OC + eiw * PL::COLS, mesh.col + (long long)colid * P.gc.col_stride,
+                 8u * PL::COLS, cb[s]);
+      }
+    }
+  };
+
+  if (lane == 0) {
+    for (int s = 0; s < 2; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar[s]) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(cb[s]) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    if (gw < ngroups) issue(gw, 0);
+    if (gw + GW < ngroups) issue(gw + GW, 1);
+  }
+  __syncthreads();  // barriers initialised
+  if (gw < ngroups) {
+    mbar_wait(bar[0], 0);
+    lookahead(gw, 0);
+  }
+  tab_bulk_wait(&tbar);
+
+  int k = 0;
+  for (long long g = gw; g < ngroups; g += GW, ++k) {
+    const int s = k & 1;
+    const unsigned par = (unsigned)((k >> 1) & 1);
+    mbar_wait(bar[s], par);  // (already complete: waited before the lookahead)
+    // this group's lookahead copies, then the next group's lookahead
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    if (terr) mbar_wait(cb[s], par);
+    __syncwarp();
+    if (g + GW < ngroups) {
+      const int s1 = s ^ 1;
+      mbar_wait(bar[s1], (unsigned)(((k + 1) >> 1) & 1));
+      lookahead(g + GW, s1);
+    }
+    double* st = W + s * PL::STG;
+    const long long e = g * EPW + eiw;
+    const bool act = slot_ok && e < mesh.n_el;
+    const int esl = act ? eiw : 0;
+    const int* rec = reinterpret_cast<const int*>(st + PL::OR) + esl * REC_INTS;
+    const uint8_t* rk = reinterpret_cast<const uint8_t*>(rec + 6);
+    uint8_t kf[NF];
+    int nf[NF];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      kf[f] = act ? rk[f] : (uint8_t)KIND_WALL;
+      nf[f] = rec[f];
+    }
+    const ElemGeo<D> g3 = geo_from_row<D>(rec + 8, P.gc);
+    hgrad_body<D, N>(P, TS, c, act, e, kf, nf, g3, st + PL::OC + esl * PL::COLS,
+                     st + PL::OX + esl * NP + c * N, st + PL::OH + esl * (NF * NC) + c, X,
+                     st + PL::OF + (slot_ok ? eiw : EPW) * (NF * NC), HW);
+    __syncwarp();  // every lane is done with this stage
+    if (lane == 0 && g + 2 * GW < ngroups) issue(g + 2 * GW, s);
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+// 64-byte element records of the pipelined kernels (see REC_INTS)
+template <int D>
+__global__ void hk_elem_records(const int* __restrict__ nbr, const uint8_t* __restrict__ kind,
+                                const int* __restrict__ elem, int n, int* __restrict__ rec) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  int r[REC_INTS];
+  for (int i = 0; i < REC_INTS; ++i) r[i] = 0;
+  for (int f = 0; f < 2 * D; ++f) r[f] = nbr[(long long)e * 2 * D + f];
+  uint8_t* kb = reinterpret_cast<uint8_t*>(r + 6);
+  for (int f = 0; f < 2 * D; ++f) kb[f] = kind[(long long)e * 2 * D + f];
+  for (int i = 0; i < 2 + D; ++i) r[8 + i] = elem[(long long)e * (2 + D) + i];
+  for (int i = 0; i < REC_INTS; ++i) rec[(long long)e * REC_INTS + i] = r[i];
 }
 
 // ---------------------------------------------------------------------- H2
@@ -807,32 +1044,15 @@ struct H2Pipe {
   static constexpr int OI = OP + EPW * NF * NC;
   static constexpr int OB = OI + EPW * NF * NC;
   static constexpr int OR = OB + EPW * NP;
-  static constexpr int STG = OR + EPW * 4;  // + 32-byte records
+  static constexpr int OC = OR + EPW * 8;   // + 64-byte records
+  static constexpr int COLS = 2 * ((ipow(N, D - 1) * D + 2 * (D - 1) * ipow(N, D - 2) + 1) / 2);
+  static constexpr int STG = OC + EPW * COLS;  // + column rows (lookahead, terrain)
   static constexpr int TSLOT = HL::odd(HL::DRAW);
   static constexpr int WT = 2 * (32 + 2);
   static constexpr int WREG = ((2 * STG + HL::NSLOT * TSLOT + WT) + 1) & ~1;  // per warp
   static constexpr int WPB = 4;
   static constexpr size_t SMEM = (size_t)(HL::TABP + WPB * WREG) * sizeof(double);
 };
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred P1;\n"
-      "HK2_WAIT:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      " @P1 bra HK2_DONE;\n"
-      " bra HK2_WAIT;\n"
-      "HK2_DONE:\n}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
 
 // the fused Gram-Schmidt dots accumulated over the groups of a warp
 // (gs_round with += into the warp's column totals)
@@ -883,7 +1103,7 @@ __device__ __forceinline__ void gs_round_acc(const KParams<N>& P, bool own, long
 #define DG_HK2P_MINB 2
 #endif
 
-template <int D, int N>
+template <int D, int N, bool LA>
 __global__ void __launch_bounds__(128, DG_HK2P_MINB)
 hdiv2_kernel(const __grid_constant__ KParams<N> P) {
   using HL = HLayout<D, N>;
@@ -891,7 +1111,7 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
   constexpr int NC = HL::NC, EPW = HL::EPW, NF = HL::NF, TSZ = HL::TSZ, NP = HL::NP;
   extern __shared__ __align__(16) double smem[];
   __shared__ unsigned long long tbar;
-  __shared__ unsigned long long sbar[PL::WPB][2];
+  __shared__ unsigned long long sbar[PL::WPB][2], cbar[PL::WPB][2];
   tab_bulk_issue(smem, P.tab_g, HL::TABD * 8, &tbar);
   const Tab<N>& TS = *reinterpret_cast<const Tab<N>*>(smem);
   const Tab<N>& TC = P.tab;
@@ -899,6 +1119,10 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int eiw = lane / NC, c = lane - eiw * NC;
   const bool slot_ok = eiw < EPW;
+  // LA: geometry from the staged records and the column rows by lookahead
+  // bulk copies; else both by (latency-exposed) global loads
+  const bool terr = LA && P.gc.terrain != 0;
+  const unsigned cb[2] = {smem_u32(&cbar[wid][0]), smem_u32(&cbar[wid][1])};
   double* W = smem + HL::TABP + wid * PL::WREG;
   double* STG0 = W;
   double* X = W + 2 * PL::STG + (slot_ok ? eiw : EPW) * PL::TSLOT;
@@ -919,7 +1143,7 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
     const int ne = (int)min((long long)EPW, (long long)mesh.n_el - e0);
     double* st = STG0 + s * PL::STG;
     const unsigned b = s ? bar1 : bar0;
-    const unsigned bytes = 8u * ne * (D * NP + NP + 2 * NF * NC + (P.has_base ? NP : 0) + 4);
+    const unsigned bytes = 8u * ne * (D * NP + NP + 2 * NF * NC + (P.has_base ? NP : 0) + 8);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes)
                  : "memory");
     bulk_g2s(st + PL::OV, P.in.p + e0 * P.in.estride, 8u * ne * D * NP, b);
@@ -927,7 +1151,7 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
     bulk_g2s(st + PL::OP, P.psi + e0 * (NF * NC), 8u * ne * NF * NC, b);
     bulk_g2s(st + PL::OI, P.pin + e0 * (NF * NC), 8u * ne * NF * NC, b);
     if (P.has_base) bulk_g2s(st + PL::OB, P.base.p + e0 * P.base.estride, 8u * ne * NP, b);
-    bulk_g2s(st + PL::OR, P.frec + e0 * 8, 32u * ne, b);
+    bulk_g2s(st + PL::OR, P.frec + e0 * REC_INTS, 64u * ne, b);
     if (dots) {
       // the fused dots' basis slices of this group into L2
       for (int i = 0; i < nv; ++i) {
@@ -938,14 +1162,36 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
       }
     }
   };
+  // all lanes, once group g's records have landed: its column rows (terrain)
+  auto lookahead = [&](long long g, int s) {
+    if (!terr) return;
+    double* st = STG0 + s * PL::STG;
+    const int ne = (int)min((long long)EPW, (long long)mesh.n_el - g * EPW);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(cb[s]),
+                   "r"(8u * ne * PL::COLS)
+                   : "memory");
+    __syncwarp();
+    if (slot_ok && c == 0 && g * EPW + eiw < mesh.n_el) {
+      const int* rec = reinterpret_cast<const int*>(st + PL::OR) + eiw * REC_INTS;
+      bulk_g2s(st + PL::OC + eiw * PL::COLS, mesh.col + (long long)rec[8 + 1 + D] * P.gc.col_stride,
+               8u * PL::COLS, cb[s]);
+    }
+  };
   if (lane == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0) : "memory");
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar1) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(cb[0]) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(cb[1]) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     if (gw < ngroups) issue(gw, 0);
     if (gw + GW < ngroups) issue(gw + GW, 1);
   }
   __syncthreads();  // the table barrier is initialised (and every stage barrier)
+  if (gw < ngroups) {
+    mbar_wait(bar0, 0);
+    lookahead(gw, 0);
+  }
   tab_bulk_wait(&tbar);
   const int fa = (D == 2) ? c : c / N;
   const int fb = (D == 2) ? 0 : c % N;
@@ -955,12 +1201,18 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
   int k = 0;
   for (long long g = gw; g < ngroups; g += GW, ++k) {
     const int s = k & 1;
-    mbar_wait(s ? bar1 : bar0, (unsigned)((k >> 1) & 1));
+    const unsigned par = (unsigned)((k >> 1) & 1);
+    mbar_wait(s ? bar1 : bar0, par);
+    if (terr) mbar_wait(cb[s], par);
+    if (g + GW < ngroups) {
+      mbar_wait(s ? bar0 : bar1, (unsigned)(((k + 1) >> 1) & 1));
+      lookahead(g + GW, s ^ 1);
+    }
     const double* st = STG0 + s * PL::STG;
     const long long e = g * EPW + eiw;
     const bool act = slot_ok && e < mesh.n_el;
     const int esl = act ? eiw : 0;
-    const int* rec = reinterpret_cast<const int*>(st + PL::OR) + esl * 8;
+    const int* rec = reinterpret_cast<const int*>(st + PL::OR) + esl * REC_INTS;
     const uint8_t* rk = reinterpret_cast<const uint8_t*>(rec + 6);
     uint8_t kf[NF];
     int nf[NF];
@@ -984,9 +1236,18 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
         fl[f] = act ? v : 0.0;
       }
     }
-    const long long es = act ? e : 0;
-    const ElemGeo<D> g3 = elem_geo<D>(mesh.elem, P.gc, es);
-    const ColData<D, N> cd = col_data<D, N>(P.gc, mesh.col, g3, c, act);
+    const ElemGeo<D> g3 = LA ? geo_from_row<D>(rec + 8, P.gc) : elem_geo<D>(mesh.elem, P.gc, act ? e : 0);
+    const double* colrow = LA ? st + PL::OC + esl * PL::COLS
+                              : mesh.col + (long long)g3.col * P.gc.col_stride;
+    ColData<D, N> cd;
+    cd.omh = 1.0;
+    cd.dh[0] = cd.dh[1] = 0.0;
+    if (P.gc.terrain && act) {
+      constexpr int NQH = ipow(N, D - 1);
+      cd.omh = colrow[c];
+#pragma unroll
+      for (int a = 0; a < D - 1; ++a) cd.dh[a] = colrow[NQH * (1 + a) + c];
+    }
     // fine side of hanging faces (as hdiv_kernel)
     auto fine_face = [&](auto ax_c, auto side_c) {
       constexpr int AX = decltype(ax_c)::value;
@@ -1042,7 +1303,9 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
       __syncwarp();
       if (fine) {
         double n[D], ws;
-        const double oe = (AX < D - 1) ? edge_omh<D, N>(P.gc, mesh.col, g3, f, c, act) : 1.0;
+        constexpr int NQH = ipow(N, D - 1), NE = ipow(N, D - 2);
+        const double oe = (AX < D - 1 && P.gc.terrain)
+                              ? colrow[NQH * D + f * NE + ((D == 2) ? 0 : c / N)] : 1.0;
         face_nplus<D, N, AX>(P.gc, g3, side, c, TS, oe, cd.dh, n, ws);
         double vn;
         if constexpr (AX < D - 1) {
@@ -1178,19 +1441,6 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
       }
     }
   }
-}
-
-// 32-byte face records for the pipelined H2: int32 nbr[2d] | uint8 kind[2d]
-template <int D>
-__global__ void hk_face_records(const int* __restrict__ nbr, const uint8_t* __restrict__ kind,
-                                int n, int* __restrict__ rec) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n) return;
-  int r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int f = 0; f < 2 * D; ++f) r[f] = nbr[(long long)e * 2 * D + f];
-  uint8_t* kb = reinterpret_cast<uint8_t*>(r + 6);
-  for (int f = 0; f < 2 * D; ++f) kb[f] = kind[(long long)e * 2 * D + f];
-  for (int i = 0; i < 8; ++i) rec[(long long)e * 8 + i] = r[i];
 }
 
 // pin rows of owned elements whose conforming neighbour is a ghost (another

@@ -127,23 +127,52 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
         if (e != cudaSuccess) return e;
       }
       if constexpr (OPK == OP_GRAD) {
+        using PL = H1Pipe<D, N>;
+        static const bool pipe1 = getenv("DG_PIPE1") && std::string(getenv("DG_PIPE1")) == "1";
+        if constexpr (PL::OK) {
+          if (pipe1 && a.pin_out != nullptr && a.frec != nullptr) {
+            static int pgrid = 0;
+            if (pgrid == 0) {
+              cudaError_t e = cudaFuncSetAttribute(
+                  hgrad2_kernel<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PL::SMEM);
+              if (e != cudaSuccess) return e;
+              int dev = 0, sms = 0, occ = 0;
+              cudaGetDevice(&dev);
+              cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+              e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hgrad2_kernel<D, N>, 128,
+                                                                PL::SMEM);
+              if (e != cudaSuccess) return e;
+              pgrid = sms * (occ > 0 ? occ : 1);
+            }
+            const long long groups = (a.mesh.n_el + HL::EPW - 1) / HL::EPW;
+            const int g = (int)std::min<long long>(pgrid, (groups + PL::WPB - 1) / PL::WPB);
+            if (info) {
+              info->threads = 128;
+              info->smem = PL::SMEM;
+              info->grid = g;
+            }
+            hgrad2_kernel<D, N><<<g, 128, PL::SMEM, st>>>(P);
+            return cudaGetLastError();
+          }
+        }
         hgrad_kernel<D, N><<<hgrid, HL::THREADS, HL::GSMEM, st>>>(P);
       } else {
         using PL = H2Pipe<D, N>;
         if constexpr (PL::OK) {
           if (a.pin != nullptr && a.frec != nullptr) {
             // persistent pipelined H2: every SM's resident CTAs, the groups
-            // strided over the warps
+            // strided over the warps (DG_H2LA=1: records / column rows staged)
+            static const bool la = !(getenv("DG_H2LA") && std::string(getenv("DG_H2LA")) == "0");
+            auto kfn = la ? hdiv2_kernel<D, N, true> : hdiv2_kernel<D, N, false>;
             static int pgrid = 0;
             if (pgrid == 0) {
               cudaError_t e = cudaFuncSetAttribute(
-                  hdiv2_kernel<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PL::SMEM);
+                  kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PL::SMEM);
               if (e != cudaSuccess) return e;
               int dev = 0, sms = 0, occ = 0;
               cudaGetDevice(&dev);
               cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-              e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hdiv2_kernel<D, N>, 128,
-                                                                PL::SMEM);
+              e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 128, PL::SMEM);
               if (e != cudaSuccess) return e;
               pgrid = sms * (occ > 0 ? occ : 1);
             }
@@ -154,7 +183,7 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
               info->smem = PL::SMEM;
               info->grid = g;  // one dot-partial row per CTA
             }
-            hdiv2_kernel<D, N><<<g, 128, PL::SMEM, st>>>(P);
+            kfn<<<g, 128, PL::SMEM, st>>>(P);
             return cudaGetLastError();
           }
         }

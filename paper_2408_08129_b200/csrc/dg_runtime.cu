@@ -104,7 +104,7 @@ struct dg_ctx {
   DevBuf<double> trV, trH;  // trace mode: face traces of V (H1 output) and of h
   DevBuf<double> psi;       // flux-trace mode: 1/2 ws h (V . n+) per face point (H1 output)
   DevBuf<double> pin;       // ... and the conforming neighbours' values, scattered by H1
-  DevBuf<int> frec;         // 32-byte face records of the pipelined H2
+  DevBuf<int> frec;         // 64-byte element records of the pipelined pair
   DevBuf<int> pinfix;       // (element, face, ghost) triples: pin rows fed by a ghost
   int n_pinfix = 0;
   int bj_valid = 0, bj_age = 1 << 30;
@@ -212,6 +212,7 @@ int op_grad(dg_ctx* c, const double* x, const double* K, double alpha, double be
   a.tr_out = tr_out;
   a.psi_out = psi_out;
   a.pin_out = pin_out;
+  a.frec = pin_out ? c->frec.p : nullptr;
   if (psi_out) a.trH = c->trH.p;  // psi = 1/2 ws h (V . n+): the own h traces
   a.in = cv(x, c->NP, c->NP);
   if (K) {
@@ -309,13 +310,13 @@ bool sep_dots(dg_ctx* c) {
 int setup_pin(dg_ctx* c, int psl) {
   CK(c->pin.alloc((size_t)c->n_tot * psl));
   CK(cudaMemsetAsync(c->pin.p, 0, (size_t)c->n_tot * psl * sizeof(double), c->stream));
-  CK(c->frec.alloc((size_t)c->n_tot * 8));
+  CK(c->frec.alloc((size_t)c->n_tot * REC_INTS));
   if (c->dim == 2)
-    hk_face_records<2><<<(c->n_tot + 255) / 256, 256, 0, c->stream>>>(c->nbr.p, c->kind.p, c->n_tot,
-                                                                      c->frec.p);
+    hk_elem_records<2><<<(c->n_tot + 255) / 256, 256, 0, c->stream>>>(
+        c->nbr.p, c->kind.p, c->elem.p, c->n_tot, c->frec.p);
   else
-    hk_face_records<3><<<(c->n_tot + 255) / 256, 256, 0, c->stream>>>(c->nbr.p, c->kind.p, c->n_tot,
-                                                                      c->frec.p);
+    hk_elem_records<3><<<(c->n_tot + 255) / 256, 256, 0, c->stream>>>(
+        c->nbr.p, c->kind.p, c->elem.p, c->n_tot, c->frec.p);
   CK(cudaGetLastError());
   return DG_OK;
 }
@@ -635,7 +636,9 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const doubl
   if (fuse) {
     // one row of <= m + 1 dot partials per element-kernel warp (>= 1 element
     // each) and per coarse element
-    const long long rows = (long long)c->n_el + 4 + c->mesh.n_coarse + 1;
+    // (or one row per block of the separate dual-dot pass: <= RED_BLOCKS)
+    const long long rows =
+        std::max((long long)c->n_el + 4 + c->mesh.n_coarse + 1, (long long)RED_BLOCKS);
     CK(c->gs_part.alloc((size_t)rows * 2 * (32 + 2)));
   }
   double* coefs = c->pin_coef();  // pinned staging for the coefficient uploads
@@ -1472,6 +1475,24 @@ int dg_ctx_set_comm(dg_ctx* c, const void* uid, int rank, int nranks, const int3
                     const int32_t* send_elems, const int32_t* recv_counts) {
   CK(cudaSetDevice(c->device));
   if (!c->comm.init(uid, rank, nranks, send_counts, send_elems, recv_counts, c->n_el, c->n_tot))
+    return fail(DG_ERR_COMM, c->comm.error());
+  long long tot = (long long)c->n_el * c->NP;
+  double v = (double)tot;
+  DevBuf<double> tmp;
+  CK(tmp.upload(&v, 1));
+  if (!c->comm.allreduce_sum(tmp.p, 1, c->stream)) return fail(DG_ERR_COMM, c->comm.error());
+  CK(cudaMemcpy(&v, tmp.p, sizeof(double), cudaMemcpyDeviceToHost));
+  tmp.release();
+  c->n_global = (long long)v;
+  return DG_OK;
+}
+
+int dg_ctx_set_comm_loopback(dg_ctx* c, int group, int rank, int nranks,
+                             const int32_t* send_counts, const int32_t* send_elems,
+                             const int32_t* recv_counts) {
+  CK(cudaSetDevice(c->device));
+  if (!c->comm.init_loopback(group, rank, nranks, send_counts, send_elems, recv_counts, c->n_el,
+                             c->n_tot))
     return fail(DG_ERR_COMM, c->comm.error());
   long long tot = (long long)c->n_el * c->NP;
   double v = (double)tot;

@@ -140,3 +140,108 @@ class DistributedSolver:
         st.absorb(cs)
         L.check(code, stats=st, **_step_error_info(cs))
         return out, st
+
+
+class LoopbackGroup:
+    """P ranks of a partitioned run inside ONE process (one host thread and
+    one CUDA stream per rank, all contexts on one device): the same halo
+    plans, exchanges and allreduces as the NCCL path, through libdg's
+    loopback backend (dg_ctx_set_comm_loopback).  It executes the multi-rank
+    code path -- ghost exchanges inside every operator, the partitioned
+    GMRES reductions, the distributed positivity and mass-rate reductions --
+    on a box with one GPU.  No kernel waits on another rank: the ranks meet
+    only in host barriers between stream-ordered copies."""
+
+    _next_group = [1]
+
+    def __init__(self, geometry, model, bcs, sponge, nranks, device=0):
+        import ctypes as C
+
+        import torch
+
+        from . import _lib as L
+        from .device import DeviceContext
+        self.torch = torch
+        self.L = L
+        self.C = C
+        self.plans = halo_plans(geometry.mesh, nranks)
+        self.nranks = nranks
+        self.device = device
+        self.ctxs = [DeviceContext(geometry, model, bcs, sponge, device=device,
+                                   local_ids=pl.local_ids, n_owned=pl.n_owned)
+                     for pl in self.plans]
+        gid = LoopbackGroup._next_group[0]
+        LoopbackGroup._next_group[0] += 1
+
+        def attach(rank, ctx):
+            pl = self.plans[rank]
+            sc = np.ascontiguousarray(pl.send_counts.astype(np.int32))
+            se = np.ascontiguousarray(pl.send_elems.astype(np.int32))
+            rc = np.ascontiguousarray(pl.recv_counts.astype(np.int32))
+            L.check(ctx.lib.dg_ctx_set_comm_loopback(
+                ctx.handle, gid, rank, nranks, sc.ctypes.data_as(C.c_void_p),
+                se.ctypes.data_as(C.c_void_p), rc.ctypes.data_as(C.c_void_p)))
+        self.run(attach)
+
+    def run(self, fn, timeout=600.0):
+        """fn(rank, ctx) on every rank concurrently (its own thread and
+        stream); returns the per-rank results, re-raising the first error."""
+        import threading
+        torch = self.torch
+        out = [None] * self.nranks
+        err = [None] * self.nranks
+
+        def body(r):
+            try:
+                torch.cuda.set_device(self.device)
+                s = torch.cuda.Stream(device=self.device)
+                with torch.cuda.stream(s):
+                    ctx = self.ctxs[r]
+                    ctx.bind_stream()
+                    out[r] = fn(r, ctx)
+                    s.synchronize()
+            except BaseException as e:  # pragma: no cover - surfaced below
+                err[r] = e
+        th = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(self.nranks)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout)
+            if t.is_alive():
+                raise RuntimeError("loopback rank did not finish (deadlock?)")
+        for e in err:
+            if e is not None:
+                raise e
+        return out
+
+    def scatter(self, global_array):
+        """Per-rank device copies of a global (n_el, ...) array: owned rows
+        then ghost rows."""
+        return [self.torch.from_numpy(np.ascontiguousarray(global_array[pl.local_ids]))
+                .to(f"cuda:{self.device}") for pl in self.plans]
+
+    def gather(self, local_arrays):
+        """The owned rows of every rank, as one global host array."""
+        return np.concatenate([a[:pl.n_owned].cpu().numpy()
+                               for a, pl in zip(local_arrays, self.plans)], axis=0)
+
+    def imex_step(self, U_local, t, dt, cfg):
+        """dg_imex_step on every rank; returns (new local states, StepStats
+        per rank)."""
+        from .device import as_ptr
+        from .imex import StepStats, _solve_cfg, _step_error_info
+        L, C = self.L, self.C
+
+        def step(r, ctx):
+            U = U_local[r]
+            out = self.torch.empty_like(U)
+            cs = L.StepStatsC()
+            ccfg = _solve_cfg(cfg, False)
+            code = ctx.lib.dg_imex_step(ctx.handle, as_ptr(U), as_ptr(out), float(t), float(dt),
+                                        C.byref(ccfg), C.byref(cs))
+            st = StepStats()
+            st.absorb(cs)
+            L.check(code, stats=st, **_step_error_info(cs))
+            return out, st
+        res = self.run(step)
+        return [r[0] for r in res], [r[1] for r in res]

@@ -232,6 +232,10 @@ class MeshGeometry:
         # the reference's own arithmetic, so the device does no division
         col = np.concatenate([1.0 - hq / zt, np.moveaxis(dhq, 2, 1).reshape(n, -1),
                               (1.0 - edges / zt).reshape(n, -1)], axis=1)
+        if col.shape[1] % 2:
+            # even row length: every column row starts 16-byte aligned (the
+            # pipelined Helmholtz kernels bring it in with one bulk copy)
+            col = np.concatenate([col, np.zeros((n, 1))], axis=1)
         return elem, np.ascontiguousarray(col), col.shape[1]
 
     # ------------------------------------------------------- volume metric

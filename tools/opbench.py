@@ -58,7 +58,7 @@ def main():
     fp64 = float(os.environ.get("DG_FP64_TFLOPS", "37.2"))
     N = n_el * nn
     # SURVEY.md §8d models: algorithmic bytes and sum-factorised flops
-    n, V = c.geometry.basis.degree + 1, d + 2
+    n, NV = c.geometry.basis.degree + 1, d + 2
     top = c.mesh.topology
     n_conf = sum(len(b.left) for b in top.conforming)
     n_hrow = sum(len(b.coarse) for b in top.hanging)
@@ -66,9 +66,9 @@ def main():
     Pv, Pf = 2.0 * n ** (d + 1), 2.0 * n ** d
     Sf = 2 * n_conf + n_hrow + (d - 1) * n_hrow + n_bdry
     nnz = d if not c.geometry.terrain else (3 if d == 2 else 5)
-    f_exp = V * (3 * d * n_el * Pv + 2 * Pf * Sf)
+    f_exp = NV * (3 * d * n_el * Pv + 2 * Pf * Sf)
     f_helm = n_el * (3 * d + nnz) * Pv + 2 * (d + 1) * Pf * Sf
-    b_exp = 8.0 * N * V * (3 if c.sponge is not None else 2)
+    b_exp = 8.0 * N * NV * (3 if c.sponge is not None else 2)
     ops = {
         "explicit": (lambda: lib.dg_explicit_residual(h, as_ptr(U), as_ptr(R), None),
                      N * (d + 2), b_exp, f_exp),
