@@ -192,6 +192,11 @@ int dg_imex_step(dg_ctx* ctx, const double* U, double* U_out, double t, double d
 
 /* ---- reductions / vector ops ---- */
 int dg_integrate_conserved(dg_ctx* ctx, const double* U, double* out_host /* d+2 */);
+/* max over the owned nodes of |U[num] / U[den]| (mask: optional uint8 per
+   node, n_el x n^d) -- the runner's max |w| diagnostic and its probes
+   (orodg/runner.py:247-260: w = data[:, d] / data[:, 0]); max over ranks */
+int dg_max_abs_ratio(dg_ctx* ctx, const double* U, int num, int den, const uint8_t* mask,
+                     double* out_host);
 /* quadrature-weighted inner product of two (n_el, ncomp, n^d) fields
    (DGOperators.global_inner_product, orodg/dgops.py:491-503) */
 int dg_global_inner_product(dg_ctx* ctx, const double* a, const double* b, int ncomp,

@@ -172,6 +172,74 @@ def farfield_bcs(geometry, background_data, wall_axes_sides=(("z", 0),)):
     return out
 
 
+def hill_profile(x, y=None, cfg=HillCaseConfig()):
+    """Bell-shaped mountain h_c / [1 + ((x-x_c)/a_c)^2 (+ ((y-y_c)/a_c)^2)]^1.5
+    (orodg/cases.py:71-77, the reference presets' terrain)."""
+    r2 = ((np.asarray(x, dtype=float) - cfg.x_c) / cfg.a_c) ** 2
+    if y is not None:
+        r2 = r2 + ((np.asarray(y, dtype=float) - cfg.y_c) / cfg.a_c) ** 2
+    return cfg.h_c / (1.0 + r2) ** 1.5
+
+
+@dataclass(frozen=True)
+class ManufacturedConfig:
+    """Gravity-free space-time-periodic exact solution on the unit box; every
+    field rides the phase theta = k (x + z) - omega t (orodg/cases.py:178-196)."""
+    rho0: float = 1.0
+    amp_rho: float = 0.15
+    u0: float = 0.4
+    amp_u: float = 0.12
+    w0: float = -0.3
+    amp_w: float = 0.1
+    p0: float = 1.0
+    amp_p: float = 0.15
+    wavenumber: float = 2.0 * math.pi
+    omega: float = 2.0 * math.pi * 0.7
+    gamma: float = CONST.gamma
+
+
+def _mms_fields(cfg, th):
+    s, c = np.sin(th), np.cos(th)
+    prim = (cfg.rho0 + cfg.amp_rho * s, cfg.u0 + cfg.amp_u * c, cfg.w0 + cfg.amp_w * s,
+            cfg.p0 + cfg.amp_p * c)
+    dprim = (cfg.amp_rho * c, -cfg.amp_u * s, cfg.amp_w * c, -cfg.amp_p * s)
+    return prim, dprim
+
+
+def manufactured_state(coords, t, cfg=ManufacturedConfig()):
+    """Exact conserved state (orodg/cases.py:213-222)."""
+    th = cfg.wavenumber * (coords[..., 0] + coords[..., 1]) - cfg.omega * t
+    (rho, ux, uz, p), _ = _mms_fields(cfg, th)
+    out = np.empty(coords.shape[:-1] + (4,))
+    out[..., 0] = rho
+    out[..., 1] = rho * ux
+    out[..., 2] = rho * uz
+    out[..., 3] = p / (cfg.gamma - 1.0) + 0.5 * rho * (ux ** 2 + uz ** 2)
+    return out
+
+
+def manufactured_forcing(coords, t, cfg=ManufacturedConfig()):
+    """S = dU/dt + div F(U) of the exact solution, by the chain rule through
+    the single phase theta (orodg/cases.py:225-260): d/dt = -omega d/dtheta,
+    d/dx = d/dz = k d/dtheta."""
+    k, om = cfg.wavenumber, cfg.omega
+    gm1 = cfg.gamma - 1.0
+    th = k * (coords[..., 0] + coords[..., 1]) - om * t
+    (rho, ux, uz, p), (dr, du, dw, dp) = _mms_fields(cfg, th)
+    ke = 0.5 * (ux * ux + uz * uz)
+    rE = p / gm1 + rho * ke
+    dE = dp / gm1 + dr * ke + rho * (ux * du + uz * dw)
+    dU = (dr, dr * ux + rho * du, dr * uz + rho * dw, dE)
+    dFx = (dr * ux + rho * du, dr * ux * ux + 2.0 * rho * ux * du + dp,
+           dr * uz * ux + rho * dw * ux + rho * uz * du, (dE + dp) * ux + (rE + p) * du)
+    dFz = (dr * uz + rho * dw, dr * ux * uz + rho * du * uz + rho * ux * dw,
+           dr * uz * uz + 2.0 * rho * uz * dw + dp, (dE + dp) * uz + (rE + p) * dw)
+    out = np.empty(coords.shape[:-1] + (4,))
+    for i in range(4):
+        out[..., i] = -om * dU[i] + k * (dFx[i] + dFz[i])
+    return out
+
+
 def gaussian_hill(h0=400.0, a=3.0e3, xc=30.0e3, yc=30.0e3):
     """BASELINE configs[3] hill: h0 exp(-(r/a)^2), half-width a (harness pin)."""
     def f(x, y):

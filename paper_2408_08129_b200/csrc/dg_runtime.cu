@@ -125,6 +125,13 @@ int sync_read(dg_ctx* c, const double* dev, int n, double* host) {
   return DG_OK;
 }
 
+// a device read of arbitrary length (pageable, synchronous)
+int sync_read_n(dg_ctx* c, const double* dev, int n, double* host) {
+  CK(cudaMemcpyAsync(host, dev, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return DG_OK;
+}
+
 // global sums over ranks (in place on the device) then read to host
 int reduce_read(dg_ctx* c, double* dev, int n, double* host) {
   if (c->comm.active()) {
@@ -1349,6 +1356,25 @@ int dg_integrate_conserved(dg_ctx* c, const double* U, double* out_host) {
   }
   CK(reduce_cols(c->stream, c->partial.p, grid, c->V, c->redout.p));
   return reduce_read(c, c->redout.p, c->V, out_host);
+}
+
+int dg_max_abs_ratio(dg_ctx* c, const double* U, int num, int den, const uint8_t* mask,
+                     double* out_host) {
+  if (num < 0 || num >= c->V || den < 0 || den >= c->V)
+    return fail(DG_ERR_USAGE, "dg_max_abs_ratio: component out of range");
+  CK(max_ratio(c->stream, c->n_el, c->V, c->NP, U, num, den, mask, c->partial.p));
+  std::vector<double> part(RED_BLOCKS);
+  RET(sync_read_n(c, c->partial.p, RED_BLOCKS, part.data()));
+  double m = 0.0;
+  for (double v : part) m = std::max(m, v);
+  if (c->comm.active()) {
+    c->pinned[0] = m;
+    CK(cudaMemcpyAsync(c->redout.p, c->pinned, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    if (!c->comm.allreduce_max(c->redout.p, 1, c->stream)) return fail(DG_ERR_COMM, c->comm.error());
+    RET(sync_read(c, c->redout.p, 1, &m));
+  }
+  *out_host = m;
+  return DG_OK;
 }
 
 int dg_global_inner_product(dg_ctx* c, const double* a, const double* b, int ncomp,

@@ -714,6 +714,40 @@ cudaError_t dual_dots(cudaStream_t st, long long n, int nv, const double* Q, lon
   return e;
 }
 
+// max over the nodes of |U[e][num][i] / U[e][den][i]| (optionally only where
+// mask[e n^d + i] != 0): the runner's max |w| diagnostic (runner.py:247-260);
+// per-block maxima in partials, exact (order-independent)
+__global__ void __launch_bounds__(RED_THREADS)
+k_max_ratio(long long n_el, int V, int np, const double* __restrict__ U, int num, int den,
+            const uint8_t* __restrict__ mask, double* __restrict__ partials) {
+  double m = 0.0;
+  const long long n = n_el * np;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    if (mask && !mask[k]) continue;
+    const long long e = k / np, i = k - e * np;
+    const double* u = U + e * V * np;
+    m = fmax(m, fabs(u[(long long)num * np + i] / u[(long long)den * np + i]));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ double red[RED_THREADS / 32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < RED_THREADS / 32; ++w) t = fmax(t, red[w]);
+    partials[blockIdx.x] = t;
+  }
+}
+
+cudaError_t max_ratio(cudaStream_t st, long long n_el, int V, int np, const double* U, int num,
+                      int den, const uint8_t* mask, double* partials) {
+  prof_begin(st);
+  k_max_ratio<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n_el, V, np, U, num, den, mask, partials);
+  prof_end(st, P_OTHER, 8.0 * n_el * np * 2, 1);
+  return cudaGetLastError();
+}
+
 cudaError_t dcgs2_update(cudaStream_t st, long long n, int nv, const double* Q, long long vstride,
                          const double* coefs_dev, double* u, const double* z, double* unext,
                          double* partials, double* out) {

@@ -1,5 +1,6 @@
 // Host wrappers of the streaming vector kernels (dg_vector.cu).
 #pragma once
+#include <cstdint>
 #include <cuda_runtime.h>
 
 namespace dg {
@@ -25,6 +26,9 @@ cudaError_t dcgs2_update(cudaStream_t st, long long n, int nv, const double* Q, 
 // DCGS2 dual dots (Q_i.z, Q_i.u, z.z, z.u, u.z, u.u) as per-block rows
 cudaError_t dual_dots(cudaStream_t st, long long n, int nv, const double* Q, long long vstride,
                       const double* z, const double* u, double* rows, int* nrows);
+// per-block maxima of |U[num] / U[den]| over (masked) nodes
+cudaError_t max_ratio(cudaStream_t st, long long n_el, int V, int np, const double* U, int num,
+                      int den, const uint8_t* mask, double* partials);
 cudaError_t scale(cudaStream_t st, long long n, double a, bool divide, const double* x,
                   double* y);
 cudaError_t frozen(cudaStream_t st, long long n_el, int np, int d, const double* U, double gm1,

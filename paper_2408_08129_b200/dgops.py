@@ -180,6 +180,21 @@ class DGOperators:
                                                 C.byref(out)))
         return float(out.value)
 
+    def max_abs_ratio(self, data, num, den, mask=None):
+        """max |data[:, num] / data[:, den]| over the nodes (optionally a
+        boolean (n_el, n_nodes) mask) on the device -- the runner's max |w|
+        (num = d, den = 0) and probe diagnostics (runner.py:247-260)."""
+        ctx = self.context()
+        U, _ = to_device(data, ctx)
+        m = None
+        if mask is not None:
+            mk = np.ascontiguousarray(np.asarray(mask, dtype=np.uint8).reshape(-1))
+            m = ctx.torch.from_numpy(mk).to(U.device)
+        out = C.c_double()
+        L.check(ctx.lib.dg_max_abs_ratio(ctx.bind_stream(), as_ptr(U), int(num), int(den),
+                                         as_ptr(m) if m is not None else None, C.byref(out)))
+        return float(out.value)
+
     def integrate_conserved(self, field_or_data):
         """Per-variable domain integrals (dgops.py:505-511)."""
         ctx = self.context()

@@ -109,7 +109,9 @@ for name in ("hang2d", "hang3d", "per3d"):
     split = SplitOperators(ops, c.model, c.bcs, c.sponge)
     R = split.explicit_residual(c.U)
     y = build_helmholtz_action(split, float(z["a_dt"]), c.U)(z["x"].ravel()).reshape(z["x"].shape)
-    out[name] = [max(per_var_rel(R, z["explicit_residual"])), rel(y, z["helm_x"])]
+    e = np.array(per_var_rel(R, z["explicit_residual"]))
+    tol = np.maximum(1e-12, 10.0 * np.asarray(z["noise_explicit_residual"]))
+    out[name] = [float(np.max(e / tol)), rel(y, z["helm_x"])]
 print(json.dumps(out))
 """
 
@@ -130,6 +132,7 @@ def test_coarse_face_modes(mode):
     assert r.returncode == 0, r.stderr[-2000:]
     res = json.loads(r.stdout.strip().splitlines()[-1])
     for name, (e_exp, e_helm) in res.items():
-        # explicit: the golden gate's sensitivity floor of these cases (<= 1e-9)
-        assert e_exp <= 1e-9, (name, e_exp)
+        # explicit: per variable within the golden gate max(1e-12, 10 x the
+        # reference's 1-ulp sensitivity) -- e_exp is the largest err / gate
+        assert e_exp <= 1.0, (name, e_exp)
         assert e_helm <= 1e-12, (name, e_helm)
