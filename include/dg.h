@@ -154,6 +154,14 @@ int dg_energy_F(dg_ctx* ctx, double a_dt, const double* h, const double* K,
                 const double* x, double* Fx);
 /* homogeneous Helmholtz action y = x - (F(x) - F(0)) (build_helmholtz_action) */
 int dg_helmholtz_apply(dg_ctx* ctx, double a_dt, const double* h, const double* x, double* y);
+/* prepare_divergence_hv + the action with h frozen (dgops.py:399-479,
+   imex.py:221-242): dg_helmholtz_prepare interpolates h to the Gauss points
+   (and its face traces) once; dg_helmholtz_apply_prepared then applies the
+   homogeneous action without redoing it (re-preparing only when a different
+   h was prepared since) -- the operator GMRES applies */
+int dg_helmholtz_prepare(dg_ctx* ctx, const double* h);
+int dg_helmholtz_apply_prepared(dg_ctx* ctx, double a_dt, const double* h, const double* x,
+                                double* y);
 
 /* ---- GMRES on the Helmholtz action (orodg/krylov.py:27-115) ---- */
 int dg_gmres_helmholtz(dg_ctx* ctx, double a_dt, const double* h, const double* rhs, double* x,

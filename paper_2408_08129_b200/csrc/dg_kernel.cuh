@@ -860,10 +860,21 @@ __device__ __forceinline__ void coarse_dots(const KParams<N>& P, long long e, in
 #ifndef DG_CMINB_GRAD
 #define DG_CMINB_GRAD 8
 #endif
-template <int OPK>
-constexpr int coarse_minb() { return OPK == OP_GRAD ? DG_CMINB_GRAD : (OPK == OP_DIVHV ? 10 : 6); }
-template <int D, int N, int OPK>
-__global__ void __launch_bounds__(Layout<D, N, OPK>::CTHREADS, coarse_minb<OPK>())
+#ifndef DG_CFLUX_THREADS
+#define DG_CFLUX_THREADS 1024
+#endif
+// FM: flux-mode instantiation (only the coarse faces' fluxes into
+// mesh.cflux, no epilogue): capped at 64 registers so DG_CFLUX_THREADS
+// threads stay resident per SM -- the kernel is latency-bound (dependent
+// record -> children -> data loads)
+template <int OPK, bool FM, int CT>
+constexpr int coarse_minb() {
+  return FM ? (DG_CFLUX_THREADS / CT > 0 ? DG_CFLUX_THREADS / CT : 1)
+            : (OPK == OP_GRAD ? DG_CMINB_GRAD : (OPK == OP_DIVHV ? 10 : 6));
+}
+template <int D, int N, int OPK, bool FM = false>
+__global__ void __launch_bounds__(Layout<D, N, OPK>::CTHREADS,
+                                  coarse_minb<OPK, FM, Layout<D, N, OPK>::CTHREADS>())
 coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clist, int ncoarse,
               double* mass_partial) {
   using L = Layout<D, N, OPK>;
@@ -884,7 +895,7 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
   const long long e = crec[0];
   // flux mode: only the coarse faces' lifted fluxes, into mesh.cflux (the
   // element kernel lifts them with the rest of its faces)
-  const bool fmode = P.mesh.cflux != nullptr;
+  const bool fmode = FM || P.mesh.cflux != nullptr;
   const int q = threadIdx.x;
   const bool act = q < NP;
   // the Helmholtz H1 output at this Gauss point (read-modify-written at the
@@ -1108,6 +1119,7 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
     }
   }
   if (fmode) return;
+  if constexpr (!FM) {
   double wq = 1.0, det = 1.0;
   if (act) {
     const ElemGeo<D> g = elem_geo<D>(mesh.elem, P.gc, e);
@@ -1214,6 +1226,7 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
     }
   }
   if constexpr (OPK == OP_DIVHV) coarse_dots<D, N, OPK>(P, e, q, act, yv, red + 64 + L::C_GS);
+  }  // !FM
 }
 
 

@@ -114,14 +114,16 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
             : cudaFuncSetAttribute(hdiv_kernel<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)HL::DSMEM);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK>,
+        e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::CSMEM);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::CSMEM);
         if (e != cudaSuccess) return e;
         hconf = true;
       }
       if (a.mesh.n_coarse > 0) {
         if (a.mesh.cflux == nullptr) return cudaErrorInvalidValue;  // flux mode required
-        coarse_kernel<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
+        coarse_kernel<D, N, OPK, true><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
             P, a.mesh.coarse_list, a.mesh.n_coarse, nullptr);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -215,7 +217,9 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
           e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
           if (e != cudaSuccess) return e;
         }
-        cudaError_t e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK>,
+        cudaError_t e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::CSMEM);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)L::CSMEM);
         if (e != cudaSuccess) return e;
@@ -224,7 +228,7 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
       const bool fmode = a.mesh.n_coarse > 0 && a.mesh.cflux != nullptr;
       if (fmode) {
         // the coarse faces' fluxes first; the element kernel lifts them
-        coarse_kernel<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
+        coarse_kernel<D, N, OPK, true><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
             P, a.mesh.coarse_list, a.mesh.n_coarse, nullptr);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -269,14 +273,16 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
           e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
           if (e != cudaSuccess) return e;
         }
-        cudaError_t e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK>,
+        cudaError_t e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::CSMEM);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::CSMEM);
         if (e != cudaSuccess) return e;
         xconf = true;
       }
       const bool fmode = a.mesh.n_coarse > 0 && a.mesh.cflux != nullptr;
       if (fmode) {
-        coarse_kernel<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
+        coarse_kernel<D, N, OPK, true><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
             P, a.mesh.coarse_list, a.mesh.n_coarse, nullptr);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -317,14 +323,16 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
     e = cudaFuncSetAttribute(elem_kernel<D, N, OPK>,
                              cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK>,
+    e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::CSMEM);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(coarse_kernel<D, N, OPK>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::CSMEM);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   const bool fmode = a.mesh.n_coarse > 0 && a.mesh.cflux != nullptr;
   if (fmode) {
-    coarse_kernel<D, N, OPK><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
+    coarse_kernel<D, N, OPK, true><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
         P, a.mesh.coarse_list, a.mesh.n_coarse, nullptr);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

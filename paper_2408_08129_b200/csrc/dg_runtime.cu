@@ -103,6 +103,7 @@ struct dg_ctx {
   DevBuf<double> bj_inv, sz, su;
   DevBuf<double> trV, trH;  // trace mode: face traces of V (H1 output) and of h
   DevBuf<double> psi;       // flux-trace mode: 1/2 ws h (V . n+) per face point (H1 output)
+  const double* hq_for = nullptr;  // the nodal h that shq / trH were last prepared from
   DevBuf<double> pin;       // ... and the conforming neighbours' values, scattered by H1
   DevBuf<int> frec;         // 64-byte element records of the pipelined pair
   DevBuf<int> pinfix;       // (element, face, ghost) triples: pin rows fed by a ghost
@@ -347,6 +348,7 @@ int tr_len(dg_ctx* c) { return (2 * (c->dim - 1) + 2 * c->dim) * c->NQF; }  // V
 // frozen h at the Gauss points (once per fixed-point iterate), + its face
 // traces in trace mode
 int interp_h(dg_ctx* c, const double* h, double* hq) {
+  c->hq_for = (hq == c->shq.p) ? h : nullptr;
   AuxArgs a;
   std::memset(&a, 0, sizeof a);
   a.elem = c->elem.p;
@@ -1232,6 +1234,22 @@ int dg_helmholtz_apply(dg_ctx* c, double a_dt, const double* h, const double* x,
     hq = c->shq.p;
   }
   return helm_apply(c, a_dt, h, hq, const_cast<double*>(x), y);
+}
+
+// prepare_divergence_hv (dgops.py:399-479): h frozen at the Gauss points
+// (and its face traces) once; the prepared apply reuses them
+int dg_helmholtz_prepare(dg_ctx* c, const double* h) {
+  RET(ensure_work(c));
+  RET(halo(c, const_cast<double*>(h), 1));
+  if (quad_mode(c)) RET(interp_h(c, h, c->shq.p));
+  return DG_OK;
+}
+
+int dg_helmholtz_apply_prepared(dg_ctx* c, double a_dt, const double* h, const double* x,
+                                double* y) {
+  RET(ensure_work(c));
+  if (quad_mode(c) && c->hq_for != h) RET(dg_helmholtz_prepare(c, h));
+  return helm_apply(c, a_dt, h, quad_mode(c) ? c->shq.p : nullptr, const_cast<double*>(x), y);
 }
 
 int dg_gmres_helmholtz(dg_ctx* c, double a_dt, const double* h, const double* rhs, double* x,

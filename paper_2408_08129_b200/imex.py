@@ -276,8 +276,10 @@ class HelmholtzAction:
         xt, host = to_device(xflat, ctx)
         xt = xt.reshape(self.shape).contiguous()
         y = ctx.empty(self.shape[1])
-        L.check(ctx.lib.dg_helmholtz_apply(ctx.bind_stream(), self.a_dt, as_ptr(self.h),
-                                           as_ptr(xt), as_ptr(y)))
+        # h frozen at construction (prepare_divergence_hv, dgops.py:399-479):
+        # its Gauss values / traces are prepared once and reused
+        L.check(ctx.lib.dg_helmholtz_apply_prepared(ctx.bind_stream(), self.a_dt,
+                                                    as_ptr(self.h), as_ptr(xt), as_ptr(y)))
         return from_device(y.reshape(-1), host)
 
     def _native_gmres(self, rhs, x0, tol_rel, restart, max_iter, precond=False):
