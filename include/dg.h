@@ -232,6 +232,12 @@ int dg_dcgs2_update(dg_ctx* ctx, long long n, int nv, const double* V, long long
                     const double* coefs_host, double* u, const double* z, double* u_next,
                     double* norm2_host);
 
+/* DCGS2 dual Gram-Schmidt dots in one streaming pass over V_0..V_{nv-1}, z, u:
+   out = (V_i.z, V_i.u) for i < nv, then (z.z, z.u), (u.z, u.u) -- 2 (nv + 2)
+   values, summed over ranks.  0 <= nv <= 31. */
+int dg_dual_dots(dg_ctx* ctx, long long n, int nv, const double* V, long long vstride,
+                 const double* z, const double* u, double* out_host);
+
 /* ---- multi-GPU (one process per GPU) ---- */
 int dg_nccl_unique_id(void* out128);
 int dg_ctx_set_comm(dg_ctx* ctx, const void* unique_id128, int rank, int nranks,

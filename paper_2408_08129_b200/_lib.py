@@ -90,6 +90,7 @@ _SIGS = {
     "dg_courant_ingredients": ([P, P, P], I),
     "dg_gs_update": ([P, LL, I, P, LL, P, P, D, P], I),
     "dg_dcgs2_update": ([P, LL, I, P, LL, P, P, P, P, P], I),
+    "dg_dual_dots": ([P, LL, I, P, LL, P, P, P], I),
     "dg_nccl_unique_id": ([P], I),
     "dg_ctx_set_comm": ([P, P, I, I, P, P, P], I),
     "dg_ctx_set_comm_loopback": ([P, I, I, I, P, P, P], I),

@@ -1549,6 +1549,19 @@ int dg_ctx_set_comm_loopback(dg_ctx* c, int group, int rank, int nranks,
   return DG_OK;
 }
 
+// DCGS2 dual dots (Q_i.z, Q_i.u for i < nv, then z.z, z.u, u.z, u.u) in one
+// streaming pass, reduced over ranks: the dots krylov.py:69-72 takes per
+// Arnoldi step, in the delayed re-orthogonalisation form
+int dg_dual_dots(dg_ctx* c, long long n, int nv, const double* V, long long vstride,
+                 const double* z, const double* u, double* out_host) {
+  if (nv < 0 || nv > 31) return fail(DG_ERR_USAGE, "dg_dual_dots: 0 <= nv <= 31");
+  CK(c->gs_part.alloc((size_t)RED_BLOCKS * 2 * (32 + 2)));
+  int rows = 0;
+  CK(dual_dots(c->stream, n, nv, V, vstride, z, u, c->gs_part.p, &rows));
+  CK(reduce_rows(c->stream, c->gs_part.p, rows, 2 * (nv + 2), c->partial.p, c->redout.p));
+  return reduce_read(c, c->redout.p, 2 * (nv + 2), out_host);
+}
+
 int dg_halo_exchange(dg_ctx* c, double* field, int ncomp) { return halo(c, field, ncomp); }
 
 long long dg_launch_count(void) { return prof().launches; }

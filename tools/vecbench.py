@@ -34,7 +34,7 @@ def main():
     vs = ((n + 31) // 32) * 32 + a.pad
     V = torch.randn(32 * vs, dtype=torch.float64, device="cuda")
     w = torch.randn(n, dtype=torch.float64, device="cuda")
-    out = (C.c_double * 40)()
+    out = (C.c_double * 80)()
     ctx.bind_stream()
     dst = torch.empty_like(w)
     coefs = (C.c_double * 32)(*([0.01] * 32))
@@ -55,8 +55,12 @@ def main():
         lib.dg_dcgs2_update(ctx.handle, n, nv, vp, vs, cf, wp, C.c_void_p(z.data_ptr()),
                             C.c_void_p(un.data_ptr()), C.byref(nrm))
 
+    def dual(nv):
+        lib.dg_dual_dots(ctx.handle, n, nv, vp, vs, C.c_void_p(z.data_ptr()), wp, out)
+
     for op in a.ops.split(","):
-        fn, extra = {"dots": (dots, 1), "update": (update, 2), "dcgs2": (dcgs2, 4)}[op]
+        fn, extra = {"dots": (dots, 1), "update": (update, 2), "dcgs2": (dcgs2, 4),
+                     "dual": (dual, 2)}[op]
         for nv in (1, 4, 8, 12, 16, 24, 31):
             for _ in range(2):
                 fn(nv)
