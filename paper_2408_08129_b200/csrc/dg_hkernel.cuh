@@ -1036,14 +1036,16 @@ template <int D, int N>
 struct H2Pipe {
   using HL = HLayout<D, N>;
   static constexpr int NP = HL::NP, NC = HL::NC, NF = HL::NF, EPW = HL::EPW;
-  static constexpr bool OK = HL::OK && (NP % 2 == 0) && ((NF * NC) % 2 == 0);
-  // stage sub-arrays (doubles, all even offsets)
+  static constexpr bool OK = HL::OK;
+  static constexpr int ev(int x) { return (x + 1) & ~1; }
+  // stage sub-arrays (doubles, all even offsets); the odd-n^d blocks (V, h,
+  // base) are copied as their 16-byte aligned superset, shifted by 0 or 1
   static constexpr int OV = 0;
-  static constexpr int OH = OV + EPW * D * NP;
-  static constexpr int OP = OH + EPW * NP;
+  static constexpr int OH = OV + ev(EPW * D * NP + 2);
+  static constexpr int OP = OH + ev(EPW * NP + 2);
   static constexpr int OI = OP + EPW * NF * NC;
   static constexpr int OB = OI + EPW * NF * NC;
-  static constexpr int OR = OB + EPW * NP;
+  static constexpr int OR = OB + ev(EPW * NP + 2);
   static constexpr int OC = OR + EPW * 8;   // + 64-byte records
   static constexpr int COLS = 2 * ((ipow(N, D - 1) * D + 2 * (D - 1) * ipow(N, D - 2) + 1) / 2);
   static constexpr int STG = OC + EPW * COLS;  // + column rows (lookahead, terrain)
@@ -1143,14 +1145,25 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
     const int ne = (int)min((long long)EPW, (long long)mesh.n_el - e0);
     double* st = STG0 + s * PL::STG;
     const unsigned b = s ? bar1 : bar0;
-    const unsigned bytes = 8u * ne * (D * NP + NP + 2 * NF * NC + (P.has_base ? NP : 0) + 8);
+    // 16-byte aligned spans covering the element blocks (odd n^d)
+    auto span = [](const double* p, int count, unsigned long long& a0) -> unsigned {
+      a0 = reinterpret_cast<unsigned long long>(p) & ~15ULL;
+      const unsigned long long a1 =
+          (reinterpret_cast<unsigned long long>(p + count) + 15ULL) & ~15ULL;
+      return (unsigned)(a1 - a0);
+    };
+    unsigned long long aV, aH, aB = 0;
+    const unsigned bV = span(P.in.p + e0 * P.in.estride, ne * D * NP, aV);
+    const unsigned bH = span(P.inH.p + e0 * P.inH.estride, ne * NP, aH);
+    const unsigned bB = P.has_base ? span(P.base.p + e0 * P.base.estride, ne * NP, aB) : 0u;
+    const unsigned bytes = bV + bH + bB + 8u * ne * (2 * NF * NC + 8);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes)
                  : "memory");
-    bulk_g2s(st + PL::OV, P.in.p + e0 * P.in.estride, 8u * ne * D * NP, b);
-    bulk_g2s(st + PL::OH, P.inH.p + e0 * P.inH.estride, 8u * ne * NP, b);
+    bulk_g2s(st + PL::OV, reinterpret_cast<const void*>(aV), bV, b);
+    bulk_g2s(st + PL::OH, reinterpret_cast<const void*>(aH), bH, b);
     bulk_g2s(st + PL::OP, P.psi + e0 * (NF * NC), 8u * ne * NF * NC, b);
     bulk_g2s(st + PL::OI, P.pin + e0 * (NF * NC), 8u * ne * NF * NC, b);
-    if (P.has_base) bulk_g2s(st + PL::OB, P.base.p + e0 * P.base.estride, 8u * ne * NP, b);
+    if (P.has_base) bulk_g2s(st + PL::OB, reinterpret_cast<const void*>(aB), bB, b);
     bulk_g2s(st + PL::OR, P.frec + e0 * REC_INTS, 64u * ne, b);
     if (dots) {
       // the fused dots' basis slices of this group into L2
@@ -1333,8 +1346,11 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
     double Zc[N];
     const double det = col_det<D>(g3, cd.omh);
     {
-      const double* Vs = st + PL::OV + esl * (D * NP) + c * N;
-      const double* Hs = st + PL::OH + esl * NP + c * N;
+      const long long e0g = g * EPW;
+      const int shV = (int)((reinterpret_cast<unsigned long long>(P.in.p + e0g * P.in.estride) >> 3) & 1);
+      const int shH = (int)((reinterpret_cast<unsigned long long>(P.inH.p + e0g * P.inH.estride) >> 3) & 1);
+      const double* Vs = st + PL::OV + shV + esl * (D * NP) + c * N;
+      const double* Hs = st + PL::OH + shH + esl * NP + c * N;
       double Gz[N];
 #pragma unroll
       for (int kz = 0; kz < N; ++kz) {
@@ -1405,7 +1421,10 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
     }
     double wv[N], uv[N];
     {
-      const double* Bs = st + PL::OB + esl * NP;
+      const int shB = P.has_base
+          ? (int)((reinterpret_cast<unsigned long long>(P.base.p + g * EPW * P.base.estride) >> 3) & 1)
+          : 0;
+      const double* Bs = st + PL::OB + shB + esl * NP;
       double v[N], o[N];
 #pragma unroll
       for (int ii = 0; ii < N; ++ii) v[ii] = X[xoff<D, N>(c, ii)];

@@ -297,12 +297,17 @@ bool psi_mode(dg_ctx* c) {
   return on && trace_mode(c) && (c->mesh.n_coarse == 0 || c->cflux.p != nullptr);
 }
 
-// Pipelined H2 (hdiv2_kernel: persistent warps fed by cp.async.bulk): needs
-// 16-byte aligned element blocks (even n^d).  Default on (DG_PIPE=0: hdiv)
+// Pipelined H2 (hdiv2_kernel: persistent warps fed by cp.async.bulk; odd
+// n^d blocks copied as their 16-byte aligned superset).  Default on
+// (DG_PIPE=0: hdiv)
 bool pipe_mode(dg_ctx* c) {
   static const char* env = getenv("DG_PIPE");
   static const bool on = env == nullptr || std::string(env) != "0";
-  return on && (c->NP % 2 == 0);
+  // small problems are launch-bound: there the non-persistent div(hV) with
+  // the fused Gram-Schmidt dots (one launch fewer per Arnoldi step) wins
+  static const long long min_dof =
+      getenv("DG_PIPE_MIN") ? atoll(getenv("DG_PIPE_MIN")) : (1LL << 20);
+  return on && (long long)c->n_el * c->NP >= min_dof;
 }
 
 // DCGS2 with the pipelined H2: the Gram-Schmidt dots in their own streaming

@@ -635,81 +635,142 @@ cudaError_t launch_dcgs2(cudaStream_t st, long long n, int nv, const double* Q, 
   return cudaGetLastError();
 }
 
-// DCGS2 dual Gram-Schmidt dots in one streaming pass (the unfused form of
-// the dots the div(hV) kernel can fuse, dg_wkernel.cuh gs_dots): row b of
-// rows = block b's partials of (Q_i.z, Q_i.u) for i < NV, then (z.z, z.u),
-// then (u.z, u.u) -- 2 (NV + 2) columns, reduced over the fixed grid by
-// reduce_rows (deterministic)
-template <int NV>
+// DCGS2 dual Gram-Schmidt dots (the unfused form of the dots the div(hV)
+// kernel can fuse, dg_wkernel.cuh gs_dots).  Row b of rows = block b's
+// partials of (Q_i.z, Q_i.u) for i < nv, then (z.z, z.u), then (u.z, u.u):
+// 2 (nv + 2) columns, summed over the rows by reduce_rows (deterministic).
+// The vectors go in groups of at most 8, one launch per group (each its own
+// one-wave grid; the last group also takes the z / u products): with all
+// 2 nv accumulators in registers the kernel spilled from nv ~ 12 on (1.5
+// TB/s at nv = 16).  Each thread handles k-pairs with 16-byte loads so a
+// group keeps 2 x (G + 2) loads in flight per thread.
+template <int G, bool LAST>
 __global__ void __launch_bounds__(RED_THREADS)
-k_dual_dots(long long n, const double* __restrict__ Q, long long vstride,
+k_dual_dots(long long n, int nv, int g0, const double* __restrict__ Q, long long vstride,
             const double* __restrict__ z, const double* __restrict__ u, double* __restrict__ rows) {
-  constexpr int NA = NV > 0 ? NV : 1;
-  constexpr int NT = 2 * (NV + 2);
-  double pz[NA], pu[NA];
+  constexpr int GA = G > 0 ? G : 1;
+  double pz[GA], pu[GA];
 #pragma unroll
-  for (int i = 0; i < NA; ++i) pz[i] = pu[i] = 0.0;
+  for (int i = 0; i < GA; ++i) pz[i] = pu[i] = 0.0;
   double zz = 0.0, zu = 0.0, uu = 0.0;
+  const long long n2 = n >> 1;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
-    double a[NA];
+  const double* Qg = Q + (long long)g0 * vstride;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n2; k += stride) {
+    double2 a[GA];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) a[i] = Q[i * vstride + k];
+    for (int i = 0; i < G; ++i) a[i] = reinterpret_cast<const double2*>(Qg + i * vstride)[k];
+    const double2 zk = reinterpret_cast<const double2*>(z)[k];
+    const double2 uk = reinterpret_cast<const double2*>(u)[k];
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      pz[i] = fma(a[i].x, zk.x, pz[i]);
+      pu[i] = fma(a[i].x, uk.x, pu[i]);
+      pz[i] = fma(a[i].y, zk.y, pz[i]);
+      pu[i] = fma(a[i].y, uk.y, pu[i]);
+    }
+    if (LAST) {
+      zz = fma(zk.x, zk.x, zz);
+      zu = fma(zk.x, uk.x, zu);
+      uu = fma(uk.x, uk.x, uu);
+      zz = fma(zk.y, zk.y, zz);
+      zu = fma(zk.y, uk.y, zu);
+      uu = fma(uk.y, uk.y, uu);
+    }
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd n: the last element
+    const long long k = n - 1;
     const double zk = z[k], uk = u[k];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      pz[i] = fma(a[i], zk, pz[i]);
-      pu[i] = fma(a[i], uk, pu[i]);
+    for (int i = 0; i < G; ++i) {
+      const double a = Qg[i * vstride + k];
+      pz[i] = fma(a, zk, pz[i]);
+      pu[i] = fma(a, uk, pu[i]);
     }
-    zz = fma(zk, zk, zz);
-    zu = fma(zk, uk, zu);
-    uu = fma(uk, uk, uu);
+    if (LAST) {
+      zz = fma(zk, zk, zz);
+      zu = fma(zk, uk, zu);
+      uu = fma(uk, uk, uu);
+    }
   }
-  __shared__ double red[RED_THREADS / 32][NT];
+  constexpr int NT = 2 * G + (LAST ? 4 : 0);
+  __shared__ double red[RED_THREADS / 32][NT > 0 ? NT : 1];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int col = 0; col < NT; ++col) {
     double v;
-    if (col < 2 * NV) v = (col & 1) ? pu[col >> 1] : pz[col >> 1];
-    else if (col == 2 * NV) v = zz;
-    else if (col == 2 * NV + 1 || col == 2 * NV + 2) v = zu;
+    if (col < 2 * G) v = (col & 1) ? pu[col >> 1] : pz[col >> 1];
+    else if (col == 2 * G) v = zz;
+    else if (col == 2 * G + 1 || col == 2 * G + 2) v = zu;
     else v = uu;
     v = warp_sum(v);
     if (lane == 0) red[wid][col] = v;
   }
   __syncthreads();
+  const int ncols = 2 * (nv + 2);
   for (int col = threadIdx.x; col < NT; col += blockDim.x) {
     double t = 0.0;
     for (int w2 = 0; w2 < RED_THREADS / 32; ++w2) t += red[w2][col];
-    rows[(long long)blockIdx.x * NT + col] = t;
+    const int dst = (col < 2 * G) ? 2 * g0 + col : 2 * nv + (col - 2 * G);
+    rows[(long long)blockIdx.x * ncols + dst] = t;
   }
 }
 
-template <int NV>
+template <int G, bool LAST>
+int dd_grid() {
+  static int grid = 0;
+  if (grid == 0) {
+    int dev = 0, nsm = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dual_dots<G, LAST>, RED_THREADS, 0);
+    grid = std::min(RED_BLOCKS, std::max(1, nsm * std::max(per_sm, 1)));
+  }
+  return grid;
+}
+
+template <int T>
+cudaError_t launch_dd_tail(cudaStream_t st, int tail, long long n, int nv, int g0,
+                           const double* Q, long long vstride, const double* z, const double* u,
+                           double* rows, int* grid) {
+  if constexpr (T > 0) {
+    if (tail < T) return launch_dd_tail<T - 1>(st, tail, n, nv, g0, Q, vstride, z, u, rows, grid);
+  }
+  *grid = dd_grid<T, true>();
+  k_dual_dots<T, true><<<*grid, RED_THREADS, 0, st>>>(n, nv, g0, Q, vstride, z, u, rows);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_dual_dots(cudaStream_t st, long long n, int nv, const double* Q,
                              long long vstride, const double* z, const double* u, double* rows,
                              int* used_grid) {
-  if constexpr (NV > 0) {
-    if (nv < NV) return launch_dual_dots<NV - 1>(st, n, nv, Q, vstride, z, u, rows, used_grid);
+  // one one-wave launch per group of 8 vectors + the tail group (1..8
+  // vectors and the u / z products); the row block is zeroed first so the
+  // groups' different grids sum exactly in reduce_rows
+  const int nfull = nv > 0 ? (nv - 1) / 8 : 0;
+  const int tail = nv - 8 * nfull;
+  const int ncols = 2 * (nv + 2);
+  cudaError_t e = cudaMemsetAsync(rows, 0, (size_t)RED_BLOCKS * ncols * sizeof(double), st);
+  if (e != cudaSuccess) return e;
+  int gmax = 1;
+  for (int g = 0; g < nfull; ++g) {
+    const int grid = dd_grid<8, false>();
+    k_dual_dots<8, false><<<grid, RED_THREADS, 0, st>>>(n, nv, 8 * g, Q, vstride, z, u, rows);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    gmax = std::max(gmax, grid);
   }
-  static int grid = 0;
-  if (grid == 0) {
-    int dev = 0, nsm = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dual_dots<NV>, RED_THREADS, 0);
-    grid = std::min(RED_BLOCKS, std::max(1, nsm * std::max(occ, 1)));
-  }
-  *used_grid = grid;
-  k_dual_dots<NV><<<grid, RED_THREADS, 0, st>>>(n, Q, vstride, z, u, rows);
-  return cudaGetLastError();
+  int gt = 1;
+  e = launch_dd_tail<8>(st, tail, n, nv, 8 * nfull, Q, vstride, z, u, rows, &gt);
+  *used_grid = std::max(gmax, gt);
+  return e;
 }
 
 cudaError_t dual_dots(cudaStream_t st, long long n, int nv, const double* Q, long long vstride,
                       const double* z, const double* u, double* rows, int* nrows) {
   if (nv > 31 || nv < 0) return cudaErrorInvalidValue;
   prof_begin(st);
-  cudaError_t e = launch_dual_dots<31>(st, n, nv, Q, vstride, z, u, rows, nrows);
+  cudaError_t e = launch_dual_dots(st, n, nv, Q, vstride, z, u, rows, nrows);
   prof_end(st, P_DOT, 8.0 * n * (nv + 2), 1);
   return e;
 }

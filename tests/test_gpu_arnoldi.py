@@ -136,3 +136,80 @@ def test_coarse_face_modes(mode):
         # reference's 1-ulp sensitivity) -- e_exp is the largest err / gate
         assert e_exp <= 1.0, (name, e_exp)
         assert e_helm <= 1e-12, (name, e_helm)
+
+
+@pytest.mark.parametrize("nv", [0, 1, 7, 8, 9, 16, 31])
+def test_dual_dots_kernel(nv):
+    """The DCGS2 dual-dot pass (grouped by 8 vectors + tail) against numpy."""
+    import torch
+    from paper_2408_08129_b200.device import DeviceContext
+    c = build("cfg1")
+    ctx = DeviceContext(c.geom, c.model, c.bcs)
+    ctx.bind_stream()
+    rng = np.random.default_rng(11 + nv)
+    n, vs = 200003, 200003 + 13
+    Q = rng.standard_normal((max(nv, 1), vs))
+    z = rng.standard_normal(n)
+    u = rng.standard_normal(n)
+    dev = torch.device("cuda:0")
+    Qd, zd, ud = (torch.from_numpy(a).to(dev) for a in (Q, z, u))
+    out = (C.c_double * (2 * (nv + 2)))()
+    assert ctx.lib.dg_dual_dots(ctx.handle, n, nv, C.c_void_p(Qd.data_ptr()), vs,
+                                C.c_void_p(zd.data_ptr()), C.c_void_p(ud.data_ptr()), out) == 0
+    got = np.array(out[:])
+    ref = []
+    for i in range(nv):
+        ref += [Q[i, :n] @ z, Q[i, :n] @ u]
+    ref += [z @ z, z @ u, u @ z, u @ u]
+    assert np.allclose(got, ref, rtol=1e-12, atol=1e-9)
+
+
+_CHILD_PIPE = r"""
+import json, sys
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import numpy as np
+from casebuild import build, golden, per_var_rel, rel
+from paper_2408_08129_b200.dgops import DGOperators
+from paper_2408_08129_b200.imex import (ImplicitSolveConfig, SplitOperators, ars222,
+                                        build_helmholtz_action, imex_step)
+from paper_2408_08129_b200.krylov import gmres
+out = {}
+for name in ("cfg1", "hang2d", "hang3d", "per3d", "hang3d_r4", "cfg5s"):
+    c, z = build(name), golden(name)
+    ops = DGOperators(c.geom)
+    split = SplitOperators(ops, c.model, c.bcs, c.sponge)
+    act = build_helmholtz_action(split, float(z["a_dt"]), c.U)
+    y = act(z["x"].ravel()).reshape(z["x"].shape)
+    r = {"helm": rel(y, z["helm_x"])}
+    if "gm_rhs" in z:
+        x, st = gmres(act, z["gm_rhs"].ravel(), x0=z["gm_x0"].ravel(), tol_rel=float(z["gm_tol"]))
+        r["gm_iters"] = [st.iterations, int(z["gm_iters"])]
+        r["gm_x"] = rel(x, z["gm_x"].ravel())
+    if "U_step1" in z:
+        U1, st = imex_step(c.U, 0.0, float(z["dt"]), ars222(), split,
+                           ImplicitSolveConfig(krylov_tol=c.krylov_tol))
+        kz = z["krylov_iters"][0]
+        r["step_iters"] = [st.krylov_iters, [int(v) for v in kz[kz >= 0]]]
+        r["step"] = rel(U1, z["U_step1"])
+    out[name] = r
+print(json.dumps(out))
+"""
+
+
+def test_pipelined_helmholtz_on_golden_cases():
+    """The large-problem path (persistent TMA-fed div(hV), separate dual-dot
+    pass; DG_PIPE_MIN=0 forces it on the small golden meshes, odd and even
+    n^d): Helmholtz action, GMRES and one step against the reference."""
+    env = dict(os.environ)
+    env["DG_PIPE_MIN"] = "0"
+    code = _CHILD_PIPE % (ROOT, os.path.join(ROOT, "tests"))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    for name, v in res.items():
+        assert v["helm"] <= 1e-12, (name, v)
+        if "gm_iters" in v:
+            assert v["gm_iters"][0] == v["gm_iters"][1] and v["gm_x"] <= 1e-10, (name, v)
+        if "step" in v:
+            assert v["step_iters"][0] == v["step_iters"][1] and v["step"] <= 1e-11, (name, v)
