@@ -573,7 +573,9 @@ k_dcgs2_update(long long n, const double* __restrict__ Q, long long vstride,
                const double* __restrict__ z, double* __restrict__ unext,
                double* __restrict__ partials) {
   // u' = z / alpha - sum_{i<NV} c_i Q_i - c_NV q with c = g / alpha + h: two
-  // coefficient sets (s, c) instead of three
+  // coefficient sets (s, c) instead of three.  k-pairs with 16-byte loads
+  // and stores (twice the bytes in flight per instruction); odd n: the last
+  // element by one thread
   __shared__ double cs[NV + 1], cc[NV + 1];
   const double alpha = coefs[3 * NV + 2];
   for (int i = threadIdx.x; i <= NV; i += blockDim.x) {
@@ -582,20 +584,43 @@ k_dcgs2_update(long long n, const double* __restrict__ Q, long long vstride,
   }
   __syncthreads();
   double acc = 0.0;
+  const long long n2 = n >> 1;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
-    double a[NV + 1];
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n2; k += stride) {
+    double2 a[NV + 1];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) a[i] = Q[i * vstride + k];
-    const double uk = u[k], zk = z[k];
+    for (int i = 0; i < NV; ++i) a[i] = reinterpret_cast<const double2*>(Q + i * vstride)[k];
+    const double2 uk = reinterpret_cast<const double2*>(u)[k];
+    const double2 zk = reinterpret_cast<const double2*>(z)[k];
+    double t1x = 0.0, t2x = 0.0, t1y = 0.0, t2y = 0.0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      t1x = fma(cs[i], a[i].x, t1x);
+      t2x = fma(cc[i], a[i].x, t2x);
+      t1y = fma(cs[i], a[i].y, t1y);
+      t2y = fma(cc[i], a[i].y, t2y);
+    }
+    double2 q, un;
+    q.x = (uk.x - t1x) / alpha;
+    q.y = (uk.y - t1y) / alpha;
+    un.x = zk.x / alpha - t2x - cc[NV] * q.x;
+    un.y = zk.y / alpha - t2y - cc[NV] * q.y;
+    reinterpret_cast<double2*>(u)[k] = q;
+    reinterpret_cast<double2*>(unext)[k] = un;
+    acc = fma(un.x, un.x, acc);
+    acc = fma(un.y, un.y, acc);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long k = n - 1;
     double t1 = 0.0, t2 = 0.0;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-      t1 = fma(cs[i], a[i], t1);
-      t2 = fma(cc[i], a[i], t2);
+      const double ai = Q[i * vstride + k];
+      t1 = fma(cs[i], ai, t1);
+      t2 = fma(cc[i], ai, t2);
     }
-    const double q = (uk - t1) / alpha;
-    const double un = zk / alpha - t2 - cc[NV] * q;
+    const double q = (u[k] - t1) / alpha;
+    const double un = z[k] / alpha - t2 - cc[NV] * q;
     u[k] = q;
     unext[k] = un;
     acc = fma(un, un, acc);
