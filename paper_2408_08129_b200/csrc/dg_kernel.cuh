@@ -69,7 +69,11 @@ struct Layout {
   static constexpr int C_CH = C_T + KOUT * NP;  // children's nodal face values (one face)
   static constexpr int C_GS = C_CH + S * KIN * NQF;  // fused-dot warp sums
   static constexpr int C_OT = C_GS + CTHREADS;       // trace mode: own face traces (one face)
-  static constexpr int CELEM = C_OT + KIN * NQF;
+  // flux mode, 3D: the separable mortar passes' partials
+  static constexpr int C_SC = C_OT + KIN * NQF;
+  static constexpr int SC_A = KIN * 2 * N * N + S * KIN * N * N;
+  static constexpr int SC_C = S * KOUT * N * N;
+  static constexpr int CELEM = C_SC + (SC_A > SC_C ? SC_A : SC_C);
   static constexpr size_t CSMEM = (size_t)(TABD + 64 + CELEM) * sizeof(double);
 };
 
@@ -979,6 +983,119 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
       }
     }
     __syncthreads();
+    // the separable path covers nodal inputs and the flux-trace (psi) mode;
+    // the Gauss-point-input variants without psi keep the generic loop
+    const bool sep_ok = (OPK != OP_DIVHV) || !P.in_quad || (P.trV != nullptr && P.psi != nullptr);
+    if (D == 3 && FM && sep_ok) {
+      // Flux mode, 3D: the mortar interpolations factor over the two
+      // tangential directions, so each is two 1D passes through a shared
+      // scratch instead of an n^2-term sum per point with product
+      // coefficients.
+      double* SC = red + 64 + L::C_SC;
+      // own traces staged (flux-trace mode) or own nodal face values (A)
+      const bool TRC = (OPK == OP_DIVHV) && P.in_quad;
+      constexpr int NN = N * N;
+      double* T1 = SC;                        // [KIN][2][N][N]  own partials
+      double* U = SC + KIN * 2 * NN;          // [S][KIN][N][N]  children's partials (nodal)
+      const int axis = f >> 1, side = f & 1;
+      // A: T1[c][b1][j0][q1] = sum_j1 M_b1[q1][j1] own[c][j0 N + j1]
+      for (int it = threadIdx.x; it < KIN * 2 * NN; it += blockDim.x) {
+        const int q1 = it % N, j0 = (it / N) % N, b1 = (it / NN) % 2, cc = it / (2 * NN);
+        double t = 0.0;
+        for (int j1 = 0; j1 < N; ++j1) {
+          const int j = j0 * N + j1;
+          const double own = TRC ? OT[cc * NQF + j] : A[cc * NP + cfnode[f * NQF + j]];
+          const double m = TRC ? T.halfq[b1][q1][j1] : T.half[b1][q1][j1];
+          t = fma(m, own, t);
+        }
+        T1[it] = t;
+      }
+      // A': U[sub][c][j0][q1] = sum_j1 B[q1][j1] child[sub][c][j0 N + j1]
+      if (!TRC) {
+        for (int it = threadIdx.x; it < S * KIN * NN; it += blockDim.x) {
+          const int q1 = it % N, j0 = (it / N) % N, r = it / NN;  // r = sub * KIN + c
+          double t = 0.0;
+          for (int j1 = 0; j1 < N; ++j1) t = fma(T.B[q1][j1], CH[r * NQF + j0 * N + j1], t);
+          U[it] = t;
+        }
+      }
+      __syncthreads();
+      // B: the subface fluxes (fine-side metric) at every fine point
+      for (int it = threadIdx.x; it < S * NQF; it += blockDim.x) {
+        const int qf = it % NQF, sub = it / NQF;
+        const int q0 = qf / N, q1 = qf % N;
+        const int b0 = sub & 1, b1 = (sub >> 1) & 1;
+        const long long child = s_child[f][sub];
+        double TO[KIN], TN[KIN];
+#pragma unroll
+        for (int cc = 0; cc < KIN; ++cc) {
+          double ao = 0.0;
+          for (int j0 = 0; j0 < N; ++j0) {
+            const double m = TRC ? T.halfq[b0][q0][j0] : T.half[b0][q0][j0];
+            ao = fma(m, T1[((cc * 2 + b1) * N + j0) * N + q1], ao);
+          }
+          TO[cc] = ao;
+          if (TRC) {
+            TN[cc] = CH[(sub * KIN + cc) * NQF + qf];
+          } else {
+            double an = 0.0;
+            for (int j0 = 0; j0 < N; ++j0)
+              an = fma(T.B[q0][j0], U[((sub * KIN + cc) * N + j0) * N + q1], an);
+            TN[cc] = an;
+          }
+        }
+        const ElemGeo<D> og = elem_geo<D>(mesh.elem, P.gc, child);
+        double n[D], ws;
+        if (axis == 0) face_metric_ax<D, N, 0>(P.gc, mesh.col, og, 1 - side, false, qf, T, n, ws);
+        else if (axis == 1) face_metric_ax<D, N, 1>(P.gc, mesh.col, og, 1 - side, false, qf, T, n, ws);
+        else face_metric_ax<D, N, D - 1>(P.gc, mesh.col, og, 1 - side, false, qf, T, n, ws);
+        const bool minus = side == 1;
+        double fl[KOUT];
+        if (OPK == OP_DIVHV && P.psi != nullptr) {
+          double vn = 0.0;
+#pragma unroll
+          for (int a = 0; a < D; ++a) vn = fma(TO[a], n[a], vn);
+          fl[0] = (minus ? 1.0 : -1.0) * (TN[0] + (0.5 * ws) * (TO[D] * vn));
+#pragma unroll
+          for (int k = 0; k < KOUT; ++k) FW[(sub * KOUT + k) * NQF + qf] = fl[k];
+        } else {
+          double TLv[KIN], TRv[KIN];
+#pragma unroll
+          for (int cc = 0; cc < KIN; ++cc) {
+            TLv[cc] = minus ? TO[cc] : TN[cc];
+            TRv[cc] = minus ? TN[cc] : TO[cc];
+          }
+          num_flux<D, OPK, KIN, KOUT>(TLv, TRv, n, P.model.kinetic_factor, fl, &P.model, P.full);
+          const double sg = minus ? ws : -ws;
+#pragma unroll
+          for (int k = 0; k < KOUT; ++k) FW[(sub * KOUT + k) * NQF + qf] = fl[k] * sg;
+        }
+      }
+      __syncthreads();
+      // C: Pp[sub][k][j0][q1] = sum_j1 halfq[b1][j1][q1] FW[sub][k][j0 N + j1]
+      double* Pp = SC;
+      for (int it = threadIdx.x; it < S * KOUT * NN; it += blockDim.x) {
+        const int q1 = it % N, j0 = (it / N) % N, r = it / NN;  // r = sub * KOUT + k
+        const int b1 = ((r / KOUT) >> 1) & 1;
+        double t = 0.0;
+        for (int j1 = 0; j1 < N; ++j1) t = fma(T.halfq[b1][j1][q1], FW[r * NQF + j0 * N + j1], t);
+        Pp[it] = t;
+      }
+      __syncthreads();
+      // C': G[k][q0 N + q1] = sum_sub sum_j0 halfq[b0][j0][q0] Pp[sub][k][j0][q1] -> cflux
+      const long long grp = s_grp[f];
+      for (int it = threadIdx.x; it < KOUT * NQF; it += blockDim.x) {
+        const int k = it / NQF, qt = it % NQF, q0 = qt / N, q1 = qt % N;
+        double acc = 0.0;
+        for (int sub = 0; sub < S; ++sub) {
+          const int b0 = sub & 1;
+          for (int j0 = 0; j0 < N; ++j0)
+            acc = fma(T.halfq[b0][j0][q0], Pp[((sub * KOUT + k) * N + j0) * N + q1], acc);
+        }
+        P.mesh.cflux[grp * KOUT * NQF + it] = acc;
+      }
+      continue;
+    }
     // subface fluxes of this coarse face
     for (int it = threadIdx.x; it < S * NQF; it += blockDim.x) {
       const int qf = it % NQF;

@@ -280,22 +280,26 @@ int op_divhv(dg_ctx* c, CView V, const double* h, int homog, int mode, MView out
 // Face-trace mode of the Helmholtz pair: V and h live at the Gauss points,
 // H1 writes V's face traces, H2 takes its neighbours' traces from them (no
 // nodal interpolation, no tangential face passes for conforming faces)
+bool psi_env_ok(dg_ctx* c) {
+  static const char* env = getenv("DG_PSI");
+  static const bool on = env == nullptr || std::string(env) != "0";
+  return on && (c->mesh.n_coarse == 0 || c->cflux.p != nullptr);
+}
+
 bool trace_mode(dg_ctx* c) {
-  // default on (the nodal path: DG_TRACE=0)
+  // default on (the nodal path: DG_TRACE=0).  The flux-trace pair needs no
+  // asynchronous staging in the general kernel, so it also enables the
+  // Gauss-point storage where that kernel could not (3D r = 4)
   static const char* env = getenv("DG_TRACE");
   static const bool on = env == nullptr || std::string(env) != "0";
-  return on && welem_enabled(c->dim, c->N) && welem_trace_ok(c->dim, c->N);
+  return on && welem_enabled(c->dim, c->N) && (welem_trace_ok(c->dim, c->N) || psi_env_ok(c));
 }
 
 // Flux-trace (psi) mode of the trace-mode pair (dg_hkernel.cuh): H1 writes
 // 1/2 ws h (V . n+) per face point, H2 sums its own and its neighbours'
 // values instead of evaluating face traces, metrics and ghosts.  Needs the
 // coarse faces in flux mode.  Default on (DG_PSI=0: the trace-mode pair)
-bool psi_mode(dg_ctx* c) {
-  static const char* env = getenv("DG_PSI");
-  static const bool on = env == nullptr || std::string(env) != "0";
-  return on && trace_mode(c) && (c->mesh.n_coarse == 0 || c->cflux.p != nullptr);
-}
+bool psi_mode(dg_ctx* c) { return psi_env_ok(c) && trace_mode(c); }
 
 // Pipelined H2 (hdiv2_kernel: persistent warps fed by cp.async.bulk; odd
 // n^d blocks copied as their 16-byte aligned superset).  Default on
