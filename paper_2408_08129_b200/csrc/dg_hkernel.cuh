@@ -36,10 +36,13 @@ template <int D, int N>
 struct HLayout {
   static constexpr int NP = ipow(N, D);
   static constexpr int NC = ipow(N, D - 1);   // lanes per element
-  static constexpr int EPW = 32 / NC;         // elements per warp
-  static constexpr int NSLOT = EPW + ((32 % NC) ? 1 : 0);
-  static constexpr int WPB = 4;
-  static constexpr int THREADS = 32 * WPB;
+  // a "team" owns whole elements: one warp for n^(d-1) <= 32, a pair of
+  // warps (named barriers) for 3D r = 5, 6
+  static constexpr int TPE = NC <= 32 ? 32 : 64;
+  static constexpr int EPW = TPE / NC;        // elements per team
+  static constexpr int NSLOT = EPW + ((TPE % NC) ? 1 : 0);
+  static constexpr int WPB = 128 / TPE;       // teams per CTA
+  static constexpr int THREADS = 128;
   static constexpr int NF = 2 * D;
   static constexpr int TSZ = tile_size<D, N>();
   static constexpr int TABD = (int)(sizeof(Tab<N>) / sizeof(double));
@@ -55,8 +58,33 @@ struct HLayout {
   static constexpr int DSLOT = odd(DRAW > 40 ? DRAW : 40);
   static constexpr size_t GSMEM = (size_t)(TABP + WPB * NSLOT * GSLOT) * sizeof(double);
   static constexpr size_t DSMEM = (size_t)(TABP + WPB * NSLOT * DSLOT) * sizeof(double);
-  static constexpr bool OK = NC <= 32;
+  static constexpr bool OK = NC <= 64;
 };
+
+// team-wide barrier and vote (a warp, or two warps on named barrier 1 + team)
+template <int TPE>
+__device__ __forceinline__ void esync(int team) {
+  if constexpr (TPE == 32) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + team), "r"(TPE) : "memory");
+  }
+}
+template <int TPE>
+__device__ __forceinline__ bool eany(bool pred, int team) {
+  if constexpr (TPE == 32) {
+    return __any_sync(0xffffffffu, pred);
+  } else {
+    unsigned out;
+    asm volatile(
+        "{\n .reg .pred p, q;\n setp.ne.u32 q, %1, 0;\n"
+        " bar.red.or.pred p, %2, %3, q;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(out)
+        : "r"((unsigned)pred), "r"(1 + team), "r"(TPE)
+        : "memory");
+    return out != 0;
+  }
+}
 
 #ifndef DG_HK1_MINB
 #define DG_HK1_MINB 5
@@ -260,7 +288,8 @@ __device__ __forceinline__ void hgrad_body(const KParams<N>& P, const Tab<N>& TS
                                            long long e, const uint8_t (&kf)[2 * D],
                                            const int (&nf)[2 * D], const ElemGeo<D>& g,
                                            const double* colrow, const double* xcol,
-                                           const double* hrow, double* X, double* FG, double* HW) {
+                                           const double* hrow, double* X, double* FG, double* HW,
+                                           int team) {
   using HL = HLayout<D, N>;
   constexpr int NC = HL::NC, NF = HL::NF, TSZ = HL::TSZ;
   constexpr int NQH = ipow(N, D - 1), NE = ipow(N, D - 2);
@@ -286,7 +315,7 @@ __device__ __forceinline__ void hgrad_body(const KParams<N>& P, const Tab<N>& TS
 #pragma unroll
     for (int k = 0; k < N; ++k) X[coff<D, N>(c, k)] = q[k];
   }
-  __syncwarp();
+  esync<HL::TPE>(team);
   if constexpr (D == 3) {
     double v[N], o[N];
 #pragma unroll
@@ -294,7 +323,7 @@ __device__ __forceinline__ void hgrad_body(const KParams<N>& P, const Tab<N>& TS
     mat_apply<N, false>(TC.B, v, o);
 #pragma unroll
     for (int jj = 0; jj < N; ++jj) X[yoff<N>(c, jj)] = o[jj];
-    __syncwarp();
+    esync<HL::TPE>(team);
   }
   {
     double v[N], o[N];
@@ -325,10 +354,10 @@ __device__ __forceinline__ void hgrad_body(const KParams<N>& P, const Tab<N>& TS
     tn[f] = t;
   }
   if constexpr (D == 3) {
-    __syncwarp();
+    esync<HL::TPE>(team);
 #pragma unroll
     for (int f = 0; f < NF; ++f) FG[f * NC + c] = tn[f];
-    __syncwarp();
+    esync<HL::TPE>(team);
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
       const int kd = kf[f] & 15;
@@ -340,7 +369,7 @@ __device__ __forceinline__ void hgrad_body(const KParams<N>& P, const Tab<N>& TS
       tn[f] = t;
     }
   }
-  __syncwarp();  // the tile holds p at the Gauss points of every lane
+  esync<HL::TPE>(team);  // the tile holds p at the Gauss points of every lane
   // ---- face fluxes  sg 1/2 ws n+ (p_own + p_x): p_x = neighbour (interior),
   // p_own (wall), 0 (far field, homogeneous); coarse side precomputed
   double flv[2 * (D - 1)];  // vertical faces: the AX component only
@@ -421,7 +450,7 @@ __device__ __forceinline__ void hgrad_body(const KParams<N>& P, const Tab<N>& TS
         Zc[k][kz] = TC.lift[0][kz] * flz[0][k] + TC.lift[1][kz] * flz[1][k] - Zc[k][kz];
     }
   }
-  __syncwarp();
+  esync<HL::TPE>(team);
   {
     double v[N], o[N];
 #pragma unroll
@@ -439,7 +468,7 @@ __device__ __forceinline__ void hgrad_body(const KParams<N>& P, const Tab<N>& TS
         X[TSZ + yoff<N>(c, jj)] = TC.lift[0][jj] * flv[2] + TC.lift[1][jj] * flv[3] - o[jj];
     }
   }
-  __syncwarp();
+  esync<HL::TPE>(team);
 #pragma unroll
   for (int kz = 0; kz < N; ++kz) {
     Zc[0][kz] += X[coff<D, N>(c, kz)];
@@ -473,12 +502,12 @@ __device__ __forceinline__ void hgrad_body(const KParams<N>& P, const Tab<N>& TS
       for (int kz = 0; kz < N; ++kz) t = fma(TC.lift[side][kz], Vg[k][kz], t);
       tz[side][k] = t;
     }
-  __syncwarp();  // every lane is done with the tile
+  esync<HL::TPE>(team);  // every lane is done with the tile
 #pragma unroll
   for (int a = 0; a < D - 1; ++a)
 #pragma unroll
     for (int kz = 0; kz < N; ++kz) X[a * TSZ + coff<D, N>(c, kz)] = Vg[a][kz];
-  __syncwarp();
+  esync<HL::TPE>(team);
   double tv[2 * (D - 1)];
 #pragma unroll
   for (int a = 0; a < D - 1; ++a)
@@ -532,7 +561,8 @@ __device__ __forceinline__ void hgrad_body(const KParams<N>& P, const Tab<N>& TS
 }
 
 template <int D, int N>
-__global__ void __launch_bounds__(HLayout<D, N>::THREADS, DG_HK1_MINB)
+__global__ void __launch_bounds__(HLayout<D, N>::THREADS,
+                                  HLayout<D, N>::TPE == 32 ? DG_HK1_MINB : 3)
 hgrad_kernel(const __grid_constant__ KParams<N> P) {
   using HL = HLayout<D, N>;
   constexpr int NC = HL::NC, EPW = HL::EPW, NF = HL::NF, TSZ = HL::TSZ;
@@ -541,7 +571,7 @@ hgrad_kernel(const __grid_constant__ KParams<N> P) {
   tab_bulk_issue(smem, P.tab_g, HL::TABD * 8, &tbar);
   const Tab<N>& TS = *reinterpret_cast<const Tab<N>*>(smem);
   const MeshDev& mesh = P.mesh;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x % HL::TPE, wid = threadIdx.x / HL::TPE;  // team lane, team
   const int eiw = lane / NC, c = lane - eiw * NC;
   const bool slot_ok = eiw < EPW;
   const long long e = ((long long)blockIdx.x * HL::WPB + wid) * EPW + eiw;
@@ -573,7 +603,7 @@ hgrad_kernel(const __grid_constant__ KParams<N> P) {
   __syncthreads();  // the table barrier is initialised
   tab_bulk_wait(&tbar);
   hgrad_body<D, N>(P, TS, c, act, e, kf, nf, g, colrow, xc, P.trH + es * (NF * NC) + c, X, FG,
-                   HW);
+                   HW, wid);
 }
 
 // H1, pipelined (hgrad2_kernel): persistent warps over strided element
@@ -588,7 +618,7 @@ struct H1Pipe {
   using HL = HLayout<D, N>;
   static constexpr int NP = HL::NP, NC = HL::NC, NF = HL::NF, EPW = HL::EPW;
   static constexpr int COLS = 2 * ((ipow(N, D - 1) * D + 2 * (D - 1) * ipow(N, D - 2) + 1) / 2);
-  static constexpr bool OK = HL::OK && (NP % 2 == 0) && ((NF * NC) % 2 == 0);
+  static constexpr bool OK = HL::OK && HL::TPE == 32 && (NP % 2 == 0) && ((NF * NC) % 2 == 0);
   static constexpr int OX = 0;                      // nodal x (bulk)
   static constexpr int OH = OX + EPW * NP;          // own h traces (bulk)
   static constexpr int OR = OH + EPW * NF * NC;     // records (bulk), 8 doubles each
@@ -734,7 +764,7 @@ hgrad2_kernel(const __grid_constant__ KParams<N> P) {
     const ElemGeo<D> g3 = geo_from_row<D>(rec + 8, P.gc);
     hgrad_body<D, N>(P, TS, c, act, e, kf, nf, g3, st + PL::OC + esl * PL::COLS,
                      st + PL::OX + esl * NP + c * N, st + PL::OH + esl * (NF * NC) + c, X,
-                     st + PL::OF + (slot_ok ? eiw : EPW) * (NF * NC), HW);
+                     st + PL::OF + (slot_ok ? eiw : EPW) * (NF * NC), HW, wid);
     __syncwarp();  // every lane is done with this stage
     if (lane == 0 && g + 2 * GW < ngroups) issue(g + 2 * GW, s);
   }
@@ -758,7 +788,8 @@ __global__ void hk_elem_records(const int* __restrict__ nbr, const uint8_t* __re
 
 // ---------------------------------------------------------------------- H2
 template <int D, int N>
-__global__ void __launch_bounds__(HLayout<D, N>::THREADS, DG_HK2_MINB)
+__global__ void __launch_bounds__(HLayout<D, N>::THREADS,
+                                  HLayout<D, N>::TPE == 32 ? DG_HK2_MINB : 3)
 hdiv_kernel(const __grid_constant__ KParams<N> P) {
   using HL = HLayout<D, N>;
   constexpr int NC = HL::NC, EPW = HL::EPW, NF = HL::NF, TSZ = HL::TSZ;
@@ -768,7 +799,7 @@ hdiv_kernel(const __grid_constant__ KParams<N> P) {
   const Tab<N>& TS = *reinterpret_cast<const Tab<N>*>(smem);
   const Tab<N>& TC = P.tab;
   const MeshDev& mesh = P.mesh;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x % HL::TPE, wid = threadIdx.x / HL::TPE;  // team lane, team
   const int eiw = lane / NC, c = lane - eiw * NC;
   const bool slot_ok = eiw < EPW;
   const long long e = ((long long)blockIdx.x * HL::WPB + wid) * EPW + eiw;
@@ -830,7 +861,7 @@ hdiv_kernel(const __grid_constant__ KParams<N> P) {
     constexpr int f = 2 * AX + side;
     const int kd = kf[f] & 15;
     const bool fine = act && kd == KIND_FINE;
-    if (!__any_sync(0xffffffffu, fine)) return;
+    if (!eany<HL::TPE>(fine, wid)) return;
     constexpr int FC = (AX < D - 1) ? 2 : D + 1;  // (V_AX, h) or (V, h)
     constexpr int TSL = tr_slots<D>() * NC, THL = 2 * D * NC;
     const long long pe = nf[f];
@@ -845,7 +876,7 @@ hdiv_kernel(const __grid_constant__ KParams<N> P) {
       }
       X[r * NC + c] = v;
     }
-    __syncwarp();
+    esync<HL::TPE>(wid);
     const int sf = (kf[f] >> 4) & 3;
     const double* Mq0 = &TS.halfq[sf & 1][0][0];
     const double* Mq1 = &TS.halfq[(sf >> 1) & 1][0][0];
@@ -863,10 +894,10 @@ hdiv_kernel(const __grid_constant__ KParams<N> P) {
       tr[r] = t;
     }
     if constexpr (D == 3) {
-      __syncwarp();
+      esync<HL::TPE>(wid);
 #pragma unroll
       for (int r = 0; r < FC; ++r) X[r * NC + c] = tr[r];
-      __syncwarp();
+      esync<HL::TPE>(wid);
 #pragma unroll
       for (int r = 0; r < FC; ++r) {
         double t = 0.0;
@@ -875,7 +906,7 @@ hdiv_kernel(const __grid_constant__ KParams<N> P) {
         tr[r] = t;
       }
     }
-    __syncwarp();  // the staging area is reused by the next face
+    esync<HL::TPE>(wid);  // the staging area is reused by the next face
     if (fine) {
       double n[D], ws;
       const double oe = (AX < D - 1) ? edge_omh<D, N>(P.gc, mesh.col, g, f, c, act) : 1.0;
@@ -930,7 +961,7 @@ hdiv_kernel(const __grid_constant__ KParams<N> P) {
     for (int kz = 0; kz < N; ++kz)
       Zc[kz] = TC.lift[0][kz] * fl[zf] + TC.lift[1][kz] * fl[zf + 1] - Zc[kz];
   }
-  __syncwarp();
+  esync<HL::TPE>(wid);
   {
     double v[N], o[N];
 #pragma unroll
@@ -948,7 +979,7 @@ hdiv_kernel(const __grid_constant__ KParams<N> P) {
         X[TSZ + yoff<N>(c, jj)] = TC.lift[0][jj] * fl[2] + TC.lift[1][jj] * fl[3] - o[jj];
     }
   }
-  __syncwarp();
+  esync<HL::TPE>(wid);
 #pragma unroll
   for (int kz = 0; kz < N; ++kz) {
     Zc[kz] += X[coff<D, N>(c, kz)];
@@ -964,10 +995,10 @@ hdiv_kernel(const __grid_constant__ KParams<N> P) {
     for (int kz = 0; kz < N; ++kz) t[kz] = Zc[kz] * (iwh * TC.iqw[kz]);
     mat_apply<N, false>(TC.Binv, t, Zc);
   }
-  __syncwarp();
+  esync<HL::TPE>(wid);
 #pragma unroll
   for (int kz = 0; kz < N; ++kz) X[coff<D, N>(c, kz)] = Zc[kz];
-  __syncwarp();
+  esync<HL::TPE>(wid);
   if constexpr (D == 3) {
     double v[N], o[N];
 #pragma unroll
@@ -975,7 +1006,7 @@ hdiv_kernel(const __grid_constant__ KParams<N> P) {
     mat_apply<N, false>(TC.Binv, v, o);
 #pragma unroll
     for (int jj = 0; jj < N; ++jj) X[yoff<N>(c, jj)] = o[jj];
-    __syncwarp();
+    esync<HL::TPE>(wid);
   }
   double wv[N], uv[N];
   {
@@ -995,8 +1026,9 @@ hdiv_kernel(const __grid_constant__ KParams<N> P) {
       }
     }
   }
-  if (P.gs_part != nullptr) {
-    // fused Gram-Schmidt dots (as gs_dots, dg_wkernel.cuh): every element is
+  if (HL::TPE == 32 && P.gs_part != nullptr) {
+    // fused Gram-Schmidt dots (one-warp teams only; two-warp teams take the
+    // separate dual-dot pass) (as gs_dots, dg_wkernel.cuh): every element is
     // complete here (coarse faces in flux mode)
     constexpr int AREA = HL::NSLOT * HL::DSLOT;
     static_assert(AREA >= 2 * (32 + 2), "warp area too small for the fused dots");
@@ -1004,7 +1036,7 @@ hdiv_kernel(const __grid_constant__ KParams<N> P) {
     const int nv = P.gs_nv;
     const int nvt = dual ? 2 * (nv + 2) : nv + 1;
     double* wtot = smem + HL::TABP + wid * AREA;
-    __syncwarp();
+    esync<HL::TPE>(wid);
     for (int c0 = 0; c0 < nvt; c0 += 16) {
       if (dual) gs_round<D, N, 2>(P, act, e, c, wv, uv, c0, nv, nvt, wtot);
       else gs_round<D, N, 1>(P, act, e, c, wv, uv, c0, nv, nvt, wtot);
@@ -1036,7 +1068,7 @@ template <int D, int N>
 struct H2Pipe {
   using HL = HLayout<D, N>;
   static constexpr int NP = HL::NP, NC = HL::NC, NF = HL::NF, EPW = HL::EPW;
-  static constexpr bool OK = HL::OK;
+  static constexpr bool OK = HL::OK && HL::TPE == 32;
   static constexpr int ev(int x) { return (x + 1) & ~1; }
   // stage sub-arrays (doubles, all even offsets); the odd-n^d blocks (V, h,
   // base) are copied as their 16-byte aligned superset, shifted by 0 or 1

@@ -363,6 +363,14 @@ inline bool welem_enabled(int D, int N) {
   return nc <= 32 && !v2;
 }
 
+// the flux-trace Helmholtz kernels (dg_hkernel.cuh): one- or two-warp teams
+inline bool hk_enabled(int D, int N) {
+  int nc = 1;
+  for (int a = 0; a < D - 1; ++a) nc *= N;
+  static const bool v2 = getenv("DG_KERNEL") && std::string(getenv("DG_KERNEL")) == "v2";
+  return nc <= 64 && !v2;
+}
+
 // can the warp-element div(hV) kernel stage face data asynchronously (and
 // with it run the face-trace mode) for this (dim, n)?
 template <int D>

@@ -292,7 +292,8 @@ bool trace_mode(dg_ctx* c) {
   // Gauss-point storage where that kernel could not (3D r = 4)
   static const char* env = getenv("DG_TRACE");
   static const bool on = env == nullptr || std::string(env) != "0";
-  return on && welem_enabled(c->dim, c->N) && (welem_trace_ok(c->dim, c->N) || psi_env_ok(c));
+  return on && ((welem_enabled(c->dim, c->N) && welem_trace_ok(c->dim, c->N)) ||
+                (hk_enabled(c->dim, c->N) && psi_env_ok(c)));
 }
 
 // Flux-trace (psi) mode of the trace-mode pair (dg_hkernel.cuh): H1 writes
@@ -311,7 +312,8 @@ bool pipe_mode(dg_ctx* c) {
   // the fused Gram-Schmidt dots (one launch fewer per Arnoldi step) wins
   static const long long min_dof =
       getenv("DG_PIPE_MIN") ? atoll(getenv("DG_PIPE_MIN")) : (1LL << 20);
-  return on && (long long)c->n_el * c->NP >= min_dof;
+  // (one-warp teams only: the stage ring is per warp)
+  return on && (long long)c->n_el * c->NP >= min_dof && c->NQF <= 32;
 }
 
 // DCGS2 with the pipelined H2: the Gram-Schmidt dots in their own streaming
@@ -319,7 +321,8 @@ bool pipe_mode(dg_ctx* c) {
 bool sep_dots(dg_ctx* c) {
   static const char* env = getenv("DG_SEPDOTS");
   static const bool on = env == nullptr || std::string(env) != "0";
-  return on && trace_mode(c) && psi_mode(c) && pipe_mode(c);
+  // (two-warp teams, 3D r >= 5, have no fused dots)
+  return on && trace_mode(c) && psi_mode(c) && (pipe_mode(c) || c->NQF > 32);
 }
 
 // the pin buffer (zero: boundary, fine and coarse faces are never written)
@@ -646,12 +649,13 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const doubl
   // (the fused dots' partial rows hold <= 32 + 2 column pairs: longer
   // restarts take the unfused CGS passes)
   const bool fuse = gs_fusable(c) && m <= 31;
+  const bool sep = sep_dots(c) && m <= 31;
   // DCGS2 (delayed re-orthogonalisation) needs the fused dual
   // dots and u = the action's input (no preconditioner); DG_GMRES=cgs2 keeps
   // the CGS + selective re-orthogonalisation path
   static const bool cgs_env = getenv("DG_GMRES") && std::string(getenv("DG_GMRES")) == "cgs2";
-  const bool dcgs2 = fuse && !pc && !cgs_env;
-  if (fuse) {
+  const bool dcgs2 = (fuse || sep) && !pc && !cgs_env;
+  if (fuse || sep) {
     // one row of <= m + 1 dot partials per element-kernel warp (>= 1 element
     // each) and per coarse element
     // (or one row per block of the separate dual-dot pass: <= RED_BLOCKS)

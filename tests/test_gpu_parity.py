@@ -258,4 +258,11 @@ def test_high_degree_periodic_vs_oracle(degree):
     x = cases.energy_like(U, 7)
     from paper_2408_08129_b200.imex import build_helmholtz_action
     y = build_helmholtz_action(split, c.a_dt, U)(x.ravel()).reshape(x.shape)
-    assert rel(y, orc.helmholtz_linear(c.a_dt, h, x)) <= 1e-12
+    check_rel(c.name, "helm_x_vs_oracle", y, orc.helmholtz_linear(c.a_dt, h, x), 1e-12)
+    # one ARS(2,2,2) step (the flux-trace pair on two-warp teams, DCGS2 with
+    # the separate dual-dot pass) against the oracle's step
+    from paper_2408_08129_b200.imex import ImplicitSolveConfig, ars222, imex_step
+    U1, st = imex_step(U, 0.0, 0.3, ars222(), split, ImplicitSolveConfig())
+    U1o, sto = O.imex_step(orc, U, 0.0, 0.3)
+    assert st.krylov_iters == list(sto.krylov_iters) and st.fp_iters == list(sto.fp_iters)
+    check_rel(c.name, "state_after_step1_vs_oracle", U1, U1o, 1e-11)
