@@ -61,31 +61,6 @@ struct HLayout {
   static constexpr bool OK = NC <= 64;
 };
 
-// team-wide barrier and vote (a warp, or two warps on named barrier 1 + team)
-template <int TPE>
-__device__ __forceinline__ void esync(int team) {
-  if constexpr (TPE == 32) {
-    __syncwarp();
-  } else {
-    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + team), "r"(TPE) : "memory");
-  }
-}
-template <int TPE>
-__device__ __forceinline__ bool eany(bool pred, int team) {
-  if constexpr (TPE == 32) {
-    return __any_sync(0xffffffffu, pred);
-  } else {
-    unsigned out;
-    asm volatile(
-        "{\n .reg .pred p, q;\n setp.ne.u32 q, %1, 0;\n"
-        " bar.red.or.pred p, %2, %3, q;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(out)
-        : "r"((unsigned)pred), "r"(1 + team), "r"(TPE)
-        : "memory");
-    return out != 0;
-  }
-}
-
 #ifndef DG_HK1_MINB
 #define DG_HK1_MINB 5
 #endif

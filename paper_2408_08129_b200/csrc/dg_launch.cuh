@@ -255,7 +255,7 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
     using XL = XLayout<D, N>;
     static const bool use_x = !(getenv("DG_KERNEL") && std::string(getenv("DG_KERNEL")) == "v2");
     if (use_x) {
-      constexpr int EPC = XL::EPW * XL::WPB;
+      constexpr int EPC = XL::EPW * XL::TEAMS;
       const int xgrid = (a.mesh.n_el + EPC - 1) / EPC;
       if (info) {
         info->epb = EPC;

@@ -79,15 +79,19 @@ struct XLayout {
   static constexpr int V = D + 2;
   static constexpr int NP = ipow(N, D);
   static constexpr int NC = ipow(N, D - 1);  // lanes per element
-  static constexpr int EPW = 32 / NC;          // elements per warp
+  // a team owns whole elements: one warp for n^(d-1) <= 32, two warps on a
+  // named barrier for 3D r = 5, 6 (dg_hkernel.cuh esync)
+  static constexpr int TPE = NC <= 32 ? 32 : 64;
+  static constexpr int EPW = TPE / NC;         // elements per team
   static constexpr int TSZ = tile_size<D, N>();  // one tensor (tile layout: coff)
 #ifndef DG_XWPB
 #define DG_XWPB 1
 #endif
-  static constexpr int WPB = DG_XWPB;          // warps per CTA
+  static constexpr int TEAMS = DG_XWPB;        // teams per CTA
+  static constexpr int WPB = TEAMS * TPE / 32;  // warps per CTA (mass-rate partial rows)
   static constexpr int THREADS = 32 * WPB;
   static constexpr int TABD = (int)(sizeof(Tab<N>) / sizeof(double));
-  static constexpr int NSLOT = EPW + ((32 % NC) ? 1 : 0);
+  static constexpr int NSLOT = EPW + ((TPE % NC) ? 1 : 0);
   static constexpr int GEON = 1 + (D - 1);
   static constexpr int NE = ipow(N, D - 2);
   static constexpr int GEE = 2 * (D - 1) * NE;
@@ -101,11 +105,14 @@ struct XLayout {
   static constexpr int SLOT0 = OFF_GE + GEON * NC + GEE;
   static constexpr int SLOT = (SLOT0 % 2 == 0) ? SLOT0 + 1 : SLOT0;  // bank shift
   static constexpr size_t SMEM = (size_t)(TABD + WPB * NSLOT * SLOT) * sizeof(double);
+  // two-warp teams (r = 5, 6) compile but measured slower than the CTA
+  // kernel (255 registers: cfg5 r=5 5.9 vs 5.0 ms, r=6 12.2 vs 7.5 ms), so
+  // the explicit operator keeps one-warp teams
   static constexpr bool OK = (NC <= 32) && (SMEM <= 200 * 1024);
 #ifndef DG_XMINB
 #define DG_XMINB 11
 #endif
-  static constexpr int MINB = DG_XMINB;
+  static constexpr int MINB = TPE == 32 ? DG_XMINB : 4;
 };
 
 // FULL: divergence_full (P.full != 0) -- a separate instantiation keeps the
@@ -122,12 +129,12 @@ xelem_kernel(const __grid_constant__ KParams<N> P) {
   const Tab<N>& TC = P.tab;
   const MeshDev& mesh = P.mesh;
   const Model& md = P.model;
-  const int lane = threadIdx.x & 31;
-  const int wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x % XL::TPE;  // lane in the team
+  const int wid = threadIdx.x / XL::TPE;   // team
   const int eiw = lane / NC;
   const int c = lane - eiw * NC;
   const bool slot_ok = eiw < EPW;
-  const long long e = ((long long)blockIdx.x * XL::WPB + wid) * EPW + eiw;
+  const long long e = ((long long)blockIdx.x * XL::TEAMS + wid) * EPW + eiw;
   const bool act = slot_ok && e < mesh.n_el;
   const long long es = act ? e : 0;
   double* S = smem + XL::TABD + (wid * XL::NSLOT + (slot_ok ? eiw : EPW)) * XL::SLOT;
@@ -182,7 +189,7 @@ xelem_kernel(const __grid_constant__ KParams<N> P) {
 #pragma unroll
     for (int k = 0; k < N; ++k) X[r * TSZ + coff<D, N>(c, k)] = o[k];
   }
-  __syncwarp();
+  esync<XL::TPE>(wid);
   if constexpr (D == 3) {
 XROLL
     for (int r = 0; r < V; ++r) {
@@ -193,7 +200,7 @@ XROLL
 #pragma unroll
       for (int jj = 0; jj < N; ++jj) X[r * TSZ + yoff<N>(c, jj)] = o[jj];
     }
-    __syncwarp();
+    esync<XL::TPE>(wid);
   }
 XROLL
   for (int r = 0; r < V; ++r) {
@@ -237,10 +244,10 @@ XROLL
       }
     }
     if constexpr (D == 3) {
-      __syncwarp();
+      esync<XL::TPE>(wid);
 #pragma unroll
       for (int r = 0; r < V; ++r) G0[r * NC + c] = t1[r];
-      __syncwarp();
+      esync<XL::TPE>(wid);
 #pragma unroll
       for (int r = 0; r < V; ++r) {
         double t = 0.0;
@@ -291,7 +298,7 @@ XROLL
         else flz[1][k] = fv[k];
       }
     } else {
-      __syncwarp();  // every lane is done reading this face's staged nodes
+      esync<XL::TPE>(wid);  // every lane is done reading this face's staged nodes
 #pragma unroll
       for (int k = 0; k < V; ++k) G0[k * NC + c] = fv[k];
     }
@@ -317,7 +324,7 @@ XROLL
 #pragma unroll 1
 #endif
   for (int side = 0; side < 2; ++side) face(std::integral_constant<int, D - 1>{}, side);
-  __syncwarp();  // every lane is done reading the Gauss tile's pencils
+  esync<XL::TPE>(wid);  // every lane is done reading the Gauss tile's pencils
 
   // ---- 3. volume: flux + metric per column point ------------------------
   double omh_c = 1.0, dh_c[D - 1];
@@ -416,7 +423,7 @@ XROLL
         Zc[r][kz] = TC.lift[0][kz] * flz[0][r] + TC.lift[1][kz] * flz[1][r] - Zc[r][kz];
     }
   }
-  __syncwarp();
+  esync<XL::TPE>(wid);
   // x (and y) directions on the lane's pencils, with that direction's lifts
 XROLL
   for (int r = 0; r < V; ++r) {
@@ -438,7 +445,7 @@ XROLL
         GY[r * TSZ + yoff<N>(c, jj)] = TC.lift[0][jj] * f2 + TC.lift[1][jj] * f3 - o[jj];
     }
   }
-  __syncwarp();
+  esync<XL::TPE>(wid);
 #pragma unroll
   for (int r = 0; r < V; ++r)
 #pragma unroll
@@ -457,7 +464,8 @@ XROLL
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) P.mass_partial[(long long)blockIdx.x * XL::WPB + wid] = v;
+    if ((threadIdx.x & 31) == 0)  // one row per warp
+      P.mass_partial[(long long)blockIdx.x * XL::WPB + (threadIdx.x >> 5)] = v;
   }
 
   // ---- 4. epilogue: B^-1 diag(1/(w det)) (MINV) or B^T (DUAL) -----------
@@ -493,12 +501,12 @@ XROLL
       mat_apply<N, true>(TC.B, t, Zc[r]);
     }
   }
-  __syncwarp();
+  esync<XL::TPE>(wid);
 #pragma unroll
   for (int r = 0; r < V; ++r)
 #pragma unroll
     for (int kz = 0; kz < N; ++kz) X[r * TSZ + coff<D, N>(c, kz)] = Zc[r][kz];
-  __syncwarp();
+  esync<XL::TPE>(wid);
   if constexpr (D == 3) {
 XROLL
     for (int r = 0; r < V; ++r) {
@@ -510,7 +518,7 @@ XROLL
 #pragma unroll
       for (int jj = 0; jj < N; ++jj) X[r * TSZ + yoff<N>(c, jj)] = o[jj];
     }
-    __syncwarp();
+    esync<XL::TPE>(wid);
   }
   if (!act) return;
   // x pass and store from the x-pencil: nodes (ii, [j,] k) of lane c
