@@ -116,18 +116,21 @@ def peaks():
 
 
 def traffic(workload, kernel_class, algorithmic_per_launch):
-    """DRAM bytes per operator call of the dominant class: the committed
-    ncu --set full capture (profiles/r1_traffic.json) gives the measured
-    excess over the algorithmic bytes of one call (neighbour gathers that miss
-    L2, the coarse-side pass); added to this run's per-launch algorithmic
-    bytes (the fused dots make the div(hV) bytes vary with the Arnoldi step).
-    None when no capture covers the class."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
-            t = json.load(f)[workload][kernel_class]
-        return algorithmic_per_launch + float(t["measured_bytes"]) - float(t["algorithmic_bytes"])
-    except Exception:
-        return None
+    """DRAM bytes per launch of the dominant kernel class, DERIVED from the
+    committed `ncu --set full` capture of this round (profiles/r2_traffic.json,
+    else r1): the capture's measured dram__bytes_read + write over its
+    algorithmic bytes, applied to this run's per-launch algorithmic bytes (the
+    class's launches differ in size, e.g. the coarse-face kernels).  Returns
+    (bytes or None, source)."""
+    for name in ("r2_traffic.json", "r1_traffic.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                t = json.load(f)[workload][kernel_class]
+            ratio = float(t["measured_bytes"]) / float(t["algorithmic_bytes"])
+            return algorithmic_per_launch * ratio, f"derived: profiles/{name} (ncu) ratio {ratio:.3f}"
+        except Exception:
+            continue
+    return None, "none"
 
 
 # ------------------------------------------------------------ CPU baseline
@@ -486,7 +489,9 @@ def main():
             "roofline": {"bound": "hbm", "kernel": classes[k_dom], "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "peak_kind": peak_kind,
-                         "traffic": traffic(args.workload, classes[k_dom], per_launch_bytes),
+                         "traffic": traffic(args.workload, classes[k_dom], per_launch_bytes)[0],
+                         "traffic_source": traffic(args.workload, classes[k_dom],
+                                                   per_launch_bytes)[1],
                          "bytes_per_launch": per_launch_bytes,
                          "ms_per_launch": per_launch_ms,
                          "share_of_step": ms_c[k_dom] / ms_total},
