@@ -260,6 +260,14 @@ int dg_halo_exchange(dg_ctx* ctx, double* field, int ncomp);
 long long dg_launch_count(void);
 int dg_profile_enable(int on);
 int dg_profile_read(double* ms /*6*/, double* bytes /*6*/, long long* count /*6*/);
+/* small-problem GMRES (device-resident Arnoldi scalars, the Givens loop of
+   orodg/krylov.py:86-96 on the device): host synchronisations taken by the
+   Arnoldi cycles so far and Arnoldi steps enqueued past a stopping step */
+int dg_arnoldi_stats(dg_ctx* ctx, long long* syncs, long long* wasted_steps);
+/* mode: 0 host-driven Arnoldi loop (two synchronisations per step), 1 device
+   scalars for small problems (default), 2 device scalars always, -1 the
+   DG_DEVARN environment default; multi-rank contexts always take mode 0 */
+int dg_set_arnoldi_mode(dg_ctx* ctx, int mode);
 
 /* ---- partitioner (orodg/partition.py:45-67): bounds has n_chunks+1 slots ---- */
 int dg_split_contiguous(const double* weights, long long n, int n_chunks, long long* bounds);

@@ -102,6 +102,8 @@ _SIGS = {
     "dg_launch_count": ([], LL),
     "dg_profile_enable": ([I], I),
     "dg_profile_read": ([P, P, P], I),
+    "dg_arnoldi_stats": ([P, C.POINTER(LL), C.POINTER(LL)], I),
+    "dg_set_arnoldi_mode": ([P, I], I),
 }
 
 PROFILE_CLASSES = ("explicit", "gradient", "div_hv", "multidot", "axpy", "other")

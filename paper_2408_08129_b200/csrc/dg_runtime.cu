@@ -112,6 +112,15 @@ struct dg_ctx {
   long long bj_gen = 0;
   LaunchInfo last{};
   Comm comm;
+  // device-resident Arnoldi scalars of the small-problem GMRES path
+  // (dcgs2_cycle_dev): state, its pinned read-back copy, and the Krylov
+  // counts of the previous time step's solves (the enqueue-ahead depth)
+  DevBuf<ArnState> arn;
+  ArnState* arn_host = nullptr;
+  std::vector<int> arn_pred;
+  int arn_ord = 0;
+  int arn_mode = -1;  // -1: DG_DEVARN (default 1), 0 host loop, 1 small problems, 2 always
+  long long arn_syncs = 0, arn_wasted = 0;
   long long scal() const { return (long long)n_tot * NP; }
   long long stat() const { return (long long)n_tot * V * NP; }
 };
@@ -631,6 +640,106 @@ int dcgs2_cycle(dg_ctx* c, double a_dt, const double* h, const double* hq, int m
   return DG_OK;
 }
 
+// The same cycle with the Arnoldi scalars on the device (k_arn_pre /
+// k_arn_post, dg_vector.cu): steps are enqueued `ahead` at a time with ONE
+// host synchronisation per chunk instead of two per step.  Steps enqueued
+// past the stopping step leave the scalar state untouched (the scalar
+// kernels return once `stop` is set) and only write basis slots >= done,
+// which the solution update never reads.  `ahead` is the Krylov count of the
+// same solve in the previous time step (c->arn_pred), so a steady run
+// synchronises about once per solve.
+bool devarn_mode(dg_ctx* c) {
+  static const int env0 = getenv("DG_DEVARN") ? atoi(getenv("DG_DEVARN")) : 1;
+  const int env = c->arn_mode >= 0 ? c->arn_mode : env0;
+  // large problems (separate dual-dot pass) keep the host loop: a step costs
+  // milliseconds there and a wasted one more than the synchronisations
+  return env != 0 && !c->comm.active() && (env == 2 || !sep_dots(c));
+}
+
+int dcgs2_cycle_dev(dg_ctx* c, double a_dt, const double* h, const double* hq, int m, int max_iter,
+                    double bn, double target, double beta, double* Vb, long long vs, Gm& st,
+                    std::vector<double>& y, int& done, int ahead) {
+  const long long n = (long long)c->n_el * c->NP;
+  double* z = c->sw.p;
+  CK(c->arn.alloc(1));
+  if (!c->arn_host) CK(cudaMallocHost(&c->arn_host, sizeof(ArnState)));
+  ArnState* A = c->arn.p;
+  CK(arn_init(c->stream, A, m, bn, target, beta, st.iterations, max_iter));
+  const ArnState& H = *c->arn_host;
+  int j = 0;
+  done = 0;
+  while (j < m) {
+    int K = std::max(1, std::min(ahead, m - j));
+    for (int jj = j; jj < j + K; ++jj) {
+      double* u = Vb + (size_t)jj * vs;
+      const int nvt = 2 * (jj + 2);
+      long long rows = 0;
+      if (sep_dots(c)) {
+        RET(helm_apply(c, a_dt, h, hq, u, z));
+        int r = 0;
+        CK(dual_dots(c->stream, n, jj, Vb, vs, z, u, c->gs_part.p, &r));
+        rows = r;
+      } else {
+        GsFuse gs{Vb, vs, jj, c->gs_part.p, 1};
+        RET(helm_apply(c, a_dt, h, hq, u, z, &gs));
+        rows = c->last.grid;
+      }
+      // few partial rows: the scalar kernel sums them itself (one launch
+      // instead of three)
+      if (rows <= 2048) {
+        CK(arn_pre(c->stream, A, jj, c->gs_part.p, (int)rows, c->coef_dev.p));
+      } else {
+        CK(reduce_rows(c->stream, c->gs_part.p, rows, nvt, c->partial.p, c->redout.p));
+        CK(arn_pre(c->stream, A, jj, c->redout.p, 0, c->coef_dev.p));
+      }
+      int nparts = 0;
+      CK(dcgs2_update_partials(c->stream, n, jj, Vb, vs, c->coef_dev.p, u, z,
+                               Vb + (size_t)(jj + 1) * vs, c->partial.p, &nparts));
+      CK(arn_post(c->stream, A, jj, c->partial.p, nparts));
+    }
+    CK(cudaMemcpyAsync(c->arn_host, A, sizeof(ArnState), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->arn_syncs += 1;
+    j += K;
+    if (H.stop) {
+      c->arn_wasted += j - H.steps_run;
+      break;
+    }
+    ahead = 3;  // the prediction was short: continue in small chunks
+  }
+  done = H.done;
+  for (int i = 0; i < H.steps_run; ++i) st.hist.push_back(H.hist[i]);
+  st.iterations = H.iterations;
+  if (H.breakdown) st.breakdown = 1;
+  if (!done) return DG_OK;
+  // least squares on the corrected Hbar, as dcgs2_cycle
+  std::vector<double> R((size_t)(m + 1) * m, 0.0), cs(m), sn(m), gg(done + 1, 0.0);
+  auto HB = [&](int i, int k) -> double { return H.Hb[(size_t)i * m + k]; };
+  auto RR = [&](int i, int k) -> double& { return R[(size_t)i * m + k]; };
+  gg[0] = beta;
+  for (int k = 0; k < done; ++k) {
+    for (int i = 0; i <= k + 1; ++i) RR(i, k) = HB(i, k);
+    for (int i = 0; i < k; ++i) {
+      const double t = cs[i] * RR(i, k) + sn[i] * RR(i + 1, k);
+      RR(i + 1, k) = -sn[i] * RR(i, k) + cs[i] * RR(i + 1, k);
+      RR(i, k) = t;
+    }
+    const double den = std::hypot(RR(k, k), RR(k + 1, k));
+    cs[k] = den != 0.0 ? RR(k, k) / den : 1.0;
+    sn[k] = den != 0.0 ? RR(k + 1, k) / den : 0.0;
+    RR(k, k) = den;
+    RR(k + 1, k) = 0.0;
+    gg[k + 1] = -sn[k] * gg[k];
+    gg[k] = cs[k] * gg[k];
+  }
+  for (int i = done - 1; i >= 0; --i) {
+    double t = gg[i];
+    for (int k = i + 1; k < done; ++k) t -= RR(i, k) * y[k];
+    y[i] = t / RR(i, i);
+  }
+  return DG_OK;
+}
+
 // right-preconditioned (pc: M = block-Jacobi inverse, krylov.py:56-66,105-109)
 int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const double* rhs, double* x,
           double tol, int restart, int max_iter, Gm& st, bool pc = false) {
@@ -655,6 +764,17 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const doubl
   // the CGS + selective re-orthogonalisation path
   static const bool cgs_env = getenv("DG_GMRES") && std::string(getenv("DG_GMRES")) == "cgs2";
   const bool dcgs2 = (fuse || sep) && !pc && !cgs_env;
+  const bool devarn = dcgs2 && m <= ARN_M && devarn_mode(c);
+  const int ord = c->arn_ord++;
+  const int pred = (devarn && ord < (int)c->arn_pred.size()) ? c->arn_pred[ord] : 0;
+  struct PredKeep {  // remember this solve's count for the next time step
+    dg_ctx* c; int ord; const Gm& st; bool on;
+    ~PredKeep() {
+      if (!on || ord >= 64) return;
+      if ((int)c->arn_pred.size() <= ord) c->arn_pred.resize(ord + 1, 0);
+      c->arn_pred[ord] = st.iterations;
+    }
+  } keep{c, ord, st, devarn};
   if (fuse || sep) {
     // one row of <= m + 1 dot partials per element-kernel warp (>= 1 element
     // each) and per coarse element
@@ -697,7 +817,13 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const doubl
     std::fill(g.begin(), g.end(), 0.0);
     g[0] = beta;
     int done = 0;
-    if (dcgs2) {
+    if (dcgs2 && devarn) {
+      // enqueue-ahead depth: what is left of the previous time step's count
+      // for this solve (first solves: a short chunk)
+      const int ahead = pred > st.iterations ? pred - st.iterations : (pred > 0 ? 3 : 4);
+      RET(dcgs2_cycle_dev(c, a_dt, h, hq, m, max_iter, bn, target, beta, Vb, vs, st, y, done,
+                          ahead));
+    } else if (dcgs2) {
       RET(dcgs2_cycle(c, a_dt, h, hq, m, max_iter, bn, target, beta, Vb, vs, st, g, y, done));
     }
     for (int j = 0; j < m && !dcgs2; ++j) {
@@ -1143,6 +1269,7 @@ int dg_ctx_destroy(dg_ctx* c) {
   c->hang.release();
   c->kind.release();
   if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->arn_host) cudaFreeHost(c->arn_host);
   c->comm.shutdown();
   delete c;
   return DG_OK;
@@ -1275,6 +1402,7 @@ int dg_gmres_helmholtz(dg_ctx* c, double a_dt, const double* h, const double* rh
 int dg_gmres_helmholtz_pc(dg_ctx* c, double a_dt, const double* h, const double* rhs, double* x,
                           double tol_rel, int restart, int max_iter, int precond,
                           dg_krylov_stats* stats, double* history, int history_cap) {
+  c->arn_ord = 0;
   RET(ensure_work(c));
   RET(halo(c, const_cast<double*>(h), 1));
   const double* hq = nullptr;
@@ -1300,6 +1428,7 @@ int dg_gmres_helmholtz_pc(dg_ctx* c, double a_dt, const double* h, const double*
 
 int dg_solve_implicit_stage(dg_ctx* c, const double* acc, const double* guess, double a_dt,
                             const dg_solve_cfg* cfg, double* iterate, dg_step_stats* stats) {
+  c->arn_ord = 0;
   RET(ensure_work(c));
   int nfp = 0;
   RET(solve_stage(c, acc, guess, a_dt, *cfg, iterate, stats, &nfp));
@@ -1310,6 +1439,7 @@ int dg_solve_implicit_stage(dg_ctx* c, const double* acc, const double* guess, d
 int dg_imex_step(dg_ctx* c, const double* U, double* U_out, double t, double dt,
                  const dg_solve_cfg* cfg, dg_step_stats* stats) {
   (void)t;
+  c->arn_ord = 0;
   RET(ensure_work(c));
   RET(ensure_states(c));
   const int d = c->dim, NP = c->NP, V = c->V;
@@ -1578,6 +1708,19 @@ int dg_dual_dots(dg_ctx* c, long long n, int nv, const double* V, long long vstr
 int dg_halo_exchange(dg_ctx* c, double* field, int ncomp) { return halo(c, field, ncomp); }
 
 long long dg_launch_count(void) { return prof().launches; }
+
+int dg_set_arnoldi_mode(dg_ctx* c, int mode) {
+  if (mode < -1 || mode > 2) return fail(DG_ERR_USAGE, "arnoldi mode must be -1, 0, 1 or 2");
+  c->arn_mode = mode;
+  c->arn_pred.clear();
+  return DG_OK;
+}
+
+int dg_arnoldi_stats(dg_ctx* c, long long* syncs, long long* wasted_steps) {
+  if (syncs) *syncs = c->arn_syncs;
+  if (wasted_steps) *wasted_steps = c->arn_wasted;
+  return DG_OK;
+}
 
 int dg_profile_enable(int on) {
   Profiler& p = prof();

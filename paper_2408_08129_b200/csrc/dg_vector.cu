@@ -943,6 +943,202 @@ cudaError_t reduce_rows(cudaStream_t st, const double* partials, long long nrows
   return cudaGetLastError();
 }
 
+// ---- device-resident DCGS2 Arnoldi scalars (ArnState, dg_vector.cuh) -------
+// One warp per kernel; every sum runs in the order of the host loop of
+// dcgs2_cycle (dg_runtime.cu), lane i owning row i of the O(j^2) products.
+__global__ void k_arn_init(ArnState* a, int m, double bn, double target, double beta,
+                           int iterations, int max_iter) {
+  const int t = threadIdx.x;
+  for (int i = t; i < (ARN_M + 1) * ARN_M; i += blockDim.x) {
+    a->Hb[i] = 0.0;
+    a->R[i] = 0.0;
+  }
+  for (int i = t; i < ARN_M; i += blockDim.x) {
+    a->cs[i] = 0.0;
+    a->sn[i] = 0.0;
+    a->hist[i] = 0.0;
+  }
+  for (int i = t; i <= ARN_M; i += blockDim.x) a->g[i] = i == 0 ? beta : 0.0;
+  if (t == 0) {
+    a->bn = bn;
+    a->target = target;
+    a->nb = 0.0;
+    a->m = m;
+    a->done = 0;
+    a->stop = 0;
+    a->breakdown = 0;
+    a->iterations = iterations;
+    a->max_iter = max_iter;
+    a->steps_run = 0;
+  }
+}
+
+// nrows > 0: `src` holds nrows partial rows of 2 (j + 2) columns (the fused
+// dots of the div(hV) kernel / the dual-dot pass); the block (1024 threads)
+// first sums them, warp w columns w, w + 32, ... with lane-strided rows and a
+// fixed warp tree (deterministic).  nrows == 0: `src` holds the reduced dots.
+__global__ void k_arn_pre(ArnState* a, int j, const double* __restrict__ src, int nrows,
+                          double* __restrict__ coefs) {
+  if (a->stop) return;
+  __shared__ double sdots[2 * (ARN_M + 2)];
+  const double* dots = src;
+  if (nrows > 0) {
+    const int ncols = 2 * (j + 2);
+    const int wl = threadIdx.x & 31, ww = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int col = ww; col < ncols; col += nw) {
+      double t = 0.0;
+      for (int r = wl; r < nrows; r += 32) t += src[(long long)r * ncols + col];
+      t = warp_sum(t);
+      if (wl == 0) sdots[col] = t;
+    }
+    __syncthreads();
+    dots = sdots;
+  }
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  const int m = a->m;
+  __shared__ double sv[ARN_M + 1], gv[ARN_M + 1];
+  __shared__ double sh_alpha, sh_st;
+  __shared__ int sh_brk;
+  if (lane < j) sv[lane] = dots[2 * lane + 1];
+  __syncwarp();
+  if (lane == 0) {
+    const double uu = dots[2 * j + 3];
+    double s2 = 0.0, st_ = 0.0;
+    for (int i = 0; i < j; ++i) {
+      s2 = __dadd_rn(s2, __dmul_rn(sv[i], sv[i]));  // (unfused, as the host loop rounds)
+      st_ = __dadd_rn(st_, __dmul_rn(sv[i], dots[2 * i]));
+    }
+    double alpha = 1.0;
+    int brk = 0;
+    if (j > 0) {
+      const double a2 = uu - s2;
+      if (!(a2 > 1e-20 * uu) || !isfinite(a2)) {
+        a->Hb[j * m + j - 1] = (a2 > 0.0 && isfinite(a2)) ? sqrt(a2) : 0.0;
+        brk = 1;
+      } else {
+        alpha = sqrt(a2);
+        a->Hb[j * m + j - 1] = alpha;
+      }
+    }
+    sh_alpha = alpha;
+    sh_st = st_;
+    sh_brk = brk;
+  }
+  __syncwarp();
+  // column j-1 of Hbar takes the re-orthogonalisation correction
+  if (j > 0 && lane < j) a->Hb[lane * m + j - 1] += sv[lane];
+  __syncwarp();
+  if (sh_brk) {
+    if (lane == 0) {
+      a->breakdown = 1;
+      a->stop = 1;
+    }
+    return;
+  }
+  const double alpha = sh_alpha;
+  // g = Hbar[0:j+1, 0:j] s
+  if (lane <= j) {
+    double t = 0.0;
+    for (int k = (lane - 1 > 0 ? lane - 1 : 0); k < j; ++k) t = __dadd_rn(t, __dmul_rn(a->Hb[lane * m + k], sv[k]));
+    gv[lane] = t;
+  }
+  __syncwarp();
+  double hv = 0.0;
+  if (lane < j) hv = (dots[2 * lane] - gv[lane]) / alpha;
+  if (lane == j) hv = ((dots[2 * j + 1] - sh_st) / alpha - gv[j]) / alpha;
+  if (lane <= j) {
+    a->Hb[lane * m + j] = hv;
+    if (lane < j) coefs[lane] = sv[lane];
+    coefs[j + lane] = gv[lane];
+    coefs[2 * j + 1 + lane] = hv;
+  }
+  if (lane == 0) {
+    coefs[3 * j + 2] = alpha;
+    const double zz = dots[2 * j];
+    a->nb = sqrt(fmax(zz, 0.0)) / alpha;
+  }
+}
+
+// nparts > 0: na2p holds the update kernel's per-CTA partials of |u'|^2
+// (summed here as k_reduce_cols would: lane-strided, fixed warp tree)
+__global__ void k_arn_post(ArnState* a, int j, const double* __restrict__ na2p, int nparts) {
+  if (a->stop || threadIdx.x >= 32) return;
+  double na2 = 0.0;
+  if (nparts > 0) {
+    for (int b = threadIdx.x; b < nparts; b += 32) na2 += na2p[b];
+    na2 = warp_sum(na2);
+  } else {
+    na2 = na2p[0];
+  }
+  if (threadIdx.x != 0) return;
+  const int m = a->m;
+  const double na = sqrt(na2);
+  a->Hb[(j + 1) * m + j] = na;
+  const bool happy = na <= 1e-14 * fmax(a->bn, a->nb);
+  a->iterations += 1;
+  a->steps_run += 1;
+  double* R = a->R;
+  for (int i = 0; i <= j + 1; ++i) R[i * m + j] = a->Hb[i * m + j];
+  for (int i = 0; i < j; ++i) {
+    const double t = __dadd_rn(__dmul_rn(a->cs[i], R[i * m + j]),
+                               __dmul_rn(a->sn[i], R[(i + 1) * m + j]));
+    R[(i + 1) * m + j] = __dadd_rn(__dmul_rn(-a->sn[i], R[i * m + j]),
+                                   __dmul_rn(a->cs[i], R[(i + 1) * m + j]));
+    R[i * m + j] = t;
+  }
+  const double den = hypot(R[j * m + j], R[(j + 1) * m + j]);
+  a->cs[j] = den != 0.0 ? R[j * m + j] / den : 1.0;
+  a->sn[j] = den != 0.0 ? R[(j + 1) * m + j] / den : 0.0;
+  R[j * m + j] = den;
+  R[(j + 1) * m + j] = 0.0;
+  a->g[j + 1] = -a->sn[j] * a->g[j];
+  a->g[j] = a->cs[j] * a->g[j];
+  a->done = j + 1;
+  const double est = fabs(a->g[j + 1]);
+  a->hist[j] = est / a->bn;
+  if (happy) {
+    a->breakdown = 1;
+    a->stop = 1;
+  }
+  if (est <= a->target || a->iterations >= a->max_iter) a->stop = 1;
+}
+
+cudaError_t arn_init(cudaStream_t st, ArnState* a, int m, double bn, double target, double beta,
+                     int iterations, int max_iter) {
+  if (m < 1 || m > ARN_M) return cudaErrorInvalidValue;
+  k_arn_init<<<1, 256, 0, st>>>(a, m, bn, target, beta, iterations, max_iter);
+  return cudaGetLastError();
+}
+
+cudaError_t arn_pre(cudaStream_t st, ArnState* a, int j, const double* src, int nrows,
+                    double* coefs) {
+  prof_begin(st);
+  k_arn_pre<<<1, nrows > 0 ? 1024 : 32, 0, st>>>(a, j, src, nrows, coefs);
+  prof_end(st, P_DOT, 8.0 * (nrows > 0 ? nrows : 1) * 2 * (j + 2), 1);
+  return cudaGetLastError();
+}
+
+cudaError_t arn_post(cudaStream_t st, ArnState* a, int j, const double* na2, int nparts) {
+  prof_begin(st);
+  k_arn_post<<<1, 32, 0, st>>>(a, j, na2, nparts);
+  prof_end(st, P_AXPY, 8.0 * (nparts > 0 ? nparts : 1), 1);
+  return cudaGetLastError();
+}
+
+// the update pass without its column reduction (arn_post sums the partials)
+cudaError_t dcgs2_update_partials(cudaStream_t st, long long n, int nv, const double* Q,
+                                  long long vstride, const double* coefs_dev, double* u,
+                                  const double* z, double* unext, double* partials, int* nparts) {
+  if (nv > 31 || nv < 0) return cudaErrorInvalidValue;
+  prof_begin(st);
+  int grid = RED_BLOCKS;
+  cudaError_t e = launch_dcgs2<31>(st, n, nv, Q, vstride, coefs_dev, u, z, unext, partials, &grid);
+  *nparts = grid;
+  prof_end(st, P_AXPY, 8.0 * n * (nv + 4), 1);
+  return e;
+}
+
 cudaError_t reduce_cols(cudaStream_t st, const double* partials, int nblocks, int ncols, double* out) {
   prof_begin(st);
   k_reduce_cols<<<(ncols + 7) / 8, 256, 0, st>>>(partials, nblocks, ncols, out);

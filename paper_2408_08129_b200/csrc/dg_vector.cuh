@@ -47,4 +47,30 @@ cudaError_t reduce_cols(cudaStream_t st, const double* partials, int nblocks, in
 cudaError_t reduce_rows(cudaStream_t st, const double* partials, long long nrows, int ncols,
                         double* tmp, double* out);
 
+// Device-resident scalar state of one DCGS2 Arnoldi cycle (restart m <= 31):
+// the small-problem GMRES path keeps Hbar, the running Givens QR and the
+// stopping tests on the device so that several Arnoldi steps are enqueued
+// per host synchronisation (dg_runtime.cu dcgs2_cycle_dev; the arithmetic
+// and its order are those of the host loop of dcgs2_cycle).
+constexpr int ARN_M = 31;
+struct ArnState {
+  double bn, target, nb;
+  double g[ARN_M + 1], cs[ARN_M], sn[ARN_M], hist[ARN_M];
+  double Hb[(ARN_M + 1) * ARN_M], R[(ARN_M + 1) * ARN_M];
+  int m, done, stop, breakdown, iterations, max_iter, steps_run, pad;
+};
+cudaError_t arn_init(cudaStream_t st, ArnState* a, int m, double bn, double target, double beta,
+                     int iterations, int max_iter);
+// step j, after the dual dots landed in dots[2 (j + 2)]: alpha, s, g, h ->
+// coefs (dcgs2_update layout), Hbar column j (and the correction of j-1)
+// (nrows > 0: src = nrows partial rows, summed by the kernel itself)
+cudaError_t arn_pre(cudaStream_t st, ArnState* a, int j, const double* src, int nrows,
+                    double* coefs);
+// step j, after the update: Hbar[j+1][j] = sqrt(|u'|^2), Givens, stop tests
+// (nparts > 0: na2 = the update kernel's per-CTA partials)
+cudaError_t arn_post(cudaStream_t st, ArnState* a, int j, const double* na2, int nparts);
+cudaError_t dcgs2_update_partials(cudaStream_t st, long long n, int nv, const double* Q,
+                                  long long vstride, const double* coefs_dev, double* u,
+                                  const double* z, double* unext, double* partials, int* nparts);
+
 }  // namespace dg

@@ -213,3 +213,38 @@ def test_pipelined_helmholtz_on_golden_cases():
             assert v["gm_iters"][0] == v["gm_iters"][1] and v["gm_x"] <= 1e-10, (name, v)
         if "step" in v:
             assert v["step_iters"][0] == v["step_iters"][1] and v["step"] <= 1e-11, (name, v)
+
+
+@pytest.mark.parametrize("name,steps", [("cfg2", 4), ("hang3d", 2), ("cfg1", 3)])
+def test_device_arnoldi_scalars(name, steps):
+    """The small-problem GMRES path keeps Hbar, the Givens QR and the stopping
+    tests on the device (k_arn_pre / k_arn_post; the Givens loop of
+    krylov.py:86-96) and enqueues Arnoldi steps ahead of ONE synchronisation
+    per chunk: same Krylov counts and the same states as the host-driven loop
+    (mode 0), far fewer synchronisations than two per Arnoldi step."""
+    from paper_2408_08129_b200.dgops import DGOperators
+    from paper_2408_08129_b200.imex import ImplicitSolveConfig, SplitOperators, ars222, imex_step
+    c = build(name)
+    ops = DGOperators(c.geom)
+    split = SplitOperators(ops, c.model, c.bcs, c.sponge)
+    ctx = split.ctx
+    cfg = ImplicitSolveConfig(krylov_tol=c.krylov_tol)
+    runs = {}
+    for mode in (0, 2):
+        assert ctx.lib.dg_set_arnoldi_mode(ctx.handle, mode) == 0
+        s0, w0 = C.c_longlong(), C.c_longlong()
+        ctx.lib.dg_arnoldi_stats(ctx.handle, C.byref(s0), C.byref(w0))
+        U, its = c.U, []
+        for k in range(steps):
+            U, st = imex_step(U, 0.5 * k, 0.5, ars222(), split, cfg)
+            its.append(list(st.krylov_iters))
+        s1, w1 = C.c_longlong(), C.c_longlong()
+        ctx.lib.dg_arnoldi_stats(ctx.handle, C.byref(s1), C.byref(w1))
+        runs[mode] = (U, its, s1.value - s0.value, w1.value - w0.value)
+    ctx.lib.dg_set_arnoldi_mode(ctx.handle, -1)
+    (Uh, ih, sh, _), (Ud, idv, sd, wd) = runs[0], runs[2]
+    assert ih == idv, (ih, idv)
+    assert rel(Ud, Uh) <= 1e-13
+    total = sum(sum(v) for v in idv)
+    assert sh == 0 and 0 < sd <= max(total // 2, 2 * sum(len(v) for v in idv) + 2), (sd, total)
+    print(f"{name}: {total} Arnoldi steps, {sd} synchronisations, {wd} steps enqueued past a stop")

@@ -3,7 +3,7 @@
 #   tools/gpu_round.sh [tests|bench|launches|full|all]...
 # tests    -> gpurun_out/pytest.log, parity.json (achieved errors), smoke.log
 # bench    -> gpurun_out/bench.json (+ bench.err)
-# small    -> gpurun_out/small_<cfg>_g<0|1>.json (cfg2 / cfg1 lines, graph mode on / off)
+# small    -> gpurun_out/small_<cfg>_g<0|1>.json (cfg2 / cfg1 lines, device Arnoldi scalars on / off)
 # launches -> gpurun_out/launches.csv (ncu launch list of one bench step)
 # full     -> gpurun_out/helm.ncu-rep, expl.ncu-rep (ncu --set full at cfg4 size:
 #             the first kernels of one GMRES solve; the explicit operator)
@@ -26,9 +26,9 @@ fi
 if has small; then
   for w in cfg2 cfg1; do
     for gm in 1 0; do
-      DG_GRAPH=$gm timeout 600 python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline \
+      DG_DEVARN=$gm timeout 600 python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline \
         > gpurun_out/small_${w}_g$gm.json 2> gpurun_out/small_${w}_g$gm.err
-      echo "small $w graph=$gm rc $?"; tail -c 300 gpurun_out/small_${w}_g$gm.json
+      echo "small $w devarn=$gm rc $?"; tail -c 300 gpurun_out/small_${w}_g$gm.json
     done
   done
 fi
