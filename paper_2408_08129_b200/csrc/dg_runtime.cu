@@ -666,7 +666,7 @@ int dcgs2_cycle_dev(dg_ctx* c, double a_dt, const double* h, const double* hq, i
   ArnState* A = c->arn.p;
   CK(arn_init(c->stream, A, m, bn, target, beta, st.iterations, max_iter));
   const ArnState& H = *c->arn_host;
-  int j = 0;
+  int j = 0, chunks = 0;
   done = 0;
   while (j < m) {
     int K = std::max(1, std::min(ahead, m - j));
@@ -705,7 +705,10 @@ int dcgs2_cycle_dev(dg_ctx* c, double a_dt, const double* h, const double* hq, i
       c->arn_wasted += j - H.steps_run;
       break;
     }
-    ahead = 3;  // the prediction was short: continue in small chunks
+    // the prediction was short (counts drift by a step or two between time
+    // steps): single steps first -- a synchronisation is cheaper than an
+    // Arnoldi step enqueued past the stop -- then small chunks
+    ahead = ++chunks <= 3 ? 1 : 3;
   }
   done = H.done;
   for (int i = 0; i < H.steps_run; ++i) st.hist.push_back(H.hist[i]);
@@ -820,7 +823,8 @@ int gmres(dg_ctx* c, double a_dt, const double* h, const double* hq, const doubl
     if (dcgs2 && devarn) {
       // enqueue-ahead depth: what is left of the previous time step's count
       // for this solve (first solves: a short chunk)
-      const int ahead = pred > st.iterations ? pred - st.iterations : (pred > 0 ? 3 : 4);
+      // (one short of the count: the last step is confirmed by a read-back)
+      const int ahead = pred > st.iterations + 1 ? pred - st.iterations - 1 : (pred > 0 ? 1 : 4);
       RET(dcgs2_cycle_dev(c, a_dt, h, hq, m, max_iter, bn, target, beta, Vb, vs, st, y, done,
                           ahead));
     } else if (dcgs2) {

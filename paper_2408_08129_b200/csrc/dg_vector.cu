@@ -949,10 +949,7 @@ cudaError_t reduce_rows(cudaStream_t st, const double* partials, long long nrows
 __global__ void k_arn_init(ArnState* a, int m, double bn, double target, double beta,
                            int iterations, int max_iter) {
   const int t = threadIdx.x;
-  for (int i = t; i < (ARN_M + 1) * ARN_M; i += blockDim.x) {
-    a->Hb[i] = 0.0;
-    a->R[i] = 0.0;
-  }
+  for (int i = t; i < (ARN_M + 1) * ARN_M; i += blockDim.x) a->Hb[i] = 0.0;
   for (int i = t; i < ARN_M; i += blockDim.x) {
     a->cs[i] = 0.0;
     a->sn[i] = 0.0;
@@ -977,13 +974,17 @@ __global__ void k_arn_init(ArnState* a, int m, double bn, double target, double 
 // dots of the div(hV) kernel / the dual-dot pass); the block (1024 threads)
 // first sums them, warp w columns w, w + 32, ... with lane-strided rows and a
 // fixed warp tree (deterministic).  nrows == 0: `src` holds the reduced dots.
+// Hbar is staged in shared memory by the whole block while the rows are
+// summed, so the serial part runs out of shared memory only.
 __global__ void k_arn_pre(ArnState* a, int j, const double* __restrict__ src, int nrows,
                           double* __restrict__ coefs) {
   if (a->stop) return;
   __shared__ double sdots[2 * (ARN_M + 2)];
-  const double* dots = src;
+  __shared__ double sH[(ARN_M + 1) * ARN_M];
+  const int m = a->m;
+  for (int i = threadIdx.x; i < (j + 1) * m; i += blockDim.x) sH[i] = a->Hb[i];
+  const int ncols = 2 * (j + 2);
   if (nrows > 0) {
-    const int ncols = 2 * (j + 2);
     const int wl = threadIdx.x & 31, ww = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int col = ww; col < ncols; col += nw) {
       double t = 0.0;
@@ -991,12 +992,13 @@ __global__ void k_arn_pre(ArnState* a, int j, const double* __restrict__ src, in
       t = warp_sum(t);
       if (wl == 0) sdots[col] = t;
     }
-    __syncthreads();
-    dots = sdots;
+  } else {
+    for (int i = threadIdx.x; i < ncols; i += blockDim.x) sdots[i] = src[i];
   }
+  __syncthreads();
   if (threadIdx.x >= 32) return;
+  const double* dots = sdots;
   const int lane = threadIdx.x;
-  const int m = a->m;
   __shared__ double sv[ARN_M + 1], gv[ARN_M + 1];
   __shared__ double sh_alpha, sh_st;
   __shared__ int sh_brk;
@@ -1013,21 +1015,27 @@ __global__ void k_arn_pre(ArnState* a, int j, const double* __restrict__ src, in
     int brk = 0;
     if (j > 0) {
       const double a2 = uu - s2;
+      double hjj;
       if (!(a2 > 1e-20 * uu) || !isfinite(a2)) {
-        a->Hb[j * m + j - 1] = (a2 > 0.0 && isfinite(a2)) ? sqrt(a2) : 0.0;
+        hjj = (a2 > 0.0 && isfinite(a2)) ? sqrt(a2) : 0.0;
         brk = 1;
       } else {
         alpha = sqrt(a2);
-        a->Hb[j * m + j - 1] = alpha;
+        hjj = alpha;
       }
+      sH[j * m + j - 1] = hjj;
+      a->Hb[j * m + j - 1] = hjj;
     }
     sh_alpha = alpha;
     sh_st = st_;
     sh_brk = brk;
   }
-  __syncwarp();
   // column j-1 of Hbar takes the re-orthogonalisation correction
-  if (j > 0 && lane < j) a->Hb[lane * m + j - 1] += sv[lane];
+  if (j > 0 && lane < j) {
+    const double v = sH[lane * m + j - 1] + sv[lane];
+    sH[lane * m + j - 1] = v;
+    a->Hb[lane * m + j - 1] = v;
+  }
   __syncwarp();
   if (sh_brk) {
     if (lane == 0) {
@@ -1040,7 +1048,8 @@ __global__ void k_arn_pre(ArnState* a, int j, const double* __restrict__ src, in
   // g = Hbar[0:j+1, 0:j] s
   if (lane <= j) {
     double t = 0.0;
-    for (int k = (lane - 1 > 0 ? lane - 1 : 0); k < j; ++k) t = __dadd_rn(t, __dmul_rn(a->Hb[lane * m + k], sv[k]));
+    for (int k = (lane - 1 > 0 ? lane - 1 : 0); k < j; ++k)
+      t = __dadd_rn(t, __dmul_rn(sH[lane * m + k], sv[k]));
     gv[lane] = t;
   }
   __syncwarp();
@@ -1061,47 +1070,54 @@ __global__ void k_arn_pre(ArnState* a, int j, const double* __restrict__ src, in
 }
 
 // nparts > 0: na2p holds the update kernel's per-CTA partials of |u'|^2
-// (summed here as k_reduce_cols would: lane-strided, fixed warp tree)
+// (summed here as k_reduce_cols would: lane-strided, fixed warp tree).  One
+// warp: the lanes stage column j of Hbar and the rotations in shared memory
+// (one round trip), lane 0 runs the dependent Givens chain from there.
 __global__ void k_arn_post(ArnState* a, int j, const double* __restrict__ na2p, int nparts) {
   if (a->stop || threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  const int m = a->m;
+  __shared__ double col[ARN_M + 2], cs[ARN_M + 1], sn[ARN_M + 1];
+  if (lane <= j) col[lane] = a->Hb[lane * m + j];
+  if (lane < j) {
+    cs[lane] = a->cs[lane];
+    sn[lane] = a->sn[lane];
+  }
+  const double bn = a->bn, nb = a->nb, target = a->target, gj = a->g[j];
+  const int it0 = a->iterations, max_iter = a->max_iter, steps0 = a->steps_run;
   double na2 = 0.0;
   if (nparts > 0) {
-    for (int b = threadIdx.x; b < nparts; b += 32) na2 += na2p[b];
+    for (int b = lane; b < nparts; b += 32) na2 += na2p[b];
     na2 = warp_sum(na2);
   } else {
     na2 = na2p[0];
   }
-  if (threadIdx.x != 0) return;
-  const int m = a->m;
+  __syncwarp();
+  if (lane != 0) return;
   const double na = sqrt(na2);
   a->Hb[(j + 1) * m + j] = na;
-  const bool happy = na <= 1e-14 * fmax(a->bn, a->nb);
-  a->iterations += 1;
-  a->steps_run += 1;
-  double* R = a->R;
-  for (int i = 0; i <= j + 1; ++i) R[i * m + j] = a->Hb[i * m + j];
+  col[j + 1] = na;
+  const bool happy = na <= 1e-14 * fmax(bn, nb);
   for (int i = 0; i < j; ++i) {
-    const double t = __dadd_rn(__dmul_rn(a->cs[i], R[i * m + j]),
-                               __dmul_rn(a->sn[i], R[(i + 1) * m + j]));
-    R[(i + 1) * m + j] = __dadd_rn(__dmul_rn(-a->sn[i], R[i * m + j]),
-                                   __dmul_rn(a->cs[i], R[(i + 1) * m + j]));
-    R[i * m + j] = t;
+    const double t = __dadd_rn(__dmul_rn(cs[i], col[i]), __dmul_rn(sn[i], col[i + 1]));
+    col[i + 1] = __dadd_rn(__dmul_rn(-sn[i], col[i]), __dmul_rn(cs[i], col[i + 1]));
+    col[i] = t;
   }
-  const double den = hypot(R[j * m + j], R[(j + 1) * m + j]);
-  a->cs[j] = den != 0.0 ? R[j * m + j] / den : 1.0;
-  a->sn[j] = den != 0.0 ? R[(j + 1) * m + j] / den : 0.0;
-  R[j * m + j] = den;
-  R[(j + 1) * m + j] = 0.0;
-  a->g[j + 1] = -a->sn[j] * a->g[j];
-  a->g[j] = a->cs[j] * a->g[j];
+  const double den = hypot(col[j], col[j + 1]);
+  const double c = den != 0.0 ? col[j] / den : 1.0;
+  const double sj = den != 0.0 ? col[j + 1] / den : 0.0;
+  a->cs[j] = c;
+  a->sn[j] = sj;
+  const double g1 = -sj * gj;
+  a->g[j + 1] = g1;
+  a->g[j] = c * gj;
   a->done = j + 1;
-  const double est = fabs(a->g[j + 1]);
-  a->hist[j] = est / a->bn;
-  if (happy) {
-    a->breakdown = 1;
-    a->stop = 1;
-  }
-  if (est <= a->target || a->iterations >= a->max_iter) a->stop = 1;
+  a->iterations = it0 + 1;
+  a->steps_run = steps0 + 1;
+  const double est = fabs(g1);
+  a->hist[j] = est / bn;
+  if (happy) a->breakdown = 1;
+  if (happy || est <= target || it0 + 1 >= max_iter) a->stop = 1;
 }
 
 cudaError_t arn_init(cudaStream_t st, ArnState* a, int m, double bn, double target, double beta,

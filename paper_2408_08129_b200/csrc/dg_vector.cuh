@@ -56,7 +56,7 @@ constexpr int ARN_M = 31;
 struct ArnState {
   double bn, target, nb;
   double g[ARN_M + 1], cs[ARN_M], sn[ARN_M], hist[ARN_M];
-  double Hb[(ARN_M + 1) * ARN_M], R[(ARN_M + 1) * ARN_M];
+  double Hb[(ARN_M + 1) * ARN_M];
   int m, done, stop, breakdown, iterations, max_iter, steps_run, pad;
 };
 cudaError_t arn_init(cudaStream_t st, ArnState* a, int m, double bn, double target, double beta,
