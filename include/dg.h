@@ -253,6 +253,18 @@ int dg_ctx_set_comm_loopback(dg_ctx* ctx, int group, int rank, int nranks,
                              const int32_t* send_counts, const int32_t* send_elems,
                              const int32_t* recv_counts);
 int dg_halo_exchange(dg_ctx* ctx, double* field, int ncomp);
+/* face-row halo plans of the Helmholtz pair ("halo face-trace
+   exchange"; the reference ships whole ghost leaves, orodg/partition.py:68-99
+   + parallel.py): per field layout `which` (0 scalar nodal x: (n_tot, n^d),
+   1 psi: (n_tot, 2d, n^(d-1)), 2 V traces: (n_tot, 2(d-1)+2d, n^(d-1))) the
+   offsets in doubles of the values sent to / received from each peer rank,
+   grouped by peer, both sides in the same (element, face, point) order.
+   Every rank sets all three (possibly empty) after dg_ctx_set_comm*. */
+int dg_ctx_set_halo_rows(dg_ctx* ctx, int which, const int64_t* send_counts /*nranks*/,
+                         const int64_t* send_idx, const int64_t* recv_counts /*nranks*/,
+                         const int64_t* recv_idx);
+/* doubles this rank has sent in halo exchanges since creation / the last reset */
+int dg_halo_stats(dg_ctx* ctx, long long* values_sent, int reset);
 
 /* ---- instrumentation (no reference counterpart; orodg/timing.py is host-only) ----
    launches of libdg kernels since load; optional per-class CUDA-event timing

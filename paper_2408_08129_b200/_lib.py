@@ -95,6 +95,8 @@ _SIGS = {
     "dg_ctx_set_comm": ([P, P, I, I, P, P, P], I),
     "dg_ctx_set_comm_loopback": ([P, I, I, I, P, P, P], I),
     "dg_halo_exchange": ([P, P, I], I),
+    "dg_ctx_set_halo_rows": ([P, I, P, P, P, P], I),
+    "dg_halo_stats": ([P, C.POINTER(LL), I], I),
     "dg_max_abs_ratio": ([P, P, I, I, P, P], I),
     "dg_helmholtz_prepare": ([P, P], I),
     "dg_helmholtz_apply_prepared": ([P, D, P, P, P], I),

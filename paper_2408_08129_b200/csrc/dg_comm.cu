@@ -37,6 +37,20 @@ __global__ void k_unpack(double* __restrict__ field, long long estride, int ncom
   }
 }
 
+// face-row plans: buf[k] = field[idx[k]] and field[idx[k]] = buf[k]
+__global__ void k_pack_idx(const double* __restrict__ field, const long long* __restrict__ idx,
+                           long long n, double* __restrict__ buf) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride)
+    buf[k] = field[idx[k]];
+}
+__global__ void k_unpack_idx(double* __restrict__ field, const long long* __restrict__ idx,
+                             long long n, const double* __restrict__ buf) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride)
+    field[idx[k]] = buf[k];
+}
+
 #define NCCK(call)                                                    \
   do {                                                                \
     ncclResult_t _r = (call);                                         \
@@ -76,6 +90,7 @@ struct LoopGroup {
   long long gen = 0;
   std::vector<const double*> sendbuf;
   std::vector<std::vector<int>> send_off;
+  std::vector<std::vector<long long>> row_send_off[Comm::N_ROW_PLANS];
   std::vector<cudaEvent_t> ev_pack, ev_copied;
   std::vector<std::vector<double>> slots;
   std::vector<long long> n_el;
@@ -139,6 +154,7 @@ bool Comm::init_loopback(int group, int rank, int nranks, const int32_t* send_co
       slot->n = nranks;
       slot->sendbuf.assign(nranks, nullptr);
       slot->send_off.assign(nranks, {});
+      for (auto& r : slot->row_send_off) r.assign(nranks, {});
       slot->ev_pack.assign(nranks, nullptr);
       slot->ev_copied.assign(nranks, nullptr);
       slot->slots.assign(nranks, {});
@@ -176,7 +192,10 @@ bool Comm::init_loopback(int group, int rank, int nranks, const int32_t* send_co
 }
 
 bool Comm::ensure_bufs(size_t per) {
-  const size_t need = std::max((size_t)n_send_, (size_t)(n_tot_ - n_el_)) * per;
+  return ensure_cap(std::max((size_t)n_send_, (size_t)(n_tot_ - n_el_)) * per);
+}
+
+bool Comm::ensure_cap(size_t need) {
   if (need > buf_cap_) {
     if (loop_) CUCK(cudaDeviceSynchronize());  // peers may still read the old buffer
     if (sendbuf_) cudaFree(sendbuf_);
@@ -315,6 +334,96 @@ bool Comm::exchange(double* field, int ncomp, int np, cudaStream_t st, long long
   return true;
 }
 
+bool Comm::set_rows(int which, const int64_t* send_counts, const int64_t* send_idx,
+                    const int64_t* recv_counts, const int64_t* recv_idx) {
+  if (which < 0 || which >= N_ROW_PLANS) {
+    err_ = "face-row plan index out of range";
+    return false;
+  }
+  if (nranks_ <= 1) return true;
+  RowPlan& R = rows_[which];
+  R.send_off.assign(nranks_ + 1, 0);
+  R.recv_off.assign(nranks_ + 1, 0);
+  for (int p = 0; p < nranks_; ++p) {
+    R.send_off[p + 1] = R.send_off[p] + send_counts[p];
+    R.recv_off[p + 1] = R.recv_off[p] + recv_counts[p];
+  }
+  R.n_send = R.send_off[nranks_];
+  R.n_recv = R.recv_off[nranks_];
+  if (R.d_send_idx) cudaFree(R.d_send_idx);
+  if (R.d_recv_idx) cudaFree(R.d_recv_idx);
+  R.d_send_idx = R.d_recv_idx = nullptr;
+  if (R.n_send > 0) {
+    CUCK(cudaMalloc(&R.d_send_idx, R.n_send * sizeof(long long)));
+    CUCK(cudaMemcpy(R.d_send_idx, send_idx, R.n_send * sizeof(long long), cudaMemcpyHostToDevice));
+  }
+  if (R.n_recv > 0) {
+    CUCK(cudaMalloc(&R.d_recv_idx, R.n_recv * sizeof(long long)));
+    CUCK(cudaMemcpy(R.d_recv_idx, recv_idx, R.n_recv * sizeof(long long), cudaMemcpyHostToDevice));
+  }
+  if (loop_) loop_->row_send_off[which][rank_] = R.send_off;
+  R.ready = true;
+  return true;
+}
+
+bool Comm::exchange_rows(double* field, int which, cudaStream_t st) {
+  if (nranks_ <= 1) return true;
+  RowPlan& R = rows_[which];
+  if (!R.ready) {
+    err_ = "face-row plan not set";
+    return false;
+  }
+  const size_t need = (size_t)std::max(R.n_send, R.n_recv);
+  auto grid_for = [](long long n) { return (int)std::min<long long>((n + 255) / 256, 4096); };
+  if (loop_) {
+    LoopGroup* G = loop_;
+    for (int q = 0; q < nranks_; ++q)
+      if (q != rank_) CUCK(cudaStreamWaitEvent(st, G->ev_copied[q], 0));
+    if (!ensure_cap(need)) return false;
+    if (R.n_send > 0) {
+      k_pack_idx<<<grid_for(R.n_send), 256, 0, st>>>(field, R.d_send_idx, R.n_send, sendbuf_);
+      CUCK(cudaGetLastError());
+    }
+    CUCK(cudaEventRecord(G->ev_pack[rank_], st));
+    G->sendbuf[rank_] = sendbuf_;
+    G->barrier();
+    for (int q = 0; q < nranks_; ++q) {
+      const long long cnt = R.recv_off[q + 1] - R.recv_off[q];
+      if (q == rank_ || cnt == 0) continue;
+      CUCK(cudaStreamWaitEvent(st, G->ev_pack[q], 0));
+      CUCK(cudaMemcpyAsync(recvbuf_ + R.recv_off[q],
+                           G->sendbuf[q] + G->row_send_off[which][q][rank_],
+                           (size_t)cnt * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
+    CUCK(cudaEventRecord(G->ev_copied[rank_], st));
+    G->barrier();
+    if (R.n_recv > 0) {
+      k_unpack_idx<<<grid_for(R.n_recv), 256, 0, st>>>(field, R.d_recv_idx, R.n_recv, recvbuf_);
+      CUCK(cudaGetLastError());
+    }
+    return true;
+  }
+  if (!ensure_cap(need)) return false;
+  if (R.n_send > 0) {
+    k_pack_idx<<<grid_for(R.n_send), 256, 0, st>>>(field, R.d_send_idx, R.n_send, sendbuf_);
+    CUCK(cudaGetLastError());
+  }
+  ncclComm_t c = (ncclComm_t)comm_;
+  NCCK(ncclGroupStart());
+  for (int p = 0; p < nranks_; ++p) {
+    if (p == rank_) continue;
+    const long long ns = R.send_off[p + 1] - R.send_off[p], nr = R.recv_off[p + 1] - R.recv_off[p];
+    if (ns > 0) NCCK(ncclSend(sendbuf_ + R.send_off[p], (size_t)ns, ncclDouble, p, c, st));
+    if (nr > 0) NCCK(ncclRecv(recvbuf_ + R.recv_off[p], (size_t)nr, ncclDouble, p, c, st));
+  }
+  NCCK(ncclGroupEnd());
+  if (R.n_recv > 0) {
+    k_unpack_idx<<<grid_for(R.n_recv), 256, 0, st>>>(field, R.d_recv_idx, R.n_recv, recvbuf_);
+    CUCK(cudaGetLastError());
+  }
+  return true;
+}
+
 bool Comm::allreduce_sum(double* dev, int n, cudaStream_t st) {
   if (nranks_ <= 1) return true;
   if (loop_) return loop_reduce(dev, n, st, 0);
@@ -376,6 +485,11 @@ void Comm::shutdown() {
   if (sendbuf_) cudaFree(sendbuf_);
   if (recvbuf_) cudaFree(recvbuf_);
   if (scratch_) cudaFree(scratch_);
+  for (auto& R : rows_) {
+    if (R.d_send_idx) cudaFree(R.d_send_idx);
+    if (R.d_recv_idx) cudaFree(R.d_recv_idx);
+    R = RowPlan{};
+  }
   d_send_elems_ = nullptr;
   sendbuf_ = recvbuf_ = scratch_ = nullptr;
   buf_cap_ = 0;

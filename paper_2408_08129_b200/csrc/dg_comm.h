@@ -32,6 +32,22 @@ class Comm {
                      const int32_t* send_elems, const int32_t* recv_counts, int n_el, int n_tot);
   bool active() const { return nranks_ > 1; }
   bool exchange(double* field, int ncomp, int np, cudaStream_t st, long long estride = -1);
+  // face-row plans (SURVEY.md §8e "halo face-trace exchange"): instead of
+  // whole ghost elements, only the values the owned elements' faces read --
+  // the ghost's nodal face values of x, its psi row and (coarse parents) its
+  // V trace slots on the shared face.  `which` names the field layout (0 x,
+  // 1 psi, 2 trV); the index lists are offsets in doubles into the local
+  // field, grouped by peer rank in the same (element, face) order on both
+  // sides.  Every rank sets every plan (possibly empty) before its first use.
+  static constexpr int N_ROW_PLANS = 3;
+  bool set_rows(int which, const int64_t* send_counts, const int64_t* send_idx,
+                const int64_t* recv_counts, const int64_t* recv_idx);
+  bool has_rows() const { return rows_[0].ready && rows_[1].ready && rows_[2].ready; }
+  bool exchange_rows(double* field, int which, cudaStream_t st);
+  // doubles sent by this rank: per exchange_rows(which), and per whole-element
+  // exchange of one value per node (accounting for tests / DESIGN.md)
+  long long row_send_values(int which) const { return rows_[which].n_send; }
+  long long elem_send_count() const { return n_send_; }
   bool allreduce_sum(double* dev, int n, cudaStream_t st);
   bool allreduce_max(double* dev, int n, cudaStream_t st);
   bool allreduce_minloc(double loc[4], cudaStream_t st);  // (v0, i0, v1, i1) global min
@@ -45,6 +61,7 @@ class Comm {
   bool init_plan(int rank, int nranks, const int32_t* send_counts, const int32_t* send_elems,
                  const int32_t* recv_counts, int n_el, int n_tot);
   bool ensure_bufs(size_t per);
+  bool ensure_cap(size_t need_values);
   bool loop_reduce(double* dev, int n, cudaStream_t st, int op);
   int rank_ = 0, nranks_ = 1, n_el_ = 0, n_tot_ = 0;
   long long offset_ = 0;
@@ -55,6 +72,13 @@ class Comm {
   double* recvbuf_ = nullptr;
   size_t buf_cap_ = 0;
   double* scratch_ = nullptr;
+  struct RowPlan {
+    bool ready = false;
+    long long n_send = 0, n_recv = 0;
+    std::vector<long long> send_off, recv_off;  // per-peer prefix sums
+    long long* d_send_idx = nullptr;
+    long long* d_recv_idx = nullptr;
+  } rows_[N_ROW_PLANS];
   std::string err_;
 };
 

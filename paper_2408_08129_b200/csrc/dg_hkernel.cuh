@@ -162,6 +162,37 @@ __device__ __forceinline__ void face_nplus(const GeoConst& gc, const ElemGeo<D>&
   }
 }
 
+// 1/2 ws n+ directly: the normal's magnitude cancels in ws n+ = fw |nt| nt/|nt|,
+// so the flux-trace pair (which only ever uses the product) needs neither the
+// square root nor the division of face_nplus -- a rounding-level change
+#ifndef DG_HK_NONORM
+#define DG_HK_NONORM 1
+#endif
+template <int D, int N, int AX>
+__device__ __forceinline__ void face_half_wn(const GeoConst& gc, const ElemGeo<D>& g, int side,
+                                             double fw, double omh_edge, const double* dh,
+                                             double hw[D]) {
+#pragma unroll
+  for (int a = 0; a < D; ++a) hw[a] = 0.0;
+  const double hfw = 0.5 * fw;
+  if constexpr (AX < D - 1) {
+    const double zzv = g.s[D - 1] * omh_edge;
+    const double mag = (D == 2) ? zzv : g.s[1 - AX] * zzv;
+    hw[AX] = hfw * fabs(mag);
+  } else {
+    const double top = (D == 2) ? g.s[0] : g.s[0] * g.s[1];
+    hw[D - 1] = hfw * top;
+    if (!gc.terrain) return;
+    const double decay = 1.0 - (g.lo[D - 1] + g.s[D - 1] * (double)side) * gc.inv_ztop;
+    if constexpr (D == 2) {
+      hw[0] = hfw * (-dh[0] * g.s[0] * decay);
+    } else {
+      hw[0] = hfw * (-g.s[1] * dh[0] * g.s[0] * decay);
+      hw[1] = hfw * (-g.s[0] * dh[1] * g.s[1] * decay);
+    }
+  }
+}
+
 // the contravariant metric rows of a Gauss point of the lane's column
 // (geometry.py:204-238): c[bx][a] = ctrv[bx][a]; det is z-independent
 template <int D, int N>
@@ -349,6 +380,7 @@ __device__ __forceinline__ void hgrad_body(const KParams<N>& P, const Tab<N>& TS
   // p_own (wall), 0 (far field, homogeneous); coarse side precomputed
   double flv[2 * (D - 1)];  // vertical faces: the AX component only
   double flz[2][D];         // z faces
+  const double wface = (D == 2) ? TS.qw[c] : TS.qw[c / N] * TS.qw[c % N];  // face point weight
   auto face = [&](auto ax_c, auto side_c) {
     constexpr int AX = decltype(ax_c)::value;
     constexpr int side = decltype(side_c)::value;
@@ -366,16 +398,19 @@ __device__ __forceinline__ void hgrad_body(const KParams<N>& P, const Tab<N>& TS
 #pragma unroll
       for (int a = 0; a < D; ++a) fl[a] = cf ? mesh.cflux[((long long)nf[f] * D + a) * NC + c] : 0.0;
     } else {
+#if DG_HK_NONORM
+      face_half_wn<D, N, AX>(P.gc, g, side, wface, (AX < D - 1) ? edge(f) : 1.0, cd.dh, hw);
+#else
       double n[D], ws;
       face_nplus<D, N, AX>(P.gc, g, side, c, TS, (AX < D - 1) ? edge(f) : 1.0, cd.dh, n, ws);
+#pragma unroll
+      for (int a = 0; a < D; ++a) hw[a] = (0.5 * ws) * n[a];
+#endif
       const double px = (kd == KIND_WALL) ? to : (kd == KIND_FARFIELD ? 0.0 : P.alpha * tn[f]);
       const double ph = to + px;
       const double sg = side ? 1.0 : -1.0;
 #pragma unroll
-      for (int a = 0; a < D; ++a) {
-        hw[a] = (0.5 * ws) * n[a];
-        fl[a] = sg * (hw[a] * ph);
-      }
+      for (int a = 0; a < D; ++a) fl[a] = sg * (hw[a] * ph);
     }
     // (a wall's mirrored ghost cancels the div(hV) flux: psi = 0 there, so
     // H2 sums psi + pin uniformly over conforming, wall and far-field faces)
@@ -403,7 +438,7 @@ __device__ __forceinline__ void hgrad_body(const KParams<N>& P, const Tab<N>& TS
   // ---- volume: G_bx,k = ctrv[bx][k] p wq; bx < d-1 through the tile
   double Zc[D][N];
   const double det = col_det<D>(g, cd.omh);
-  const double wcol = (D == 3) ? TS.qw[c / N] * TS.qw[c % N] : TS.qw[c];
+  const double wcol = wface;
   {
     double Gz[D][N];
 #pragma unroll

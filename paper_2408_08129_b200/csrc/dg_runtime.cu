@@ -118,6 +118,7 @@ struct dg_ctx {
   DevBuf<ArnState> arn;
   ArnState* arn_host = nullptr;
   std::vector<int> arn_pred;
+  long long halo_values = 0;  // doubles this rank has sent in halo exchanges
   int arn_ord = 0;
   int arn_mode = -1;  // -1: DG_DEVARN (default 1), 0 host loop, 1 small problems, 2 always
   long long arn_syncs = 0, arn_wasted = 0;
@@ -153,6 +154,7 @@ int reduce_read(dg_ctx* c, double* dev, int n, double* host) {
 int halo(dg_ctx* c, double* field, int ncomp) {
   if (!c->comm.active()) return DG_OK;
   if (!c->comm.exchange(field, ncomp, c->NP, c->stream)) return fail(DG_ERR_COMM, c->comm.error());
+  c->halo_values += c->comm.elem_send_count() * (long long)ncomp * c->NP;
   return DG_OK;
 }
 
@@ -361,6 +363,25 @@ bool quad_mode(dg_ctx* c) {
 int halo_elems(dg_ctx* c, double* field, int per_elem) {
   if (!c->comm.active()) return DG_OK;
   if (!c->comm.exchange(field, 1, per_elem, c->stream)) return fail(DG_ERR_COMM, c->comm.error());
+  c->halo_values += c->comm.elem_send_count() * (long long)per_elem;
+  return DG_OK;
+}
+
+// face-row halo of the flux-trace Helmholtz pair (Comm::exchange_rows):
+// which = 0 x (nodal face values), 1 psi (face rows), 2 trV (the coarse
+// parents' trace slots).  DG_HALO_POISON=1 first fills the ghost rows with
+// NaN, so a kernel reading an unshipped ghost value shows up in the tests.
+bool lean_halo(dg_ctx* c) {
+  static const bool off = getenv("DG_LEAN_HALO") && std::string(getenv("DG_LEAN_HALO")) == "0";
+  return !off && c->comm.active() && c->comm.has_rows();
+}
+int halo_rows(dg_ctx* c, double* field, int which, int per_elem) {
+  static const bool poison = getenv("DG_HALO_POISON") && atoi(getenv("DG_HALO_POISON")) != 0;
+  if (poison && c->n_tot > c->n_el)
+    CK(cudaMemsetAsync(field + (size_t)c->n_el * per_elem, 0xFF,
+                       (size_t)(c->n_tot - c->n_el) * per_elem * sizeof(double), c->stream));
+  if (!c->comm.exchange_rows(field, which, c->stream)) return fail(DG_ERR_COMM, c->comm.error());
+  c->halo_values += c->comm.row_send_values(which);
   return DG_OK;
 }
 
@@ -401,11 +422,15 @@ int interp_h(dg_ctx* c, const double* h, double* hq) {
 int helm_apply(dg_ctx* c, double a_dt, const double* h, const double* hq, double* x, double* y,
                const GsFuse* gs = nullptr) {
   const int d = c->dim;
-  RET(halo(c, x, 1));
   const double gm1 = c->model.gamma - 1.0;
   const int qd = hq != nullptr;
   const bool tm = qd && trace_mode(c);
   const bool pm = tm && psi_mode(c);
+  // flux-trace pair: the ghosts' face rows only (x face nodes, psi rows, the
+  // coarse parents' trV slots) instead of whole ghost elements
+  const bool lean = pm && lean_halo(c);
+  if (lean) RET(halo_rows(c, x, 0, c->NP));
+  else RET(halo(c, x, 1));
   if (tm) CK(c->trV.alloc((size_t)c->n_tot * tr_len(c)));
   const int psl = 2 * d * c->NQF;  // psi values per element
   const bool pp = pm && pipe_mode(c);
@@ -414,14 +439,16 @@ int helm_apply(dg_ctx* c, double a_dt, const double* h, const double* hq, double
   RET(op_grad(c, x, nullptr, gm1, 0.0, 1, OUT_MINV, mv(c->sV.p, (long long)d * c->NP, c->NP),
               CView{}, 0, -(a_dt * c->model.inv_mach_sq), qd, tm ? c->trV.p : nullptr,
               pm ? c->psi.p : nullptr, pp ? c->pin.p : nullptr));
-  if (pm) RET(halo_elems(c, c->psi.p, psl));        // H2 reads its neighbours' psi
+  if (lean) RET(halo_rows(c, c->psi.p, 1, psl));
+  else if (pm) RET(halo_elems(c, c->psi.p, psl));   // H2 reads its neighbours' psi
   if (pp && c->n_pinfix > 0) {
     const long long nt = (long long)c->n_pinfix * c->NQF;
     hk_pin_fixup<<<(unsigned)((nt + 255) / 256), 256, 0, c->stream>>>(
         c->pinfix.p, c->n_pinfix, c->NQF, 2 * d, c->psi.p, c->pin.p);
     CK(cudaGetLastError());
   }
-  if (tm) RET(halo_elems(c, c->trV.p, tr_len(c)));  // (and the coarse parents' traces)
+  if (lean) RET(halo_rows(c, c->trV.p, 2, tr_len(c)));
+  else if (tm) RET(halo_elems(c, c->trV.p, tr_len(c)));  // (and the coarse parents' traces)
   else RET(halo(c, c->sV.p, d));
   RET(op_divhv(c, cv(c->sV.p, (long long)d * c->NP, c->NP), qd ? hq : h, 1, OUT_MINV,
                mv(y, c->NP, c->NP), cv(x, c->NP, c->NP), 1, a_dt, qd, gs,
@@ -1693,6 +1720,21 @@ int dg_ctx_set_comm_loopback(dg_ctx* c, int group, int rank, int nranks,
   CK(cudaMemcpy(&v, tmp.p, sizeof(double), cudaMemcpyDeviceToHost));
   tmp.release();
   c->n_global = (long long)v;
+  return DG_OK;
+}
+
+int dg_ctx_set_halo_rows(dg_ctx* c, int which, const int64_t* send_counts,
+                         const int64_t* send_idx, const int64_t* recv_counts,
+                         const int64_t* recv_idx) {
+  CK(cudaSetDevice(c->device));
+  if (!c->comm.set_rows(which, send_counts, send_idx, recv_counts, recv_idx))
+    return fail(DG_ERR_COMM, c->comm.error());
+  return DG_OK;
+}
+
+int dg_halo_stats(dg_ctx* c, long long* values_sent, int reset) {
+  if (values_sent) *values_sent = c->halo_values;
+  if (reset) c->halo_values = 0;
   return DG_OK;
 }
 

@@ -65,6 +65,166 @@ def halo_plans(mesh, nranks, weights=None, part=None):
     return plans
 
 
+@dataclass
+class RowPlan:
+    """One rank's face-row exchange lists for one field layout: offsets (in
+    doubles, into the local [owned..., ghosts...] field) of the values sent
+    to / received from each peer, grouped by peer."""
+    send_counts: np.ndarray
+    send_idx: np.ndarray
+    recv_counts: np.ndarray
+    recv_idx: np.ndarray
+
+
+ROW_X, ROW_PSI, ROW_TRV = 0, 1, 2
+
+
+def face_nodes(dim, n):
+    """Nodal indices (C order, axis 0 slowest) of the n^(d-1) nodes on face
+    2*axis+side, ascending."""
+    idx = np.arange(n ** dim).reshape((n,) * dim)
+    out = []
+    for a in range(dim):
+        for side in (0, 1):
+            out.append(np.sort(np.take(idx, (n - 1) if side else 0, axis=a).ravel()))
+    return np.stack(out)
+
+
+def trace_slots(dim, face):
+    """V-trace slots of a face (dg_operator.cuh tr_slot): vertical faces carry
+    the normal component only, z faces all d components."""
+    nv = 2 * (dim - 1)
+    if face < nv:
+        return [face]
+    return [nv + (face - nv) * dim + k for k in range(dim)]
+
+
+def face_row_plans(mesh, plans, degree):
+    """Face-row halo plans of the flux-trace Helmholtz pair:
+    for every rank and field layout (x nodal, psi, V traces) the values its
+    owned elements' faces read from ghosts, nothing else.
+
+    An owned element reads, across face f, its ghost neighbour's face f^1:
+    the nodal face values of x (H1 and the coarse-face kernel), its psi row
+    (H2 through hk_pin_fixup, the coarse-face kernel for ghost children) and,
+    when the ghost is the coarse parent of an owned fine element, its V trace
+    slots there (the fine side's mortar).  Returns plans[rank][which]."""
+    d = mesh.dim
+    n = degree + 1
+    NP, NC = n ** d, n ** (d - 1)
+    TRL = (2 * (d - 1) + 2 * d) * NC
+    nranks = len(plans)
+    topo = mesh.topology
+    owner = np.empty(mesh.n_leaves, dtype=np.int64)
+    for pl in plans:
+        owner[pl.owned[0]:pl.owned[1]] = pl.rank
+    rk, el, fc, tv = [], [], [], []
+
+    def need(by, elem, face, trv):
+        m = owner[by] != owner[elem]
+        rk.append(owner[by][m])
+        el.append(np.asarray(elem)[m])
+        fc.append(np.full(int(m.sum()), face, dtype=np.int64))
+        tv.append(np.full(int(m.sum()), trv, dtype=np.int64))
+    for bt in topo.conforming:
+        a = bt.axis
+        need(bt.right, bt.left, 2 * a + 1, 0)
+        need(bt.left, bt.right, 2 * a, 0)
+    for bt in topo.hanging:
+        a, o = bt.axis, bt.orient
+        need(bt.fine, bt.coarse, 2 * a + o, 1)          # fine owner reads the coarse parent
+        need(bt.coarse, bt.fine, 2 * a + 1 - o, 0)      # coarse owner reads the children
+    if rk:
+        rk, el, fc, tv = (np.concatenate(v) for v in (rk, el, fc, tv))
+    else:
+        rk = el = fc = tv = np.empty(0, np.int64)
+    # unique (rank, element, face); trv = any
+    key = (rk * mesh.n_leaves + el) * (2 * d) + fc
+    order = np.argsort(key, kind="stable")
+    key, rk, el, fc, tv = key[order], rk[order], el[order], fc[order], tv[order]
+    first = np.ones(len(key), dtype=bool)
+    first[1:] = key[1:] != key[:-1]
+    grp = np.cumsum(first) - 1
+    tvu = np.zeros(int(first.sum()), dtype=np.int64)
+    np.maximum.at(tvu, grp, tv)
+    rk, el, fc, tv = rk[first], el[first], fc[first], tvu
+    fn = face_nodes(d, n)
+    ar = np.arange(NC, dtype=np.int64)
+
+    def offsets(which, lid, face, trv):
+        """(values per need, flat offsets) of the needs in the given order."""
+        if which == ROW_X:
+            return (lid[:, None] * NP + fn[face]).ravel()
+        if which == ROW_PSI:
+            return (lid[:, None] * (2 * d * NC) + face[:, None] * NC + ar).ravel()
+        rows = []
+        sel = np.nonzero(trv)[0]          # (only the coarse parents of hanging faces)
+        for l, f in zip(lid[sel], face[sel]):
+            for sl in trace_slots(d, int(f)):
+                rows.append(l * TRL + sl * NC + ar)
+        return np.concatenate(rows) if rows else np.empty(0, np.int64)
+
+    out = []
+    for pl in plans:
+        p = pl.rank
+        g2l = np.full(mesh.n_leaves, -1, dtype=np.int64)
+        g2l[pl.local_ids] = np.arange(len(pl.local_ids))
+        per_which = []
+        for which in (ROW_X, ROW_PSI, ROW_TRV):
+            sc = np.zeros(nranks, dtype=np.int64)
+            rc = np.zeros(nranks, dtype=np.int64)
+            sidx, ridx = [], []
+            for q in range(nranks):
+                if q == p:
+                    continue
+                # received from q: my needs of q's elements, (element, face) order
+                m = (rk == p) & (owner[el] == q)
+                o = offsets(which, g2l[el[m]], fc[m], tv[m])
+                rc[q] = len(o)
+                ridx.append(o)
+                # sent to q: q's needs of my elements, same order
+                m = (rk == q) & (owner[el] == p)
+                o = offsets(which, el[m] - pl.owned[0], fc[m], tv[m])
+                sc[q] = len(o)
+                sidx.append(o)
+            cat = lambda v: (np.concatenate(v) if v else np.empty(0, np.int64)).astype(np.int64)  # noqa: E731
+            per_which.append(RowPlan(sc, cat(sidx), rc, cat(ridx)))
+        out.append(per_which)
+    return out
+
+
+def attach_row_plans(ctx, row_plans):
+    """Hand one rank's three face-row plans to its libdg context."""
+    import ctypes as C
+
+    from . import _lib as L
+    for which, rp in enumerate(row_plans):
+        arrs = [np.ascontiguousarray(a, dtype=np.int64)
+                for a in (rp.send_counts, rp.send_idx, rp.recv_counts, rp.recv_idx)]
+        arrs = [a if len(a) else np.zeros(1, np.int64) for a in arrs]
+        L.check(ctx.lib.dg_ctx_set_halo_rows(ctx.handle, which,
+                                             *[a.ctypes.data_as(C.c_void_p) for a in arrs]))
+
+
+def exchange_rows_host(row_plans, which, local_flat):
+    """Host execution of one face-row exchange for all ranks (test oracle of
+    Comm::exchange_rows): local_flat[p] is rank p's flattened field."""
+    out = [a.copy() for a in local_flat]
+    nranks = len(row_plans)
+    for p in range(nranks):
+        rp = row_plans[p][which]
+        r0 = 0
+        for q in range(nranks):
+            n = int(rp.recv_counts[q])
+            if n == 0:
+                continue
+            sq = row_plans[q][which]
+            s0 = int(np.sum(sq.send_counts[:p]))
+            out[p][rp.recv_idx[r0:r0 + n]] = local_flat[q][sq.send_idx[s0:s0 + n]]
+            r0 += n
+    return out
+
+
 def exchange_host(plans, local_arrays):
     """Reference (host) execution of one halo exchange for all ranks:
     local_arrays[p] has rows [owned..., ghosts...]; ghost rows are filled
@@ -117,6 +277,9 @@ class DistributedSolver:
                                             sc.ctypes.data_as(C.c_void_p),
                                             se.ctypes.data_as(C.c_void_p),
                                             rc.ctypes.data_as(C.c_void_p)))
+        all_plans = halo_plans(case.mesh, world)
+        attach_row_plans(self.ctx, face_row_plans(case.mesh, all_plans,
+                                                  case.geometry.basis.degree)[rank])
         self.case = case
         self.cfg = cfg
         self.n_owned = pl.n_owned
@@ -154,7 +317,7 @@ class LoopbackGroup:
 
     _next_group = [1]
 
-    def __init__(self, geometry, model, bcs, sponge, nranks, device=0):
+    def __init__(self, geometry, model, bcs, sponge, nranks, device=0, lean=True):
         import ctypes as C
 
         import torch
@@ -182,6 +345,18 @@ class LoopbackGroup:
                 ctx.handle, gid, rank, nranks, sc.ctypes.data_as(C.c_void_p),
                 se.ctypes.data_as(C.c_void_p), rc.ctypes.data_as(C.c_void_p)))
         self.run(attach)
+        self.row_plans = face_row_plans(geometry.mesh, self.plans, geometry.basis.degree)
+        if lean:
+            self.run(lambda r, ctx: attach_row_plans(ctx, self.row_plans[r]))
+
+    def halo_values(self, reset=False):
+        """Doubles each rank has sent in halo exchanges (dg_halo_stats)."""
+        out = []
+        for ctx in self.ctxs:
+            v = self.C.c_longlong()
+            ctx.lib.dg_halo_stats(ctx.handle, self.C.byref(v), 1 if reset else 0)
+            out.append(v.value)
+        return out
 
     def run(self, fn, timeout=600.0):
         """fn(rank, ctx) on every rank concurrently (its own thread and

@@ -140,3 +140,70 @@ def test_gloo_multirank_halo(name, world):
     assert all(p.exitcode == 0 for p in procs)
     for rank, ok_ghost, ok_op, ok_dot in res:
         assert ok_ghost and ok_op and ok_dot, (rank, ok_ghost, ok_op, ok_dot)
+
+
+@pytest.mark.parametrize("name,P", [("hang2d", 3), ("hang3d", 2), ("hang3d", 3), ("per3d", 3),
+                                    ("cfg2", 4)])
+def test_face_row_plans(name, P):
+    """Face-row halo plans: what q sends to p is what p
+    expects, every value an owned face reads from a ghost arrives (x face
+    nodes, psi rows, the coarse parents' V trace slots), nothing else is
+    touched, and the volume is a fraction of the whole-element exchange."""
+    from paper_2408_08129_b200.device import face_tables
+    from paper_2408_08129_b200.distributed import (ROW_PSI, ROW_TRV, ROW_X, exchange_rows_host,
+                                                   face_nodes, face_row_plans, trace_slots)
+    from paper_2408_08129_b200 import _lib as L
+    c = build(name)
+    d, n = c.mesh.dim, c.geom.basis.degree + 1
+    NP, NC = n ** d, n ** (d - 1)
+    widths = {ROW_X: NP, ROW_PSI: 2 * d * NC, ROW_TRV: (2 * (d - 1) + 2 * d) * NC}
+    plans = _plans(name, P)
+    rows = face_row_plans(c.mesh, plans, c.geom.basis.degree)
+    for which, w in widths.items():
+        for p in range(P):
+            for q in range(P):
+                assert rows[p][which].send_counts[q] == rows[q][which].recv_counts[p]
+        rng = np.random.default_rng(which)
+        G = rng.standard_normal((c.mesh.n_leaves, w))
+        loc = []
+        for pl in plans:
+            a = np.full((len(pl.local_ids), w), np.nan)
+            a[:pl.n_owned] = G[pl.owned[0]:pl.owned[1]]
+            loc.append(a.ravel())
+        out = exchange_rows_host(rows, which, loc)
+        for pl, a in zip(plans, out):
+            a = a.reshape(-1, w)
+            got = np.isfinite(a[pl.n_owned:])
+            # everything that arrived is the owner's value
+            assert np.array_equal(a[pl.n_owned:][got], G[pl.ghosts][got])
+    # coverage: every (ghost, face) an owned face reads
+    kind, nbr, hang, *_ = face_tables(c.mesh, c.bcs, c.model, c.geom.basis)
+    fn = face_nodes(d, n)
+    for pl, rp in zip(plans, rows):
+        g2l = {int(g): i for i, g in enumerate(pl.local_ids)}
+        have = {w: set(rp[w].recv_idx.tolist()) for w in widths}
+        for e in range(*pl.owned):
+            for f in range(2 * d):
+                k = int(kind[e, f]) & 15
+                if k == L.FACE_CONF or k == L.FACE_FINE:
+                    nbs = [int(nbr[e, f])]
+                elif k == L.FACE_COARSE:
+                    nbs = [int(v) for v in hang[int(nbr[e, f])]]
+                else:
+                    continue
+                for g in nbs:
+                    lid = g2l[g]
+                    if lid < pl.n_owned:
+                        continue
+                    fo = f ^ 1
+                    assert all(lid * NP + int(v) in have[ROW_X] for v in fn[fo])
+                    assert all(lid * widths[ROW_PSI] + fo * NC + j in have[ROW_PSI]
+                               for j in range(NC))
+                    if k == L.FACE_FINE:
+                        for sl in trace_slots(d, fo):
+                            assert all(lid * widths[ROW_TRV] + sl * NC + j in have[ROW_TRV]
+                                       for j in range(NC))
+    # volume per Helmholtz apply vs whole ghost elements (x + psi + V traces)
+    lean = sum(int(rp[w].send_counts.sum()) for rp in rows for w in widths)
+    whole = sum(int(pl.send_counts.sum()) for pl in plans) * sum(widths.values())
+    assert lean < 0.5 * whole, (lean, whole)

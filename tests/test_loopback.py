@@ -69,3 +69,61 @@ def test_loopback_positivity_error_carries_global_element():
         grp.imex_step(U, 0.0, 0.5, ImplicitSolveConfig())
     record("hang3d", "loopback_positivity_element", [float(ei.value.element)], [float(victim)])
     assert ei.value.element == victim
+
+
+_CHILD_LEAN = r"""
+import json, sys
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import numpy as np
+from casebuild import build, golden, rel
+from paper_2408_08129_b200.dgops import DGOperators
+from paper_2408_08129_b200.distributed import LoopbackGroup
+from paper_2408_08129_b200.imex import ImplicitSolveConfig, SplitOperators, ars222, imex_step
+out = {}
+for name, P in (("hang3d", 3), ("hang2d", 3), ("per3d", 2), ("hang3d_r4", 2)):
+    c = build(name)
+    z = golden(name)
+    dt = float(z["dt"]) if "dt" in z else (c.dt or (0.05 if name == "per3d" else 0.5))
+    cfg = ImplicitSolveConfig(krylov_tol=c.krylov_tol)
+    split = SplitOperators(DGOperators(c.geom), c.model, c.bcs, c.sponge)
+    U_ref, st_ref = imex_step(c.U, 0.0, dt, ars222(), split, cfg)
+    res = {}
+    for lean in (True, False):
+        grp = LoopbackGroup(c.geom, c.model, c.bcs, c.sponge, P, lean=lean)
+        grp.halo_values(reset=True)
+        U, sts = grp.imex_step(grp.scatter(c.U), 0.0, dt, cfg)
+        res[lean] = (rel(grp.gather(U), np.asarray(U_ref)), sts[0].krylov_iters,
+                     sum(grp.halo_values()))
+    out[name] = {"err_lean": res[True][0], "err_whole": res[False][0],
+                 "iters": [res[True][1], res[False][1], st_ref.krylov_iters],
+                 "values_lean": res[True][2], "values_whole": res[False][2]}
+print(json.dumps(out))
+"""
+
+
+def test_loopback_face_row_halo():
+    """The Helmholtz pair's halo as face rows (x face nodes, psi rows, the
+    coarse parents' V trace slots) against whole ghost
+    elements: the same step as the single domain with every ghost row
+    poisoned with NaN before each lean exchange (DG_HALO_POISON=1: a kernel
+    reading an unshipped ghost value would poison the state), at a fraction
+    of the exchanged volume."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env["DG_HALO_POISON"] = "1"
+    code = _CHILD_LEAN % (root, os.path.join(root, "tests"))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    for name, v in res.items():
+        record(name, "loopback_lean_halo_step_vs_single_domain", [v["err_lean"]], [1e-12])
+        assert v["err_lean"] <= 1e-12 and v["err_whole"] <= 1e-12, (name, v)
+        assert v["iters"][0] == v["iters"][2] and v["iters"][1] == v["iters"][2], (name, v)
+        assert v["values_lean"] < 0.5 * v["values_whole"], (name, v)
+        print(f"{name}: halo doubles per step lean {v['values_lean']} vs whole "
+              f"{v['values_whole']} ({v['values_whole'] / v['values_lean']:.1f}x)")
