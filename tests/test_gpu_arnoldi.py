@@ -196,12 +196,16 @@ print(json.dumps(out))
 """
 
 
-def test_pipelined_helmholtz_on_golden_cases():
+@pytest.mark.parametrize("devarn", ["1", "2"])
+def test_pipelined_helmholtz_on_golden_cases(devarn):
     """The large-problem path (persistent TMA-fed div(hV), separate dual-dot
     pass; DG_PIPE_MIN=0 forces it on the small golden meshes, odd and even
-    n^d): Helmholtz action, GMRES and one step against the reference."""
+    n^d): Helmholtz action, GMRES and one step against the reference -- with
+    the host-driven Arnoldi loop (the default of that path) and with the
+    device-resident Arnoldi scalars forced onto it (DG_DEVARN=2)."""
     env = dict(os.environ)
     env["DG_PIPE_MIN"] = "0"
+    env["DG_DEVARN"] = devarn
     code = _CHILD_PIPE % (ROOT, os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=900)
