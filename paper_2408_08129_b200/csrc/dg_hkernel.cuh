@@ -1074,9 +1074,16 @@ hdiv_kernel(const __grid_constant__ KParams<N> P) {
 // the next group's loads are in flight while this one is computed and the
 // memory parallelism no longer depends on registers or occupancy.  Same
 // arithmetic as hdiv_kernel.  Even n^d only (16-byte aligned element blocks).
+// DG_H2_SLIM=1: the base (the action's input) and the column rows are read
+// by plain loads instead of being staged -- 4 KB less shared memory per warp,
+// which lets a third CTA (12 instead of 8 warps) share an SM
+#ifndef DG_H2_SLIM
+#define DG_H2_SLIM 0
+#endif
 template <int D, int N>
 struct H2Pipe {
   using HL = HLayout<D, N>;
+  static constexpr bool SLIM = DG_H2_SLIM != 0;
   static constexpr int NP = HL::NP, NC = HL::NC, NF = HL::NF, EPW = HL::EPW;
   static constexpr bool OK = HL::OK && HL::TPE == 32;
   static constexpr int ev(int x) { return (x + 1) & ~1; }
@@ -1087,10 +1094,10 @@ struct H2Pipe {
   static constexpr int OP = OH + ev(EPW * NP + 2);
   static constexpr int OI = OP + EPW * NF * NC;
   static constexpr int OB = OI + EPW * NF * NC;
-  static constexpr int OR = OB + ev(EPW * NP + 2);
+  static constexpr int OR = OB + (SLIM ? 0 : ev(EPW * NP + 2));
   static constexpr int OC = OR + EPW * 8;   // + 64-byte records
   static constexpr int COLS = 2 * ((ipow(N, D - 1) * D + 2 * (D - 1) * ipow(N, D - 2) + 1) / 2);
-  static constexpr int STG = OC + EPW * COLS;  // + column rows (lookahead, terrain)
+  static constexpr int STG = OC + (SLIM ? 0 : EPW * COLS);  // + column rows (lookahead, terrain)
   static constexpr int TSLOT = HL::odd(HL::DRAW);
   static constexpr int WT = 2 * (32 + 2);
   static constexpr int WREG = ((2 * STG + HL::NSLOT * TSLOT + WT) + 1) & ~1;  // per warp
@@ -1165,7 +1172,7 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
   const bool slot_ok = eiw < EPW;
   // LA: geometry from the staged records and the column rows by lookahead
   // bulk copies; else both by (latency-exposed) global loads
-  const bool terr = LA && P.gc.terrain != 0;
+  const bool terr = LA && !PL::SLIM && P.gc.terrain != 0;
   const unsigned cb[2] = {smem_u32(&cbar[wid][0]), smem_u32(&cbar[wid][1])};
   double* W = smem + HL::TABP + wid * PL::WREG;
   double* STG0 = W;
@@ -1197,7 +1204,8 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
     unsigned long long aV, aH, aB = 0;
     const unsigned bV = span(P.in.p + e0 * P.in.estride, ne * D * NP, aV);
     const unsigned bH = span(P.inH.p + e0 * P.inH.estride, ne * NP, aH);
-    const unsigned bB = P.has_base ? span(P.base.p + e0 * P.base.estride, ne * NP, aB) : 0u;
+    const unsigned bB = (P.has_base && !PL::SLIM)
+                            ? span(P.base.p + e0 * P.base.estride, ne * NP, aB) : 0u;
     const unsigned bytes = bV + bH + bB + 8u * ne * (2 * NF * NC + 8);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes)
                  : "memory");
@@ -1205,7 +1213,7 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
     bulk_g2s(st + PL::OH, reinterpret_cast<const void*>(aH), bH, b);
     bulk_g2s(st + PL::OP, P.psi + e0 * (NF * NC), 8u * ne * NF * NC, b);
     bulk_g2s(st + PL::OI, P.pin + e0 * (NF * NC), 8u * ne * NF * NC, b);
-    if (P.has_base) bulk_g2s(st + PL::OB, reinterpret_cast<const void*>(aB), bB, b);
+    if (P.has_base && !PL::SLIM) bulk_g2s(st + PL::OB, reinterpret_cast<const void*>(aB), bB, b);
     bulk_g2s(st + PL::OR, P.frec + e0 * REC_INTS, 64u * ne, b);
     if (dots) {
       // the fused dots' basis slices of this group into L2
@@ -1292,8 +1300,8 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
       }
     }
     const ElemGeo<D> g3 = LA ? geo_from_row<D>(rec + 8, P.gc) : elem_geo<D>(mesh.elem, P.gc, act ? e : 0);
-    const double* colrow = LA ? st + PL::OC + esl * PL::COLS
-                              : mesh.col + (long long)g3.col * P.gc.col_stride;
+    const double* colrow = (LA && !PL::SLIM) ? st + PL::OC + esl * PL::COLS
+                                             : mesh.col + (long long)g3.col * P.gc.col_stride;
     ColData<D, N> cd;
     cd.omh = 1.0;
     cd.dh[0] = cd.dh[1] = 0.0;
@@ -1466,7 +1474,8 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
       const int shB = P.has_base
           ? (int)((reinterpret_cast<unsigned long long>(P.base.p + g * EPW * P.base.estride) >> 3) & 1)
           : 0;
-      const double* Bs = st + PL::OB + shB + esl * NP;
+      const double* Bs = PL::SLIM ? P.base.p + (act ? e : 0) * P.base.estride
+                                  : st + PL::OB + shB + esl * NP;
       double v[N], o[N];
 #pragma unroll
       for (int ii = 0; ii < N; ++ii) v[ii] = X[xoff<D, N>(c, ii)];
