@@ -32,6 +32,15 @@
 
 namespace dg {
 
+// DG_HK1_ASYNC=1: H1 stages the neighbours' face nodes and its own h-trace
+// rows with cp.async (no register, no scoreboard wait at the staging store)
+// and waits for them only after the own-column interpolation passes; the
+// vertical faces' terrain scalars are loaded with the column data.  ncu of
+// the synchronous version: long_scoreboard 4.7 of ~10.7 stall cycles per
+// issue (the staging stores and the late h-trace loads).
+#ifndef DG_HK1_ASYNC
+#define DG_HK1_ASYNC 1
+#endif
 template <int D, int N>
 struct HLayout {
   static constexpr int NP = ipow(N, D);
@@ -51,7 +60,8 @@ struct HLayout {
   static constexpr int NHW = 2 * (D - 1) + 2 * D;       // 1/2 ws n+ values per face point
   static constexpr int odd(int s) { return (s % 2 == 0) ? s + 1 : s; }
   // H1 slot: tile | neighbour face nodes (NF x NC) | 1/2 ws n+ (NHW x NC)
-  static constexpr int GSLOT = odd(KX * TSZ + NF * NC + NHW * NC);
+  // | own h traces (NF x NC, staged by cp.async; DG_HK1_ASYNC)
+  static constexpr int GSLOT = odd(KX * TSZ + NF * NC + NHW * NC + (DG_HK1_ASYNC ? NF * NC : 0));
   // H2 slot: tile (the fine-face staging (d+1) x NC and the fused dots'
   // warp totals reuse it)
   static constexpr int DRAW = KX * TSZ > (D + 1) * NC ? KX * TSZ : (D + 1) * NC;
@@ -289,7 +299,7 @@ __device__ __forceinline__ ElemGeo<D> geo_from_row(const int* r, const GeoConst&
 // traces hf(f) = hrow[f n^(d-1)], the element's face records, geometry and
 // column row (terrain).  Writes V, psi (+ pin scatter, + trV for elements
 // with a coarse face).
-template <int D, int N>
+template <int D, int N, bool AS = false>
 __device__ __forceinline__ void hgrad_body(const KParams<N>& P, const Tab<N>& TS, int c, bool act,
                                            long long e, const uint8_t (&kf)[2 * D],
                                            const int (&nf)[2 * D], const ElemGeo<D>& g,
@@ -309,9 +319,12 @@ __device__ __forceinline__ void hgrad_body(const KParams<N>& P, const Tab<N>& TS
 #pragma unroll
     for (int a = 0; a < D - 1; ++a) cd.dh[a] = colrow[NQH * (1 + a) + c];
   }
-  auto edge = [&](int f) -> double {
-    return (P.gc.terrain && act) ? colrow[NQH * D + f * NE + ((D == 2) ? 0 : c / N)] : 1.0;
-  };
+  // 1 - h_edge/z_top of the vertical faces, loaded with the column data
+  double oedge[2 * (D - 1)];
+#pragma unroll
+  for (int f = 0; f < 2 * (D - 1); ++f)
+    oedge[f] = (P.gc.terrain && act) ? colrow[NQH * D + f * NE + ((D == 2) ? 0 : c / N)] : 1.0;
+  auto edge = [&](int f) -> double { return oedge[f < 2 * (D - 1) ? f : 0]; };
   // ---- p = alpha x to the Gauss points (z in registers, y / x via the tile)
   {
     double col[N], q[N];
@@ -338,6 +351,11 @@ __device__ __forceinline__ void hgrad_body(const KParams<N>& P, const Tab<N>& TS
     mat_apply<N, false>(TC.B, v, o);
 #pragma unroll
     for (int ii = 0; ii < N; ++ii) X[xoff<D, N>(c, ii)] = o[ii];
+  }
+  if constexpr (AS) {
+    // the staged face nodes / h traces (cp.async) have landed, for every lane
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    esync<HL::TPE>(team);
   }
   // ---- neighbour traces at face point c: tangential passes over the staged
   // face nodes (B, or the mortar halves for a fine leaf's coarse parent)
@@ -597,9 +615,35 @@ hgrad_kernel(const __grid_constant__ KParams<N> P) {
     kf[f] = act ? mesh.kind[es * NF + f] : (uint8_t)KIND_WALL;
     nf[f] = act ? mesh.nbr[es * NF + f] : 0;
   }
+  // every first-level load (face records, element row, own column, own h
+  // traces) is issued before the first use of any of them: the in-order
+  // warp then waits ONE memory latency, not one per dependent chain (ncu:
+  // the element-row load used to issue only after the wait on the face kinds)
+  int er[2 + D];
+#pragma unroll
+  for (int k = 0; k < 2 + D; ++k) er[k] = mesh.elem[es * (2 + D) + k];
   double xc[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) xc[k] = act ? P.in.p[es * P.in.estride + c * N + k] : 0.0;
+#if DG_HK1_ASYNC
+  double* HR = HW + HL::NHW * NC;
+  if (act) {
+#pragma unroll
+    for (int f = 0; f < NF; ++f) cp_async8(&HR[f * NC + c], P.trH + es * (NF * NC) + f * NC + c);
+  }
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    const int kd = kf[f] & 15;
+    const bool inter = act && (kd == KIND_CONF || kd == KIND_FINE);
+    if (inter)
+      cp_async8(&FG[f * NC + c],
+                P.in.p + (long long)nf[f] * P.in.estride + nbr_face_node<D, N>(f >> 1, f & 1, c));
+    else
+      FG[f * NC + c] = 0.0;
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  const double* hrow = HR + c;
+#else
 #pragma unroll
   for (int f = 0; f < NF; ++f) {
     const int kd = kf[f] & 15;
@@ -608,12 +652,14 @@ hgrad_kernel(const __grid_constant__ KParams<N> P) {
         inter ? P.in.p[(long long)nf[f] * P.in.estride + nbr_face_node<D, N>(f >> 1, f & 1, c)]
               : 0.0;
   }
-  const ElemGeo<D> g = elem_geo<D>(mesh.elem, P.gc, es);
+  const double* hrow = P.trH + es * (NF * NC) + c;
+#endif
+  const ElemGeo<D> g = geo_from_row<D>(er, P.gc);
   const double* colrow = P.gc.terrain ? mesh.col + (long long)g.col * P.gc.col_stride : nullptr;
   __syncthreads();  // the table barrier is initialised
   tab_bulk_wait(&tbar);
-  hgrad_body<D, N>(P, TS, c, act, e, kf, nf, g, colrow, xc, P.trH + es * (NF * NC) + c, X, FG,
-                   HW, wid);
+  hgrad_body<D, N, DG_HK1_ASYNC != 0>(P, TS, c, act, e, kf, nf, g, colrow, xc, hrow, X, FG, HW,
+                                      wid);
 }
 
 // H1, pipelined (hgrad2_kernel): persistent warps over strided element
@@ -1153,6 +1199,9 @@ __device__ __forceinline__ void gs_round_acc(const KParams<N>& P, bool own, long
 #ifndef DG_HK2P_MINB
 #define DG_HK2P_MINB 2
 #endif
+#ifndef DG_H2_LATE_LA
+#define DG_H2_LATE_LA 1
+#endif
 
 template <int D, int N, bool LA>
 __global__ void __launch_bounds__(128, DG_HK2P_MINB)
@@ -1267,10 +1316,12 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
     const unsigned par = (unsigned)((k >> 1) & 1);
     mbar_wait(s ? bar1 : bar0, par);
     if (terr) mbar_wait(cb[s], par);
+#if !DG_H2_LATE_LA
     if (g + GW < ngroups) {
       mbar_wait(s ? bar0 : bar1, (unsigned)(((k + 1) >> 1) & 1));
       lookahead(g + GW, s ^ 1);
     }
+#endif
     const double* st = STG0 + s * PL::STG;
     const long long e = g * EPW + eiw;
     const bool act = slot_ok && e < mesh.n_el;
@@ -1425,6 +1476,17 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
         Zc[kz] = TC.lift[0][kz] * fl[zf] + TC.lift[1][kz] * fl[zf + 1] - Zc[kz];
     }
     __syncwarp();
+#if DG_H2_LATE_LA
+    // the next group's column rows: its records were requested at the end of
+    // the previous iteration, so by now (half of this group's arithmetic
+    // later) they have landed and this wait costs nothing -- at the top of
+    // the iteration it exposed a full memory latency per group (ncu: 15 % of
+    // the warp time in that wait)
+    if (terr && g + GW < ngroups) {
+      mbar_wait(s ? bar0 : bar1, (unsigned)(((k + 1) >> 1) & 1));
+      lookahead(g + GW, s ^ 1);
+    }
+#endif
     {
       double v[N], o[N];
 #pragma unroll
