@@ -111,6 +111,25 @@ __device__ __forceinline__ void tab_bulk_wait(unsigned long long* bar) {
       : "memory");
 }
 
+// global loads that keep their program order among each other and the
+// cp.async staging (volatile asm): the prologue of H1 issues all of its
+// first-level loads before anything consumes one
+__device__ __forceinline__ double ldg_f64_ordered(const double* p) {
+  double v;
+  asm volatile("ld.global.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ldg_s32_ordered(const int* p) {
+  int v;
+  asm volatile("ld.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint8_t ldg_u8_ordered(const uint8_t* p) {
+  unsigned v;
+  asm volatile("ld.global.u8 %0, [%1];\n" : "=r"(v) : "l"(p));
+  return (uint8_t)v;
+}
+
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
@@ -608,29 +627,53 @@ hgrad_kernel(const __grid_constant__ KParams<N> P) {
   double* X = smem + HL::TABP + (wid * HL::NSLOT + (slot_ok ? eiw : EPW)) * HL::GSLOT;
   double* FG = X + HL::KX * TSZ;
   double* HW = FG + NF * NC;
+  // Every first-level load (own column, own h traces, element row, face
+  // records) is issued -- as volatile asm, in this order -- before the first
+  // use of any of them, so the in-order warp waits ONE memory latency.  Left
+  // to the scheduler, the face-kind compares were hoisted above the
+  // element-row and own-column loads and each chain paid its own latency
+  // (ncu, per source line: three long-scoreboard waits of ~8 % of the warp
+  // time each).  Inactive lanes load element 0 and discard it.
   uint8_t kf[NF];
   int nf[NF];
+  int er[2 + D];
+  double xc[N];
+#if DG_HK1_ASYNC
+  double* HR = HW + HL::NHW * NC;
+#pragma unroll
+  for (int k = 0; k < N; ++k) xc[k] = ldg_f64_ordered(P.in.p + es * P.in.estride + c * N + k);
+#pragma unroll
+  for (int f = 0; f < NF; ++f) cp_async8(&HR[f * NC + c], P.trH + es * (NF * NC) + f * NC + c);
+#pragma unroll
+  for (int k = 0; k < 2 + D; ++k) er[k] = ldg_s32_ordered(mesh.elem + es * (2 + D) + k);
+#pragma unroll
+  for (int f = 0; f < NF; ++f) nf[f] = ldg_s32_ordered(mesh.nbr + es * NF + f);
+#pragma unroll
+  for (int f = 0; f < NF; ++f) kf[f] = ldg_u8_ordered(mesh.kind + es * NF + f);
+  // (ptxas does not sink loads below a warp barrier: without it the
+  // element-row and own-column loads were scheduled after the first wait)
+  __syncwarp();
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    if (!act) {
+      kf[f] = (uint8_t)KIND_WALL;
+      nf[f] = 0;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < N; ++k) xc[k] = act ? xc[k] : 0.0;
+#else
 #pragma unroll
   for (int f = 0; f < NF; ++f) {
     kf[f] = act ? mesh.kind[es * NF + f] : (uint8_t)KIND_WALL;
     nf[f] = act ? mesh.nbr[es * NF + f] : 0;
   }
-  // every first-level load (face records, element row, own column, own h
-  // traces) is issued before the first use of any of them: the in-order
-  // warp then waits ONE memory latency, not one per dependent chain (ncu:
-  // the element-row load used to issue only after the wait on the face kinds)
-  int er[2 + D];
 #pragma unroll
   for (int k = 0; k < 2 + D; ++k) er[k] = mesh.elem[es * (2 + D) + k];
-  double xc[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) xc[k] = act ? P.in.p[es * P.in.estride + c * N + k] : 0.0;
+#endif
 #if DG_HK1_ASYNC
-  double* HR = HW + HL::NHW * NC;
-  if (act) {
-#pragma unroll
-    for (int f = 0; f < NF; ++f) cp_async8(&HR[f * NC + c], P.trH + es * (NF * NC) + f * NC + c);
-  }
 #pragma unroll
   for (int f = 0; f < NF; ++f) {
     const int kd = kf[f] & 15;
