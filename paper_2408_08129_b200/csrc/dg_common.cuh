@@ -112,4 +112,19 @@ __device__ __forceinline__ ElemGeo<D> elem_geo(const int* elem, const GeoConst& 
   return g;
 }
 
+// the same from an element row already in registers / shared memory
+// (level, integer origin[d], column)
+template <int D>
+__device__ __forceinline__ ElemGeo<D> geo_from_row(const int* r, const GeoConst& gc) {
+  ElemGeo<D> g;
+  const double scale = __longlong_as_double((long long)(1023 - r[0]) << 52);
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    g.s[a] = gc.per_root[a] * scale;
+    g.lo[a] = g.s[a] * (double)r[1 + a];
+  }
+  g.col = r[1 + D];
+  return g;
+}
+
 }  // namespace dg

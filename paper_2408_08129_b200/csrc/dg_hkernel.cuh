@@ -299,18 +299,6 @@ __device__ __forceinline__ double edge_omh(const GeoConst& gc, const double* col
 // int32 nbr[2d] | uint8 kind[2d] at byte 24 | int32 elem row (level,
 // origin[d], column) at byte 32
 constexpr int REC_INTS = 16;
-template <int D>
-__device__ __forceinline__ ElemGeo<D> geo_from_row(const int* r, const GeoConst& gc) {
-  ElemGeo<D> g;
-  const double scale = __longlong_as_double((long long)(1023 - r[0]) << 52);
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    g.s[a] = gc.per_root[a] * scale;
-    g.lo[a] = g.s[a] * (double)r[1 + a];
-  }
-  g.col = r[1 + D];
-  return g;
-}
 
 // One element's H1 on lane c (see the file comment).  Inputs: the lane's
 // nodal x column (xcol[k], k < n), the neighbours' raw face nodes staged at
