@@ -1464,7 +1464,11 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
         fl[f] += sg * ((0.5 * ws) * (tr[FC - 1] * vn));
       }
     };
-    if (mesh.n_coarse > 0) {
+    // (one vote per group: most warps own no fine side of a hanging face)
+    bool has_fine = false;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) has_fine |= act && (kf[f] & 15) == KIND_FINE;
+    if (mesh.n_coarse > 0 && __any_sync(0xffffffffu, has_fine)) {
       fine_face(std::integral_constant<int, 0>{}, std::integral_constant<int, 0>{});
       fine_face(std::integral_constant<int, 0>{}, std::integral_constant<int, 1>{});
       if constexpr (D == 3) {
@@ -1474,6 +1478,12 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
       fine_face(std::integral_constant<int, D - 1>{}, std::integral_constant<int, 0>{});
       fine_face(std::integral_constant<int, D - 1>{}, std::integral_constant<int, 1>{});
     }
+#if DG_H2_LATE_LA == 2
+    if (terr && g + GW < ngroups) {  // (variant: the lookahead before the volume phase)
+      mbar_wait(s ? bar0 : bar1, (unsigned)(((k + 1) >> 1) & 1));
+      lookahead(g + GW, s ^ 1);
+    }
+#endif
     // volume
     double Zc[N];
     const double det = col_det<D>(g3, cd.omh);
@@ -1507,7 +1517,7 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
         Zc[kz] = TC.lift[0][kz] * fl[zf] + TC.lift[1][kz] * fl[zf + 1] - Zc[kz];
     }
     __syncwarp();
-#if DG_H2_LATE_LA
+#if DG_H2_LATE_LA == 1
     // the next group's column rows: its records were requested at the end of
     // the previous iteration, so by now (half of this group's arithmetic
     // later) they have landed and this wait costs nothing -- at the top of
