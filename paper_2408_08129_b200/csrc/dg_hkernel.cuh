@@ -312,7 +312,7 @@ __device__ __forceinline__ void hgrad_body(const KParams<N>& P, const Tab<N>& TS
                                            const int (&nf)[2 * D], const ElemGeo<D>& g,
                                            const double* colrow, const double* xcol,
                                            const double* hrow, double* X, double* FG, double* HW,
-                                           int team) {
+                                           int team, unsigned long long* tbar = nullptr) {
   using HL = HLayout<D, N>;
   constexpr int NC = HL::NC, NF = HL::NF, TSZ = HL::TSZ;
   constexpr int NQH = ipow(N, D - 1), NE = ipow(N, D - 2);
@@ -363,6 +363,10 @@ __device__ __forceinline__ void hgrad_body(const KParams<N>& P, const Tab<N>& TS
     // the staged face nodes / h traces (cp.async) have landed, for every lane
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     esync<HL::TPE>(team);
+    // ... and the CTA's 1D tables (first read by the passes below; waiting
+    // here instead of before the own-column passes keeps the CTA's warps
+    // from meeting at a barrier right after their first-level loads)
+    if (tbar != nullptr) tab_bulk_wait(tbar);
   }
   // ---- neighbour traces at face point c: tangential passes over the staged
   // face nodes (B, or the mortar halves for a fine leaf's coarse parent)
@@ -604,6 +608,9 @@ hgrad_kernel(const __grid_constant__ KParams<N> P) {
   extern __shared__ __align__(16) double smem[];
   __shared__ unsigned long long tbar;
   tab_bulk_issue(smem, P.tab_g, HL::TABD * 8, &tbar);
+#if DG_HK1_ASYNC
+  __syncthreads();  // the table barrier is initialised (waited for in hgrad_body)
+#endif
   const Tab<N>& TS = *reinterpret_cast<const Tab<N>*>(smem);
   const MeshDev& mesh = P.mesh;
   const int lane = threadIdx.x % HL::TPE, wid = threadIdx.x / HL::TPE;  // team lane, team
@@ -687,10 +694,13 @@ hgrad_kernel(const __grid_constant__ KParams<N> P) {
 #endif
   const ElemGeo<D> g = geo_from_row<D>(er, P.gc);
   const double* colrow = P.gc.terrain ? mesh.col + (long long)g.col * P.gc.col_stride : nullptr;
+#if DG_HK1_ASYNC
+  hgrad_body<D, N, true>(P, TS, c, act, e, kf, nf, g, colrow, xc, hrow, X, FG, HW, wid, &tbar);
+#else
   __syncthreads();  // the table barrier is initialised
   tab_bulk_wait(&tbar);
-  hgrad_body<D, N, DG_HK1_ASYNC != 0>(P, TS, c, act, e, kf, nf, g, colrow, xc, hrow, X, FG, HW,
-                                      wid);
+  hgrad_body<D, N, false>(P, TS, c, act, e, kf, nf, g, colrow, xc, hrow, X, FG, HW, wid);
+#endif
 }
 
 // H1, pipelined (hgrad2_kernel): persistent warps over strided element
