@@ -8,6 +8,7 @@
 //   col table    (n_col, stride)    float64 terrain data per leaf footprint
 //   face table   nbr (n_el_total, 2d) int32 + kind (n_el_total, 2d) uint8
 #pragma once
+#include "dg_pdl.cuh"
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -126,5 +127,6 @@ __device__ __forceinline__ ElemGeo<D> geo_from_row(const int* r, const GeoConst&
   g.col = r[1 + D];
   return g;
 }
+
 
 }  // namespace dg

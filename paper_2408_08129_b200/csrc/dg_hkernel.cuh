@@ -608,6 +608,8 @@ hgrad_kernel(const __grid_constant__ KParams<N> P) {
   extern __shared__ __align__(16) double smem[];
   __shared__ unsigned long long tbar;
   tab_bulk_issue(smem, P.tab_g, HL::TABD * 8, &tbar);
+  pdl_trigger();
+  pdl_wait();  // (programmatic dependent launch, small problems: dg_common.cuh)
 #if DG_HK1_ASYNC
   __syncthreads();  // the table barrier is initialised (waited for in hgrad_body)
 #endif
@@ -893,6 +895,8 @@ hdiv_kernel(const __grid_constant__ KParams<N> P) {
   extern __shared__ __align__(16) double smem[];
   __shared__ unsigned long long tbar;
   tab_bulk_issue(smem, P.tab_g, HL::TABD * 8, &tbar);
+  pdl_trigger();
+  pdl_wait();  // (programmatic dependent launch, small problems)
   const Tab<N>& TS = *reinterpret_cast<const Tab<N>*>(smem);
   const Tab<N>& TC = P.tab;
   const MeshDev& mesh = P.mesh;

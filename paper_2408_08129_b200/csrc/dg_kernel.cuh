@@ -886,7 +886,9 @@ coarse_kernel(const __grid_constant__ KParams<N> P, const int* __restrict__ clis
   extern __shared__ double smem[];
   // tables from their global copy (coalesced; the kernel-parameter copy
   // serialises on divergent constant-bank reads)
+  pdl_trigger();
   for (int i = threadIdx.x; i < L::TABD; i += blockDim.x) smem[i] = P.tab_g[i];
+  pdl_wait();  // (programmatic dependent launch, small problems: dg_common.cuh)
   const Tab<N>& T = *reinterpret_cast<const Tab<N>*>(smem);
   double* red = smem + L::TABD;
   double* A = red + 64 + L::C_A;

@@ -123,9 +123,9 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
       }
       if (a.mesh.n_coarse > 0) {
         if (a.mesh.cflux == nullptr) return cudaErrorInvalidValue;  // flux mode required
-        coarse_kernel<D, N, OPK, true><<<a.mesh.n_coarse, L::CTHREADS, L::CSMEM, st>>>(
-            P, a.mesh.coarse_list, a.mesh.n_coarse, nullptr);
-        cudaError_t e = cudaGetLastError();
+        cudaError_t e = launch_k(coarse_kernel<D, N, OPK, true>, dim3(a.mesh.n_coarse),
+                                 dim3(L::CTHREADS), L::CSMEM, st, P, a.mesh.coarse_list,
+                                 (int)a.mesh.n_coarse, (double*)nullptr);
         if (e != cudaSuccess) return e;
       }
       if constexpr (OPK == OP_GRAD) {
@@ -157,7 +157,7 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
             return cudaGetLastError();
           }
         }
-        hgrad_kernel<D, N><<<hgrid, HL::THREADS, HL::GSMEM, st>>>(P);
+        return launch_k(hgrad_kernel<D, N>, dim3(hgrid), dim3(HL::THREADS), HL::GSMEM, st, P);
       } else {
         using PL = H2Pipe<D, N>;
         if constexpr (PL::OK) {
@@ -189,7 +189,7 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
             return cudaGetLastError();
           }
         }
-        hdiv_kernel<D, N><<<hgrid, HL::THREADS, HL::DSMEM, st>>>(P);
+        return launch_k(hdiv_kernel<D, N>, dim3(hgrid), dim3(HL::THREADS), HL::DSMEM, st, P);
       }
       return cudaGetLastError();
     }

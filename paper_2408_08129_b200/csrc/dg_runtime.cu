@@ -695,6 +695,13 @@ int dcgs2_cycle_dev(dg_ctx* c, double a_dt, const double* h, const double* hq, i
   const ArnState& H = *c->arn_host;
   int j = 0, chunks = 0;
   done = 0;
+  // the steps' kernels are launched as programmatic dependents of one
+  // another (dg_pdl.cuh; DG_PDL=0: plain stream order)
+  static const bool pdl_env = !(getenv("DG_PDL") && std::string(getenv("DG_PDL")) == "0");
+  struct PdlScope {
+    PdlScope(bool on) { tl_pdl = on ? 1 : 0; }
+    ~PdlScope() { tl_pdl = 0; }
+  } pdl_scope(pdl_env && !prof().on);
   while (j < m) {
     int K = std::max(1, std::min(ahead, m - j));
     for (int jj = j; jj < j + K; ++jj) {

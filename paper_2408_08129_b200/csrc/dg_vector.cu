@@ -12,6 +12,7 @@
 #include <cstdlib>
 
 #include "dg_vector.cuh"
+#include "dg_pdl.cuh"
 #include "dg_prof.h"
 
 namespace dg {
@@ -577,6 +578,8 @@ k_dcgs2_update(long long n, const double* __restrict__ Q, long long vstride,
   // and stores (twice the bytes in flight per instruction); odd n: the last
   // element by one thread
   __shared__ double cs[NV + 1], cc[NV + 1];
+  pdl_trigger();
+  pdl_wait();  // (programmatic dependent launch, small problems: dg_common.cuh)
   const double alpha = coefs[3 * NV + 2];
   for (int i = threadIdx.x; i <= NV; i += blockDim.x) {
     cs[i] = i < NV ? coefs[i] : 0.0;
@@ -656,8 +659,8 @@ cudaError_t launch_dcgs2(cudaStream_t st, long long n, int nv, const double* Q, 
     grid = std::min(RED_BLOCKS, std::max(1, nsm * std::max(occ, 1)));
   }
   *used_grid = grid;
-  k_dcgs2_update<NV><<<grid, RED_THREADS, 0, st>>>(n, Q, vstride, coefs, u, z, unext, partials);
-  return cudaGetLastError();
+  return launch_k(k_dcgs2_update<NV>, dim3(grid), dim3(RED_THREADS), 0, st, n, Q, vstride, coefs, u,
+                  z, unext, partials);
 }
 
 // DCGS2 dual Gram-Schmidt dots (the unfused form of the dots the div(hV)
@@ -978,6 +981,8 @@ __global__ void k_arn_init(ArnState* a, int m, double bn, double target, double 
 // summed, so the serial part runs out of shared memory only.
 __global__ void k_arn_pre(ArnState* a, int j, const double* __restrict__ src, int nrows,
                           double* __restrict__ coefs) {
+  pdl_trigger();
+  pdl_wait();
   if (a->stop) return;
   __shared__ double sdots[2 * (ARN_M + 2)];
   __shared__ double sH[(ARN_M + 1) * ARN_M];
@@ -1074,6 +1079,8 @@ __global__ void k_arn_pre(ArnState* a, int j, const double* __restrict__ src, in
 // warp: the lanes stage column j of Hbar and the rotations in shared memory
 // (one round trip), lane 0 runs the dependent Givens chain from there.
 __global__ void k_arn_post(ArnState* a, int j, const double* __restrict__ na2p, int nparts) {
+  pdl_trigger();
+  pdl_wait();
   if (a->stop || threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
   const int m = a->m;
@@ -1130,14 +1137,14 @@ cudaError_t arn_init(cudaStream_t st, ArnState* a, int m, double bn, double targ
 cudaError_t arn_pre(cudaStream_t st, ArnState* a, int j, const double* src, int nrows,
                     double* coefs) {
   prof_begin(st);
-  k_arn_pre<<<1, nrows > 0 ? 1024 : 32, 0, st>>>(a, j, src, nrows, coefs);
+  launch_k(k_arn_pre, dim3(1), dim3(nrows > 0 ? 1024 : 32), 0, st, a, j, src, nrows, coefs);
   prof_end(st, P_DOT, 8.0 * (nrows > 0 ? nrows : 1) * 2 * (j + 2), 1);
   return cudaGetLastError();
 }
 
 cudaError_t arn_post(cudaStream_t st, ArnState* a, int j, const double* na2, int nparts) {
   prof_begin(st);
-  k_arn_post<<<1, 32, 0, st>>>(a, j, na2, nparts);
+  launch_k(k_arn_post, dim3(1), dim3(32), 0, st, a, j, na2, nparts);
   prof_end(st, P_AXPY, 8.0 * (nparts > 0 ? nparts : 1), 1);
   return cudaGetLastError();
 }
