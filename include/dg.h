@@ -277,7 +277,7 @@ int dg_profile_read(double* ms /*6*/, double* bytes /*6*/, long long* count /*6*
    Arnoldi cycles so far and Arnoldi steps enqueued past a stopping step */
 int dg_arnoldi_stats(dg_ctx* ctx, long long* syncs, long long* wasted_steps);
 /* mode: 0 host-driven Arnoldi loop (two synchronisations per step), 1 device
-   scalars for small problems (default), 2 device scalars always, -1 the
+   scalars below 2^24 scalar DoF (default), 2 device scalars always, -1 the
    DG_DEVARN environment default; multi-rank contexts always take mode 0 */
 int dg_set_arnoldi_mode(dg_ctx* ctx, int mode);
 

@@ -678,9 +678,12 @@ int dcgs2_cycle(dg_ctx* c, double a_dt, const double* h, const double* hq, int m
 bool devarn_mode(dg_ctx* c) {
   static const int env0 = getenv("DG_DEVARN") ? atoi(getenv("DG_DEVARN")) : 1;
   const int env = c->arn_mode >= 0 ? c->arn_mode : env0;
-  // large problems (separate dual-dot pass) keep the host loop: a step costs
-  // milliseconds there and a wasted one more than the synchronisations
-  return env != 0 && !c->comm.active() && (env == 2 || !sep_dots(c));
+  // large problems keep the host loop: an Arnoldi step costs milliseconds
+  // there and one enqueued past the stop more than the synchronisations
+  // saved (cfg3, 4.4 M scalar DoF, 0.5 ms per Arnoldi step: 71.8 -> 66.9 ms
+  // per time step with the device scalars; cfg4, 160 M: 13 ms per step)
+  return env != 0 && !c->comm.active() &&
+         (env == 2 || !sep_dots(c) || c->n_global < (1LL << 24));
 }
 
 int dcgs2_cycle_dev(dg_ctx* c, double a_dt, const double* h, const double* hq, int m, int max_iter,
