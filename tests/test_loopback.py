@@ -127,3 +127,44 @@ def test_loopback_face_row_halo():
         assert v["values_lean"] < 0.5 * v["values_whole"], (name, v)
         print(f"{name}: halo doubles per step lean {v['values_lean']} vs whole "
               f"{v['values_whole']} ({v['values_whole'] / v['values_lean']:.1f}x)")
+
+
+def test_distributed_solver_world_of_one():
+    """bench.py's N > 1 driver (DistributedSolver: gloo control plane, NCCL
+    unique-id broadcast, halo + face-row plans, dg_imex_step per rank) run
+    with a world of one rank: the same step as the single-domain API."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    code = r"""
+import json, sys
+sys.path.insert(0, %r)
+import numpy as np, torch
+from paper_2408_08129_b200.cases import baseline_case
+from paper_2408_08129_b200.dgops import DGOperators
+from paper_2408_08129_b200.distributed import DistributedSolver
+from paper_2408_08129_b200.imex import ImplicitSolveConfig, SplitOperators, ars222, imex_step
+case = baseline_case("cfg1")
+cfg = ImplicitSolveConfig(**case.solve)
+sol = DistributedSolver(case, cfg, 0, 1, 0)
+U, st = sol.step(sol.local_state(), 0.0)
+split = SplitOperators(DGOperators(case.geometry), case.model, case.bcs, case.sponge)
+Ur, sr = imex_step(case.U0, 0.0, case.dt, ars222(), split, cfg)
+err = float(np.linalg.norm(U.cpu().numpy() - Ur) / np.linalg.norm(Ur))
+print(json.dumps({"err": err, "it": [list(st.krylov_iters), list(sr.krylov_iters)]}))
+""" % root
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0",
+               WORLD_SIZE="1", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    import json
+    v = json.loads(r.stdout.strip().splitlines()[-1])
+    record("cfg1", "distributed_solver_world1_step", [v["err"]], [1e-13])
+    assert v["err"] <= 1e-13 and v["it"][0] == v["it"][1], v
