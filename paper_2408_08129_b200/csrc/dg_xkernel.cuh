@@ -61,8 +61,12 @@ __device__ __forceinline__ void point_metric_reg(const GeoConst& gc, const Tab<N
 
 // smem-only component loops are kept rolled (instruction-cache footprint of
 // the d+2-variable kernel); DG_XUNROLL=1 unrolls them
-#if defined(DG_XUNROLL) && DG_XUNROLL
+#if defined(DG_XUNROLL) && DG_XUNROLL == 1
 #define XROLL _Pragma("unroll")
+#elif defined(DG_XUNROLL) && DG_XUNROLL == 2
+#define XROLL _Pragma("unroll 2")
+#elif defined(DG_XUNROLL) && DG_XUNROLL == 3
+#define XROLL _Pragma("unroll 3")
 #else
 #define XROLL _Pragma("unroll 1")
 #endif
