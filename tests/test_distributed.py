@@ -207,3 +207,65 @@ def test_face_row_plans(name, P):
     lean = sum(int(rp[w].send_counts.sum()) for rp in rows for w in widths)
     whole = sum(int(pl.send_counts.sum()) for pl in plans) * sum(widths.values())
     assert lean < 0.5 * whole, (lean, whole)
+
+
+def _row_worker(rank, world, port, name, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2408_08129_b200.distributed import ROW_PSI, face_row_plans, halo_plans
+        c = build(name)
+        d, n = c.mesh.dim, c.geom.basis.degree + 1
+        w = 2 * d * n ** (d - 1)
+        plans = halo_plans(c.mesh, world)
+        rp = face_row_plans(c.mesh, plans, c.geom.basis.degree)[rank][ROW_PSI]
+        pl = plans[rank]
+        G = np.random.default_rng(3).standard_normal((c.mesh.n_leaves, w))
+        a = np.full((len(pl.local_ids), w), np.nan)
+        a[:pl.n_owned] = G[pl.owned[0]:pl.owned[1]]
+        flat = a.ravel()
+        # Comm::exchange_rows over gloo: pack by index, grouped send/recv, unpack
+        s_off = np.concatenate([[0], np.cumsum(rp.send_counts)])
+        r_off = np.concatenate([[0], np.cumsum(rp.recv_counts)])
+        reqs, bufs = [], {}
+        for p in range(world):
+            if p == rank:
+                continue
+            if rp.send_counts[p]:
+                t = torch.from_numpy(np.ascontiguousarray(flat[rp.send_idx[s_off[p]:s_off[p + 1]]]))
+                reqs.append(dist.isend(t, p))
+            if rp.recv_counts[p]:
+                bufs[p] = torch.empty(int(rp.recv_counts[p]), dtype=torch.float64)
+                reqs.append(dist.irecv(bufs[p], p))
+        for r in reqs:
+            r.wait()
+        for p, t in bufs.items():
+            flat[rp.recv_idx[r_off[p]:r_off[p + 1]]] = t.numpy()
+        got = flat.reshape(-1, w)[pl.n_owned:]
+        fin = np.isfinite(got)
+        ok = bool(np.array_equal(got[fin], G[pl.ghosts][fin])) and int(fin.sum()) == int(rp.recv_counts.sum())
+        q.put((rank, ok, int(fin.sum()), got.size))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,world", [("hang3d", 2), ("hang2d", 3)])
+def test_gloo_face_row_exchange(name, world):
+    """The face-row exchange (Comm::exchange_rows: pack by index, grouped
+    send / recv per peer, unpack by index) between real processes over gloo:
+    every received value is the owner's, and only the planned values move."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_row_worker, args=(r, world, port, name, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    for rank, ok, moved, total in res:
+        assert ok and 0 < moved < total, (rank, ok, moved, total)
