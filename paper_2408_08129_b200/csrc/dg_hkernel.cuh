@@ -1258,6 +1258,8 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
   __shared__ unsigned long long tbar;
   __shared__ unsigned long long sbar[PL::WPB][2], cbar[PL::WPB][2];
   tab_bulk_issue(smem, P.tab_g, HL::TABD * 8, &tbar);
+  pdl_trigger();
+  pdl_wait();  // (programmatic dependent launch below 2^24 DoF: dg_pdl.cuh)
   const Tab<N>& TS = *reinterpret_cast<const Tab<N>*>(smem);
   const Tab<N>& TC = P.tab;
   const MeshDev& mesh = P.mesh;

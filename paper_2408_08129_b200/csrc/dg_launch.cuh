@@ -185,8 +185,7 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
               info->smem = PL::SMEM;
               info->grid = g;  // one dot-partial row per CTA
             }
-            kfn<<<g, 128, PL::SMEM, st>>>(P);
-            return cudaGetLastError();
+            return launch_k(kfn, dim3(g), dim3(128), PL::SMEM, st, P);
           }
         }
         return launch_k(hdiv_kernel<D, N>, dim3(hgrid), dim3(HL::THREADS), HL::DSMEM, st, P);

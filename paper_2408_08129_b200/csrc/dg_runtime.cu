@@ -680,7 +680,7 @@ bool devarn_mode(dg_ctx* c) {
   const int env = c->arn_mode >= 0 ? c->arn_mode : env0;
   // large problems keep the host loop: an Arnoldi step costs milliseconds
   // there and one enqueued past the stop more than the synchronisations
-  // saved (cfg3, 4.4 M scalar DoF, 0.5 ms per Arnoldi step: 71.8 -> 66.9 ms
+  // saved (cfg3, 4.4 M scalar DoF, 0.5 ms per Arnoldi step: 71.3 -> 68.5 ms
   // per time step with the device scalars; cfg4, 160 M: 13 ms per step)
   return env != 0 && !c->comm.active() &&
          (env == 2 || !sep_dots(c) || c->n_global < (1LL << 24));
@@ -704,7 +704,10 @@ int dcgs2_cycle_dev(dg_ctx* c, double a_dt, const double* h, const double* hq, i
   struct PdlScope {
     PdlScope(bool on) { tl_pdl = on ? 1 : 0; }
     ~PdlScope() { tl_pdl = 0; }
-  } pdl_scope(pdl_env && !prof().on);
+  } pdl_scope(pdl_env && !prof().on && !sep_dots(c));
+  // (only where a kernel is a single wave: at cfg3, 4.4 M scalar DoF, the
+  // early-resident dependents take SM resources from the kernel still
+  // running and the step gets slower, 70.6 vs 68.4 ms)
   while (j < m) {
     int K = std::max(1, std::min(ahead, m - j));
     for (int jj = j; jj < j + K; ++jj) {

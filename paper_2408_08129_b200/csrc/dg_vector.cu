@@ -162,6 +162,8 @@ k_axpy_div(long long n, int nv, const double* __restrict__ V, long long vstride,
 // out[c] = sum_b partials[b][c]   (one warp per column, fixed order)
 __global__ void k_reduce_cols(const double* __restrict__ partials, int nblocks, int ncols,
                               double* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int col = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (col >= ncols) return;
@@ -718,6 +720,8 @@ __global__ void __launch_bounds__(RED_THREADS)
 k_dual_dots(long long n, int nv, int g0, const double* __restrict__ Q, long long vstride,
             const double* __restrict__ z, const double* __restrict__ u, double* __restrict__ rows) {
   constexpr int GA = G > 0 ? G : 1;
+  pdl_trigger();
+  pdl_wait();  // (programmatic dependent launch below 2^24 DoF: dg_pdl.cuh)
   double pz[GA], pu[GA];
 #pragma unroll
   for (int i = 0; i < GA; ++i) pz[i] = pu[i] = 0.0;
@@ -806,7 +810,8 @@ cudaError_t launch_dd_tail(cudaStream_t st, int tail, long long n, int nv, int g
     if (tail < T) return launch_dd_tail<T - 1>(st, tail, n, nv, g0, Q, vstride, z, u, rows, grid);
   }
   *grid = dd_grid<T, true>();
-  k_dual_dots<T, true><<<*grid, RED_THREADS, 0, st>>>(n, nv, g0, Q, vstride, z, u, rows);
+  launch_k(k_dual_dots<T, true>, dim3(*grid), dim3(RED_THREADS), 0, st, n, nv, g0, Q, vstride, z, u,
+           rows);
   return cudaGetLastError();
 }
 
@@ -824,7 +829,8 @@ cudaError_t launch_dual_dots(cudaStream_t st, long long n, int nv, const double*
   int gmax = 1;
   for (int g = 0; g < nfull; ++g) {
     const int grid = dd_grid<8, false>();
-    k_dual_dots<8, false><<<grid, RED_THREADS, 0, st>>>(n, nv, 8 * g, Q, vstride, z, u, rows);
+    launch_k(k_dual_dots<8, false>, dim3(grid), dim3(RED_THREADS), 0, st, n, nv, 8 * g, Q, vstride,
+             z, u, rows);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     gmax = std::max(gmax, grid);
@@ -957,6 +963,8 @@ cudaError_t positivity(cudaStream_t st, long long n_el, int np, int d, const dou
 __global__ void __launch_bounds__(RED_THREADS)
 k_reduce_rows(const double* __restrict__ partials, long long nrows, int ncols,
               double* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const long long per = (nrows + gridDim.x - 1) / gridDim.x;
   const long long r0 = (long long)blockIdx.x * per;
   const long long r1 = r0 + per < nrows ? r0 + per : nrows;
@@ -981,8 +989,9 @@ k_reduce_rows(const double* __restrict__ partials, long long nrows, int ncols,
 cudaError_t reduce_rows(cudaStream_t st, const double* partials, long long nrows, int ncols,
                         double* tmp, double* out) {
   prof_begin(st);
-  k_reduce_rows<<<RED_BLOCKS, RED_THREADS, 0, st>>>(partials, nrows, ncols, tmp);
-  k_reduce_cols<<<(ncols + 7) / 8, 256, 0, st>>>(tmp, RED_BLOCKS, ncols, out);
+  launch_k(k_reduce_rows, dim3(RED_BLOCKS), dim3(RED_THREADS), 0, st, partials, nrows, ncols, tmp);
+  launch_k(k_reduce_cols, dim3((ncols + 7) / 8), dim3(256), 0, st, (const double*)tmp,
+           (int)RED_BLOCKS, ncols, out);
   prof_end(st, P_DOT, 8.0 * nrows * ncols, 2);
   return cudaGetLastError();
 }
