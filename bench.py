@@ -217,18 +217,29 @@ def reference_case(workload, workers):
     return split, U0, dt, dof, desc, cfg, pool
 
 
-def reference_steps(workload, workers, n_steps, warmup=0):
-    """Time n_steps ARS(2,2,2) steps of the real reference on the sample."""
+def reference_steps(workload, workers, n_steps, warmup=0, budget_s=240.0):
+    """Time n_steps ARS(2,2,2) steps of the real reference on the sample.
+    The whole run (warm-up included) is bounded by budget_s: a step of the
+    cfg4 window takes ~17-21 s on the host cores, so a long --steps K ends
+    early after the steps that fit (>= 1; the line reports how many)."""
     import time as _t
     from orodg import imex as ri
     split, U, dt, dof, desc, cfg, pool = reference_case(workload, workers)
     tab = ri.ars222()
     t = 0.0
-    for _ in range(warmup):
+    start = _t.perf_counter()
+    last = 0.0
+    for k in range(warmup):
+        if k > 0 and _t.perf_counter() - start + 2.0 * last > 0.25 * budget_s:
+            break
+        t0 = _t.perf_counter()
         U, st = ri.imex_step(U, t, dt, tab, split, cfg)
+        last = _t.perf_counter() - t0
         t += dt
     secs, kry = [], []
     for _ in range(n_steps):
+        if secs and _t.perf_counter() - start + secs[-1] > budget_s:
+            break
         t0 = _t.perf_counter()
         U, st = ri.imex_step(U, t, dt, tab, split, cfg)
         secs.append(_t.perf_counter() - t0)
