@@ -284,6 +284,24 @@ int dg_set_arnoldi_mode(dg_ctx* ctx, int mode);
 /* ---- partitioner (orodg/partition.py:45-67): bounds has n_chunks+1 slots ---- */
 int dg_split_contiguous(const double* weights, long long n, int n_chunks, long long* bounds);
 
+/* ---- native face-topology builder (host; orodg/mesh.py:178-242, the
+   ForestMesh topology): from the Morton-sorted leaves (level, integer origin
+   (n, dim)) of a forest over root_counts[dim] the reference's face batches --
+   conforming per axis, hanging per (axis, orient) sorted by (coarse,
+   subface), boundary per (axis, side).  Returns 0, or non-zero for a mesh the
+   reference rejects (tiling gap, 2:1 violation) or outside the key range; the
+   Python caller then runs its numpy builder, which raises the reference's
+   MeshError.  counts: n_conf[dim], n_hang[2 dim] ((axis, orient) -> 2 axis +
+   orient), n_bdry[2 dim]; copy: the batches concatenated in that order. ---- */
+typedef struct dg_topo dg_topo;
+int dg_topology_build(int dim, const int64_t* root_counts, const uint8_t* periodic, int64_t n,
+                      const int64_t* levels, const int64_t* origins, dg_topo** out);
+int dg_topology_counts(const dg_topo* t, int64_t* n_conf, int64_t* n_hang, int64_t* n_bdry);
+int dg_topology_copy(const dg_topo* t, int64_t* conf_left, int64_t* conf_right,
+                     int64_t* hang_coarse, int64_t* hang_fine, int64_t* hang_subface,
+                     int64_t* bdry_leaves);
+void dg_topology_free(dg_topo* t);
+
 #ifdef __cplusplus
 }
 #endif

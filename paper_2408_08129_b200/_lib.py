@@ -106,6 +106,10 @@ _SIGS = {
     "dg_profile_read": ([P, P, P], I),
     "dg_arnoldi_stats": ([P, C.POINTER(LL), C.POINTER(LL)], I),
     "dg_set_arnoldi_mode": ([P, I], I),
+    "dg_topology_build": ([I, P, P, LL, P, P, C.POINTER(P)], I),
+    "dg_topology_counts": ([P, P, P, P], I),
+    "dg_topology_copy": ([P, P, P, P, P, P, P], I),
+    "dg_topology_free": ([P], None),
 }
 
 PROFILE_CLASSES = ("explicit", "gradient", "div_hv", "multidot", "axpy", "other")

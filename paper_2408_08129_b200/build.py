@@ -26,7 +26,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
 SOURCES = ["dg_ops_d2.cu", "dg_ops_d3.cu", "dg_vector.cu", "dg_runtime.cu", "dg_comm.cu",
-           "dg_precond.cu"]
+           "dg_precond.cu", "dg_topology.cu"]
 
 
 def _digest():

@@ -241,7 +241,76 @@ class ForestMesh:
             valid = ~out
         return n, valid
 
+    def _build_topology_native(self):
+        """The face batches from libdg's C++ builder (csrc/dg_topology.cu);
+        None when the library is not built or the mesh is one the reference
+        rejects (the numpy builder below then raises its MeshError)."""
+        import ctypes as C
+        import os
+        if os.environ.get("DG_NATIVE_TOPOLOGY", "1") == "0":
+            return None
+        try:
+            from . import _lib
+            lib = _lib.lib()
+        except Exception:
+            return None
+        d = self.dim
+        n = self.n_leaves
+        root = np.ascontiguousarray(self.root_counts, dtype=np.int64)
+        per = np.ascontiguousarray(self.periodic, dtype=np.uint8)
+        lv = np.ascontiguousarray(self.levels, dtype=np.int64)
+        og = np.ascontiguousarray(self.origins, dtype=np.int64)
+        ptr = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        h = C.c_void_p()
+        if lib.dg_topology_build(d, ptr(root), ptr(per), n, ptr(lv), ptr(og), C.byref(h)) != 0:
+            return None
+        try:
+            nc = np.zeros(d, dtype=np.int64)
+            nh = np.zeros(2 * d, dtype=np.int64)
+            nb = np.zeros(2 * d, dtype=np.int64)
+            lib.dg_topology_counts(h, ptr(nc), ptr(nh), ptr(nb))
+            cl = np.empty(max(int(nc.sum()), 1), dtype=np.int64)
+            cr = np.empty_like(cl)
+            hc = np.empty(max(int(nh.sum()), 1), dtype=np.int64)
+            hf = np.empty_like(hc)
+            hs = np.empty_like(hc)
+            bl = np.empty(max(int(nb.sum()), 1), dtype=np.int64)
+            lib.dg_topology_copy(h, ptr(cl), ptr(cr), ptr(hc), ptr(hf), ptr(hs), ptr(bl))
+        finally:
+            lib.dg_topology_free(h)
+        conf, hanging, boundary = [], [], []
+        k = 0
+        for a in range(d):
+            m = int(nc[a])
+            if m:
+                conf.append(ConformingFaces(axis=a, left=cl[k:k + m].copy(),
+                                            right=cr[k:k + m].copy()))
+            k += m
+        k = 0
+        for a in range(d):
+            for o in (0, 1):
+                m = int(nh[2 * a + o])
+                if m:
+                    hanging.append(HangingFaces(axis=a, orient=o, coarse=hc[k:k + m].copy(),
+                                                fine=hf[k:k + m].copy(),
+                                                subface=hs[k:k + m].copy()))
+                k += m
+        k = 0
+        for a in range(d):
+            for s_ in (0, 1):
+                m = int(nb[2 * a + s_])
+                if m:
+                    boundary.append(BoundaryFaces(axis=a, side=s_, leaves=bl[k:k + m].copy()))
+                k += m
+        return MeshTopology(conf, hanging, boundary)
+
     def _build_topology(self):
+        native = self._build_topology_native()
+        if native is not None:
+            return native
+        return self._build_topology_numpy()
+
+    def _build_topology_numpy(self):
         d = self.dim
         L = self.levels
         O = self.origins

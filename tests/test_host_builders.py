@@ -209,3 +209,56 @@ def test_cfg5_recipe():
     frac = n_rows / (n_conf + n_rows)
     assert 0.2 < frac < 0.4, frac
     assert np.isfinite(c.U0).all() and c.U0.shape == (c.mesh.n_leaves, 5, 64)
+
+
+def _topo_equal(a, b):
+    assert len(a.conforming) == len(b.conforming)
+    for x, y in zip(a.conforming, b.conforming):
+        assert x.axis == y.axis
+        assert np.array_equal(x.left, y.left) and np.array_equal(x.right, y.right)
+    assert len(a.hanging) == len(b.hanging)
+    for x, y in zip(a.hanging, b.hanging):
+        assert (x.axis, x.orient) == (y.axis, y.orient)
+        assert np.array_equal(x.coarse, y.coarse) and np.array_equal(x.fine, y.fine)
+        assert np.array_equal(x.subface, y.subface)
+    assert len(a.boundary) == len(b.boundary)
+    for x, y in zip(a.boundary, b.boundary):
+        assert (x.axis, x.side) == (y.axis, y.side) and np.array_equal(x.leaves, y.leaves)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "hang2d", "hang3d", "per3d", "per3d_r4",
+                                  "cfg5s", "cfg3s"])
+def test_native_topology_matches_numpy(name):
+    """libdg's C++ face-topology builder (csrc/dg_topology.cu; SURVEY §8 f1,
+    orodg/mesh.py:178-242) gives the numpy builder's batches array by array
+    on every fixture mesh (uniform, hanging 2D / 3D, periodic, two levels)."""
+    from casebuild import build
+    m = build(name).mesh
+    native = m._build_topology_native()
+    assert native is not None, "libdg.so not built"
+    _topo_equal(native, m._build_topology_numpy())
+
+
+def test_native_topology_large_and_rejects_bad_mesh():
+    """A quarter-scale cfg4 recipe (39 k leaves, 3 levels, terrain-free
+    topology) matches; a mesh violating 2:1 balance makes the native builder
+    decline so that the numpy builder raises the reference's MeshError."""
+    import time
+    from paper_2408_08129_b200.cases import baseline_case
+    from paper_2408_08129_b200.errors import MeshError
+    from paper_2408_08129_b200.mesh import ForestMesh
+    m = baseline_case("cfg4", root_scale=0.125, with_state=False).mesh
+    t0 = time.perf_counter()
+    native = m._build_topology_native()
+    t1 = time.perf_counter()
+    ref = m._build_topology_numpy()
+    t2 = time.perf_counter()
+    assert native is not None
+    _topo_equal(native, ref)
+    print(f"{m.n_leaves} leaves: native {t1 - t0:.3f} s, numpy {t2 - t1:.3f} s")
+    # level-0 leaf next to level-2 leaves: 2:1 violated
+    leaves = [(0, (0, 0))] + [(2, (4 + i, j)) for i in range(4) for j in range(4)]
+    bad = ForestMesh(2, (2.0, 1.0), (2, 1), leaves)
+    assert bad._build_topology_native() is None
+    with pytest.raises(MeshError):
+        bad.topology
