@@ -300,7 +300,7 @@ int dg_topology_counts(const dg_topo* t, int64_t* n_conf, int64_t* n_hang, int64
 int dg_topology_copy(const dg_topo* t, int64_t* conf_left, int64_t* conf_right,
                      int64_t* hang_coarse, int64_t* hang_fine, int64_t* hang_subface,
                      int64_t* bdry_leaves);
-void dg_topology_free(dg_topo* t);
+int dg_topology_free(dg_topo* t);
 
 #ifdef __cplusplus
 }

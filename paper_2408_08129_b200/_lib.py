@@ -109,7 +109,7 @@ _SIGS = {
     "dg_topology_build": ([I, P, P, LL, P, P, C.POINTER(P)], I),
     "dg_topology_counts": ([P, P, P, P], I),
     "dg_topology_copy": ([P, P, P, P, P, P, P], I),
-    "dg_topology_free": ([P], None),
+    "dg_topology_free": ([P], I),
 }
 
 PROFILE_CLASSES = ("explicit", "gradient", "div_hv", "multidot", "axpy", "other")

@@ -218,6 +218,9 @@ int dg_topology_copy(const dg_topo* tp, int64_t* conf_left, int64_t* conf_right,
   return 0;
 }
 
-void dg_topology_free(dg_topo* tp) { delete tp; }
+int dg_topology_free(dg_topo* tp) {
+  delete tp;
+  return 0;
+}
 
 }  // extern "C"
