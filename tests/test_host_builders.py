@@ -233,9 +233,11 @@ def test_native_topology_matches_numpy(name):
     orodg/mesh.py:178-242) gives the numpy builder's batches array by array
     on every fixture mesh (uniform, hanging 2D / 3D, periodic, two levels)."""
     from casebuild import build
+    from paper_2408_08129_b200.build import build as build_lib
+    build_lib(verbose=False)          # no-op when libdg.so is up to date
     m = build(name).mesh
     native = m._build_topology_native()
-    assert native is not None, "libdg.so not built"
+    assert native is not None, "libdg.so not loadable"
     _topo_equal(native, m._build_topology_numpy())
 
 
@@ -246,7 +248,9 @@ def test_native_topology_large_and_rejects_bad_mesh():
     import time
     from paper_2408_08129_b200.cases import baseline_case
     from paper_2408_08129_b200.errors import MeshError
+    from paper_2408_08129_b200.build import build as build_lib
     from paper_2408_08129_b200.mesh import ForestMesh
+    build_lib(verbose=False)
     m = baseline_case("cfg4", root_scale=0.125, with_state=False).mesh
     t0 = time.perf_counter()
     native = m._build_topology_native()
