@@ -789,6 +789,13 @@ k_dual_dots(long long n, int nv, int g0, const double* __restrict__ Q, long long
   }
 }
 
+// vectors per dual-dot launch (z and u are re-read once per group): 12 (80
+// registers) measured best at cfg4 size -- nv = 12 / 24 / 31: 2.74 / 5.54 /
+// 7.36 ms against 3.15 / 6.01 / 7.97 with groups of 8 and 2.73 / 6.69 / 7.73
+// with groups of 16 (100 registers)
+#ifndef DG_DD_GROUP
+#define DG_DD_GROUP 12
+#endif
 template <int G, bool LAST>
 int dd_grid() {
   static int grid = 0;
@@ -818,25 +825,26 @@ cudaError_t launch_dd_tail(cudaStream_t st, int tail, long long n, int nv, int g
 cudaError_t launch_dual_dots(cudaStream_t st, long long n, int nv, const double* Q,
                              long long vstride, const double* z, const double* u, double* rows,
                              int* used_grid) {
-  // one one-wave launch per group of 8 vectors + the tail group (1..8
-  // vectors and the u / z products); the row block is zeroed first so the
+  // one one-wave launch per group of DG_DD_GROUP vectors + the tail group
+  // (1..DG_DD_GROUP vectors and the u / z products); the row block is zeroed first so the
   // groups' different grids sum exactly in reduce_rows
-  const int nfull = nv > 0 ? (nv - 1) / 8 : 0;
-  const int tail = nv - 8 * nfull;
+  constexpr int GF = DG_DD_GROUP;
+  const int nfull = nv > 0 ? (nv - 1) / GF : 0;
+  const int tail = nv - GF * nfull;
   const int ncols = 2 * (nv + 2);
   cudaError_t e = cudaMemsetAsync(rows, 0, (size_t)RED_BLOCKS * ncols * sizeof(double), st);
   if (e != cudaSuccess) return e;
   int gmax = 1;
   for (int g = 0; g < nfull; ++g) {
-    const int grid = dd_grid<8, false>();
-    launch_k(k_dual_dots<8, false>, dim3(grid), dim3(RED_THREADS), 0, st, n, nv, 8 * g, Q, vstride,
-             z, u, rows);
+    const int grid = dd_grid<GF, false>();
+    launch_k(k_dual_dots<GF, false>, dim3(grid), dim3(RED_THREADS), 0, st, n, nv, GF * g, Q,
+             vstride, z, u, rows);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     gmax = std::max(gmax, grid);
   }
   int gt = 1;
-  e = launch_dd_tail<8>(st, tail, n, nv, 8 * nfull, Q, vstride, z, u, rows, &gt);
+  e = launch_dd_tail<GF>(st, tail, n, nv, GF * nfull, Q, vstride, z, u, rows, &gt);
   *used_grid = std::max(gmax, gt);
   return e;
 }
