@@ -43,7 +43,7 @@ if has full; then
     -o gpurun_out/helm python tools/opbench.py --case cfg4 --scale 1.0 --ops gmres --reps 1 \
     > gpurun_out/ncu_helm.log 2>&1
   echo "full helm rc $?"
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"xelem|coarse" -c 2 -f \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"xelem_kernel" -s 1 -c 1 -f \
     -o gpurun_out/expl python tools/opbench.py --case cfg4 --scale 1.0 --ops explicit --reps 1 \
     > gpurun_out/ncu_expl.log 2>&1
   echo "full expl rc $?"
