@@ -1171,6 +1171,12 @@ hdiv_kernel(const __grid_constant__ KParams<N> P) {
 #ifndef DG_H2_SLIM
 #define DG_H2_SLIM 0
 #endif
+#ifndef DG_H2_WPB
+#define DG_H2_WPB 0   // 0: the most warps per SM that fit (H2Pipe::pick)
+#endif
+#ifndef DG_HK2P_MINB
+#define DG_HK2P_MINB 2  // CTAs per SM when DG_H2_WPB forces the warps per CTA
+#endif
 template <int D, int N>
 struct H2Pipe {
   using HL = HLayout<D, N>;
@@ -1192,7 +1198,29 @@ struct H2Pipe {
   static constexpr int TSLOT = HL::odd(HL::DRAW);
   static constexpr int WT = 2 * (32 + 2);
   static constexpr int WREG = ((2 * STG + HL::NSLOT * TSLOT + WT) + 1) & ~1;  // per warp
-  static constexpr int WPB = 4;
+  // CTAs per SM x warps per CTA: the stage ring's shared memory (21.9 KB per
+  // warp at 3D r = 3) limits the resident warps, and H2 is short of warps (2
+  // per scheduler at 2 x 4): take the split with the most warps per SM that
+  // fits (3D r = 3: 2 x 5, 6.48 -> 6.25 ms per apply; 3 x 3: 6.40)
+  static constexpr long SM_BYTES = 228 * 1024, CTA_BYTES = 227 * 1024, CTA_RES = 1024;
+  static constexpr bool fits(int ctas, int w) {
+    const long per = (long)(HL::TABP + w * WREG) * (long)sizeof(double);
+    // (<= 12 warps per SM: the kernel needs up to 168 registers per thread)
+    return ctas * w <= 12 && per <= CTA_BYTES && ctas * (per + CTA_RES) <= SM_BYTES;
+  }
+  static constexpr int pick(bool want_ctas) {
+    int bc = 1, bw = 1, best = 0;
+    for (int ctas = 3; ctas >= 1; --ctas)
+      for (int w = 1; w <= 8; ++w)
+        if (fits(ctas, w) && ctas * w > best) {
+          best = ctas * w;
+          bc = ctas;
+          bw = w;
+        }
+    return want_ctas ? bc : bw;
+  }
+  static constexpr int WPB = DG_H2_WPB > 0 ? DG_H2_WPB : pick(false);
+  static constexpr int CTAS = DG_H2_WPB > 0 ? DG_HK2P_MINB : pick(true);
   static constexpr size_t SMEM = (size_t)(HL::TABP + WPB * WREG) * sizeof(double);
 };
 
@@ -1241,15 +1269,12 @@ __device__ __forceinline__ void gs_round_acc(const KParams<N>& P, bool own, long
   if ((lane & 1) == 0 && col < nvt) wtot[col] += sv[0];
 }
 
-#ifndef DG_HK2P_MINB
-#define DG_HK2P_MINB 2
-#endif
 #ifndef DG_H2_LATE_LA
 #define DG_H2_LATE_LA 1
 #endif
 
 template <int D, int N, bool LA>
-__global__ void __launch_bounds__(128, DG_HK2P_MINB)
+__global__ void __launch_bounds__(32 * H2Pipe<D, N>::WPB, H2Pipe<D, N>::CTAS)
 hdiv2_kernel(const __grid_constant__ KParams<N> P) {
   using HL = HLayout<D, N>;
   using PL = H2Pipe<D, N>;

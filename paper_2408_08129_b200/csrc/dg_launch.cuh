@@ -174,18 +174,18 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
               int dev = 0, sms = 0, occ = 0;
               cudaGetDevice(&dev);
               cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-              e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 128, PL::SMEM);
+              e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 32 * PL::WPB, PL::SMEM);
               if (e != cudaSuccess) return e;
               pgrid = sms * (occ > 0 ? occ : 1);
             }
             const long long groups = (a.mesh.n_el + HL::EPW - 1) / HL::EPW;
             const int g = (int)std::min<long long>(pgrid, (groups + PL::WPB - 1) / PL::WPB);
             if (info) {
-              info->threads = 128;
+              info->threads = 32 * PL::WPB;
               info->smem = PL::SMEM;
               info->grid = g;  // one dot-partial row per CTA
             }
-            return launch_k(kfn, dim3(g), dim3(128), PL::SMEM, st, P);
+            return launch_k(kfn, dim3(g), dim3(32 * PL::WPB), PL::SMEM, st, P);
           }
         }
         return launch_k(hdiv_kernel<D, N>, dim3(hgrid), dim3(HL::THREADS), HL::DSMEM, st, P);
