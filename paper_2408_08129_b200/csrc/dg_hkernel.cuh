@@ -1171,6 +1171,12 @@ hdiv_kernel(const __grid_constant__ KParams<N> P) {
 #ifndef DG_H2_SLIM
 #define DG_H2_SLIM 0
 #endif
+#ifndef DG_H2_COLDIRECT
+#define DG_H2_COLDIRECT 1  // the column rows by plain loads issued at the top of the iteration
+#endif
+#ifndef DG_H2_FUSED_DOTS
+#define DG_H2_FUSED_DOTS 0
+#endif
 #ifndef DG_H2_WPB
 #define DG_H2_WPB 0   // 0: the most warps per SM that fit (H2Pipe::pick)
 #endif
@@ -1194,9 +1200,15 @@ struct H2Pipe {
   static constexpr int OR = OB + (SLIM ? 0 : ev(EPW * NP + 2));
   static constexpr int OC = OR + EPW * 8;   // + 64-byte records
   static constexpr int COLS = 2 * ((ipow(N, D - 1) * D + 2 * (D - 1) * ipow(N, D - 2) + 1) / 2);
-  static constexpr int STG = OC + (SLIM ? 0 : EPW * COLS);  // + column rows (lookahead, terrain)
+  static constexpr bool COLDIRECT = DG_H2_COLDIRECT != 0;
+  static constexpr int STG = OC + ((SLIM || COLDIRECT) ? 0 : EPW * COLS);  // + column rows (lookahead, terrain)
   static constexpr int TSLOT = HL::odd(HL::DRAW);
-  static constexpr int WT = 2 * (32 + 2);
+  // fused Gram-Schmidt dots in this kernel (measured slower than the separate
+  // dual-dot pass; DG_H2_FUSED_DOTS=1 keeps the code and its
+  // per-warp totals): without them the launcher sends a fused request to the
+  // non-pipelined kernel
+  static constexpr bool FUSED = DG_H2_FUSED_DOTS != 0;
+  static constexpr int WT = FUSED ? 2 * (32 + 2) : 0;
   static constexpr int WREG = ((2 * STG + HL::NSLOT * TSLOT + WT) + 1) & ~1;  // per warp
   // CTAs per SM x warps per CTA: the stage ring's shared memory (21.9 KB per
   // warp at 3D r = 3) limits the resident warps, and H2 is short of warps (2
@@ -1293,7 +1305,7 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
   const bool slot_ok = eiw < EPW;
   // LA: geometry from the staged records and the column rows by lookahead
   // bulk copies; else both by (latency-exposed) global loads
-  const bool terr = LA && !PL::SLIM && P.gc.terrain != 0;
+  const bool terr = LA && !PL::SLIM && !PL::COLDIRECT && P.gc.terrain != 0;
   const unsigned cb[2] = {smem_u32(&cbar[wid][0]), smem_u32(&cbar[wid][1])};
   double* W = smem + HL::TABP + wid * PL::WREG;
   double* STG0 = W;
@@ -1303,7 +1315,7 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
   const long long ngroups = ((long long)mesh.n_el + EPW - 1) / EPW;
   const long long gw = (long long)blockIdx.x * PL::WPB + wid;
   const long long GW = (long long)gridDim.x * PL::WPB;
-  const bool dots = P.gs_part != nullptr;
+  const bool dots = PL::FUSED && P.gs_part != nullptr;
   const bool dual = P.gs_dual != 0;
   const int nv = P.gs_nv;
   const int nvt = dual ? 2 * (nv + 2) : nv + 1;
@@ -1407,6 +1419,20 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
       kf[f] = act ? rk[f] : (uint8_t)KIND_WALL;
       nf[f] = rec[f];
     }
+    // (the column's terrain scalars first: with DG_H2_COLDIRECT they are
+    // plain loads, in flight during the face-flux phase)
+    const ElemGeo<D> g3 = LA ? geo_from_row<D>(rec + 8, P.gc) : elem_geo<D>(mesh.elem, P.gc, act ? e : 0);
+    const double* colrow = (LA && !PL::SLIM && !PL::COLDIRECT) ? st + PL::OC + esl * PL::COLS
+                                             : mesh.col + (long long)g3.col * P.gc.col_stride;
+    ColData<D, N> cd;
+    cd.omh = 1.0;
+    cd.dh[0] = cd.dh[1] = 0.0;
+    if (P.gc.terrain && act) {
+      constexpr int NQH = ipow(N, D - 1);
+      cd.omh = colrow[c];
+#pragma unroll
+      for (int a = 0; a < D - 1; ++a) cd.dh[a] = colrow[NQH * (1 + a) + c];
+    }
     // face fluxes: psi + pin (conforming, wall, far field, fine), coarse side
     // precomputed
     double fl[NF];
@@ -1421,18 +1447,6 @@ hdiv2_kernel(const __grid_constant__ KParams<N> P) {
         if (kd == KIND_COARSE) v = (mesh.cflux != nullptr) ? mesh.cflux[(long long)nf[f] * NC + c] : 0.0;
         fl[f] = act ? v : 0.0;
       }
-    }
-    const ElemGeo<D> g3 = LA ? geo_from_row<D>(rec + 8, P.gc) : elem_geo<D>(mesh.elem, P.gc, act ? e : 0);
-    const double* colrow = (LA && !PL::SLIM) ? st + PL::OC + esl * PL::COLS
-                                             : mesh.col + (long long)g3.col * P.gc.col_stride;
-    ColData<D, N> cd;
-    cd.omh = 1.0;
-    cd.dh[0] = cd.dh[1] = 0.0;
-    if (P.gc.terrain && act) {
-      constexpr int NQH = ipow(N, D - 1);
-      cd.omh = colrow[c];
-#pragma unroll
-      for (int a = 0; a < D - 1; ++a) cd.dh[a] = colrow[NQH * (1 + a) + c];
     }
     // fine side of hanging faces (as hdiv_kernel)
     auto fine_face = [&](auto ax_c, auto side_c) {

@@ -161,7 +161,7 @@ cudaError_t launch_elem(const OpArgs& a, cudaStream_t st, LaunchInfo* info) {
       } else {
         using PL = H2Pipe<D, N>;
         if constexpr (PL::OK) {
-          if (a.pin != nullptr && a.frec != nullptr) {
+          if (a.pin != nullptr && a.frec != nullptr && (a.gs_part == nullptr || PL::FUSED)) {
             // persistent pipelined H2: every SM's resident CTAs, the groups
             // strided over the warps (DG_H2LA=1: records / column rows staged)
             static const bool la = !(getenv("DG_H2LA") && std::string(getenv("DG_H2LA")) == "0");
