@@ -41,6 +41,9 @@ namespace dg {
 #ifndef DG_HK1_ASYNC
 #define DG_HK1_ASYNC 1
 #endif
+#ifndef DG_HK_THREADS
+#define DG_HK_THREADS 128  // threads per CTA of the non-persistent pair (a multiple of 64)
+#endif
 template <int D, int N>
 struct HLayout {
   static constexpr int NP = ipow(N, D);
@@ -50,8 +53,8 @@ struct HLayout {
   static constexpr int TPE = NC <= 32 ? 32 : 64;
   static constexpr int EPW = TPE / NC;        // elements per team
   static constexpr int NSLOT = EPW + ((TPE % NC) ? 1 : 0);
-  static constexpr int WPB = 128 / TPE;       // teams per CTA
-  static constexpr int THREADS = 128;
+  static constexpr int THREADS = DG_HK_THREADS;
+  static constexpr int WPB = THREADS / TPE;   // teams per CTA
   static constexpr int NF = 2 * D;
   static constexpr int TSZ = tile_size<D, N>();
   static constexpr int TABD = (int)(sizeof(Tab<N>) / sizeof(double));
